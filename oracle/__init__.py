@@ -1,0 +1,144 @@
+"""CPU oracle of the paper's definitions — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2504_05808_b200``) never imports it and shares no code with it.
+
+Thin ctypes wrapper over ``oracle/liboracle.so`` (built from ``oracle/oracle.cpp`` with
+g++; see that file's header for what is computed and which paper passage each step
+follows).  Inputs are numpy arrays; all outputs are fresh numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "oracle.cpp")
+_lock = threading.Lock()
+_lib = None
+
+BORDER_BACKGROUND = 1
+
+STATUS = {0: "OK", 1: "EINVAL", 2: "ENOSITE", 6: "EINTERNAL"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int):
+        super().__init__(f"oracle returned {STATUS.get(code, code)}")
+        self.code = code
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so in-tree (plain g++ -O2; building the checker is not using it)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-pthread",
+                               _SRC, "-o", _SO + ".tmp"])
+        os.replace(_SO + ".tmp", _SO)
+    return _SO
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_SO)
+            vp, i64, i32, u32, ci, cd = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                          ctypes.c_uint32, ctypes.c_int, ctypes.c_double)
+            lib.fastrs_oracle_edt_sq.argtypes = [vp, vp, ci, i64, u32, vp, ci]
+            lib.fastrs_oracle_edt_sq.restype = ci
+            lib.fastrs_oracle_fields.argtypes = [vp, vp, ci, i64, i32, u32, vp, vp, vp, ci]
+            lib.fastrs_oracle_fields.restype = ci
+            lib.fastrs_oracle_sphericity_roundness.argtypes = [vp, vp, ci, i64, i32, u32] + [vp] * 10 + [ci]
+            lib.fastrs_oracle_sphericity_roundness.restype = ci
+            for name in ("spheroid_area", "ramanujan_perimeter", "sphericity_3d", "sphericity_2d"):
+                f = getattr(lib, "fastrs_oracle_" + name)
+                f.argtypes = [cd, cd]
+                f.restype = cd
+            _lib = lib
+    return _lib
+
+
+def _geom(labels: np.ndarray, ndim: int | None, batch: int | None):
+    labels = np.ascontiguousarray(labels, dtype=np.int32)
+    if ndim is None:
+        ndim = labels.ndim
+    if batch is None:
+        batch = 1 if labels.ndim == ndim else labels.shape[0]
+    dims = np.ascontiguousarray(labels.shape[-ndim:], dtype=np.int64)
+    return labels, ndim, int(batch), dims
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def edt_sq(labels, flags=BORDER_BACKGROUND, ndim=None, batch=None, nthreads=0) -> np.ndarray:
+    """Exact squared label-aware EDT, uint32, 0 on background."""
+    labels, ndim, batch, dims = _geom(labels, ndim, batch)
+    out = np.zeros(labels.shape, np.uint32)
+    st = _load().fastrs_oracle_edt_sq(_p(labels), _p(dims), ndim, batch, flags, _p(out), nthreads)
+    if st:
+        raise OracleError(st)
+    return out
+
+
+def fields(labels, max_label=None, flags=BORDER_BACKGROUND, ndim=None, batch=None, nthreads=0):
+    """Return (D, LT^2, shell) full-grid fields (uint32, uint32, uint8)."""
+    labels, ndim, batch, dims = _geom(labels, ndim, batch)
+    if max_label is None:
+        max_label = max(1, int(labels.max(initial=0)))
+    d2 = np.zeros(labels.shape, np.uint32)
+    lt2 = np.zeros(labels.shape, np.uint32)
+    sh = np.zeros(labels.shape, np.uint8)
+    st = _load().fastrs_oracle_fields(_p(labels), _p(dims), ndim, batch, max_label, flags,
+                                      _p(d2), _p(lt2), _p(sh), nthreads)
+    if st:
+        raise OracleError(st)
+    return d2, lt2, sh
+
+
+def sphericity_roundness(labels, max_label=None, flags=BORDER_BACKGROUND, ndim=None, batch=None,
+                         label_mask=None, nthreads=0) -> dict:
+    """Per-object metrics; arrays of batch*max_label entries, index b*max_label + label-1."""
+    labels, ndim, batch, dims = _geom(labels, ndim, batch)
+    if max_label is None:
+        max_label = max(1, int(labels.max(initial=0)))
+    M = batch * max_label
+    out = dict(sphericity=np.empty(M), roundness=np.empty(M), volume=np.empty(M, np.int64),
+               n_shell=np.empty(M, np.int64), max_lt2=np.empty(M, np.uint32), mean_lt=np.empty(M),
+               shell_mean_lt=np.empty(M), axis_a=np.empty(M), axis_cb=np.empty(M))
+    mask = None
+    if label_mask is not None:
+        mask = np.ascontiguousarray(label_mask, dtype=np.uint8).reshape(-1)
+        assert mask.size == M
+    st = _load().fastrs_oracle_sphericity_roundness(
+        _p(labels), _p(dims), ndim, batch, int(max_label), flags,
+        *[_p(out[k]) for k in ("sphericity", "roundness", "volume", "n_shell", "max_lt2", "mean_lt",
+                               "shell_mean_lt", "axis_a", "axis_cb")],
+        _p(mask), nthreads)
+    if st:
+        raise OracleError(st)
+    return out
+
+
+def spheroid_area(a: float, c: float) -> float:
+    return _load().fastrs_oracle_spheroid_area(a, c)
+
+
+def ramanujan_perimeter(a: float, b: float) -> float:
+    return _load().fastrs_oracle_ramanujan_perimeter(a, b)
+
+
+def sphericity_3d(V: float, mean_lt: float) -> float:
+    return _load().fastrs_oracle_sphericity_3d(V, mean_lt)
+
+
+def sphericity_2d(A: float, mean_lt: float) -> float:
+    return _load().fastrs_oracle_sphericity_2d(A, mean_lt)

@@ -1,0 +1,33 @@
+"""Generator scaffolding: determinism and the realised workload statistics."""
+import numpy as np
+
+import synth
+
+
+def test_deterministic_c1_c2():
+    for i in (1, 2):
+        a, ia = synth.make_config(i)
+        b, ib = synth.make_config(i)
+        assert ia["sha256"] == ib["sha256"]
+        np.testing.assert_array_equal(a, b)
+
+
+def test_c1_c2_contents():
+    lab, info = synth.make_config(1)
+    assert lab.shape == (256, 256) and lab.dtype == np.int32
+    assert info["max_label"] == 21 and info["n_labels_present"] == 21
+    # disc r=20 at (128,128) is label 21 (closed-form check object)
+    np.testing.assert_array_equal(lab[108:149, 108:149] == 21, synth.disk(20, canvas=41) == 1)
+    lab, info = synth.make_config(2)
+    assert lab.shape == (128, 128, 128) and info["max_label"] == 51
+    assert 0.25 < info["fill"] < 0.45
+    assert (lab[0] == 0).all() and (lab[-1] == 0).all()  # >= 1 element margin
+
+
+def test_c5_small_batch_touching():
+    lab, info = synth.make_config(5, batch=2)
+    assert lab.shape == (2, 2048, 2048)
+    assert 0.25 < info["fill"] < 0.5
+    # touching allowed: some face-adjacent pairs of different non-zero labels exist
+    a, b = lab[0, :, 1:], lab[0, :, :-1]
+    assert ((a != b) & (a > 0) & (b > 0)).any()
