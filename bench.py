@@ -1,0 +1,313 @@
+#!/usr/bin/env python3
+"""Benchmark: one step = one pass of the whole hot path (EDT + LT + shell/reductions +
+sphericity/roundness) over one synthetic label volume.
+
+Default workload: BASELINE.json configs[3] (C4: 3D 1024^3 int32, ~20000 smooth + rough
+grains, ~30 % fill) — the 1024^3 volume the north-star target is quoted on; it fits one
+GPU.  With --gpus N (torchrun, one rank per GPU) every rank processes its own C4 volume:
+independent volumes sharded across GPUs, no data-path
+collective, "scaling": "weak".
+
+Timing: W warm-up steps, then K steps between barrier + cudaDeviceSynchronize, CUDA events
+on the call's stream, max over ranks.  Inputs (4 GiB labels, ~16 GiB workspace) are larger
+than the 126 MB L2, so no explicit flush is needed (stated in config).
+
+--impl reference times the CPU oracle (the reference arm of this tier) on a bounded
+sample of the same workload on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gvoxels/s end-to-end (EDT+LT+sphericity+roundness); % of HBM roofline"
+UNIT = "Gvoxels/s"
+
+# algorithmic HBM bytes per grid element of each stage, 3D path
+STAGE_BYTES_PER_ELEM = {"edt_x": 8.0, "edt_y": 8.0, "edt_z": 8.0, "prune": 4.0, "dilate": 8.0, "metrics": 0.0}
+STAGE_BYTES_PER_KEPT = {"prune": 8.0, "dilate": 8.0}  # centre entries written / read once
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="fastrs", choices=["fastrs", "reference"])
+    p.add_argument("--config", type=int, default=4, help="BASELINE.json config C1..C5 (default C4)")
+    p.add_argument("--batch", type=int, default=None, help="C5 images per rank")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--cpu-sample-labels", type=int, default=1000)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def workload_name(cfg: int) -> str:
+    return {1: "C1: 2D 256^2 int32, 20 ellipses + disc r=20",
+            2: "C2: 3D 128^3 int32, 50 spheroids + sphere r=15",
+            3: "C3: 3D 512^3 int32, 2000 smooth+rough grains, ~28% fill",
+            4: "C4: 3D 1024^3 int32, ~20000 smooth+rough grains (r_eq power law 3-40), ~30% fill",
+            5: "C5: batch of 2D 2048^2 int32 images, ~500 touching cells each"}[cfg]
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 9 for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_input(cfg: int, batch):
+    import synth
+    t0 = time.time()
+    lab, info = synth.make_config(cfg, batch=batch) if cfg == 5 else synth.make_config(cfg)
+    info["gen_seconds"] = round(time.time() - t0, 1)
+    ndim = 2 if cfg in (1, 5) else 3
+    return lab, info, ndim
+
+
+def cpu_baseline(lab, info, ndim, n_labels: int, seed: int = 12345) -> dict:
+    """Time the oracle, as it stands, on a seeded sample of labels of the same workload."""
+    import oracle
+    ml = info["max_label"]
+    B = lab.shape[0] if lab.ndim == ndim + 1 else 1
+    M = B * ml
+    counts = np.bincount(lab.reshape(-1), minlength=ml + 1) if B == 1 else None
+    rng = np.random.default_rng(seed)
+    k = min(n_labels, M)
+    mask = np.zeros(M, np.uint8)
+    mask[rng.choice(M, k, replace=False)] = 1
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.sphericity_roundness(lab, max_label=ml, ndim=ndim, label_mask=mask, nthreads=cores)
+    dt = time.perf_counter() - t0
+    if counts is not None:
+        fg_all = int(counts[1:].sum())
+        fg_s = int(counts[1:][mask.astype(bool)].sum())
+    else:
+        fg_all, fg_s = int(np.count_nonzero(lab)), int(np.count_nonzero(lab)) * k / M
+    frac = fg_s / max(fg_all, 1)
+    value = lab.size * frac / dt / 1e9
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": (f"{k} of {M} labels (seed {seed}), all {lab.size} grid elements scanned for "
+                       f"bounding boxes; value = grid elements x sampled-foreground fraction "
+                       f"({frac:.4f}) / oracle wall time ({dt:.2f} s)"),
+            "seconds": dt}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    lab, info, ndim = make_input(args.config, args.batch)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(lab, info, ndim, max(50, args.cpu_sample_labels // 4), seed=1000 + i)
+        if i >= args.warmup:
+            vals.append(cb)
+    v = statistics.mean(c["value"] for c in vals)
+    sec = statistics.mean(c["seconds"] for c in vals)
+    cb = dict(vals[-1])
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
+            "config": {"workload": workload_name(args.config), "seed": info["seed"],
+                       "elements": int(lab.size), "fill": round(info["fill"], 4)},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_fastrs(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_05808_b200 as F
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    F.load()
+
+    lab, info, ndim = make_input(args.config, args.batch)
+    ml = info["max_label"]
+    B = lab.shape[0] if lab.ndim == ndim + 1 else 1
+    M = B * ml
+    t = torch.from_numpy(lab).to(dev)
+    out = {"sphericity": torch.empty(M, dtype=torch.float64, device=dev),
+           "roundness": torch.empty(M, dtype=torch.float64, device=dev)}
+    ws = F.workspace(F.workspace_bytes(lab.shape, ndim, ml, F.HOST_IO), dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        F.sphericity_roundness(t, max_label=ml, ndim=ndim, ws=ws, out=out)
+
+    for _ in range(args.warmup):
+        step()
+    diag = F.diagnostics(ws)
+
+    # ---- timed region -----------------------------------------------------------------
+    clocks = ClockSampler(local)
+    clocks.start()
+    F.profile(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    stage_ms, calls = F.profile_read()
+    F.profile(False)
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    total_elems = lab.size * world
+    value = total_elems / (ms_max * 1e-3) / 1e9
+
+    # ---- end to end through the host-buffer C entry point -------------------------------
+    pinned = torch.from_numpy(lab).pin_memory()
+    hs, hr = np.empty(M), np.empty(M)
+    F.sphericity_roundness_host(pinned, max_label=ml, ndim=ndim, ws=ws, out=(hs, hr), device=dev)  # warm
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        F.sphericity_roundness_host(pinned, max_label=ml, ndim=ndim, ws=ws, out=(hs, hr), device=dev)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = total_elems / (float(e2e_ms.item()) * 1e-3) / 1e9
+    np.testing.assert_array_equal(hs, out["sphericity"].cpu().numpy())
+
+    # ---- roofline of the dominant kernel ---------------------------------------------------
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    per_launch = {k: v / max(calls, 1) for k, v in stage_ms.items()}
+    dom = max(per_launch, key=lambda k: per_launch[k])
+    n = lab.size
+    alg_bytes = STAGE_BYTES_PER_ELEM[dom] * n + STAGE_BYTES_PER_KEPT.get(dom, 0.0) * diag["n_kept"]
+    achieved = alg_bytes / (per_launch[dom] * 1e-3) / 1e9
+    stage_gbs = {}
+    for k, v in per_launch.items():
+        if v > 0:
+            b = STAGE_BYTES_PER_ELEM[k] * n + STAGE_BYTES_PER_KEPT.get(k, 0.0) * diag["n_kept"]
+            stage_gbs[k] = {"ms": round(v, 4), "GB/s": round(b / (v * 1e-3) / 1e9, 1),
+                            "frac": round(b / (v * 1e-3) / 1e9 / hbm_peak, 4)}
+    model_bytes = sum(STAGE_BYTES_PER_ELEM[k] for k in per_launch if per_launch[k] > 0) * n \
+        + 16.0 * diag["n_kept"]
+    pipe_gbs = model_bytes / (ms * 1e-3) / 1e9
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cb = None
+    if not args.no_cpu_baseline and world == 1:
+        cb = cpu_baseline(lab, info, ndim, args.cpu_sample_labels)
+        cb.pop("seconds", None)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
+        "config": {"workload": workload_name(args.config), "seed": info["seed"], "elements_per_gpu": int(n),
+                   "fill": round(info["fill"], 4), "max_label": ml, "parallelism": f"dp{world} (independent volumes)",
+                   "l2": "inputs larger than L2 (4 GiB labels + ~16 GiB workspace per step), no flush",
+                   "input_sha256": info["sha256"], "input_hash_kind": info.get("sha256_kind")},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(lab.nbytes),
+                "d2h_bytes_per_step": int(2 * M * 8), "ms_per_step": float(e2e_ms.item())},
+        "gpu_launches": int((6 if ndim == 3 else 5) * args.steps),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg_bytes},
+        "stages": stage_gbs,
+        "pipeline_model": {"bytes_per_step": model_bytes, "GB/s": pipe_gbs, "frac": pipe_gbs / hbm_peak},
+        "diagnostics": {k: int(v) for k, v in diag.items()},
+        "clocks": clk,
+        "cpu_baseline": cb,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_fastrs(args)
+
+
+if __name__ == "__main__":
+    main()

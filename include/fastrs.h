@@ -1,0 +1,158 @@
+/*
+ * fastrs.h — C ABI of the B200 (sm_100a) local-thickness sphericity/roundness library
+ * (libfastrs.so).  Method: arXiv 2504.05808 ("fast_rs"), §4.
+ *
+ * The problem statement follows the paper: given a mask of many labelled objects, compute
+ * sphericity and roundness for all objects at once from ONE local-thickness pass
+ * (§1, §4, §5.3).  Four stages, all in hand-written
+ * CUDA kernels:
+ *   1. exact label-aware squared EDT  D(p)      (substrate of LT)
+ *   2. local thickness LT^2(p) = max{D(q): |p-q|^2 < D(q)}  (radius, c3)
+ *   3. shell (4/6-connected contour) + per-label segmented reductions:
+ *      V, mean LT (a_s / a_e), max LT (R),
+ *      mean shell LT (r_bar)
+ *   4. closed forms: 3D Eqs. 1,6,7,8, 2D Eqs. 2,9,10,11
+ *      (PAPER.md:45-48,129-137), roundness R = r_bar / R_max.
+ * Readings of silent/garbled passages (eccentricity form, label-aware sites, border
+ * convention, ...) are listed in DESIGN.md "Readings" and follow SURVEY.md §8(c).
+ *
+ * Conventions (all entry points)
+ *  - labels: int32, C order.  ndim = 3: dims = {Z, Y, X}; ndim = 2: dims = {Y, X}.
+ *    batch >= 1 independent images/volumes are stacked outermost: [batch][Z][Y][X].
+ *    0 = background; objects are labels 1..max_label, independent per batch item.
+ *  - Every element with a different label (other objects included) is a site of an
+ *    object's distance transform; with FASTRS_BORDER_BACKGROUND the virtual layer just
+ *    outside the grid is a site too (and counts as a background neighbour for the shell).
+ *  - All data pointers are DEVICE pointers owned by the caller (except the _host entry
+ *    point and the pure math functions).  Work is enqueued on `stream` (a cudaStream_t;
+ *    NULL = legacy default stream).  By default each call synchronises the stream once,
+ *    at its end, to read a 4-byte status word; FASTRS_ASYNC skips that synchronisation
+ *    (the status then stays in the workspace: read it with fastrs_read_diagnostics).
+ *  - `ws` is caller-owned device scratch of at least fastrs_workspace_bytes() bytes,
+ *    256-byte aligned.  The library allocates nothing per call; it keeps one per-device
+ *    cache (lattice containment table, ~0.6 MB) until fastrs_release().
+ *  - Limits: every dim in [1, 16384]; X <= 16384; squared distances < 2^30.
+ *  - Return value: a fastrs_status.  On a non-OK return fastrs_last_error() gives a
+ *    thread-local message.  Outputs are unspecified after a non-OK return.
+ *  - Per-label outputs have batch*max_label entries, index b*max_label + (label-1).
+ *    Labels absent from an item (V = 0) get NaN metrics and zero counts.
+ */
+#ifndef FASTRS_H
+#define FASTRS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FASTRS_API __attribute__((visibility("default")))
+#else
+#define FASTRS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FASTRS_OK = 0,
+  FASTRS_EINVAL = 1,    /* bad argument: ndim not 2/3, dim < 1 or > 16384, batch < 1, null
+                           pointer, label < 0 or > max_label (SPEC.md:48 invalid-argument) */
+  FASTRS_ENOSITE = 2,   /* some object element has no site at all (an object fills every
+                           line it lies on and the border is not background) */
+  FASTRS_ENOMEM = 3,    /* ws_bytes smaller than fastrs_workspace_bytes() */
+  FASTRS_ECUDA = 4,     /* a CUDA runtime error (message in fastrs_last_error) */
+  FASTRS_ENCCL = 5,     /* reserved for the multi-GPU slab path */
+  FASTRS_EINTERNAL = 6  /* a device-side invariant failed (e.g. LT^2 < D) */
+} fastrs_status;
+
+enum {
+  FASTRS_BORDER_BACKGROUND = 1u, /* the grid border is background   */
+  FASTRS_DETERMINISTIC = 2u,     /* accepted for compatibility: sums are ALWAYS exact
+                                    fixed-point integers, bit-identical across runs     */
+  FASTRS_ASYNC = 4u,             /* do not synchronise the stream at the end of the call  */
+  FASTRS_HOST_IO = 8u            /* size the workspace for fastrs_sphericity_roundness_host */
+};
+
+/* Optional per-label statistics (device pointers, each nullable, batch*max_label long). */
+typedef struct {
+  int64_t* volume;        /* V (3D) or A (2D): element count           */
+  int64_t* n_shell;       /* number of shell elements (D == 1 <=> face neighbour ≠)  */
+  uint32_t* max_lt2;      /* max LT^2 = max D (exact integer)                         */
+  double* mean_lt;        /* a_s / a_e: mean of sqrt(LT^2) over the object            */
+  double* max_lt;         /* R = sqrt(max_lt2)                                        */
+  double* shell_mean_lt;  /* r_bar: mean of sqrt(LT^2) over the shell                 */
+  double* axis_a;         /* model semi-axis a (= mean_lt)                            */
+  double* axis_cb;        /* c_s = 3V/(4 pi a^2) (Eq. 8) or b_e = A/(pi a) (Eq. 10)   */
+} fastrs_object_stats;
+
+/* Counters left in the workspace by the last call that used it (diagnostics / bench). */
+typedef struct {
+  uint32_t status_bits;   /* bit0 bad label, bit1 no site, bit2 internal invariant       */
+  uint32_t dmax;          /* max squared distance over the grid                          */
+  uint64_t n_fg;          /* foreground elements                                         */
+  uint64_t n_kept;        /* maximal-ball centres kept by the lattice pruning (K4)       */
+  uint64_t n_intervals;   /* (ball, row) intervals emitted by the dilation (K5)          */
+  int32_t sum_scale_log2; /* fixed-point scale of the LT sums (2^s)                      */
+  int32_t reserved;
+} fastrs_diagnostics;
+
+/* Bytes of device workspace needed by every entry point below for this geometry.
+ * max_label may be 0 for edt/LT-only use.  flags: FASTRS_HOST_IO adds room for the
+ * labels and outputs of fastrs_sphericity_roundness_host.  Returns FASTRS_OK/EINVAL. */
+FASTRS_API int fastrs_workspace_bytes(const int64_t* dims, int ndim, int64_t batch, int32_t max_label,
+                           uint32_t flags, size_t* bytes);
+
+/* Stage 1 only: exact squared label-aware EDT.  d2_out: uint32 [batch][Z][Y][X] (device),
+ * 0 on background, D >= 1 on objects. */
+FASTRS_API int fastrs_edt_sq(const int32_t* labels, const int64_t* dims, int ndim, int64_t batch,
+                  uint32_t flags, uint32_t* d2_out, void* ws, size_t ws_bytes, void* stream);
+
+/* Stages 1-2: exact local thickness.  lt2_out: uint32 LT^2 (nullable); lt_out: float32
+ * LT radius = (float)sqrt((double)LT^2) (nullable); at least one non-null; both 0 on
+ * background. */
+FASTRS_API int fastrs_local_thickness(const int32_t* labels, const int64_t* dims, int ndim, int64_t batch,
+                           uint32_t flags, uint32_t* lt2_out, float* lt_out, void* ws,
+                           size_t ws_bytes, void* stream);
+
+/* Stages 1-4: per-object sphericity and roundness for every label 1..max_label of every
+ * batch item.  sphericity, roundness: float64 device arrays of batch*max_label (either may
+ * be NULL); stats: optional host struct of device pointers (NULL = none).
+ * (§4.1-4.2) */
+FASTRS_API int fastrs_sphericity_roundness(const int32_t* labels, const int64_t* dims, int ndim,
+                                int64_t batch, int32_t max_label, uint32_t flags,
+                                double* sphericity, double* roundness,
+                                const fastrs_object_stats* stats, void* ws, size_t ws_bytes,
+                                void* stream);
+
+/* Same as fastrs_sphericity_roundness with HOST buffers: labels_host (ideally pinned) is
+ * copied to the device inside the call, results are copied back to sphericity_host /
+ * roundness_host (batch*max_label float64 each, nullable) before it returns.  The
+ * workspace must be sized with FASTRS_HOST_IO.  Always synchronises.  This is the
+ * end-to-end ("e2e") entry point timed by bench.py. */
+FASTRS_API int fastrs_sphericity_roundness_host(const int32_t* labels_host, const int64_t* dims, int ndim,
+                                     int64_t batch, int32_t max_label, uint32_t flags,
+                                     double* sphericity_host, double* roundness_host, void* ws,
+                                     size_t ws_bytes, void* stream);
+
+/* Copy the diagnostics counters of the last call on `ws` to the host (synchronises). */
+FASTRS_API int fastrs_read_diagnostics(const void* ws, fastrs_diagnostics* out, void* stream);
+
+/* Per-stage device time (ms) accumulated over calls while profiling is on: stages are
+ * 0 edt_x, 1 edt_y, 2 edt_z, 3 prune, 4 dilate, 5 metrics.  Events are recorded on the
+ * call's stream.  fastrs_profile(1) enables and resets; fastrs_profile(0) disables. */
+FASTRS_API void fastrs_profile(int enable);
+FASTRS_API int fastrs_profile_read(double* ms_out, int64_t* calls_out, int n_stages);
+
+/* Host-callable closed forms, the same __host__ __device__ code as the metrics kernel. */
+FASTRS_API double fastrs_spheroid_area(double a, double c);         /* Eqs. 6-7, reading c1/c12 */
+FASTRS_API double fastrs_ramanujan_perimeter(double a, double b);   /* Eq. 9                    */
+FASTRS_API double fastrs_sphericity_3d(double V, double mean_lt);   /* Eqs. 1, 8                */
+FASTRS_API double fastrs_sphericity_2d(double A, double mean_lt);   /* Eqs. 2, 10, 11           */
+
+FASTRS_API const char* fastrs_last_error(void);  /* thread-local message of the last failure */
+FASTRS_API void fastrs_release(void);            /* free the per-device caches                */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTRS_H */

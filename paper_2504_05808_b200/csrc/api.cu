@@ -1,0 +1,351 @@
+// C ABI of libfastrs.so (include/fastrs.h): argument checks, workspace carving, the
+// stream-ordered launch sequence K1..K6 and the single status read at the end.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+#include "fastrs.h"
+
+namespace fastrs {
+namespace {
+
+thread_local std::string t_err = "";
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(FASTRS_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+constexpr int64_t kMaxDim = 16384;
+
+int make_geom(const int64_t* dims, int ndim, int64_t batch, Geom& g) {
+  if (!dims) return fail(FASTRS_EINVAL, "dims is NULL");
+  if (ndim != 2 && ndim != 3) return fail(FASTRS_EINVAL, "ndim must be 2 or 3 (got %d)", ndim);
+  if (batch < 1) return fail(FASTRS_EINVAL, "batch must be >= 1");
+  for (int i = 0; i < ndim; ++i)
+    if (dims[i] < 1 || dims[i] > kMaxDim) return fail(FASTRS_EINVAL, "dims[%d] = %lld outside [1, 16384]", i, (long long)dims[i]);
+  g.ndim = ndim;
+  g.B = batch;
+  g.Z = ndim == 3 ? dims[0] : 1;
+  g.Y = dims[ndim - 2];
+  g.X = dims[ndim - 1];
+  g.N = g.B * g.Z * g.Y * g.X;
+  g.TY = ndim == 3 ? 8 : 64;
+  g.TZ = ndim == 3 ? 8 : 1;
+  g.ntx = (g.X + kTX - 1) / kTX;
+  g.nty = (g.Y + g.TY - 1) / g.TY;
+  g.ntz = (g.Z + g.TZ - 1) / g.TZ;
+  g.ntiles = g.B * g.ntz * g.nty * g.ntx;
+  if (g.ntiles >= (1ll << 32)) return fail(FASTRS_EINVAL, "grid too large");
+  return FASTRS_OK;
+}
+
+inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+struct Layout {
+  size_t hdr, A, B, meta, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd, total;
+};
+
+Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
+  Layout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  const size_t M = (size_t)g.B * (size_t)(max_label > 0 ? max_label : 0);
+  L.hdr = take(256);
+  L.A = take((size_t)g.N * 4);
+  L.B = take((size_t)g.N * 4);
+  L.meta = take((size_t)g.ntiles * sizeof(TileMeta));
+  L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
+  L.vol = take(M * 8);
+  L.nsh = take(M * 8);
+  L.sum = take(M * 8);
+  L.sumsh = take(M * 8);
+  L.mx = take(M * 4);
+  if (flags & kFlagHostIO) {
+    L.h_labels = take((size_t)g.N * 4);
+    L.h_sph = take(M * 8);
+    L.h_rnd = take(M * 8);
+  }
+  L.total = off;
+  return L;
+}
+
+// ---- profiling -------------------------------------------------------------------------
+constexpr int kStages = 6;
+std::mutex g_prof_mu;
+bool g_prof = false;
+double g_prof_ms[kStages];
+int64_t g_prof_calls = 0;
+cudaEvent_t g_ev[64][kStages + 1];
+bool g_ev_init[64];
+
+struct StageTimer {
+  bool on = false;
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  bool used[kStages] = {};
+  int last = -1;
+  void begin(cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    on = g_prof;
+    st = s;
+    if (!on) return;
+    cudaGetDevice(&dev);
+    if (!g_ev_init[dev]) {
+      for (auto& e : g_ev[dev]) cudaEventCreate(&e);
+      g_ev_init[dev] = true;
+    }
+    cudaEventRecord(g_ev[dev][0], st);
+  }
+  // mark the end of stage k (events are recorded after each stage, in order)
+  void mark(int k) {
+    if (!on) return;
+    cudaEventRecord(g_ev[dev][k + 1], st);
+    used[k] = true;
+    last = k;
+  }
+  void finish() {
+    if (!on || last < 0) return;
+    cudaEventSynchronize(g_ev[dev][last + 1]);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    int prev = 0;
+    for (int k = 0; k < kStages; ++k) {
+      if (!used[k]) continue;
+      float ms = 0;
+      cudaEventElapsedTime(&ms, g_ev[dev][prev], g_ev[dev][k + 1]);
+      g_prof_ms[k] += ms;
+      prev = k + 1;
+    }
+    g_prof_calls += 1;
+  }
+};
+
+enum Stage { kEdtOnly, kLtOnly, kFull };
+
+int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags, Stage stage, uint32_t* d2_out,
+        uint32_t* lt2_out, float* lt_out, const Outputs* outs, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!labels) return fail(FASTRS_EINVAL, "labels is NULL");
+  if (!ws) return fail(FASTRS_EINVAL, "workspace is NULL");
+  if (((uintptr_t)ws & 255) != 0) return fail(FASTRS_EINVAL, "workspace must be 256-byte aligned");
+  const Layout L = make_layout(g, stage == kFull ? max_label : 0, 0);
+  if (ws_bytes < L.total)
+    return fail(FASTRS_ENOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+  char* w = (char*)ws;
+  WsHeader* hdr = (WsHeader*)(w + L.hdr);
+  uint32_t* A = (uint32_t*)(w + L.A);
+  uint32_t* B = (uint32_t*)(w + L.B);
+  TileMeta* meta = (TileMeta*)(w + L.meta);
+  uint2* cent = (uint2*)(w + L.cent);
+  const bool border = (flags & kFlagBorder) != 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (stage != kEdtOnly) {
+    e = ensure_mtables(dev);
+    if (e != cudaSuccess) return cuda_fail(e, "building the lattice containment table");
+  }
+  StageTimer tm;
+  tm.begin(st);
+  e = cudaMemsetAsync(hdr, 0, 256, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  Accum acc{};
+  if (stage == kFull) {
+    acc.vol = (unsigned long long*)(w + L.vol);
+    acc.nshell = (unsigned long long*)(w + L.nsh);
+    acc.sum = (unsigned long long*)(w + L.sum);
+    acc.sumshell = (unsigned long long*)(w + L.sumsh);
+    acc.maxlt2 = (uint32_t*)(w + L.mx);
+    acc.M = g.B * (int64_t)max_label;
+    acc.max_label = max_label;
+    cudaMemsetAsync(w + L.vol, 0, (L.mx - L.vol) + align256((size_t)acc.M * 4), st);
+  }
+  if (lt2_out) cudaMemsetAsync(lt2_out, 0, (size_t)g.N * 4, st);
+  if (lt_out) cudaMemsetAsync(lt_out, 0, (size_t)g.N * 4, st);
+
+  // K1..K3: EDT
+  launch_edt_x(labels, A, g, stage == kFull ? max_label : INT32_MAX, border, hdr, st);
+  tm.mark(0);
+  uint32_t* D;
+  if (g.ndim == 2) {
+    D = stage == kEdtOnly ? d2_out : B;
+    launch_edt_col(A, D, g, 1, true, border, hdr, st);
+    tm.mark(1);
+  } else {
+    launch_edt_col(A, B, g, 1, false, border, hdr, st);
+    tm.mark(1);
+    D = stage == kEdtOnly ? d2_out : A;
+    launch_edt_col(B, D, g, 2, true, border, hdr, st);
+    tm.mark(2);
+  }
+  if (stage != kEdtOnly) {
+    launch_prune(D, g, meta, cent, hdr, st);  // K4
+    tm.mark(3);
+    launch_dilate(labels, D, meta, cent, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out, hdr, st);  // K5
+    tm.mark(4);
+    if (stage == kFull) {
+      launch_metrics(acc, g, *outs, hdr, st);  // K6
+      tm.mark(5);
+    }
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  if (flags & kFlagAsync) return FASTRS_OK;
+  uint32_t status = 0;
+  e = cudaMemcpyAsync(&status, &hdr->status, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "status read");
+  tm.finish();
+  if (status & kStBadLabel) return fail(FASTRS_EINVAL, "a label is < 0 or > max_label");
+  if (status & kStNoSite)
+    return fail(FASTRS_ENOSITE, "an object element has no site (no other label and the border is not background)");
+  if (status & kStInternal) return fail(FASTRS_EINTERNAL, "device invariant violated");
+  return FASTRS_OK;
+}
+
+}  // namespace
+}  // namespace fastrs
+
+using namespace fastrs;
+
+extern "C" {
+
+int fastrs_workspace_bytes(const int64_t* dims, int ndim, int64_t batch, int32_t max_label, uint32_t flags,
+                           size_t* bytes) {
+  Geom g;
+  int rc = make_geom(dims, ndim, batch, g);
+  if (rc) return rc;
+  if (!bytes) return fail(FASTRS_EINVAL, "bytes is NULL");
+  if (max_label < 0) return fail(FASTRS_EINVAL, "max_label < 0");
+  *bytes = make_layout(g, max_label, flags).total;
+  return FASTRS_OK;
+}
+
+int fastrs_edt_sq(const int32_t* labels, const int64_t* dims, int ndim, int64_t batch, uint32_t flags,
+                  uint32_t* d2_out, void* ws, size_t ws_bytes, void* stream) {
+  Geom g;
+  int rc = make_geom(dims, ndim, batch, g);
+  if (rc) return rc;
+  if (!d2_out) return fail(FASTRS_EINVAL, "d2_out is NULL");
+  return run(labels, g, 0, flags, kEdtOnly, d2_out, nullptr, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int fastrs_local_thickness(const int32_t* labels, const int64_t* dims, int ndim, int64_t batch, uint32_t flags,
+                           uint32_t* lt2_out, float* lt_out, void* ws, size_t ws_bytes, void* stream) {
+  Geom g;
+  int rc = make_geom(dims, ndim, batch, g);
+  if (rc) return rc;
+  if (!lt2_out && !lt_out) return fail(FASTRS_EINVAL, "both lt2_out and lt_out are NULL");
+  return run(labels, g, 0, flags, kLtOnly, nullptr, lt2_out, lt_out, nullptr, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int fastrs_sphericity_roundness(const int32_t* labels, const int64_t* dims, int ndim, int64_t batch,
+                                int32_t max_label, uint32_t flags, double* sphericity, double* roundness,
+                                const fastrs_object_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+  Geom g;
+  int rc = make_geom(dims, ndim, batch, g);
+  if (rc) return rc;
+  if (max_label < 1) return fail(FASTRS_EINVAL, "max_label must be >= 1");
+  Outputs o{};
+  o.sphericity = sphericity;
+  o.roundness = roundness;
+  if (stats) {
+    o.volume = stats->volume;
+    o.n_shell = stats->n_shell;
+    o.max_lt2 = stats->max_lt2;
+    o.mean_lt = stats->mean_lt;
+    o.max_lt = stats->max_lt;
+    o.shell_mean_lt = stats->shell_mean_lt;
+    o.axis_a = stats->axis_a;
+    o.axis_cb = stats->axis_cb;
+  }
+  return run(labels, g, max_label, flags, kFull, nullptr, nullptr, nullptr, &o, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int fastrs_sphericity_roundness_host(const int32_t* labels_host, const int64_t* dims, int ndim, int64_t batch,
+                                     int32_t max_label, uint32_t flags, double* sphericity_host,
+                                     double* roundness_host, void* ws, size_t ws_bytes, void* stream) {
+  Geom g;
+  int rc = make_geom(dims, ndim, batch, g);
+  if (rc) return rc;
+  if (max_label < 1) return fail(FASTRS_EINVAL, "max_label must be >= 1");
+  if (!labels_host || !ws) return fail(FASTRS_EINVAL, "NULL pointer");
+  const Layout L = make_layout(g, max_label, kFlagHostIO);
+  if (ws_bytes < L.total) return fail(FASTRS_ENOMEM, "workspace too small for HOST_IO: %zu < %zu", ws_bytes, L.total);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  int32_t* dlab = (int32_t*)(w + L.h_labels);
+  double* dsph = (double*)(w + L.h_sph);
+  double* drnd = (double*)(w + L.h_rnd);
+  cudaError_t e = cudaMemcpyAsync(dlab, labels_host, (size_t)g.N * 4, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D labels");
+  Outputs o{};
+  o.sphericity = dsph;
+  o.roundness = drnd;
+  rc = run(dlab, g, max_label, flags | kFlagAsync, kFull, nullptr, nullptr, nullptr, &o, ws, ws_bytes, st);
+  if (rc) return rc;
+  const size_t M = (size_t)g.B * max_label;
+  uint32_t status = 0;
+  e = cudaMemcpyAsync(&status, w + make_layout(g, max_label, 0).hdr, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && sphericity_host) e = cudaMemcpyAsync(sphericity_host, dsph, M * 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && roundness_host) e = cudaMemcpyAsync(roundness_host, drnd, M * 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H results");
+  if (status & kStBadLabel) return fail(FASTRS_EINVAL, "a label is < 0 or > max_label");
+  if (status & kStNoSite) return fail(FASTRS_ENOSITE, "an object element has no site");
+  if (status & kStInternal) return fail(FASTRS_EINTERNAL, "device invariant violated");
+  return FASTRS_OK;
+}
+
+int fastrs_read_diagnostics(const void* ws, fastrs_diagnostics* out, void* stream) {
+  if (!ws || !out) return fail(FASTRS_EINVAL, "NULL pointer");
+  WsHeader h;
+  cudaError_t e = cudaMemcpyAsync(&h, ws, sizeof h, cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "read diagnostics");
+  out->status_bits = h.status;
+  out->dmax = h.dmax;
+  out->n_fg = h.n_fg;
+  out->n_kept = h.n_kept;
+  out->n_intervals = h.n_intervals;
+  out->sum_scale_log2 = h.scale_log2;
+  out->reserved = 0;
+  return FASTRS_OK;
+}
+
+void fastrs_profile(int enable) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof = enable != 0;
+  if (g_prof) {
+    for (double& v : g_prof_ms) v = 0;
+    g_prof_calls = 0;
+  }
+}
+
+int fastrs_profile_read(double* ms_out, int64_t* calls_out, int n_stages) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (int k = 0; k < n_stages && k < kStages; ++k) ms_out[k] = g_prof_ms[k];
+  if (calls_out) *calls_out = g_prof_calls;
+  return kStages;
+}
+
+const char* fastrs_last_error(void) { return t_err.c_str(); }
+
+void fastrs_release(void) { release_mtables(); }
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+// Internal declarations shared by the libfastrs.so translation units (NOT the oracle).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fastrs {
+
+// ---- packed EDT word (S2): [b31 y-run start][b30 z-run start][b29..0 partial D] -----
+constexpr uint32_t kInf = 0x3FFFFFFFu;   // "no site yet"; also the D mask
+constexpr uint32_t kMask = 0x3FFFFFFFu;
+constexpr uint32_t kBitY = 0x80000000u;  // element is the first of its y-run
+constexpr uint32_t kBitZ = 0x40000000u;  // element is the first of its z-run
+
+// ---- status bits in the workspace header ---------------------------------------------
+constexpr uint32_t kStBadLabel = 1u, kStNoSite = 2u, kStInternal = 4u;
+
+constexpr uint32_t kFlagBorder = 1u, kFlagAsync = 4u, kFlagHostIO = 8u;
+
+// ---- dilation / pruning tiles ---------------------------------------------------------
+// 3D tile 32 x 8 x 8 (x fastest), 2D tile 32 x 64; both 64 rows of 32 = 2048 elements.
+constexpr int kTX = 32;
+constexpr int kTileVol = 2048;
+constexpr int kRows = 64;
+constexpr int kLevels = 6;              // sparse-table levels for 32-wide rows: 1..32
+constexpr int kRowStride = kLevels * 32 + 1;  // +1: rows start in different banks
+
+// ---- lattice containment table (S4) ---------------------------------------------------
+constexpr int kDcap3 = 8192;   // 3D: centres with D > kDcap3 are always kept
+constexpr int kDcap2 = 32768;  // 2D
+constexpr int kClasses3 = 12;  // offset classes with |s|^2 <= 12 (178 offsets)
+constexpr int kClasses2 = 5;   // offset classes with |s|^2 <= 8  (24 offsets)
+constexpr int kStage1Classes3 = 3;  // 26-neighbourhood
+constexpr int kStage1Classes2 = 2;  // 8-neighbourhood
+constexpr int kHalo3 = 3, kHalo2 = 2;
+
+struct Geom {
+  int ndim;
+  int64_t B, Z, Y, X;  // 2D: Z = 1
+  int64_t N;           // B*Z*Y*X
+  int TY, TZ;          // tile extents (3D: 8,8; 2D: 64,1)
+  int64_t ntx, nty, ntz, ntiles;  // tile grid per item: ntz*nty*ntx, ntiles includes B
+};
+
+struct WsHeader {
+  uint32_t status;
+  uint32_t dmax;
+  unsigned long long n_fg;
+  unsigned long long n_kept;
+  unsigned long long n_intervals;
+  int32_t scale_log2;
+  int32_t pad[7];
+};
+static_assert(sizeof(WsHeader) <= 256, "header");
+
+// per-tile metadata written by the pruning kernel
+struct TileMeta {
+  uint32_t count;  // kept centres
+  uint32_t maxD;   // max D over kept centres
+  uint32_t nfg;    // foreground elements of the tile
+  uint32_t pad;
+};
+
+// per-label accumulators (SoA)
+struct Accum {
+  unsigned long long* vol;
+  unsigned long long* nshell;
+  unsigned long long* sum;       // fixed point, scale 2^scale_log2
+  unsigned long long* sumshell;  // fixed point
+  uint32_t* maxlt2;
+  int64_t M;                     // batch*max_label
+  int32_t max_label;
+};
+
+struct Outputs {
+  double* sphericity;
+  double* roundness;
+  int64_t* volume;
+  int64_t* n_shell;
+  uint32_t* max_lt2;
+  double* mean_lt;
+  double* max_lt;
+  double* shell_mean_lt;
+  double* axis_a;
+  double* axis_cb;
+};
+
+__host__ __device__ inline int ceil_log2_u64(unsigned long long v) {
+  int r = 0;
+  while ((1ull << r) < v && r < 63) ++r;
+  return r;
+}
+
+// Fixed-point scale of the LT sums: every term sqrt(LT^2)*2^s < 2^15 * 2^s and an object
+// has at most Nb elements, so choosing s with Nb * (isqrt(Dmax)+1) * 2^s <= 2^62 makes the
+// u64 sums overflow-free and exact (integer adds are order-independent).  s in [0, 32].
+__host__ __device__ inline int sum_scale_log2(int64_t Nb, uint32_t dmax) {
+  unsigned long long r = 1;
+  while ((r + 1) * (r + 1) <= (unsigned long long)dmax) ++r;  // ~isqrt(dmax), small loop
+  int s = 62 - ceil_log2_u64((unsigned long long)Nb) - ceil_log2_u64(r + 1);
+  return s < 0 ? 0 : (s > 32 ? 32 : s);
+}
+
+// ---- kernel launchers (stream-ordered) -----------------------------------------------
+void launch_edt_x(const int32_t* labels, uint32_t* out, const Geom& g, int32_t max_label,
+                  bool border, WsHeader* hdr, cudaStream_t st);
+void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, bool final_pass,
+                    bool border, WsHeader* hdr, cudaStream_t st);
+cudaError_t ensure_mtables(int device);  // builds the per-device lattice tables (sync, once)
+void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, WsHeader* hdr,
+                  cudaStream_t st);
+void launch_dilate(const int32_t* labels, const uint32_t* D, const TileMeta* meta,
+                   const uint2* centres, const Geom& g, const Accum* acc, uint32_t* lt2_out,
+                   float* lt_out, WsHeader* hdr, cudaStream_t st);
+void launch_metrics(const Accum& acc, const Geom& g, const Outputs& o, WsHeader* hdr,
+                    cudaStream_t st);
+void release_mtables();
+
+}  // namespace fastrs

@@ -1,0 +1,235 @@
+// Exact label-aware squared EDT as three separable passes.
+//
+// D(p) = min over sites s of |p - s|^2, sites = elements with another label (plus the
+// virtual border layer with FASTRS_BORDER_BACKGROUND): the substrate of local thickness
+// (§4, "exact squared-distance computation via separable per-axis
+// passes").  The passes reduce the global label-aware problem to per-RUN problems: along
+// each axis an element only interacts with the same-label run it lies in, because every
+// element beyond a run end is dominated by the run end's neighbour, which is itself a site
+// at distance 0 in the partial field.
+//
+//   K1 edt_x : warp per row.  Two warp sweeps with ballot/ffs find run starts and ends;
+//              g = (distance to the nearest run end's neighbour)^2.  Fused: label
+//              validation (a1) and the y/z run-start flags packed into bits 31/30 (S2), so
+//              later passes never re-read labels.
+//   K2/K3    : column passes along y / z.  A CTA stages a [256 + 2*32][32] column tile of
+//              packed words in shared memory (coalesced 128-byte rows) and each thread runs
+//              the exact windowed scan  best = min(best, g(p +- dq) + dq^2)  until dq^2 >=
+//              best or a run end (a site at distance dq) is met; reads outside the staged
+//              window fall back to global (L2).  The final pass emits D, Dmax, n_fg and
+//              flags elements with no site (ENOSITE).
+#include "common.cuh"
+
+namespace fastrs {
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+__global__ void __launch_bounds__(256) k_edt_x(const int32_t* __restrict__ lab, uint32_t* __restrict__ out,
+                                               int64_t nrows, int X, int64_t Y, int64_t Z,
+                                               int32_t max_label, int border, int is3d,
+                                               WsHeader* __restrict__ hdr) {
+  extern __shared__ uint16_t s_end[];
+  const int warps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * warps + warp;
+  if (row >= nrows) return;
+  uint16_t* ends = s_end + (size_t)warp * X;
+  const int64_t y = row % Y;
+  const int64_t z = (row / Y) % Z;
+  const int32_t* L = lab + row * X;
+  const int32_t* Ly = y > 0 ? L - X : nullptr;
+  const int32_t* Lz = (is3d && z > 0) ? L - X * Y : nullptr;
+  uint32_t* O = out + row * X;
+  const int nchunk = (X + 31) >> 5;
+
+  // sweep 1 (right to left): end of the run containing x
+  int carry_end = X - 1;
+  int32_t right_next = 0;
+  for (int c = nchunk - 1; c >= 0; --c) {
+    const int x = (c << 5) + lane;
+    const int32_t v = x < X ? __ldg(L + x) : 0;
+    int32_t r = __shfl_down_sync(kFull, v, 1);
+    if (lane == 31) r = right_next;
+    const bool is_end = x < X && (x == X - 1 || v != r);
+    const uint32_t m = __ballot_sync(kFull, is_end);
+    const uint32_t ge = m & (kFull << lane);
+    const int e = ge ? (c << 5) + __ffs(ge) - 1 : carry_end;
+    if (x < X) ends[x] = (uint16_t)e;
+    if (m) carry_end = (c << 5) + __ffs(m) - 1;
+    right_next = __shfl_sync(kFull, v, 0);
+  }
+
+  // sweep 2 (left to right): start of the run, distances, flags
+  int carry_start = 0;
+  int32_t left_prev = 0;
+  uint32_t bad = 0;
+  for (int c = 0; c < nchunk; ++c) {
+    const int x = (c << 5) + lane;
+    const int32_t v = x < X ? __ldg(L + x) : 0;
+    int32_t l = __shfl_up_sync(kFull, v, 1);
+    if (lane == 0) l = left_prev;
+    const bool is_start = x < X && (x == 0 || v != l);
+    const uint32_t m = __ballot_sync(kFull, is_start);
+    const uint32_t le = m & (kFull >> (31 - lane));
+    const int s = le ? (c << 5) + 31 - __clz(le) : carry_start;
+    if (m) carry_start = (c << 5) + 31 - __clz(m);
+    left_prev = __shfl_sync(kFull, v, 31);
+    if (x < X) {
+      uint32_t g = 0;
+      if (v != 0) {
+        if (v < 0 || v > max_label) bad = 1;
+        const int e = ends[x];
+        const uint32_t dl = (s > 0 || border) ? (uint32_t)(x - s + 1) : kFull;
+        const uint32_t dr = (e < X - 1 || border) ? (uint32_t)(e + 1 - x) : kFull;
+        const uint32_t d = min(dl, dr);
+        g = d == kFull ? kInf : d * d;
+      }
+      uint32_t bits = 0;
+      if (!Ly || __ldg(Ly + x) != v) bits |= kBitY;
+      if (!Lz || __ldg(Lz + x) != v) bits |= kBitZ;
+      O[x] = g | bits;
+    }
+  }
+  if (__any_sync(kFull, bad) && lane == 0) atomicOr(&hdr->status, kStBadLabel);
+}
+
+constexpr int kColS = 256;  // positions per CTA
+constexpr int kColH = 32;   // staged halo on each side
+constexpr int kColRows = kColS + 2 * kColH;
+constexpr int kColWarps = 8;
+
+template <bool FINAL>
+__global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                 int64_t L, int64_t astride, int X, int nxb, int nseg,
+                                                 int64_t n_inner, int64_t inner_mult, int64_t outer_mult,
+                                                 uint32_t chbit, int border, WsHeader* __restrict__ hdr) {
+  __shared__ uint32_t tile[kColRows * 32];
+  int64_t bid = blockIdx.x;
+  const int xb = (int)(bid % nxb);
+  bid /= nxb;
+  const int seg = (int)(bid % nseg);
+  const int64_t outer = bid / nseg;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t base = (outer / n_inner) * outer_mult + (outer % n_inner) * inner_mult + (int64_t)xb * 32 + lane;
+  const bool xin = xb * 32 + lane < X;
+  const int64_t s0 = (int64_t)seg * kColS;
+  const int64_t lo = s0 - kColH > 0 ? s0 - kColH : 0;
+  const int64_t hi = s0 + kColS + kColH < L ? s0 + kColS + kColH : L;
+  for (int64_t r = lo + warp; r < hi; r += kColWarps)
+    tile[(r - lo) * 32 + lane] = xin ? __ldg(in + base + r * astride) : 0u;
+  __syncthreads();
+
+  auto fetch = [&](int64_t q) -> uint32_t {
+    return (q >= lo && q < hi) ? tile[(q - lo) * 32 + lane] : __ldg(in + base + q * astride);
+  };
+
+  uint32_t dmax = 0, nfg = 0, nosite = 0;
+  const int64_t pend = s0 + kColS < L ? s0 + kColS : L;
+  for (int64_t p = s0 + warp; p < pend; p += kColWarps) {
+    const uint32_t v = tile[(p - lo) * 32 + lane];
+    const uint32_t g = v & kMask;
+    uint32_t res = FINAL ? 0u : v;
+    if (xin && g != 0) {
+      uint32_t best = g;
+      bool dn = true, up = true;
+      uint32_t chk = v & chbit;  // run-start flag of element p - dq + 1
+      for (uint32_t dq = 1; dn || up; ++dq) {
+        const uint32_t dq2 = dq * dq;
+        if (dq2 >= best) break;
+        if (dn) {
+          if (chk) {  // p - dq lies outside the run: a site (or the border / nothing)
+            if (p - (int64_t)dq >= 0 || border) best = min(best, dq2);
+            dn = false;
+          } else {
+            const uint32_t w = fetch(p - (int64_t)dq);
+            best = min(best, (w & kMask) + dq2);
+            chk = w & chbit;
+          }
+        }
+        if (up) {
+          const int64_t q = p + (int64_t)dq;
+          if (q >= L) {
+            if (border) best = min(best, dq2);
+            up = false;
+          } else {
+            const uint32_t w = fetch(q);
+            if (w & chbit) {
+              best = min(best, dq2);
+              up = false;
+            } else {
+              best = min(best, (w & kMask) + dq2);
+            }
+          }
+        }
+      }
+      if (FINAL) {
+        res = best;
+        dmax = max(dmax, best);
+        nfg += 1;
+        nosite |= best >= kInf;
+      } else {
+        res = best | (v & (kBitY | kBitZ));
+      }
+    }
+    if (xin) out[base + p * astride] = res;
+  }
+  if (FINAL) {
+    dmax = __reduce_max_sync(kFull, dmax);
+    nfg = __reduce_add_sync(kFull, nfg);
+    nosite = __any_sync(kFull, nosite);
+    if (lane == 0) {
+      if (dmax) atomicMax(&hdr->dmax, dmax);
+      if (nfg) atomicAdd(&hdr->n_fg, (unsigned long long)nfg);
+      if (nosite) atomicOr(&hdr->status, kStNoSite);
+    }
+  }
+}
+
+}  // namespace
+
+void launch_edt_x(const int32_t* labels, uint32_t* out, const Geom& g, int32_t max_label, bool border,
+                  WsHeader* hdr, cudaStream_t st) {
+  const int64_t nrows = g.B * g.Z * g.Y;
+  int warps = (int)(49152 / (2 * g.X));
+  warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
+  const size_t smem = (size_t)warps * g.X * sizeof(uint16_t);
+  const int64_t blocks = (nrows + warps - 1) / warps;
+  k_edt_x<<<(unsigned)blocks, warps * 32, smem, st>>>(labels, out, nrows, (int)g.X, g.Y, g.Z, max_label,
+                                                      border ? 1 : 0, g.ndim == 3 ? 1 : 0, hdr);
+}
+
+// axis 1 = y, axis 2 = z.
+void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, bool final_pass, bool border,
+                    WsHeader* hdr, cudaStream_t st) {
+  int64_t L, astride, n_outer, n_inner, inner_mult, outer_mult;
+  uint32_t chbit;
+  if (axis == 1) {
+    L = g.Y;
+    astride = g.X;
+    n_outer = g.B * g.Z;
+    n_inner = 1;
+    inner_mult = 0;
+    outer_mult = g.Y * g.X;
+    chbit = kBitY;
+  } else {
+    L = g.Z;
+    astride = g.Y * g.X;
+    n_outer = g.B * g.Y;
+    n_inner = g.Y;
+    inner_mult = g.X;
+    outer_mult = g.Z * g.Y * g.X;
+    chbit = kBitZ;
+  }
+  const int nxb = (int)((g.X + 31) / 32);
+  const int nseg = (int)((L + kColS - 1) / kColS);
+  const int64_t blocks = (int64_t)nxb * nseg * n_outer;
+  if (final_pass)
+    k_edt_col<true><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(in, out, L, astride, (int)g.X, nxb, nseg, n_inner,
+                                                                  inner_mult, outer_mult, chbit, border ? 1 : 0, hdr);
+  else
+    k_edt_col<false><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(in, out, L, astride, (int)g.X, nxb, nseg, n_inner,
+                                                                   inner_mult, outer_mult, chbit, border ? 1 : 0, hdr);
+}
+
+}  // namespace fastrs

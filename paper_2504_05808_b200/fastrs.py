@@ -1,0 +1,266 @@
+"""Thin ctypes binding of libfastrs.so (include/fastrs.h) — argument marshalling only.
+
+Every step of the computation runs in the CUDA kernels behind the C ABI; this module only
+turns torch CUDA tensors into raw device pointers + the current stream, sizes and caches
+the device workspace, and maps status codes to exceptions.  There is no CPU fallback: if
+the library cannot be loaded, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+import torch
+
+from . import _build
+
+BORDER_BACKGROUND = 1
+DETERMINISTIC = 2
+ASYNC = 4
+HOST_IO = 8
+
+STAGES = ("edt_x", "edt_y", "edt_z", "prune", "dilate", "metrics")
+
+_STATUS = {0: "OK", 1: "EINVAL", 2: "ENOSITE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "EINTERNAL"}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class FastrsError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"fastrs {_STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.name = _STATUS.get(code, str(code))
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("volume", "n_shell", "max_lt2", "mean_lt", "max_lt",
+                                               "shell_mean_lt", "axis_a", "axis_cb")]
+
+
+class _Diag(ctypes.Structure):
+    _fields_ = [("status_bits", ctypes.c_uint32), ("dmax", ctypes.c_uint32), ("n_fg", ctypes.c_uint64),
+                ("n_kept", ctypes.c_uint64), ("n_intervals", ctypes.c_uint64),
+                ("sum_scale_log2", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+def load(build_if_missing: bool = True) -> ctypes.CDLL:
+    """Load libfastrs.so (built in-tree).  Raises if it cannot be built or loaded."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if build_if_missing and not _build.up_to_date():
+                _build.build()
+            if not os.path.exists(_build.SO):
+                raise ImportError(f"libfastrs.so missing at {_build.SO}; run __graft_entry__.build()")
+            lib = ctypes.CDLL(_build.SO)
+            vp, i64, i32, u32, ci, cd, sz = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32,
+                                              ctypes.c_int, ctypes.c_double, ctypes.c_size_t)
+            lib.fastrs_workspace_bytes.argtypes = [vp, ci, i64, i32, u32, ctypes.POINTER(sz)]
+            lib.fastrs_edt_sq.argtypes = [vp, vp, ci, i64, u32, vp, vp, sz, vp]
+            lib.fastrs_local_thickness.argtypes = [vp, vp, ci, i64, u32, vp, vp, vp, sz, vp]
+            lib.fastrs_sphericity_roundness.argtypes = [vp, vp, ci, i64, i32, u32, vp, vp, vp, vp, sz, vp]
+            lib.fastrs_sphericity_roundness_host.argtypes = [vp, vp, ci, i64, i32, u32, vp, vp, vp, sz, vp]
+            lib.fastrs_read_diagnostics.argtypes = [vp, ctypes.POINTER(_Diag), vp]
+            lib.fastrs_profile.argtypes = [ci]
+            lib.fastrs_profile.restype = None
+            lib.fastrs_profile_read.argtypes = [vp, vp, ci]
+            lib.fastrs_last_error.restype = ctypes.c_char_p
+            lib.fastrs_release.restype = None
+            for n in ("spheroid_area", "ramanujan_perimeter", "sphericity_3d", "sphericity_2d"):
+                f = getattr(lib, "fastrs_" + n)
+                f.argtypes = [cd, cd]
+                f.restype = cd
+            for n in ("workspace_bytes", "edt_sq", "local_thickness", "sphericity_roundness",
+                      "sphericity_roundness_host", "read_diagnostics", "profile_read"):
+                getattr(lib, "fastrs_" + n).restype = ci
+            _lib = lib
+    return _lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise FastrsError(rc, load().fastrs_last_error().decode(errors="replace"))
+
+
+def _geometry(shape, ndim, batch):
+    shape = tuple(int(s) for s in shape)
+    if ndim is None:
+        if len(shape) not in (2, 3):
+            raise ValueError("pass ndim= for batched input")
+        ndim = len(shape)
+    if len(shape) == ndim:
+        b = 1
+    elif len(shape) == ndim + 1:
+        b = shape[0]
+    else:
+        raise ValueError(f"labels of shape {shape} do not match ndim={ndim}")
+    if batch is not None and batch != b:
+        raise ValueError("batch does not match the labels' shape")
+    dims = (ctypes.c_int64 * ndim)(*shape[-ndim:])
+    return ndim, b, dims
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def workspace_bytes(shape, ndim=None, max_label=0, flags=0) -> int:
+    ndim, b, dims = _geometry(shape, ndim, None)
+    out = ctypes.c_size_t(0)
+    _check(load().fastrs_workspace_bytes(dims, ndim, b, int(max_label), flags, ctypes.byref(out)))
+    return out.value
+
+
+_ws_cache: dict = {}
+
+
+def workspace(nbytes: int, device) -> torch.Tensor:
+    """Cached per-device workspace (grown on demand; 256-byte aligned by the allocator)."""
+    device = torch.device(device)
+    key = device.index if device.index is not None else torch.cuda.current_device()
+    t = _ws_cache.get(key)
+    if t is None or t.numel() < nbytes:
+        _ws_cache.pop(key, None)
+        t = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = t
+    return t
+
+
+def _labels_arg(labels: torch.Tensor) -> torch.Tensor:
+    if not isinstance(labels, torch.Tensor) or not labels.is_cuda:
+        raise TypeError("labels must be a CUDA torch.Tensor (use sphericity_roundness_host for host arrays)")
+    if labels.dtype != torch.int32:
+        raise TypeError("labels must be int32")
+    return labels.contiguous()
+
+
+def edt_sq(labels: torch.Tensor, ndim=None, flags=BORDER_BACKGROUND, out=None, ws=None) -> torch.Tensor:
+    """Exact squared label-aware EDT (int32 tensor holding the uint32 D; 0 on background)."""
+    labels = _labels_arg(labels)
+    ndim, b, dims = _geometry(labels.shape, ndim, None)
+    if out is None:
+        out = torch.empty_like(labels)
+    nb = workspace_bytes(labels.shape, ndim, 0, flags)
+    ws = workspace(nb, labels.device) if ws is None else ws
+    _check(load().fastrs_edt_sq(labels.data_ptr(), dims, ndim, b, flags, out.data_ptr(), ws.data_ptr(),
+                                ws.numel(), _stream(labels.device)))
+    return out
+
+
+def local_thickness(labels: torch.Tensor, ndim=None, flags=BORDER_BACKGROUND, lt2=True, lt=False, ws=None):
+    """Exact local thickness.  Returns LT^2 (int32 tensor), the float32 radius, or both."""
+    labels = _labels_arg(labels)
+    ndim, b, dims = _geometry(labels.shape, ndim, None)
+    o2 = torch.empty_like(labels) if lt2 else None
+    o1 = torch.empty(labels.shape, dtype=torch.float32, device=labels.device) if lt else None
+    nb = workspace_bytes(labels.shape, ndim, 0, flags)
+    ws = workspace(nb, labels.device) if ws is None else ws
+    _check(load().fastrs_local_thickness(labels.data_ptr(), dims, ndim, b, flags,
+                                         None if o2 is None else o2.data_ptr(),
+                                         None if o1 is None else o1.data_ptr(), ws.data_ptr(), ws.numel(),
+                                         _stream(labels.device)))
+    if lt2 and lt:
+        return o2, o1
+    return o2 if lt2 else o1
+
+
+def sphericity_roundness(labels: torch.Tensor, max_label=None, ndim=None, flags=BORDER_BACKGROUND,
+                         stats=False, ws=None, out=None) -> dict:
+    """Per-object sphericity and roundness (float64 tensors of batch*max_label entries,
+    index b*max_label + label-1).  With stats=True also the per-label statistics."""
+    labels = _labels_arg(labels)
+    ndim, b, dims = _geometry(labels.shape, ndim, None)
+    if max_label is None:
+        max_label = max(1, int(labels.max().item()))
+    M = b * max_label
+    dev = labels.device
+    res = out if out is not None else {}
+    if "sphericity" not in res:
+        res["sphericity"] = torch.empty(M, dtype=torch.float64, device=dev)
+        res["roundness"] = torch.empty(M, dtype=torch.float64, device=dev)
+    st = None
+    if stats:
+        for k, dt in (("volume", torch.int64), ("n_shell", torch.int64), ("max_lt2", torch.int32),
+                      ("mean_lt", torch.float64), ("max_lt", torch.float64), ("shell_mean_lt", torch.float64),
+                      ("axis_a", torch.float64), ("axis_cb", torch.float64)):
+            if k not in res:
+                res[k] = torch.empty(M, dtype=dt, device=dev)
+        st = _Stats(*[res[n].data_ptr() for n, _ in _Stats._fields_])
+    nb = workspace_bytes(labels.shape, ndim, max_label, flags)
+    ws = workspace(nb, dev) if ws is None else ws
+    _check(load().fastrs_sphericity_roundness(labels.data_ptr(), dims, ndim, b, int(max_label), flags,
+                                              res["sphericity"].data_ptr(), res["roundness"].data_ptr(),
+                                              None if st is None else ctypes.byref(st), ws.data_ptr(),
+                                              ws.numel(), _stream(dev)))
+    return res
+
+
+def sphericity_roundness_host(labels, max_label: int, ndim=None, flags=BORDER_BACKGROUND, device="cuda",
+                              ws=None, out=None):
+    """End-to-end entry point with HOST buffers: labels (numpy or pinned CPU tensor) are
+    copied to the device inside the C call; results come back as numpy float64 arrays."""
+    if isinstance(labels, torch.Tensor):
+        if labels.is_cuda or labels.dtype != torch.int32:
+            raise TypeError("labels must be a CPU int32 tensor or numpy array")
+        ptr, shape = labels.data_ptr(), labels.shape
+    else:
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        ptr, shape = labels.ctypes.data, labels.shape
+    ndim, b, dims = _geometry(shape, ndim, None)
+    M = b * max_label
+    if out is None:
+        out = (np.empty(M), np.empty(M))
+    nb = workspace_bytes(shape, ndim, max_label, flags | HOST_IO)
+    dev = torch.device(device)
+    ws = workspace(nb, dev) if ws is None else ws
+    _check(load().fastrs_sphericity_roundness_host(ptr, dims, ndim, b, int(max_label), flags,
+                                                   out[0].ctypes.data, out[1].ctypes.data, ws.data_ptr(),
+                                                   ws.numel(), _stream(dev)))
+    return out
+
+
+def diagnostics(ws: torch.Tensor) -> dict:
+    d = _Diag()
+    _check(load().fastrs_read_diagnostics(ws.data_ptr(), ctypes.byref(d), _stream(ws.device)))
+    return {n: getattr(d, n) for n, _ in _Diag._fields_ if n != "reserved"}
+
+
+def last_workspace(device=None) -> torch.Tensor:
+    device = torch.device(device or "cuda")
+    key = device.index if device.index is not None else torch.cuda.current_device()
+    return _ws_cache[key]
+
+
+def profile(enable: bool):
+    load().fastrs_profile(1 if enable else 0)
+
+
+def profile_read() -> tuple[dict, int]:
+    ms = (ctypes.c_double * len(STAGES))()
+    calls = ctypes.c_int64(0)
+    load().fastrs_profile_read(ms, ctypes.byref(calls), len(STAGES))
+    return {s: ms[i] for i, s in enumerate(STAGES)}, calls.value
+
+
+def spheroid_area(a, c):
+    return load().fastrs_spheroid_area(a, c)
+
+
+def ramanujan_perimeter(a, b):
+    return load().fastrs_ramanujan_perimeter(a, b)
+
+
+def sphericity_3d(V, mean_lt):
+    return load().fastrs_sphericity_3d(V, mean_lt)
+
+
+def sphericity_2d(A, mean_lt):
+    return load().fastrs_sphericity_2d(A, mean_lt)
+
+
+def release():
+    load().fastrs_release()

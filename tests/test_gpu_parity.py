@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): bit-exact for squared distances, LT^2, counts and shell
+masks; float64 sphericity / roundness within 1e-5 relative (the derivation of the much
+tighter actual error is in DESIGN.md "Tolerances": the fixed-point LT sums err by
+<= V * 2^-(s+1) absolute, s >= 20).
+"""
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests import _refs
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def F():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2504_05808_b200 import fastrs
+    fastrs.load()
+    return fastrs
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).cuda()
+
+
+def _u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def compare_metrics(got: dict, want: dict, where=""):
+    g = {k: v.cpu().numpy() for k, v in got.items()}
+    np.testing.assert_array_equal(g["volume"], want["volume"], err_msg=where)
+    np.testing.assert_array_equal(g["n_shell"], want["n_shell"], err_msg=where)
+    np.testing.assert_array_equal(g["max_lt2"].view(np.uint32), want["max_lt2"], err_msg=where)
+    present = want["volume"] > 0
+    assert np.isnan(g["sphericity"][~present]).all() and np.isnan(g["roundness"][~present]).all()
+    for k in ("sphericity", "roundness", "mean_lt", "shell_mean_lt", "axis_cb"):
+        np.testing.assert_allclose(g[k][present], want[k][present], rtol=RTOL, atol=0, err_msg=f"{where} {k}")
+
+
+def full_check(F, lab, flags, ndim=None, max_label=None, fields=True):
+    """D, LT^2 and all per-label outputs vs the oracle."""
+    ndim = ndim or lab.ndim
+    ml = max_label or max(1, int(lab.max()))
+    t = _dev(lab)
+    if fields:
+        d2, lt2, sh = oracle.fields(lab, max_label=ml, flags=flags, ndim=ndim)
+        np.testing.assert_array_equal(_u32(F.edt_sq(t, ndim=ndim, flags=flags)), d2)
+        np.testing.assert_array_equal(_u32(F.local_thickness(t, ndim=ndim, flags=flags)), lt2)
+        lt_f = F.local_thickness(t, ndim=ndim, flags=flags, lt2=False, lt=True).cpu().numpy()
+        np.testing.assert_array_equal(lt_f, np.sqrt(lt2.astype(np.float64)).astype(np.float32))
+    got = F.sphericity_roundness(t, max_label=ml, ndim=ndim, flags=flags, stats=True)
+    want = oracle.sphericity_roundness(lab, max_label=ml, flags=flags, ndim=ndim)
+    compare_metrics(got, want)
+    return got, want
+
+
+# ------------------------------------------------------------------------------------------
+# tiny random grids: touching labels, ragged sizes, both border modes
+# ------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("border", [1, 0])
+@pytest.mark.parametrize("seed", range(40))
+def test_random_tiny(F, seed, border):
+    rng = np.random.default_rng(seed)
+    if seed % 2:
+        shape = tuple(int(v) for v in rng.integers(3, 40, 3))
+    else:
+        shape = tuple(int(v) for v in rng.integers(3, 150, 2))
+    lab = synth.random_labels(shape, nlabels=int(rng.integers(1, 6)), seed=seed, fill=float(rng.uniform(0.3, 0.95)),
+                              blob=int(rng.integers(1, 6)))
+    try:
+        oracle.edt_sq(lab, flags=border)
+    except oracle.OracleError as e:
+        assert e.code == 2
+        with pytest.raises(F.FastrsError) as ge:
+            F.edt_sq(_dev(lab), flags=border)
+        assert ge.value.name == "ENOSITE"
+        return
+    if lab.max() == 0:
+        lab[0, 0] = 1
+    full_check(F, lab, border)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 77), (77, 1), (2, 3, 1), (1, 1, 1), (9, 1, 40), (33, 65),
+                                   (17, 9, 33), (8, 8, 32), (8, 64, 64), (3, 16384)])
+def test_ragged_and_degenerate_shapes(F, shape):
+    lab = synth.random_labels(shape, nlabels=3, seed=sum(shape), fill=0.7, blob=3)
+    if lab.max() == 0:
+        lab.flat[0] = 1
+    full_check(F, lab, 1)
+
+
+def test_closed_form_objects(F):
+    cf = _refs.load_closed_forms()
+    got, _ = full_check(F, synth.disk(20), 1)
+    assert got["sphericity"][0].item() == pytest.approx(cf["digital_disk_r20"]["sphericity"], rel=1e-9)
+    assert got["roundness"][0].item() == pytest.approx(1.0, abs=1e-12)
+    got, _ = full_check(F, synth.sphere(15), 1)
+    assert got["sphericity"][0].item() == pytest.approx(cf["digital_sphere_r15"]["sphericity"], rel=1e-9)
+    assert got["roundness"][0].item() == pytest.approx(1.0, abs=1e-12)
+    assert int(got["max_lt2"][0]) == 226 and int(got["n_shell"][0]) == 2262
+
+
+def test_spec_examples(F):
+    for name, c in _refs.load_spec_examples().items():
+        if "labels" not in c:
+            continue
+        lab = c["labels"].astype(np.int32)
+        np.testing.assert_array_equal(_u32(F.edt_sq(_dev(lab))), c["d2"], err_msg=name)
+        if "lt2" in c:
+            np.testing.assert_array_equal(_u32(F.local_thickness(_dev(lab))), c["lt2"], err_msg=name)
+
+
+def test_large_balls_beyond_table_and_halo(F):
+    """Objects whose D exceeds the staged column halo (32) and the 3D containment table cap
+    (8192 -> radius > 90): exercises the global-memory window fallback and unpruned centres."""
+    full_check(F, synth.disk(150, canvas=311), 1)
+    full_check(F, synth.sphere(95, canvas=193), 1, fields=False)
+
+
+def test_empty_and_single_element_objects(F):
+    lab = np.zeros((20, 21, 22), np.int32)
+    r = F.sphericity_roundness(_dev(lab), max_label=3)
+    assert torch.isnan(r["sphericity"]).all()
+    lab[3, 4, 5] = 2
+    lab[10, 10, 10] = 3
+    lab[10, 10, 11] = 1  # touching another label
+    full_check(F, lab, 1, max_label=5)
+    full_check(F, lab, 0, max_label=5)
+
+
+def test_errors(F):
+    lab = np.zeros((8, 8), np.int32)
+    lab[2, 2] = 9
+    with pytest.raises(F.FastrsError) as e:
+        F.sphericity_roundness(_dev(lab), max_label=4)
+    assert e.value.name == "EINVAL"
+    lab[2, 2] = -1
+    with pytest.raises(F.FastrsError) as e:
+        F.edt_sq(_dev(lab))
+    assert e.value.name == "EINVAL"
+    with pytest.raises(F.FastrsError) as e:
+        F.edt_sq(_dev(np.ones((5, 6, 7), np.int32)), flags=0)
+    assert e.value.name == "ENOSITE"
+
+
+def test_batched_items_are_independent(F):
+    a = synth.random_labels((3, 40, 50), nlabels=4, seed=3, fill=0.8, blob=4)
+    full_check(F, a, 1, ndim=2)
+    b = synth.random_labels((2, 12, 20, 33), nlabels=4, seed=4, fill=0.8, blob=3)
+    full_check(F, b, 1, ndim=3)
+    # a batch equals its items run one by one
+    t = _dev(a)
+    rb = F.sphericity_roundness(t, max_label=4, ndim=2)["roundness"].cpu().numpy().reshape(3, 4)
+    for i in range(3):
+        ri = F.sphericity_roundness(_dev(a[i]), max_label=4)["roundness"].cpu().numpy()
+        np.testing.assert_array_equal(rb[i], ri)
+
+
+# ------------------------------------------------------------------------------------------
+# BASELINE.json configs
+# ------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_config_full(F, cfg):
+    lab, info = synth.make_config(cfg)
+    got, want = full_check(F, lab, 1, max_label=info["max_label"])
+    cf = _refs.load_closed_forms()["digital_disk_r20" if cfg == 1 else "digital_sphere_r15"]
+    i = info["max_label"] - 1
+    assert got["sphericity"][i].item() == pytest.approx(cf["sphericity"], rel=1e-9)
+
+
+def test_config_c3_full(F):
+    lab, info = synth.make_config(3)
+    full_check(F, lab, 1, max_label=info["max_label"], fields=False)
+
+
+def test_config_c5_subset(F):
+    lab, info = synth.make_config(5, batch=3)
+    full_check(F, lab, 1, ndim=2, max_label=info["max_label"], fields=False)
+
+
+def test_config_c4_sampled(F):
+    """C4 at full size in the bench's launch configuration; the oracle evaluates a seeded
+    sample of labels one by one (exact by crop exactness)."""
+    lab, info = synth.make_config(4)
+    ml = info["max_label"]
+    t = _dev(lab)
+    got = F.sphericity_roundness(t, max_label=ml, stats=True)
+    rng = np.random.default_rng(44)
+    mask = np.zeros(ml, np.uint8)
+    mask[rng.choice(ml, 300, replace=False)] = 1
+    want = oracle.sphericity_roundness(lab, max_label=ml, label_mask=mask)
+    sel = mask.astype(bool)
+    g = {k: v.cpu().numpy()[sel] for k, v in got.items()}
+    w = {k: v[sel] for k, v in want.items()}
+    compare_metrics({k: torch.from_numpy(v) for k, v in g.items()}, w)
+    # whole-grid invariants
+    assert int(got["volume"].sum()) == int(np.count_nonzero(lab))
+    ok = got["volume"] > 0
+    assert bool((got["roundness"][ok] <= 1 + 1e-12).all()) and bool((got["roundness"][ok] > 0).all())
+    assert bool((got["sphericity"][ok] <= 1 + 1e-12).all())
+
+
+def test_deterministic_and_host_path(F):
+    lab, info = synth.make_config(2)
+    t = _dev(lab)
+    r1 = F.sphericity_roundness(t, max_label=51)
+    r2 = F.sphericity_roundness(t, max_label=51)
+    assert torch.equal(r1["sphericity"], r2["sphericity"]) and torch.equal(r1["roundness"], r2["roundness"])
+    s, r = F.sphericity_roundness_host(lab, max_label=51)
+    np.testing.assert_array_equal(s, r1["sphericity"].cpu().numpy())
+    np.testing.assert_array_equal(r, r1["roundness"].cpu().numpy())
+
+
+def test_diagnostics_counters(F):
+    lab = synth.sphere(15)
+    t = _dev(lab)
+    F.sphericity_roundness(t, max_label=1)
+    d = F.diagnostics(F.last_workspace(t.device))
+    assert d["status_bits"] == 0 and d["dmax"] == 226 and d["n_fg"] == 14147
+    # exact lattice pruning with the 26-neighbourhood then |s|^2 <= 12 keeps 121 centres on
+    # the digital sphere r=15 (SURVEY.md §8(c) "Kept-centre counts")
+    assert d["n_kept"] == 121
+    F.sphericity_roundness(_dev(synth.disk(20)), max_label=1)
+    d = F.diagnostics(F.last_workspace(t.device))
+    assert d["n_fg"] == 1257 and d["dmax"] == 401
