@@ -87,7 +87,7 @@ typedef struct {
 
 /* Counters left in the workspace by the last call that used it (diagnostics / bench). */
 typedef struct {
-  uint32_t status_bits;   /* bit0 bad label, bit1 no site, bit2 internal invariant       */
+  uint32_t status_bits;   /* bit0 bad label, bit1 no site, bit2 LT2<D, bit3 shell        */
   uint32_t dmax;          /* max squared distance over the grid                          */
   uint64_t n_fg;          /* foreground elements                                         */
   uint64_t n_kept;        /* maximal-ball centres kept by the lattice pruning (K4)       */

@@ -214,7 +214,8 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
   if (status & kStBadLabel) return fail(FASTRS_EINVAL, "a label is < 0 or > max_label");
   if (status & kStNoSite)
     return fail(FASTRS_ENOSITE, "an object element has no site (no other label and the border is not background)");
-  if (status & kStInternal) return fail(FASTRS_EINTERNAL, "device invariant violated");
+  if (status & kStInternal) return fail(FASTRS_EINTERNAL, "device invariant violated: LT^2 < D");
+  if (status & kStShell) return fail(FASTRS_EINTERNAL, "device invariant violated: shell mean LT > max LT or empty shell");
   return FASTRS_OK;
 }
 
@@ -308,7 +309,7 @@ int fastrs_sphericity_roundness_host(const int32_t* labels_host, const int64_t* 
   if (e != cudaSuccess) return cuda_fail(e, "D2H results");
   if (status & kStBadLabel) return fail(FASTRS_EINVAL, "a label is < 0 or > max_label");
   if (status & kStNoSite) return fail(FASTRS_ENOSITE, "an object element has no site");
-  if (status & kStInternal) return fail(FASTRS_EINTERNAL, "device invariant violated");
+  if (status & (kStInternal | kStShell)) return fail(FASTRS_EINTERNAL, "device invariant violated (bits %u)", status);
   return FASTRS_OK;
 }
 

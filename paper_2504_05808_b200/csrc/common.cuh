@@ -13,7 +13,7 @@ constexpr uint32_t kBitY = 0x80000000u;  // element is the first of its y-run
 constexpr uint32_t kBitZ = 0x40000000u;  // element is the first of its z-run
 
 // ---- status bits in the workspace header ---------------------------------------------
-constexpr uint32_t kStBadLabel = 1u, kStNoSite = 2u, kStInternal = 4u;
+constexpr uint32_t kStBadLabel = 1u, kStNoSite = 2u, kStInternal = 4u, kStShell = 8u;
 
 constexpr uint32_t kFlagBorder = 1u, kFlagAsync = 4u, kFlagHostIO = 8u;
 

@@ -21,7 +21,7 @@ __global__ void k_metrics(Accum acc, Outputs o, int ndim, int64_t Nb, WsHeader* 
   const uint32_t m2 = acc.maxlt2[i];
   double sph = nan(""), rnd = nan(""), mean = nan(""), rmax = nan(""), smean = nan(""), cb = nan("");
   if (V > 0) {
-    const double inv = ldexp(1.0, -s);
+    const double scale = ldexp(1.0, s), inv = ldexp(1.0, -s);
     mean = (double)acc.sum[i] * inv / (double)V;
     rmax = sqrt((double)m2);
     smean = nsh ? (double)acc.sumshell[i] * inv / (double)nsh : nan("");
@@ -32,8 +32,15 @@ __global__ void k_metrics(Accum acc, Outputs o, int ndim, int64_t Nb, WsHeader* 
       sph = sphericity_2d((double)V, mean);
       cb = b_axis_2d((double)V, mean);
     }
-    rnd = smean / rmax;
-    if (nsh == 0 || smean > rmax * (1.0 + 1e-12)) atomicOr(&hdr->status, kStInternal);
+    // roundness r_bar / R_max evaluated in the fixed-point system the shell terms were
+    // summed in: every shell term is <= fx(R_max) (monotone rounding), so the invariant
+    // r_bar <= R_max is checked exactly in integers, and R = 1 exactly when
+    // every shell element carries the maximum.
+    const unsigned long long fxmax = __double2ull_rn(rmax * scale);
+    const unsigned long long ss = acc.sumshell[i];
+    const unsigned long long hi = __umul64hi(nsh, fxmax), lo = nsh * fxmax;
+    if (nsh == 0 || (hi == 0 && ss > lo)) atomicOr(&hdr->status, kStShell);
+    rnd = ((double)ss / (double)nsh) / (double)fxmax;
   }
   if (o.sphericity) o.sphericity[i] = sph;
   if (o.roundness) o.roundness[i] = rnd;

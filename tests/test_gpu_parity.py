@@ -106,12 +106,14 @@ def test_ragged_and_degenerate_shapes(F, shape):
 
 def test_closed_form_objects(F):
     cf = _refs.load_closed_forms()
+    # LT sums are exact fixed-point integers of terms rounded to 2^-s (s = 32 here): the
+    # means carry <= 2^-(s+1) absolute error, i.e. ~1e-11 relative at lt ~ 15-20
     got, _ = full_check(F, synth.disk(20), 1)
     assert got["sphericity"][0].item() == pytest.approx(cf["digital_disk_r20"]["sphericity"], rel=1e-9)
-    assert got["roundness"][0].item() == pytest.approx(1.0, abs=1e-12)
+    assert got["roundness"][0].item() == pytest.approx(1.0, abs=1e-9)
     got, _ = full_check(F, synth.sphere(15), 1)
     assert got["sphericity"][0].item() == pytest.approx(cf["digital_sphere_r15"]["sphericity"], rel=1e-9)
-    assert got["roundness"][0].item() == pytest.approx(1.0, abs=1e-12)
+    assert got["roundness"][0].item() == pytest.approx(1.0, abs=1e-9)
     assert int(got["max_lt2"][0]) == 226 and int(got["n_shell"][0]) == 2262
 
 
@@ -126,10 +128,23 @@ def test_spec_examples(F):
 
 
 def test_large_balls_beyond_table_and_halo(F):
-    """Objects whose D exceeds the staged column halo (32) and the 3D containment table cap
-    (8192 -> radius > 90): exercises the global-memory window fallback and unpruned centres."""
-    full_check(F, synth.disk(150, canvas=311), 1)
-    full_check(F, synth.sphere(95, canvas=193), 1, fields=False)
+    """Objects whose D exceeds the staged column halo (32^2) and the 3D containment-table cap
+    (8192 -> radius > 90): exercises the global-memory window fallback and never-pruned
+    centres.  Too big for the all-balls oracle, so pinned by closed forms instead: the EDT
+    of a single label is scipy's binary EDT of the padded mask, and a digital disk/sphere of
+    radius r centred on an element has D(centre) = r^2 + 1 and LT^2 = r^2 + 1 everywhere
+    (the centre ball covers the whole object)."""
+    import scipy.ndimage
+    for lab, r in ((synth.disk(150, canvas=311), 150), (synth.sphere(95, canvas=193), 95)):
+        t = _dev(lab)
+        ref = np.rint(scipy.ndimage.distance_transform_edt(np.pad(lab > 0, 1)) ** 2).astype(np.uint32)
+        ref = ref[(slice(1, -1),) * lab.ndim]
+        np.testing.assert_array_equal(_u32(F.edt_sq(t)), ref)
+        lt2 = _u32(F.local_thickness(t))
+        assert (lt2[lab > 0] == r * r + 1).all() and (lt2[lab == 0] == 0).all()
+        got = F.sphericity_roundness(t, max_label=1, stats=True)
+        assert got["roundness"][0].item() == 1.0
+        assert int(got["volume"][0]) == int((lab > 0).sum())
 
 
 def test_empty_and_single_element_objects(F):
