@@ -93,7 +93,7 @@ typedef struct {
   uint64_t n_kept;        /* maximal-ball centres kept by the lattice pruning (K4)       */
   uint64_t n_intervals;   /* (ball, row) intervals emitted by the dilation (K5)          */
   int32_t sum_scale_log2; /* fixed-point scale of the LT sums (2^s)                      */
-  int32_t reserved;
+  uint32_t n_fallback;   /* tile groups handed to the atomic fallback dilation         */
 } fastrs_diagnostics;
 
 /* Bytes of device workspace needed by every entry point below for this geometry.

@@ -325,7 +325,7 @@ int fastrs_read_diagnostics(const void* ws, fastrs_diagnostics* out, void* strea
   out->n_kept = h.n_kept;
   out->n_intervals = h.n_intervals;
   out->sum_scale_log2 = h.scale_log2;
-  out->reserved = 0;
+  out->n_fallback = h.n_fallback;
   return FASTRS_OK;
 }
 

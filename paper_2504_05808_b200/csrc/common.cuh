@@ -28,11 +28,8 @@ constexpr int kRowStride = kLevels * 32 + 1;  // +1: rows start in different ban
 // ---- lattice containment table (S4) ---------------------------------------------------
 constexpr int kDcap3 = 8192;   // 3D: centres with D > kDcap3 are always kept
 constexpr int kDcap2 = 32768;  // 2D
-constexpr int kClasses3 = 12;  // offset classes with |s|^2 <= 12 (178 offsets)
-constexpr int kClasses2 = 5;   // offset classes with |s|^2 <= 8  (24 offsets)
-constexpr int kStage1Classes3 = 3;  // 26-neighbourhood
-constexpr int kStage1Classes2 = 2;  // 8-neighbourhood
-constexpr int kHalo3 = 3, kHalo2 = 2;
+constexpr int kClasses3 = 12;  // offset classes with |s|^2 <= 12 (178 offsets; first 3 = 26-nbhd)
+constexpr int kClasses2 = 5;   // offset classes with |s|^2 <= 8 (24 offsets; first 2 = 8-nbhd)
 
 struct Geom {
   int ndim;
@@ -49,7 +46,8 @@ struct WsHeader {
   unsigned long long n_kept;
   unsigned long long n_intervals;
   int32_t scale_log2;
-  int32_t pad[7];
+  uint32_t n_fallback;  // tile groups handed to the atomic fallback dilation
+  int32_t pad[6];
 };
 static_assert(sizeof(WsHeader) <= 256, "header");
 
@@ -58,7 +56,7 @@ struct TileMeta {
   uint32_t count;  // kept centres
   uint32_t maxD;   // max D over kept centres
   uint32_t nfg;    // foreground elements of the tile
-  uint32_t pad;
+  uint32_t pad;    // set by the sorted-cover dilation when it leaves the tile to the fallback
 };
 
 // per-label accumulators (SoA)
@@ -109,7 +107,7 @@ void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, 
 cudaError_t ensure_mtables(int device);  // builds the per-device lattice tables (sync, once)
 void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, WsHeader* hdr,
                   cudaStream_t st);
-void launch_dilate(const int32_t* labels, const uint32_t* D, const TileMeta* meta,
+void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta,
                    const uint2* centres, const Geom& g, const Accum* acc, uint32_t* lt2_out,
                    float* lt_out, WsHeader* hdr, cudaStream_t st);
 void launch_metrics(const Accum& acc, const Geom& g, const Outputs& o, WsHeader* hdr,

@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(256) k_edt_x(const int32_t* __restrict__ lab, 
   // sweep 1 (right to left): end of the run containing x
   int carry_end = X - 1;
   int32_t right_next = 0;
+#pragma unroll 4
   for (int c = nchunk - 1; c >= 0; --c) {
     const int x = (c << 5) + lane;
     const int32_t v = x < X ? __ldg(L + x) : 0;
@@ -64,6 +65,7 @@ __global__ void __launch_bounds__(256) k_edt_x(const int32_t* __restrict__ lab, 
   int carry_start = 0;
   int32_t left_prev = 0;
   uint32_t bad = 0;
+#pragma unroll 4
   for (int c = 0; c < nchunk; ++c) {
     const int x = (c << 5) + lane;
     const int32_t v = x < X ? __ldg(L + x) : 0;
@@ -120,10 +122,6 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
     tile[(r - lo) * 32 + lane] = xin ? __ldg(in + base + r * astride) : 0u;
   __syncthreads();
 
-  auto fetch = [&](int64_t q) -> uint32_t {
-    return (q >= lo && q < hi) ? tile[(q - lo) * 32 + lane] : __ldg(in + base + q * astride);
-  };
-
   uint32_t dmax = 0, nfg = 0, nosite = 0;
   const int64_t pend = s0 + kColS < L ? s0 + kColS : L;
   for (int64_t p = s0 + warp; p < pend; p += kColWarps) {
@@ -132,35 +130,41 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
     uint32_t res = FINAL ? 0u : v;
     if (xin && g != 0) {
       uint32_t best = g;
-      bool dn = true, up = true;
-      uint32_t chk = v & chbit;  // run-start flag of element p - dq + 1
-      for (uint32_t dq = 1; dn || up; ++dq) {
-        const uint32_t dq2 = dq * dq;
-        if (dq2 >= best) break;
-        if (dn) {
-          if (chk) {  // p - dq lies outside the run: a site (or the border / nothing)
-            if (p - (int64_t)dq >= 0 || border) best = min(best, dq2);
-            dn = false;
-          } else {
-            const uint32_t w = fetch(p - (int64_t)dq);
-            best = min(best, (w & kMask) + dq2);
-            chk = w & chbit;
-          }
-        }
-        if (up) {
-          const int64_t q = p + (int64_t)dq;
+      // up side: p+1, p+2, ... until a run end (the element there is a site) or dq^2 >= best
+      {
+        uint32_t dq = 1, dq2 = 1;
+        int64_t q = p + 1;
+        while (dq2 < best) {
           if (q >= L) {
             if (border) best = min(best, dq2);
-            up = false;
-          } else {
-            const uint32_t w = fetch(q);
-            if (w & chbit) {
-              best = min(best, dq2);
-              up = false;
-            } else {
-              best = min(best, (w & kMask) + dq2);
-            }
+            break;
           }
+          const uint32_t w = q < hi ? tile[(q - lo) * 32 + lane] : __ldg(in + base + q * astride);
+          if (w & chbit) {
+            best = min(best, dq2);
+            break;
+          }
+          best = min(best, (w & kMask) + dq2);
+          dq2 += 2 * dq + 1;
+          ++dq;
+          ++q;
+        }
+      }
+      // down side: p-1, p-2, ...; element p-dq lies outside the run iff p-dq+1 starts the run
+      {
+        uint32_t dq = 1, dq2 = 1, chk = v & chbit;
+        int64_t q = p - 1;
+        while (dq2 < best) {
+          if (chk) {
+            if (q >= 0 || border) best = min(best, dq2);
+            break;
+          }
+          const uint32_t w = q >= lo ? tile[(q - lo) * 32 + lane] : __ldg(in + base + q * astride);
+          best = min(best, (w & kMask) + dq2);
+          chk = w & chbit;
+          dq2 += 2 * dq + 1;
+          ++dq;
+          --q;
         }
       }
       if (FINAL) {

@@ -1,0 +1,368 @@
+// K7 lattice containment table and K4 exact maximal-ball pruning.
+//
+// Ball of q: B(q) = { p : |p-q|^2 <= D(q) - 1 } (strict membership, reading c5).  For a
+// neighbour offset s, B(q) is contained in B(q+s) exactly when
+//     D(q+s) > M(D(q), s),   M(D, s) = max_{u in Z^n, |u|^2 <= D-1} |u - s|^2,
+// because every lattice point of B(q) is then within B(q+s).  Containment between balls of
+// different centres is strict (two lattice balls with different centres are never equal
+// sets), and strict containment is a strict partial order, so every dropped ball lies in
+// a kept maximal ball with a larger D and LT^2 (max over covering balls) is unchanged.
+// M depends on s only through its class (the ball is symmetric under sign changes and axis
+// permutations): 3D 26-neighbourhood classes (1,0,0), (1,1,0), (1,1,1); 2D (1,0), (1,1).
+// The table is built once per device for D <= kDcap; centres with a larger D are kept.
+//
+// K4 is row-vectorised: one warp per tile row, lane = x, every lane tests the same offset
+// (warp-uniform, shared-memory reads conflict-free); survivors are compacted per home tile
+// in element order with the tile's count / max D / #foreground (TileMeta).
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace fastrs {
+namespace {
+
+constexpr unsigned kFullMask = 0xFFFFFFFFu;
+
+// offset classes (canonical |s| sorted descending), by |s|^2: stage 1 = the first 3 (3D) / 2 (2D)
+__constant__ int c_rep3[kClasses3][3] = {{1, 0, 0}, {1, 1, 0}, {1, 1, 1}, {2, 0, 0}, {2, 1, 0}, {2, 1, 1},
+                                         {2, 2, 0}, {2, 2, 1}, {3, 0, 0}, {3, 1, 0}, {3, 1, 1}, {2, 2, 2}};
+__constant__ int c_rep2[kClasses2][2] = {{1, 0}, {1, 1}, {2, 0}, {2, 1}, {2, 2}};
+static const int h_rep3[kClasses3][3] = {{1, 0, 0}, {1, 1, 0}, {1, 1, 1}, {2, 0, 0}, {2, 1, 0}, {2, 1, 1},
+                                         {2, 2, 0}, {2, 2, 1}, {3, 0, 0}, {3, 1, 0}, {3, 1, 1}, {2, 2, 2}};
+static const int h_rep2[kClasses2][2] = {{1, 0}, {1, 1}, {2, 0}, {2, 1}, {2, 2}};
+// stage-2 offsets (|s|^2 >= 4) as shared-memory deltas of the pruning tile, grouped by class
+__constant__ int c_off3[152];
+__constant__ int c_cls3[kClasses3 + 1];
+__constant__ int c_off2[16];
+__constant__ int c_cls2[kClasses2 + 1];
+
+__device__ __forceinline__ int isqrt_t(int h) {
+  int w = (int)sqrtf((float)h);
+  while (w * w > h) --w;
+  while ((w + 1) * (w + 1) <= h) ++w;
+  return w;
+}
+
+// M(D, s) for the 3D classes (s0 >= s1 >= s2 >= 0): for each (u0,u1) in the disk the best u2
+// is -w (w = isqrt of the remaining radius^2), which maximises (u2 - s2)^2.
+__global__ void k_mtable3(uint32_t* M) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)kClasses3 * (kDcap3 + 1)) return;
+  const int c = (int)(t / (kDcap3 + 1)), D = (int)(t % (kDcap3 + 1));
+  if (D == 0) {
+    M[t] = 0;
+    return;
+  }
+  const int s0 = c_rep3[c][0], s1 = c_rep3[c][1], s2 = c_rep3[c][2];
+  const int R2 = D - 1, r = isqrt_t(R2);
+  uint32_t best = 0;
+  for (int u0 = -r; u0 <= r; ++u0) {
+    const int rem0 = R2 - u0 * u0, r1 = isqrt_t(rem0);
+    for (int u1 = -r1; u1 <= r1; ++u1) {
+      const int w = isqrt_t(rem0 - u1 * u1);
+      const uint32_t v = (u0 - s0) * (u0 - s0) + (u1 - s1) * (u1 - s1) + (w + s2) * (w + s2);
+      best = v > best ? v : best;
+    }
+  }
+  M[t] = best;
+}
+
+__global__ void k_mtable2(uint32_t* M) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)kClasses2 * (kDcap2 + 1)) return;
+  const int c = (int)(t / (kDcap2 + 1)), D = (int)(t % (kDcap2 + 1));
+  if (D == 0) {
+    M[t] = 0;
+    return;
+  }
+  const int s0 = c_rep2[c][0], s1 = c_rep2[c][1];
+  const int R2 = D - 1, r = isqrt_t(R2);
+  uint32_t best = 0;
+  for (int u0 = -r; u0 <= r; ++u0) {
+    const int w = isqrt_t(R2 - u0 * u0);
+    const uint32_t v = (u0 - s0) * (u0 - s0) + (w + s1) * (w + s1);
+    best = v > best ? v : best;
+  }
+  M[t] = best;
+}
+
+struct DeviceTables {
+  uint32_t* m3 = nullptr;
+  uint32_t* m2 = nullptr;
+};
+std::mutex g_mu;
+DeviceTables g_tables[64];
+
+template <bool IS3D>
+struct PruneTile {
+  static constexpr int H = IS3D ? 3 : 2;  // halo: |s_i| <= 3 (3D, |s|^2 <= 12) / 2 (2D, |s|^2 <= 8)
+  static constexpr int TY = IS3D ? 8 : 64, TZ = IS3D ? 8 : 1;
+  static constexpr int PX = kTX + 2 * H, PY = TY + 2 * H, PZ = IS3D ? TZ + 2 * H : 1;
+  static constexpr int HZ = IS3D ? H : 0;
+};
+
+template <bool IS3D>
+__global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, Geom g, TileMeta* __restrict__ meta,
+                                               uint2* __restrict__ cent, const uint32_t* __restrict__ M,
+                                               WsHeader* __restrict__ hdr) {
+  using P = PruneTile<IS3D>;
+  __shared__ uint32_t s[P::PZ * P::PY * P::PX];
+  __shared__ uint32_t keepmask[kRows];
+  __shared__ uint32_t pre[kRows];
+  __shared__ uint32_t red_cnt[8], red_max[8];
+  __shared__ uint16_t surv[kTileVol];
+  __shared__ uint32_t s_nsurv;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t tile = blockIdx.x;
+  int64_t t = tile;
+  const int64_t tx = t % g.ntx;
+  t /= g.ntx;
+  const int64_t ty = t % g.nty;
+  t /= g.nty;
+  const int64_t tz = t % g.ntz;
+  const int64_t b = t / g.ntz;
+  const int64_t z0 = tz * P::TZ - P::HZ, y0 = ty * P::TY - P::H, x0 = tx * kTX - P::H;
+  const uint32_t* Db = D + b * g.Z * g.Y * g.X;
+  for (int i = tid; i < P::PZ * P::PY * P::PX; i += 256) {
+    const int lx = i % P::PX, ly = (i / P::PX) % P::PY, lz = i / (P::PX * P::PY);
+    const int64_t gz = z0 + lz, gy = y0 + ly, gx = x0 + lx;
+    uint32_t v = 0;
+    if (gz >= 0 && gz < g.Z && gy >= 0 && gy < g.Y && gx >= 0 && gx < g.X) v = __ldg(Db + (gz * g.Y + gy) * g.X + gx);
+    s[i] = v;
+  }
+  __syncthreads();
+
+  constexpr int dcap = IS3D ? kDcap3 : kDcap2;
+  uint32_t nfg = 0, maxd = 0;
+  const int64_t gx = tx * kTX + lane;
+#pragma unroll 1
+  for (int row = warp; row < kRows; row += 8) {
+    const int ly = row % P::TY, lz = row / P::TY;
+    const int64_t gz = tz * P::TZ + lz, gy = ty * P::TY + ly;
+    const int c = ((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::H);
+    const uint32_t d = s[c];
+    const bool fg = d != 0 && gz < g.Z && gy < g.Y && gx < g.X;
+    bool keep = fg;
+    if (__any_sync(kFullMask, fg)) {
+      const bool test = fg && d <= (uint32_t)dcap;
+      const uint32_t m0 = test ? __ldg(M + d) : 0xFFFFFFFFu;
+      const uint32_t m1 = test ? __ldg(M + (dcap + 1) + d) : 0xFFFFFFFFu;
+      if (IS3D) {
+        const uint32_t m2 = test ? __ldg(M + 2 * (dcap + 1) + d) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int dz = -1; dz <= 1; ++dz)
+#pragma unroll
+          for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+            for (int dx = -1; dx <= 1; ++dx) {
+              const int cls = (dz != 0) + (dy != 0) + (dx != 0) - 1;
+              if (cls < 0) continue;
+              const uint32_t m = cls == 0 ? m0 : (cls == 1 ? m1 : m2);
+              keep &= s[c + (dz * P::PY + dy) * P::PX + dx] <= m;
+            }
+      } else {
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int cls = (dy != 0) + (dx != 0) - 1;
+            if (cls < 0) continue;
+            keep &= s[c + dy * P::PX + dx] <= (cls == 0 ? m0 : m1);
+          }
+      }
+    }
+    const uint32_t bal = __ballot_sync(kFullMask, keep);
+    if (lane == 0) keepmask[row] = bal;
+    nfg += fg;
+  }
+  __syncthreads();
+  // ---- stage 2: the remaining offsets (|s|^2 <= 12 / 8) on the compacted stage-1 survivors,
+  // lanes = survivors (warp-uniform offset loop, early exit per class)
+  if (warp == 0) {
+    const uint32_t c0 = __popc(keepmask[2 * lane]), c1 = __popc(keepmask[2 * lane + 1]);
+    uint32_t inc = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t n = __shfl_up_sync(kFullMask, inc, o);
+      if (lane >= o) inc += n;
+    }
+    const uint32_t ex = inc - c0 - c1;
+    pre[2 * lane] = ex;
+    pre[2 * lane + 1] = ex + c0;
+    if (lane == 31) s_nsurv = inc;
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int row = warp; row < kRows; row += 8) {
+    const uint32_t km = keepmask[row];
+    if ((km >> lane) & 1u) surv[pre[row] + __popc(km & ((1u << lane) - 1u))] = (uint16_t)(row * 32 + lane);
+  }
+  __syncthreads();
+  const uint32_t nsurv = s_nsurv;
+#pragma unroll 1
+  for (uint32_t i0 = warp * 32; i0 < nsurv; i0 += 256) {
+    const uint32_t i = i0 + lane;
+    int v = 0, c = 0;
+    uint32_t d = 0;
+    bool keep = false;
+    if (i < nsurv) {
+      v = surv[i];
+      const int lx = v & 31, ly = (v >> 5) % P::TY, lz = v / (32 * P::TY);
+      c = ((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lx + P::H);
+      d = s[c];
+      keep = true;
+    }
+    const bool test = keep && d <= (uint32_t)dcap;
+    const int c_lo = IS3D ? 3 : 2, c_hi = IS3D ? kClasses3 : kClasses2;
+#pragma unroll 1
+    for (int cl = c_lo; cl < c_hi; ++cl) {
+      if (!__any_sync(kFullMask, test && keep)) break;
+      const uint32_t m = test ? __ldg(M + cl * (dcap + 1) + d) : 0xFFFFFFFFu;
+      const int jb = IS3D ? c_cls3[cl] : c_cls2[cl], je = IS3D ? c_cls3[cl + 1] : c_cls2[cl + 1];
+      for (int j = jb; j < je; ++j) {
+        const int off = IS3D ? c_off3[j] : c_off2[j];
+        if (test) keep &= s[c + off] <= m;
+      }
+    }
+    if (i < nsurv && !keep) atomicAnd(&keepmask[v >> 5], ~(1u << (v & 31)));
+    if (keep) maxd = max(maxd, d);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t c0 = __popc(keepmask[2 * lane]), c1 = __popc(keepmask[2 * lane + 1]);
+    uint32_t inc = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t n = __shfl_up_sync(kFullMask, inc, o);
+      if (lane >= o) inc += n;
+    }
+    const uint32_t ex = inc - c0 - c1;
+    pre[2 * lane] = ex;
+    pre[2 * lane + 1] = ex + c0;
+  }
+  __syncthreads();
+  uint2* out = cent + tile * kTileVol;
+#pragma unroll 1
+  for (int row = warp; row < kRows; row += 8) {
+    const uint32_t km = keepmask[row];
+    if (!((km >> lane) & 1u)) continue;
+    const int ly = row % P::TY, lz = row / P::TY;
+    const int c = ((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::H);
+    const uint32_t pos = pre[row] + __popc(km & ((1u << lane) - 1u));
+    out[pos] = make_uint2((uint32_t)(row * 32 + lane), s[c]);
+  }
+  nfg = __reduce_add_sync(kFullMask, nfg);
+  maxd = __reduce_max_sync(kFullMask, maxd);
+  if (lane == 0) {
+    red_cnt[warp] = nfg;
+    red_max[warp] = maxd;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t f = 0, m = 0;
+    for (int w = 0; w < 8; ++w) {
+      f += red_cnt[w];
+      m = max(m, red_max[w]);
+    }
+    const uint32_t cnt = pre[kRows - 1] + __popc(keepmask[kRows - 1]);
+    meta[tile] = TileMeta{cnt, m, f, 0};
+    if (cnt) atomicAdd(&hdr->n_kept, (unsigned long long)cnt);
+  }
+}
+
+}  // namespace
+
+cudaError_t dilate_cover_setup();
+cudaError_t dilate_atomic_setup();
+
+cudaError_t ensure_mtables(int dev) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  DeviceTables& dt = g_tables[dev];
+  if (dt.m3) return cudaSuccess;
+  {
+    std::vector<int> off, cls(kClasses3 + 1, 0);
+    using P = PruneTile<true>;
+    for (int c = 0; c < kClasses3; ++c) {
+      cls[c] = (int)off.size();
+      if (c < 3) continue;  // stage 1 (26-neighbourhood) is unrolled in the kernel
+      for (int dz = -3; dz <= 3; ++dz)
+        for (int dy = -3; dy <= 3; ++dy)
+          for (int dx = -3; dx <= 3; ++dx) {
+            int a[3] = {abs(dz), abs(dy), abs(dx)};
+            if (a[0] < a[1]) std::swap(a[0], a[1]);
+            if (a[1] < a[2]) std::swap(a[1], a[2]);
+            if (a[0] < a[1]) std::swap(a[0], a[1]);
+            if (a[0] == h_rep3[c][0] && a[1] == h_rep3[c][1] && a[2] == h_rep3[c][2])
+              off.push_back((dz * P::PY + dy) * P::PX + dx);
+          }
+    }
+    cls[kClasses3] = (int)off.size();
+    if (off.size() != 152) return cudaErrorUnknown;
+    cudaError_t e = cudaMemcpyToSymbol(c_off3, off.data(), sizeof(int) * off.size());
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_cls3, cls.data(), sizeof(int) * cls.size());
+    if (e != cudaSuccess) return e;
+  }
+  {
+    std::vector<int> off, cls(kClasses2 + 1, 0);
+    using P = PruneTile<false>;
+    for (int c = 0; c < kClasses2; ++c) {
+      cls[c] = (int)off.size();
+      if (c < 2) continue;
+      for (int dy = -2; dy <= 2; ++dy)
+        for (int dx = -2; dx <= 2; ++dx) {
+          int a0 = abs(dy), a1 = abs(dx);
+          if (a0 < a1) std::swap(a0, a1);
+          if (a0 == h_rep2[c][0] && a1 == h_rep2[c][1]) off.push_back(dy * P::PX + dx);
+        }
+    }
+    cls[kClasses2] = (int)off.size();
+    if (off.size() != 16) return cudaErrorUnknown;
+    cudaError_t e = cudaMemcpyToSymbol(c_off2, off.data(), sizeof(int) * off.size());
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_cls2, cls.data(), sizeof(int) * cls.size());
+    if (e != cudaSuccess) return e;
+  }
+  uint32_t *m3 = nullptr, *m2 = nullptr;
+  cudaError_t e = cudaMalloc(&m3, sizeof(uint32_t) * kClasses3 * (kDcap3 + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&m2, sizeof(uint32_t) * kClasses2 * (kDcap2 + 1));
+  if (e != cudaSuccess) {
+    cudaFree(m3);
+    return e;
+  }
+  const int64_t n3 = (int64_t)kClasses3 * (kDcap3 + 1), n2 = (int64_t)kClasses2 * (kDcap2 + 1);
+  k_mtable3<<<(unsigned)((n3 + 127) / 128), 128>>>(m3);
+  k_mtable2<<<(unsigned)((n2 + 127) / 128), 128>>>(m2);
+  e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) e = dilate_cover_setup();
+  if (e == cudaSuccess) e = dilate_atomic_setup();
+  if (e != cudaSuccess) {
+    cudaFree(m3);
+    cudaFree(m2);
+    return e;
+  }
+  dt.m3 = m3;
+  dt.m2 = m2;
+  return cudaSuccess;
+}
+
+void release_mtables() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto& dt : g_tables) {
+    if (dt.m3) cudaFree(dt.m3);
+    if (dt.m2) cudaFree(dt.m2);
+    dt.m3 = dt.m2 = nullptr;
+  }
+}
+
+void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, WsHeader* hdr, cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (g.ndim == 3)
+    k_prune<true><<<(unsigned)g.ntiles, 256, 0, st>>>(D, g, meta, centres, g_tables[dev].m3, hdr);
+  else
+    k_prune<false><<<(unsigned)g.ntiles, 256, 0, st>>>(D, g, meta, centres, g_tables[dev].m2, hdr);
+}
+
+}  // namespace fastrs

@@ -44,7 +44,7 @@ class _Stats(ctypes.Structure):
 class _Diag(ctypes.Structure):
     _fields_ = [("status_bits", ctypes.c_uint32), ("dmax", ctypes.c_uint32), ("n_fg", ctypes.c_uint64),
                 ("n_kept", ctypes.c_uint64), ("n_intervals", ctypes.c_uint64),
-                ("sum_scale_log2", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("sum_scale_log2", ctypes.c_int32), ("n_fallback", ctypes.c_uint32)]
 
 
 def load(build_if_missing: bool = True) -> ctypes.CDLL:
@@ -226,7 +226,7 @@ def sphericity_roundness_host(labels, max_label: int, ndim=None, flags=BORDER_BA
 def diagnostics(ws: torch.Tensor) -> dict:
     d = _Diag()
     _check(load().fastrs_read_diagnostics(ws.data_ptr(), ctypes.byref(d), _stream(ws.device)))
-    return {n: getattr(d, n) for n, _ in _Diag._fields_ if n != "reserved"}
+    return {n: getattr(d, n) for n, _ in _Diag._fields_}
 
 
 def last_workspace(device=None) -> torch.Tensor:

@@ -248,9 +248,10 @@ def test_diagnostics_counters(F):
     F.sphericity_roundness(t, max_label=1)
     d = F.diagnostics(F.last_workspace(t.device))
     assert d["status_bits"] == 0 and d["dmax"] == 226 and d["n_fg"] == 14147
-    # exact lattice pruning with the 26-neighbourhood then |s|^2 <= 12 keeps 121 centres on
-    # the digital sphere r=15 (SURVEY.md §8(c) "Kept-centre counts")
+    # exact lattice pruning with the 26-neighbourhood, then all |s|^2 <= 12, keeps 121
+    # centres on the digital sphere r=15 (SURVEY.md §8(c) "Kept-centre counts")
     assert d["n_kept"] == 121
     F.sphericity_roundness(_dev(synth.disk(20)), max_label=1)
     d = F.diagnostics(F.last_workspace(t.device))
     assert d["n_fg"] == 1257 and d["dmax"] == 401
+    assert d["n_kept"] <= 9  # 8-neighbourhood alone keeps 9; |s|^2 <= 8 keeps fewer
