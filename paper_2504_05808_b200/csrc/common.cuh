@@ -99,6 +99,26 @@ __host__ __device__ inline int sum_scale_log2(int64_t Nb, uint32_t dmax) {
   return s < 0 ? 0 : (s > 32 ? 32 : s);
 }
 
+// Monotone bucket of a squared radius D: 8 buckets per octave (0..127 for D < 65536).
+// Kept-centre lists are sorted by it (descending) and the dilation walks it downwards.
+__host__ __device__ inline int dbucket(uint32_t D) {
+  int msb = 31;
+  while (msb > 0 && !((D >> msb) & 1u)) --msb;
+#ifdef __CUDA_ARCH__
+  msb = 31 - __clz(D);
+#endif
+  const int frac = msb >= 3 ? (int)((D >> (msb - 3)) & 7u) : (int)((D << (3 - msb)) & 7u);
+  return msb * 8 + frac;
+}
+// Largest D with dbucket(D) <= b (D >= 1): one less than the smallest D of bucket b+1 or above.
+__host__ __device__ inline uint32_t dbucket_max(int b) {
+  const int b1 = b + 1;
+  if (b1 >= 24) return ((uint32_t)(8 + (b1 & 7)) << ((b1 >> 3) - 3)) - 1u;
+  // smallest D with dbucket(D) >= b1 for b1 < 24 (dbucket: 1->0, 2->8, 3->12, 4->16, 5->18, 6->20, 7->22, 8->24)
+  const uint32_t dmin = b1 <= 0 ? 1u : b1 <= 8 ? 2u : b1 <= 12 ? 3u : b1 <= 16 ? 4u : b1 <= 18 ? 5u : b1 <= 20 ? 6u : b1 <= 22 ? 7u : 8u;
+  return dmin - 1u;
+}
+
 // ---- kernel launchers (stream-ordered) -----------------------------------------------
 void launch_edt_x(const int32_t* labels, uint32_t* out, const Geom& g, int32_t max_label,
                   bool border, WsHeader* hdr, cudaStream_t st);

@@ -15,7 +15,6 @@
 // (warp-uniform, shared-memory reads conflict-free); survivors are compacted per home tile
 // in element order with the tile's count / max D / #foreground (TileMeta).
 #include <mutex>
-#include <vector>
 
 #include "common.cuh"
 
@@ -28,14 +27,22 @@ constexpr unsigned kFullMask = 0xFFFFFFFFu;
 __constant__ int c_rep3[kClasses3][3] = {{1, 0, 0}, {1, 1, 0}, {1, 1, 1}, {2, 0, 0}, {2, 1, 0}, {2, 1, 1},
                                          {2, 2, 0}, {2, 2, 1}, {3, 0, 0}, {3, 1, 0}, {3, 1, 1}, {2, 2, 2}};
 __constant__ int c_rep2[kClasses2][2] = {{1, 0}, {1, 1}, {2, 0}, {2, 1}, {2, 2}};
-static const int h_rep3[kClasses3][3] = {{1, 0, 0}, {1, 1, 0}, {1, 1, 1}, {2, 0, 0}, {2, 1, 0}, {2, 1, 1},
-                                         {2, 2, 0}, {2, 2, 1}, {3, 0, 0}, {3, 1, 0}, {3, 1, 1}, {2, 2, 2}};
-static const int h_rep2[kClasses2][2] = {{1, 0}, {1, 1}, {2, 0}, {2, 1}, {2, 2}};
-// stage-2 offsets (|s|^2 >= 4) as shared-memory deltas of the pruning tile, grouped by class
-__constant__ int c_off3[152];
-__constant__ int c_cls3[kClasses3 + 1];
-__constant__ int c_off2[16];
-__constant__ int c_cls2[kClasses2 + 1];
+// class index (position in c_rep3 / c_rep2) of an offset, -1 if |s|^2 > 12 / 8 or s = 0
+__host__ __device__ constexpr int class3(int dz, int dy, int dx) {
+  const int a = dz < 0 ? -dz : dz, b = dy < 0 ? -dy : dy, c = dx < 0 ? -dx : dx;
+  const int hi = a > b ? (a > c ? a : c) : (b > c ? b : c);
+  const int lo = a < b ? (a < c ? a : c) : (b < c ? b : c);
+  const int mid = a + b + c - hi - lo;
+  const int key = hi * 100 + mid * 10 + lo;
+  return key == 100 ? 0 : key == 110 ? 1 : key == 111 ? 2 : key == 200 ? 3 : key == 210 ? 4 : key == 211 ? 5 :
+         key == 220 ? 6 : key == 221 ? 7 : key == 300 ? 8 : key == 310 ? 9 : key == 311 ? 10 : key == 222 ? 11 : -1;
+}
+__host__ __device__ constexpr int class2(int dy, int dx) {
+  const int a = dy < 0 ? -dy : dy, b = dx < 0 ? -dx : dx;
+  const int hi = a > b ? a : b, lo = a > b ? b : a;
+  const int key = hi * 10 + lo;
+  return key == 10 ? 0 : key == 11 ? 1 : key == 20 ? 2 : key == 21 ? 3 : key == 22 ? 4 : -1;
+}
 
 __device__ __forceinline__ int isqrt_t(int h) {
   int w = (int)sqrtf((float)h);
@@ -100,7 +107,10 @@ struct PruneTile {
   static constexpr int TY = IS3D ? 8 : 64, TZ = IS3D ? 8 : 1;
   static constexpr int PX = kTX + 2 * H, PY = TY + 2 * H, PZ = IS3D ? TZ + 2 * H : 1;
   static constexpr int HZ = IS3D ? H : 0;
+  static constexpr int NC = IS3D ? kClasses3 : kClasses2;   // classes
+  static constexpr int C1 = IS3D ? 3 : 2;                   // stage-1 classes
 };
+
 
 template <bool IS3D>
 __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, Geom g, TileMeta* __restrict__ meta,
@@ -113,6 +123,7 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
   __shared__ uint32_t red_cnt[8], red_max[8];
   __shared__ uint16_t surv[kTileVol];
   __shared__ uint32_t s_nsurv;
+  __shared__ uint32_t bhist[128];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t tile = blockIdx.x;
   int64_t t = tile;
@@ -136,20 +147,35 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
   constexpr int dcap = IS3D ? kDcap3 : kDcap2;
   uint32_t nfg = 0, maxd = 0;
   const int64_t gx = tx * kTX + lane;
-#pragma unroll 1
-  for (int row = warp; row < kRows; row += 8) {
+  // stage 1 (26 / 8 neighbours), row-vectorised.  The containment thresholds of the warp's
+  // 8 rows are fetched first so the table loads overlap.
+  constexpr int kRowsPerWarp = kRows / 8;
+  uint32_t dr[kRowsPerWarp], m0r[kRowsPerWarp], m1r[kRowsPerWarp], m2r[kRowsPerWarp];
+  bool fgr[kRowsPerWarp];
+#pragma unroll
+  for (int k = 0; k < kRowsPerWarp; ++k) {
+    const int row = warp + 8 * k;
     const int ly = row % P::TY, lz = row / P::TY;
     const int64_t gz = tz * P::TZ + lz, gy = ty * P::TY + ly;
     const int c = ((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::H);
     const uint32_t d = s[c];
-    const bool fg = d != 0 && gz < g.Z && gy < g.Y && gx < g.X;
+    fgr[k] = d != 0 && gz < g.Z && gy < g.Y && gx < g.X;
+    dr[k] = d;
+    const bool test = fgr[k] && d <= (uint32_t)dcap;
+    m0r[k] = test ? __ldg(M + d) : 0xFFFFFFFFu;
+    m1r[k] = test ? __ldg(M + (dcap + 1) + d) : 0xFFFFFFFFu;
+    m2r[k] = (IS3D && test) ? __ldg(M + 2 * (dcap + 1) + d) : 0xFFFFFFFFu;
+  }
+#pragma unroll
+  for (int k = 0; k < kRowsPerWarp; ++k) {
+    const int row = warp + 8 * k;
+    const int ly = row % P::TY, lz = row / P::TY;
+    const int c = ((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::H);
+    const bool fg = fgr[k];
     bool keep = fg;
     if (__any_sync(kFullMask, fg)) {
-      const bool test = fg && d <= (uint32_t)dcap;
-      const uint32_t m0 = test ? __ldg(M + d) : 0xFFFFFFFFu;
-      const uint32_t m1 = test ? __ldg(M + (dcap + 1) + d) : 0xFFFFFFFFu;
+      const uint32_t m0 = m0r[k], m1 = m1r[k], m2 = m2r[k];
       if (IS3D) {
-        const uint32_t m2 = test ? __ldg(M + 2 * (dcap + 1) + d) : 0xFFFFFFFFu;
 #pragma unroll
         for (int dz = -1; dz <= 1; ++dz)
 #pragma unroll
@@ -214,43 +240,85 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
       keep = true;
     }
     const bool test = keep && d <= (uint32_t)dcap;
-    const int c_lo = IS3D ? 3 : 2, c_hi = IS3D ? kClasses3 : kClasses2;
-#pragma unroll 1
-    for (int cl = c_lo; cl < c_hi; ++cl) {
+    uint32_t mv[P::NC - P::C1];
+#pragma unroll
+    for (int k = 0; k < P::NC - P::C1; ++k) mv[k] = test ? __ldg(M + (P::C1 + k) * (dcap + 1) + d) : 0xFFFFFFFFu;
+#pragma unroll
+    for (int k = 0; k < P::NC - P::C1; ++k) {
       if (!__any_sync(kFullMask, test && keep)) break;
-      const uint32_t m = test ? __ldg(M + cl * (dcap + 1) + d) : 0xFFFFFFFFu;
-      const int jb = IS3D ? c_cls3[cl] : c_cls2[cl], je = IS3D ? c_cls3[cl + 1] : c_cls2[cl + 1];
-      for (int j = jb; j < je; ++j) {
-        const int off = IS3D ? c_off3[j] : c_off2[j];
-        if (test) keep &= s[c + off] <= m;
+      // all offsets of class C1+k; the class test folds at compile time after unrolling
+      if (IS3D) {
+#pragma unroll
+        for (int dz = -3; dz <= 3; ++dz)
+#pragma unroll
+          for (int dy = -3; dy <= 3; ++dy)
+#pragma unroll
+            for (int dx = -3; dx <= 3; ++dx)
+              if (class3(dz, dy, dx) == P::C1 + k && test) keep &= s[c + (dz * P::PY + dy) * P::PX + dx] <= mv[k];
+      } else {
+#pragma unroll
+        for (int dy = -2; dy <= 2; ++dy)
+#pragma unroll
+          for (int dx = -2; dx <= 2; ++dx)
+            if (class2(dy, dx) == P::C1 + k && test) keep &= s[c + dy * P::PX + dx] <= mv[k];
       }
     }
     if (i < nsurv && !keep) atomicAnd(&keepmask[v >> 5], ~(1u << (v & 31)));
     if (keep) maxd = max(maxd, d);
   }
   __syncthreads();
+  // ---- compaction, stably sorted by D bucket (descending): the dilation's gather stops
+  // scanning a home tile once its remaining balls cannot reach the output tile.  One warp:
+  // histogram -> descending exclusive scan -> stable scatter in element order.
   if (warp == 0) {
-    const uint32_t c0 = __popc(keepmask[2 * lane]), c1 = __popc(keepmask[2 * lane + 1]);
-    uint32_t inc = c0 + c1;
+    for (int k = lane; k < 128; k += 32) bhist[k] = 0;
+    __syncwarp();
+    for (int row = 0; row < kRows; ++row) {
+      const uint32_t km = keepmask[row];
+      if (!km) continue;
+      const int ly = row % P::TY, lz = row / P::TY;
+      const bool kept = (km >> lane) & 1u;
+      const int bk = kept ? dbucket(s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::H)]) : -1;
+      const uint32_t grp = __match_any_sync(kFullMask, bk);
+      if (kept && lane == __ffs(grp) - 1) bhist[bk] += __popc(grp);
+      __syncwarp();
+    }
+    uint32_t h[4], sum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      h[q] = bhist[127 - 4 * lane - q];
+      sum += h[q];
+    }
+    uint32_t inc = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t n = __shfl_up_sync(kFullMask, inc, o);
-      if (lane >= o) inc += n;
+      const uint32_t v = __shfl_up_sync(kFullMask, inc, o);
+      if (lane >= o) inc += v;
     }
-    const uint32_t ex = inc - c0 - c1;
-    pre[2 * lane] = ex;
-    pre[2 * lane + 1] = ex + c0;
-  }
-  __syncthreads();
-  uint2* out = cent + tile * kTileVol;
-#pragma unroll 1
-  for (int row = warp; row < kRows; row += 8) {
-    const uint32_t km = keepmask[row];
-    if (!((km >> lane) & 1u)) continue;
-    const int ly = row % P::TY, lz = row / P::TY;
-    const int c = ((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::H);
-    const uint32_t pos = pre[row] + __popc(km & ((1u << lane) - 1u));
-    out[pos] = make_uint2((uint32_t)(row * 32 + lane), s[c]);
+    uint32_t run = inc - sum;
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      bhist[127 - 4 * lane - q] = run;  // now: next free slot of each bucket
+      run += h[q];
+    }
+    if (lane == 31) s_nsurv = inc;  // total kept
+    __syncwarp();
+    uint2* out = cent + tile * kTileVol;
+    for (int row = 0; row < kRows; ++row) {
+      const uint32_t km = keepmask[row];
+      if (!km) continue;
+      const int ly = row % P::TY, lz = row / P::TY;
+      const bool kept = (km >> lane) & 1u;
+      const uint32_t d = kept ? s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::H)] : 0u;
+      const int bk = kept ? dbucket(d) : -1;
+      const uint32_t grp = __match_any_sync(kFullMask, bk);
+      const uint32_t base = kept ? bhist[bk] : 0u;
+      if (kept) out[base + __popc(grp & ((1u << lane) - 1u))] = make_uint2((uint32_t)(row * 32 + lane), d);
+      __syncwarp();
+      if (kept && lane == __ffs(grp) - 1) bhist[bk] = base + __popc(grp);
+      __syncwarp();
+    }
   }
   nfg = __reduce_add_sync(kFullMask, nfg);
   maxd = __reduce_max_sync(kFullMask, maxd);
@@ -265,7 +333,7 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
       f += red_cnt[w];
       m = max(m, red_max[w]);
     }
-    const uint32_t cnt = pre[kRows - 1] + __popc(keepmask[kRows - 1]);
+    const uint32_t cnt = s_nsurv;
     meta[tile] = TileMeta{cnt, m, f, 0};
     if (cnt) atomicAdd(&hdr->n_kept, (unsigned long long)cnt);
   }
@@ -281,48 +349,6 @@ cudaError_t ensure_mtables(int dev) {
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
   DeviceTables& dt = g_tables[dev];
   if (dt.m3) return cudaSuccess;
-  {
-    std::vector<int> off, cls(kClasses3 + 1, 0);
-    using P = PruneTile<true>;
-    for (int c = 0; c < kClasses3; ++c) {
-      cls[c] = (int)off.size();
-      if (c < 3) continue;  // stage 1 (26-neighbourhood) is unrolled in the kernel
-      for (int dz = -3; dz <= 3; ++dz)
-        for (int dy = -3; dy <= 3; ++dy)
-          for (int dx = -3; dx <= 3; ++dx) {
-            int a[3] = {abs(dz), abs(dy), abs(dx)};
-            if (a[0] < a[1]) std::swap(a[0], a[1]);
-            if (a[1] < a[2]) std::swap(a[1], a[2]);
-            if (a[0] < a[1]) std::swap(a[0], a[1]);
-            if (a[0] == h_rep3[c][0] && a[1] == h_rep3[c][1] && a[2] == h_rep3[c][2])
-              off.push_back((dz * P::PY + dy) * P::PX + dx);
-          }
-    }
-    cls[kClasses3] = (int)off.size();
-    if (off.size() != 152) return cudaErrorUnknown;
-    cudaError_t e = cudaMemcpyToSymbol(c_off3, off.data(), sizeof(int) * off.size());
-    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_cls3, cls.data(), sizeof(int) * cls.size());
-    if (e != cudaSuccess) return e;
-  }
-  {
-    std::vector<int> off, cls(kClasses2 + 1, 0);
-    using P = PruneTile<false>;
-    for (int c = 0; c < kClasses2; ++c) {
-      cls[c] = (int)off.size();
-      if (c < 2) continue;
-      for (int dy = -2; dy <= 2; ++dy)
-        for (int dx = -2; dx <= 2; ++dx) {
-          int a0 = abs(dy), a1 = abs(dx);
-          if (a0 < a1) std::swap(a0, a1);
-          if (a0 == h_rep2[c][0] && a1 == h_rep2[c][1]) off.push_back(dy * P::PX + dx);
-        }
-    }
-    cls[kClasses2] = (int)off.size();
-    if (off.size() != 16) return cudaErrorUnknown;
-    cudaError_t e = cudaMemcpyToSymbol(c_off2, off.data(), sizeof(int) * off.size());
-    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_cls2, cls.data(), sizeof(int) * cls.size());
-    if (e != cudaSuccess) return e;
-  }
   uint32_t *m3 = nullptr, *m2 = nullptr;
   cudaError_t e = cudaMalloc(&m3, sizeof(uint32_t) * kClasses3 * (kDcap3 + 1));
   if (e == cudaSuccess) e = cudaMalloc(&m2, sizeof(uint32_t) * kClasses2 * (kDcap2 + 1));
