@@ -70,7 +70,9 @@ enum {
   FASTRS_DETERMINISTIC = 2u,     /* accepted for compatibility: sums are ALWAYS exact
                                     fixed-point integers, bit-identical across runs     */
   FASTRS_ASYNC = 4u,             /* do not synchronise the stream at the end of the call  */
-  FASTRS_HOST_IO = 8u            /* size the workspace for fastrs_sphericity_roundness_host */
+  FASTRS_HOST_IO = 8u,           /* size the workspace for fastrs_sphericity_roundness_host */
+  FASTRS_FORCE_FALLBACK = 16u    /* run K5 with the atomic sparse-table kernel on every tile
+                                    (a GPU-internal cross-check of the default dilation)    */
 };
 
 /* Optional per-label statistics (device pointers, each nullable, batch*max_label long). */

@@ -5,13 +5,13 @@ Public API (torch CUDA tensors in, torch tensors out; all compute in libfastrs.s
     diagnostics, profile, profile_read, spheroid_area, ramanujan_perimeter,
     sphericity_3d, sphericity_2d, release
 """
-from .fastrs import (ASYNC, BORDER_BACKGROUND, DETERMINISTIC, HOST_IO, STAGES, FastrsError, diagnostics,
+from .fastrs import (ASYNC, BORDER_BACKGROUND, DETERMINISTIC, FORCE_FALLBACK, HOST_IO, STAGES, FastrsError, diagnostics,
                      edt_sq, last_workspace, load, local_thickness, profile, profile_read, ramanujan_perimeter,
                      release, sphericity_2d, sphericity_3d, sphericity_roundness, sphericity_roundness_host,
                      spheroid_area, workspace, workspace_bytes)
 
 __all__ = [
-    "ASYNC", "BORDER_BACKGROUND", "DETERMINISTIC", "HOST_IO", "STAGES", "FastrsError", "diagnostics", "edt_sq",
+    "ASYNC", "BORDER_BACKGROUND", "DETERMINISTIC", "FORCE_FALLBACK", "HOST_IO", "STAGES", "FastrsError", "diagnostics", "edt_sq",
     "last_workspace", "load", "local_thickness", "profile", "profile_read", "ramanujan_perimeter", "release",
     "sphericity_2d", "sphericity_3d", "sphericity_roundness", "sphericity_roundness_host", "spheroid_area",
     "workspace", "workspace_bytes",

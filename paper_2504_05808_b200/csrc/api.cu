@@ -196,7 +196,8 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
   if (stage != kEdtOnly) {
     launch_prune(D, g, meta, cent, hdr, st);  // K4
     tm.mark(3);
-    launch_dilate(labels, D, meta, cent, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out, hdr, st);  // K5
+    launch_dilate(labels, D, meta, cent, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out,
+                  (flags & kFlagForceFallback) != 0, hdr, st);  // K5
     tm.mark(4);
     if (stage == kFull) {
       launch_metrics(acc, g, *outs, hdr, st);  // K6

@@ -15,7 +15,7 @@ constexpr uint32_t kBitZ = 0x40000000u;  // element is the first of its z-run
 // ---- status bits in the workspace header ---------------------------------------------
 constexpr uint32_t kStBadLabel = 1u, kStNoSite = 2u, kStInternal = 4u, kStShell = 8u;
 
-constexpr uint32_t kFlagBorder = 1u, kFlagAsync = 4u, kFlagHostIO = 8u;
+constexpr uint32_t kFlagBorder = 1u, kFlagAsync = 4u, kFlagHostIO = 8u, kFlagForceFallback = 16u;
 
 // ---- dilation / pruning tiles ---------------------------------------------------------
 // 3D tile 32 x 8 x 8 (x fastest), 2D tile 32 x 64; both 64 rows of 32 = 2048 elements.
@@ -129,7 +129,7 @@ void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centr
                   cudaStream_t st);
 void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta,
                    const uint2* centres, const Geom& g, const Accum* acc, uint32_t* lt2_out,
-                   float* lt_out, WsHeader* hdr, cudaStream_t st);
+                   float* lt_out, bool force_fallback, WsHeader* hdr, cudaStream_t st);
 void launch_metrics(const Accum& acc, const Geom& g, const Outputs& o, WsHeader* hdr,
                     cudaStream_t st);
 void release_mtables();

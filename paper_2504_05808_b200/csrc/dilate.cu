@@ -1,32 +1,29 @@
 // K5 (default path): exact ball dilation LT^2(p) = max{ D(q) : |p-q|^2 < D(q) }
-// by "sorted cover", fused with the shell test and the per-label reductions.
+// by "exact-order cover", fused with the shell test and the per-label reductions.
 //
 // Work organisation.  A CTA of 4 warps owns a group of 4 output tiles (3D: 1x2x2 tiles of
-// 32x8x8, 2D: 2x2 tiles of 32x64; a tile = 64 rows of 32 elements); each warp owns one
-// tile privately (values, coverage masks), so the hot loop has no atomics and no
-// inter-warp conflicts, while the candidate gather is shared by the 4 tiles.
-//   1. gather   : the CTA collects every kept maximal ball (K4 output) whose ball reaches
-//                 the group's box into a shared list (8-byte packed centre + D) and a
-//                 histogram of a monotone bucket of D (8 buckets per octave).  K4's lists
-//                 are sorted by bucket, so a home tile is abandoned as soon as its remaining
-//                 balls are too small to reach the group.
-//   2. sort     : a counting sort of list indices by bucket, descending.
-//   3. cover    : each warp walks the non-empty buckets from the largest D down.  A ball is
-//                 tested against the bounding boxes of the still-uncovered foreground
-//                 elements of its tile (8 regions) and skipped when it cannot reach any of
-//                 them; else its rows are visited (lanes over the ball's rows): rows whose
-//                 uncovered mask misses the ball's x-extent are skipped, the others get the
-//                 interval |x-qx| <= isqrt(D-1-dy^2-dz^2), and only cells not covered by an
-//                 EARLIER bucket are max-updated.  Cells covered by an earlier bucket hold a
-//                 value >= every D of later buckets, so skipping them is exact; within a
-//                 bucket updates are plain max, so the result does not depend on the order
-//                 inside a bucket.
+// 32x8x8, 2D: 2x2 tiles of 32x64; a tile = 64 rows of 32 elements); each warp owns one tile
+// (values, coverage masks), while the candidate gather and sort are shared by the 4 tiles.
+//   1. gather : the CTA collects every kept maximal ball (K4 output) whose ball reaches the
+//               group's box into a shared list (packed centre + D) and a histogram of a
+//               monotone bucket of D.  K4's lists are sorted by bucket, so a home tile is
+//               abandoned as soon as its remaining balls are too small to reach the group.
+//   2. sort   : an exact counting sort of the list by D, descending (a round covers at most
+//               kCap candidates and a D range of at most kHist values; larger gathers run in
+//               several D-descending rounds).
+//   3. cover  : each warp walks the sorted list: lanes screen 32 balls at a time (the ball
+//               reaches the tile, and its bounding rows hold still-uncovered foreground within
+//               its x-extent, tracked as four 64-bit row masks, one per 8-column chunk); each
+//               surviving ball is painted with the lanes over the tile's rows: per row the
+//               interval |x-qx| <= isqrt(D-1-dy^2-dz^2), restricted to uncovered foreground.
+//               Exactness: balls arrive in exactly descending D, so the first ball covering a
+//               cell carries the max D over all kept balls containing it; each cell is written
+//               once and marked covered at once.  A warp stops when nothing is left uncovered.
 //   4. epilogue : LT^2 per element, shell (D == 1), per-label reductions (shared with the
-//                 fallback kernel in lt.cu).
-// Exactness never depends on a test being tight: every skip is justified by cells already
-// holding a value >= D.  Gathers larger than the list are processed in D-descending rounds;
-// the pathological case (one bucket alone larger than the list) hands the group to the
-// atomic fallback kernel k_dilate_atomic (lt.cu), which also handles Dmax > 65535.
+//               fallback kernel in lt.cu).
+// The pathological case (a single bucket exceeding the list or the sort range) hands the
+// group to the atomic sparse-table kernel k_dilate_atomic (lt.cu), which also handles
+// Dmax > 65535 (FASTRS_FORCE_FALLBACK sends every tile there: a GPU-internal cross-check).
 #include "common.cuh"
 #include "dilate_common.cuh"
 
@@ -34,31 +31,24 @@ namespace fastrs {
 namespace {
 
 constexpr int kWarps = 4;  // warps per CTA = tiles per group
-constexpr int kCap = 2048;
+constexpr int kCap = 3072;   // candidate list capacity per round
 constexpr int kBuckets = 128;
-constexpr int kRegions = 8;
+constexpr int kHist = 1536;  // exact-D counting-sort bins per round
+constexpr int kPoint = 128;  // uncovered cells at which a warp switches to point tests
 constexpr int kOff = 16384;  // coordinate bias of packed candidates
-
-// ceil(2^16 / n): (r * c_magic[n]) >> 16 == r / n exactly for r < 64
-__constant__ uint32_t c_magic[65] = {
-    0,    65536, 32768, 21846, 16384, 13108, 10923, 9363, 8192, 7282, 6554, 5958, 5462, 5042, 4682, 4370, 4096,
-    3856, 3641,  3450,  3277,  3121,  2979,  2850,  2731, 2622, 2521, 2428, 2341, 2260, 2185, 2115, 2048, 1986,
-    1928, 1873,  1821,  1772,  1725,  1681,  1639,  1599, 1561, 1525, 1490, 1457, 1425, 1395, 1366, 1338, 1311,
-    1286, 1261,  1237,  1214,  1192,  1171,  1150,  1130, 1111, 1093, 1075, 1058, 1041, 1024};
 
 struct Smem {
   unsigned long long list[kCap];     // gathered candidates (centre relative to the group), gather order
   uint16_t val[kWarps][kRows * 32];  // LT^2 per element of each warp's tile (D <= 65535 here)
-  uint16_t idx[kCap];                // indices into list, sorted by D bucket (descending)
+  uint32_t hist[kHist];              // exact-D counting sort: bin Dhi - D
+  uint16_t idx[kCap];                // indices into list, sorted by D (descending)
   uint32_t fg[kWarps][kRows];        // foreground mask per row
-  uint32_t cov[kWarps][kRows];       // covered by an earlier bucket
-  uint32_t cur[kWarps][kRows];       // covered in the current bucket
-  int box[kWarps][kRegions][6];      // uncovered-foreground bounding boxes (x0,x1,y0,y1,z0,z1)
-  uint32_t hist[kBuckets];
-  uint32_t start[kBuckets + 1];
-  uint32_t nonempty[4];              // non-empty buckets of the round (bitmask)
-  uint32_t count;
-  int round_lo, round_hi, next_hi, fallback;
+  uint32_t cov[kWarps][kRows];       // covered (final value written)
+  uint16_t ulist[kWarps][kPoint];    // point mode: the still-uncovered cells (row*32 + x)
+  uint32_t bhist[kBuckets];
+  uint32_t wsum[kWarps];
+  uint32_t count, total;
+  int round_lo, round_hi, round_top, next_hi, fallback, rounds;
 };
 
 template <bool IS3D>
@@ -153,7 +143,7 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
         if (tm) {
           if (HIST) {
             const uint32_t grp = __match_any_sync(kFull, take ? bk : -1);
-            if (take && lane == __ffs(grp) - 1) atomicAdd(&S.hist[bk], (uint32_t)__popc(grp));
+            if (take && lane == __ffs(grp) - 1) atomicAdd(&S.bhist[bk], (uint32_t)__popc(grp));
           }
           uint32_t base = 0;
           if (lane == 0) base = atomicAdd(&S.count, (uint32_t)__popc(tm));
@@ -167,12 +157,39 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
   }
 }
 
+// position of the n-th (0-based) set bit of m (requires popc(m) > n)
+__device__ __forceinline__ int nth_bit(uint32_t m, int n) {
+  int pos = 0, c = __popc(m & 0xFFFFu);
+  if (n >= c) { n -= c; m >>= 16; pos += 16; }
+  c = __popc(m & 0xFFu);
+  if (n >= c) { n -= c; m >>= 8; pos += 8; }
+  c = __popc(m & 0xFu);
+  if (n >= c) { n -= c; m >>= 4; pos += 4; }
+  c = __popc(m & 0x3u);
+  if (n >= c) { n -= c; m >>= 2; pos += 2; }
+  return pos + (n >= (int)(m & 1u) ? 1 : 0);
+}
+
+// 64-bit mask of the tile rows (row = lz*TY + ly) inside [ya,yb] x [za,zb]
 template <bool IS3D>
-__global__ void __launch_bounds__(kWarps * 32) k_dilate_cover(const int32_t* __restrict__ lab,
+__device__ __forceinline__ unsigned long long row_box(int ya, int yb, int za, int zb) {
+  if (IS3D) {
+    const unsigned long long ym = (unsigned long long)range_mask(ya, yb) * 0x0101010101010101ull;
+    const unsigned long long zhi = zb >= 7 ? ~0ull : ((1ull << (8 * (zb + 1))) - 1ull);
+    return ym & zhi & (~0ull << (8 * za));
+  } else {
+    const unsigned long long hi = yb >= 63 ? ~0ull : ((1ull << (yb + 1)) - 1ull);
+    return hi & (~0ull << ya);
+  }
+}
+
+template <bool IS3D>
+__global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const int32_t* __restrict__ lab,
                                                              const uint32_t* __restrict__ Dg,
                                                              TileMeta* __restrict__ meta,
                                                              const uint2* __restrict__ cent, Geom g, Accum acc,
-                                                             int do_reduce, uint32_t* __restrict__ lt2_out,
+                                                             int do_reduce, int force_fallback,
+                                                             uint32_t* __restrict__ lt2_out,
                                                              float* __restrict__ lt_out, WsHeader* __restrict__ hdr) {
   using P = Shape<IS3D>;
   constexpr int TY = P::TY, TZ = P::TZ;
@@ -200,85 +217,52 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_cover(const int32_t* __r
   const int mox = wx * kTX, moy = wy * TY, moz = wz * TZ;  // my tile origin within the group
   const bool active = have_tile && meta[mtile].nfg != 0;
   if (__syncthreads_or(active) == 0) return;  // the whole group is background
+  if (force_fallback) {
+    if (lane == 0 && have_tile) meta[mtile].pad = 1u;
+    return;
+  }
   const int64_t item = b * g.Z * g.Y * g.X;
 
   // ---- per-warp init: values, foreground masks, coverage ----------------------------------
   uint16_t* val = S.val[warp];
   uint32_t* fgw = S.fg[warp];
   uint32_t* covw = S.cov[warp];
-  uint32_t* curw = S.cur[warp];
-  for (int i = lane; i < kRows * 32 / 2; i += 32) reinterpret_cast<uint32_t*>(val)[i] = 0;
+  {
+    uint4* v4 = reinterpret_cast<uint4*>(val);
 #pragma unroll 4
-  for (int row = 0; row < kRows; ++row) {
-    const int ly = row % TY, lz = row / TY;
-    const int64_t gz = roz + moz + lz, gy = roy + moy + ly, gx = rox + mox + lane;
-    bool f = false;
-    if (active && gz < g.Z && gy < g.Y && gx < g.X) f = __ldg(Dg + item + (gz * g.Y + gy) * g.X + gx) != 0;
-    const uint32_t m = __ballot_sync(kFull, f);
-    if (lane == 0) {
-      fgw[row] = m;
-      covw[row] = 0;
-      curw[row] = 0;
+    for (int i = lane; i < kRows * 32 / 8; i += 32) v4[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  // rows of my tile that still hold uncovered foreground, per 8-column chunk of x
+  unsigned long long Uc[4] = {0, 0, 0, 0};
+  {
+    const int64_t gx = rox + mox + lane;
+#pragma unroll
+    for (int r0 = 0; r0 < kRows; r0 += 16) {
+      uint32_t dv[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int row = r0 + k, ly = row % TY, lz = row / TY;
+        const int64_t gz = roz + moz + lz, gy = roy + moy + ly;
+        dv[k] = (active && gz < g.Z && gy < g.Y && gx < g.X) ? __ldg(Dg + item + (gz * g.Y + gy) * g.X + gx) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t m = __ballot_sync(kFull, dv[k] != 0);
+        if (lane == ((r0 + k) & 31)) {
+          fgw[r0 + k] = m;
+          covw[r0 + k] = 0;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if ((m >> (8 * c)) & 0xFFu) Uc[c] |= 1ull << (r0 + k);
+      }
     }
   }
   __syncwarp();
-
-  // uncovered-foreground bounding boxes of the 8 regions of my tile (tile coordinates):
-  // 3D: x halves x y halves x z halves; 2D: x halves x y quarters
-  auto refresh_boxes = [&]() {
-    int* bxs = &S.box[warp][0][0];
-    uint32_t u[2];
-    int ly[2], lz[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {  // each lane inspects rows lane and lane+32
-      const int row = lane + 32 * k;
-      ly[k] = row % TY;
-      lz[k] = row / TY;
-      u[k] = fgw[row] & ~covw[row];
-    }
-#pragma unroll
-    for (int r = 0; r < kRegions; ++r) {
-      uint32_t xm = 0;
-      int ylo = 1 << 20, yhi = -1, zlo = 1 << 20, zhi = -1;
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        bool inreg;
-        if (IS3D)
-          inreg = ((ly[k] >> 2) == ((r >> 1) & 1)) && ((lz[k] >> 2) == (r >> 2));
-        else
-          inreg = ((ly[k] >> 4) == (r >> 1));
-        const uint32_t ur = inreg ? (u[k] & ((r & 1) ? 0xFFFF0000u : 0x0000FFFFu)) : 0u;
-        if (ur) {
-          xm |= ur;
-          ylo = min(ylo, ly[k]);
-          yhi = max(yhi, ly[k]);
-          zlo = min(zlo, lz[k]);
-          zhi = max(zhi, lz[k]);
-        }
-      }
-      xm = __reduce_or_sync(kFull, xm);
-      ylo = __reduce_min_sync(kFull, ylo);
-      yhi = __reduce_max_sync(kFull, yhi);
-      zlo = __reduce_min_sync(kFull, zlo);
-      zhi = __reduce_max_sync(kFull, zhi);
-      if (lane == 0) {
-        int* bx = bxs + r * 6;
-        if (xm) {
-          bx[0] = __ffs(xm) - 1;
-          bx[1] = 31 - __clz(xm);
-          bx[2] = ylo;
-          bx[3] = yhi;
-          bx[4] = zlo;
-          bx[5] = zhi;
-        } else {
-          bx[0] = 1;
-          bx[1] = 0;  // empty
-        }
-      }
-    }
-    __syncwarp();
-  };
-  if (active) refresh_boxes();
+  // uncovered foreground cells of my tile (warp-uniform); point mode once it is small
+  int nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(fgw[lane]) + __popc(fgw[lane + 32])));
+  bool pmode = false;
+  uint16_t* ulist = S.ulist[warp];
 
   const int rmax = dmax > 0 ? isqrt16((int)(dmax - 1)) : 0;
   const int nrx = (rmax + kTX - 1) / kTX, nry = (rmax + TY - 1) / TY, nrz = IS3D ? (rmax + TZ - 1) / TZ : 0;
@@ -288,23 +272,26 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_cover(const int32_t* __r
   if (tid == 0) {
     S.round_hi = kBuckets - 1;
     S.fallback = 0;
+    S.rounds = 0;
   }
   __syncthreads();
   for (;;) {
+    // every tile of the group fully covered: nothing left to gather
+    if (__syncthreads_or(nu != 0) == 0) break;
     const int rhi = S.round_hi;
-    for (int i = tid; i < kBuckets; i += kWarps * 32) S.hist[i] = 0;
+    for (int i = tid; i < kBuckets; i += kWarps * 32) S.bhist[i] = 0;
     if (tid == 0) S.count = 0;
     __syncthreads();
     gather<IS3D, true>(S, meta, cent, g, b, tx0, ty0, tz0, nrx, nry, nrz, 0, rhi);
     __syncthreads();
-    // --- this round's bucket range [rlo, rhi]: as many buckets as fit the list (warp 0:
-    // descending inclusive scan of the histogram, 4 buckets per lane)
+    // --- this round's bucket range [rlo, rhi]: as many buckets as fit the list and the sort
+    // range (warp 0: descending inclusive scan of the histogram, 4 buckets per lane)
     if (warp == 0) {
       uint32_t h[4], sum = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {  // lane l holds buckets 127-4l .. 124-4l (descending order)
         const int k = kBuckets - 1 - 4 * lane - q;
-        h[q] = k <= rhi ? S.hist[k] : 0u;
+        h[q] = k <= rhi ? S.bhist[k] : 0u;
         sum += h[q];
       }
       uint32_t inc = sum;
@@ -313,32 +300,38 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_cover(const int32_t* __r
         const uint32_t v = __shfl_up_sync(kFull, inc, o);
         if (lane >= o) inc += v;
       }
-      uint32_t run = inc - sum;  // exclusive prefix before my first bucket
-      int lo_l = -1;             // the highest bucket whose inclusive prefix exceeds kCap
+      uint32_t run = inc - sum;
+      // the highest non-empty bucket bounds the round's D range from above
+      int top_l = -1;
+#pragma unroll
+      for (int q = 3; q >= 0; --q) {
+        const int k = kBuckets - 1 - 4 * lane - q;
+        if (h[q] && k <= rhi) top_l = k;
+      }
+      const int top = __reduce_max_sync(kFull, top_l);
+      const uint32_t dtop = dbucket_max(top < 0 ? 0 : top);
+      int lo_l = -1;  // the highest bucket that no longer fits (count or D range)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int k = kBuckets - 1 - 4 * lane - q;
-        S.start[k + 1] = run;
         run += h[q];
-        if (lo_l < 0 && k <= rhi && run > kCap) lo_l = k;
+        const uint32_t dmin_k = k == 0 ? 1u : dbucket_max(k - 1) + 1u;
+        if (lo_l < 0 && k <= top && (run > kCap || dtop + 1u > (uint32_t)kHist + dmin_k)) lo_l = k;
       }
       const int lo = __reduce_max_sync(kFull, lo_l);
-      // non-empty buckets of the round [lo+1, rhi]
+      uint32_t below = 0;  // candidates left for later rounds
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        uint32_t bits = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int k = kBuckets - 1 - 4 * lane - q;
-          if (h[q] && k > lo && k <= rhi && (k >> 5) == w) bits |= 1u << (k & 31);
-        }
-        bits = __reduce_or_sync(kFull, bits);
-        if (lane == 0) S.nonempty[w] = bits;
+      for (int q = 0; q < 4; ++q) {
+        const int k = kBuckets - 1 - 4 * lane - q;
+        if (k <= lo) below += h[q];
       }
+      below = __reduce_add_sync(kFull, below);
       if (lane == 0) {
-        S.fallback = (lo == rhi && lo >= 0) ? 1 : 0;  // a single bucket exceeds the list
+        // a single bucket exceeds the list / range, or (defensive) too many rounds
+        S.fallback = ((lo == top && lo >= 0) || ++S.rounds > kBuckets) ? 1 : 0;
         S.round_lo = lo + 1;
-        S.next_hi = lo;
+        S.round_top = top;
+        S.next_hi = below ? lo : -1;
       }
     }
     __syncthreads();
@@ -351,115 +344,195 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_cover(const int32_t* __r
       gather<IS3D, false>(S, meta, cent, g, b, tx0, ty0, tz0, nrx, nry, nrz, rlo, rhi);
       __syncthreads();
     }
-    // --- counting sort of the list indices by bucket (descending)
-    const uint32_t total = min(S.count, (uint32_t)kCap);
-    for (uint32_t i0 = warp * 32; i0 < total; i0 += kWarps * 32) {
-      const uint32_t i = i0 + lane;
-      int bk = -1;
-      if (i < total) {
-        bk = dbucket((uint32_t)(S.list[i] & 0xFFFFu));
-        if (bk < rlo || bk > rhi) bk = -1;
-      }
-      const uint32_t grp = __match_any_sync(kFull, bk);
-      uint32_t base = 0;
-      if (bk >= 0 && lane == __ffs(grp) - 1) base = atomicAdd(&S.start[bk + 1], (uint32_t)__popc(grp));
-      base = __shfl_sync(kFull, base, __ffs(grp) - 1);
-      if (bk >= 0) S.idx[base + __popc(grp & ((1u << lane) - 1u))] = (uint16_t)i;
+    // --- exact counting sort of the list indices by D (descending), D in [dlo, dhi]
+    const int rtop = S.round_top;
+    const uint32_t dhi = dbucket_max(rtop < 0 ? 0 : rtop), dlo = rlo == 0 ? 1u : dbucket_max(rlo - 1) + 1u;
+    const int nb = (int)(dhi - dlo) + 1;
+    const uint32_t n = min(S.count, (uint32_t)kCap);
+    for (int k = tid; k < nb; k += kWarps * 32) S.hist[k] = 0;
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += kWarps * 32) {
+      const uint32_t D = (uint32_t)(S.list[i] & 0xFFFFu);
+      if (D >= dlo && D <= dhi) atomicAdd(&S.hist[dhi - D], 1u);
     }
     __syncthreads();
+    {
+      constexpr int kPer = kHist / (kWarps * 32);
+      const int base = tid * kPer;
+      uint32_t loc[kPer], sum = 0;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        loc[j] = base + j < nb ? S.hist[base + j] : 0u;
+        sum += loc[j];
+      }
+      uint32_t inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += v;
+      }
+      if (lane == 31) S.wsum[warp] = inc;
+      __syncthreads();
+      uint32_t run = inc - sum;
+      for (int w = 0; w < warp; ++w) run += S.wsum[w];
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        if (base + j < nb) S.hist[base + j] = run;
+        run += loc[j];
+      }
+      if (tid == kWarps * 32 - 1) S.total = run;
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += kWarps * 32) {
+      const uint32_t D = (uint32_t)(S.list[i] & 0xFFFFu);
+      if (D >= dlo && D <= dhi) S.idx[atomicAdd(&S.hist[dhi - D], 1u)] = (uint16_t)i;
+    }
+    __syncthreads();
+    const uint32_t total = S.total;
     const bool last_round = S.next_hi < 0;
 
-    // --- cover: my tile, non-empty buckets from high to low ----------------------------------
-    if (active) {
-      for (int w4 = 3; w4 >= 0; --w4) {
-        uint32_t bits = S.nonempty[w4];
-        while (bits) {
-          const int bk = w4 * 32 + 31 - __clz(bits);
-          bits &= ~(1u << (bk & 31));
-          // after the sort, start[bk+1] is the end of bucket bk and start[bk+2] its beginning
-          const uint32_t s0 = bk == kBuckets - 1 ? 0u : S.start[bk + 2];
-          const uint32_t s1 = S.start[bk + 1];
-          for (uint32_t i0 = s0; i0 < s1; i0 += 32) {
-            const uint32_t i = i0 + lane;
-            bool need = false;
-            int cx = 0, cy = 0, cz = 0, D = 0;
-            if (i < s1) {
-              const unsigned long long e = S.list[S.idx[i]];
-              D = (int)(e & 0xFFFFu);
-              cx = (int)((e >> 16) & 0xFFFFu) - kOff - mox;
-              cy = (int)((e >> 32) & 0xFFFFu) - kOff - moy;
-              cz = (int)((e >> 48) & 0xFFFFu) - kOff - moz;
-              const int R2 = D - 1;
-              // reaches my tile, and some region with uncovered foreground
-              const int ddx = gap(0, kTX - 1, cx), ddy = gap(0, TY - 1, cy), ddz = gap(0, TZ - 1, cz);
-              if (ddx * ddx + ddy * ddy + ddz * ddz <= R2) {
-                const int* bxs = &S.box[warp][0][0];
+    // --- cover: my tile, balls in descending D.  Lanes first screen 32 balls at a time (reach
+    // + rows with uncovered foreground inside the ball's x-extent); the surviving balls are
+    // then painted one by one with the lanes over the tile's rows (lane = row, row + 32).
+    // Because the order is exactly descending, the first ball that covers a cell carries its
+    // final value: each cell is written once and coverage is updated immediately.
+    for (uint32_t i0 = 0; i0 < total && nu != 0; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      if (!pmode && nu <= kPoint) {
+        // switch to point mode: list the still-uncovered cells
+        uint32_t left[2];
 #pragma unroll
-                for (int r = 0; r < kRegions; ++r) {
-                  const int* bx = bxs + r * 6;
-                  if (bx[0] > bx[1]) continue;
-                  const int gx = gap(bx[0], bx[1], cx), gy = gap(bx[2], bx[3], cy), gz = gap(bx[4], bx[5], cz);
-                  need |= gx * gx + gy * gy + gz * gz <= R2;
-                }
-              }
-            }
-            uint32_t act = __ballot_sync(kFull, need);
-            while (act) {
-              const int k = __ffs(act) - 1;
-              act &= act - 1;
-              const int jx = __shfl_sync(kFull, cx, k), jy = __shfl_sync(kFull, cy, k), jz = __shfl_sync(kFull, cz, k);
-              const int jD = __shfl_sync(kFull, D, k);
-              const int R2 = jD - 1, rho = isqrt16(R2);
-              const int y0 = max(0, jy - rho), y1 = min(TY - 1, jy + rho);
-              const int z0 = max(0, jz - rho), z1 = min(TZ - 1, jz + rho);
-              const int nyr = y1 - y0 + 1, nrows = nyr * (z1 - z0 + 1);
-              const uint32_t magic = c_magic[nyr];
-              const uint32_t xbox = range_mask(max(jx - rho, 0), min(jx + rho, kTX - 1));
-              const uint16_t dv = (uint16_t)jD;
-              for (int r = lane; r < nrows; r += 32) {
-                const int zo = (int)(((uint32_t)r * magic) >> 16);
-                const int yy = y0 + (r - zo * nyr), zz = z0 + zo;
-                const int row = zz * TY + yy;
-                // cheap row skip: nothing uncovered in this row under the ball's x-extent
-                uint32_t m = fgw[row] & ~covw[row] & xbox;
-                if (!m) continue;
-                const int dy = yy - jy, dz = zz - jz;
-                const int hrem = R2 - dy * dy - dz * dz;
-                if (hrem < 0) continue;
-                const int w = isqrt16(hrem);
-                const int l = max(jx - w, 0), rr = min(jx + w, kTX - 1);
-                if (l > rr) continue;
-                ++n_rows;
-                m &= range_mask(l, rr);
-                if (!m) continue;
-                curw[row] |= m;
-                uint16_t* vr = val + row * 32;
-                while (m) {
-                  const int c = __ffs(m) - 1;
-                  m &= m - 1;
-                  if (vr[c] < dv) vr[c] = dv;
-                }
-              }
-            }
-          }
-          __syncwarp();
-          // bucket done: its coverage becomes "earlier-bucket" coverage
-          uint32_t chg = 0;
+        for (int kk = 0; kk < 2; ++kk) left[kk] = fgw[lane + 32 * kk] & ~covw[lane + 32 * kk];
+        const uint32_t cnt = __popc(left[0]) + __popc(left[1]);
+        uint32_t inc = cnt;
 #pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const int row = lane + 32 * k;
-            const uint32_t c = curw[row];
-            chg |= c & ~covw[row];
-            covw[row] |= c;
-            curw[row] = 0;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t v = __shfl_up_sync(kFull, inc, o);
+          if (lane >= o) inc += v;
+        }
+        uint32_t pos = inc - cnt;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          uint32_t m = left[kk];
+          while (m) {
+            const int c = __ffs(m) - 1;
+            m &= m - 1;
+            ulist[pos++] = (uint16_t)((lane + 32 * kk) * 32 + c);
           }
-          const bool any_new = __any_sync(kFull, chg != 0);
+        }
+        pmode = true;
+        __syncwarp();
+      }
+      if (pmode) {
+        // point tests: lanes = the next 32 balls (descending D), loop over the uncovered cells;
+        // a cell takes the D of the first (largest) ball containing it
+        int cx = 0, cy = 0, cz = 0, D = 0;
+        if (i < total) {
+          const unsigned long long e = S.list[S.idx[i]];
+          D = (int)(e & 0xFFFFu);
+          cx = (int)((e >> 16) & 0xFFFFu) - kOff - mox;
+          cy = (int)((e >> 32) & 0xFFFFu) - kOff - moy;
+          cz = (int)((e >> 48) & 0xFFFFu) - kOff - moz;
+          const int ddx = gap(0, kTX - 1, cx), ddy = gap(0, TY - 1, cy), ddz = gap(0, TZ - 1, cz);
+          if (ddx * ddx + ddy * ddy + ddz * ddz > D - 1) D = 0;
+        }
+        if (__ballot_sync(kFull, D != 0) == 0) continue;
+        bool hit = false;
+        for (int q = 0; q < nu; ++q) {
+          const uint32_t e = ulist[q];
+          const int x = (int)(e & 31u), row = (int)(e >> 5);
+          const int ly = IS3D ? (row & 7) : row, lz = IS3D ? (row >> 3) : 0;
+          const int dx = x - cx, dy = ly - cy, dz = lz - cz;
+          const uint32_t bm = __ballot_sync(kFull, dx * dx + dy * dy + dz * dz < D);
+          if (bm) {
+            const int wD = __shfl_sync(kFull, D, __ffs(bm) - 1);
+            if (lane == 0) {
+              val[e] = (uint16_t)wD;
+              ulist[q] = (uint16_t)(e | 0x8000u);
+            }
+            hit = true;
+          }
+        }
+        if (hit) {  // drop the covered cells from the list
           __syncwarp();
-          if (any_new) refresh_boxes();
+          uint32_t newn = 0;
+          for (int q0 = 0; q0 < nu; q0 += 32) {
+            const int q = q0 + lane;
+            const uint32_t e = q < nu ? ulist[q] : 0x8000u;
+            const bool keep = !(e & 0x8000u);
+            const uint32_t km = __ballot_sync(kFull, keep);
+            __syncwarp();
+            if (keep) ulist[newn + __popc(km & ((1u << lane) - 1u))] = (uint16_t)e;
+            newn += __popc(km);
+            __syncwarp();
+          }
+          nu = (int)newn;
+        }
+        continue;
+      }
+      unsigned long long cand = 0;
+      int cx = 0, cy = 0, cz = 0, D = 0;
+      if (i < total) {
+        const unsigned long long e = S.list[S.idx[i]];
+        D = (int)(e & 0xFFFFu);
+        cx = (int)((e >> 16) & 0xFFFFu) - kOff - mox;
+        cy = (int)((e >> 32) & 0xFFFFu) - kOff - moy;
+        cz = (int)((e >> 48) & 0xFFFFu) - kOff - moz;
+        const int R2 = D - 1;
+        const int ddx = gap(0, kTX - 1, cx), ddy = gap(0, TY - 1, cy), ddz = gap(0, TZ - 1, cz);
+        if (ddx * ddx + ddy * ddy + ddz * ddz <= R2) {
+          const int rho = isqrt16(R2);
+          const int xa = max(cx - rho, 0), xb = min(cx + rho, kTX - 1);
+          unsigned long long ux = 0;  // rows with uncovered foreground inside the ball's x-extent
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (xa <= 8 * c + 7 && xb >= 8 * c) ux |= Uc[c];
+          cand = row_box<IS3D>(max(cy - rho, 0), min(cy + rho, TY - 1), max(cz - rho, 0), min(cz + rho, TZ - 1)) & ux;
         }
       }
+      uint32_t act = __ballot_sync(kFull, cand != 0);
+      while (act) {
+        const int j = __ffs(act) - 1;
+        act &= act - 1;
+        const int jx = __shfl_sync(kFull, cx, j), jy = __shfl_sync(kFull, cy, j), jz = __shfl_sync(kFull, cz, j);
+        const int jD = __shfl_sync(kFull, D, j), jR2 = jD - 1;
+        const uint32_t jm[2] = {__shfl_sync(kFull, (uint32_t)cand, j), __shfl_sync(kFull, (uint32_t)(cand >> 32), j)};
+        const uint16_t dv = (uint16_t)jD;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          if (!((jm[half] >> lane) & 1u)) continue;
+          const int row = 32 * half + lane;
+          const int ly = IS3D ? (row & 7) : row, lz = IS3D ? (row >> 3) : 0;
+          const int dy = ly - jy, dz = lz - jz;
+          const int hrem = jR2 - dy * dy - dz * dz;
+          if (hrem < 0) continue;
+          const int w = isqrt16(hrem);
+          const int l = max(jx - w, 0), rr = min(jx + w, kTX - 1);
+          if (l > rr) continue;
+          ++n_rows;
+          uint32_t m = fgw[row] & ~covw[row] & range_mask(l, rr);
+          if (!m) continue;
+          covw[row] |= m;
+          uint16_t* vr = val + row * 32;
+          do {
+            const int c = __ffs(m) - 1;
+            m &= m - 1;
+            vr[c] = dv;
+          } while (m);
+        }
+        __syncwarp();
+      }
+      // refresh the uncovered-row masks
+      uint32_t left[2];
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) left[kk] = fgw[lane + 32 * kk] & ~covw[lane + 32 * kk];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        Uc[c] = (unsigned long long)__ballot_sync(kFull, (left[0] >> (8 * c)) & 0xFFu) |
+                ((unsigned long long)__ballot_sync(kFull, (left[1] >> (8 * c)) & 0xFFu) << 32);
+      nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(left[0]) + __popc(left[1])));
     }
-    if (last_round) break;  // no trailing barrier: warps go straight to their epilogue
+    if (last_round) break;
     __syncthreads();
     if (tid == 0) S.round_hi = S.next_hi;
     __syncthreads();
@@ -494,16 +567,16 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_cover(const int32_t* __r
 size_t dilate_cover_smem() { return sizeof(Smem); }
 
 void launch_dilate_cover(const int32_t* labels, const uint32_t* D, TileMeta* meta, const uint2* centres,
-                         const Geom& g, const Accum& a, int do_reduce, uint32_t* lt2_out, float* lt_out, WsHeader* hdr,
-                         cudaStream_t st) {
+                         const Geom& g, const Accum& a, int do_reduce, int force_fallback, uint32_t* lt2_out,
+                         float* lt_out, WsHeader* hdr, cudaStream_t st) {
   const int GX = g.ndim == 3 ? 1 : 2, GY = 2, GZ = g.ndim == 3 ? 2 : 1;
   const int64_t ngroups = g.B * ((g.ntx + GX - 1) / GX) * ((g.nty + GY - 1) / GY) * ((g.ntz + GZ - 1) / GZ);
   const size_t smem = sizeof(Smem);
   if (g.ndim == 3)
-    k_dilate_cover<true><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(labels, D, meta, centres, g, a, do_reduce,
+    k_dilate_cover<true><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(labels, D, meta, centres, g, a, do_reduce, force_fallback,
                                                                         lt2_out, lt_out, hdr);
   else
-    k_dilate_cover<false><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(labels, D, meta, centres, g, a, do_reduce,
+    k_dilate_cover<false><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(labels, D, meta, centres, g, a, do_reduce, force_fallback,
                                                                          lt2_out, lt_out, hdr);
 }
 

@@ -62,7 +62,7 @@ static __device__ __forceinline__ uint32_t row_epilogue(uint32_t c, int lane, bo
 size_t dilate_cover_smem();
 cudaError_t dilate_cover_setup();
 void launch_dilate_cover(const int32_t* labels, const uint32_t* D, TileMeta* meta, const uint2* centres,
-                         const Geom& g, const Accum& a, int do_reduce, uint32_t* lt2_out, float* lt_out, WsHeader* hdr,
-                         cudaStream_t st);
+                         const Geom& g, const Accum& a, int do_reduce, int force_fallback, uint32_t* lt2_out,
+                         float* lt_out, WsHeader* hdr, cudaStream_t st);
 
 }  // namespace fastrs

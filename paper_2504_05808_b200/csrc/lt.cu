@@ -201,13 +201,13 @@ cudaError_t dilate_atomic_setup() {
 }
 
 void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta, const uint2* centres,
-                   const Geom& g, const Accum* acc, uint32_t* lt2_out, float* lt_out, WsHeader* hdr,
-                   cudaStream_t st) {
+                   const Geom& g, const Accum* acc, uint32_t* lt2_out, float* lt_out, bool force_fallback,
+                   WsHeader* hdr, cudaStream_t st) {
   Accum a{};
   if (acc) a = *acc;
   // both kernels read Dmax / the per-tile fallback flag on the device; the atomic kernel only
   // processes tiles the sorted-cover kernel left to it
-  launch_dilate_cover(labels, D, meta, centres, g, a, acc ? 1 : 0, lt2_out, lt_out, hdr, st);
+  launch_dilate_cover(labels, D, meta, centres, g, a, acc ? 1 : 0, force_fallback ? 1 : 0, lt2_out, lt_out, hdr, st);
   const size_t smem = (size_t)kRows * kRowStride * 4;
   if (g.ndim == 3)
     k_dilate_atomic<true><<<(unsigned)g.ntiles, 256, smem, st>>>(labels, D, meta, centres, g, a, acc ? 1 : 0, lt2_out,

@@ -135,12 +135,19 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
   const int64_t b = t / g.ntz;
   const int64_t z0 = tz * P::TZ - P::HZ, y0 = ty * P::TY - P::H, x0 = tx * kTX - P::H;
   const uint32_t* Db = D + b * g.Z * g.Y * g.X;
-  for (int i = tid; i < P::PZ * P::PY * P::PX; i += 256) {
-    const int lx = i % P::PX, ly = (i / P::PX) % P::PY, lz = i / (P::PX * P::PY);
-    const int64_t gz = z0 + lz, gy = y0 + ly, gx = x0 + lx;
-    uint32_t v = 0;
-    if (gz >= 0 && gz < g.Z && gy >= 0 && gy < g.Y && gx >= 0 && gx < g.X) v = __ldg(Db + (gz * g.Y + gy) * g.X + gx);
-    s[i] = v;
+  // halo staging, one warp per (z, y) row of the padded tile (lanes over x: no per-element
+  // index division)
+  for (int r = warp; r < P::PZ * P::PY; r += 8) {
+    const int lz = r / P::PY, ly = r - lz * P::PY;
+    const int64_t gz = z0 + lz, gy = y0 + ly;
+    const bool rowok = gz >= 0 && gz < g.Z && gy >= 0 && gy < g.Y;
+    const uint32_t* src = Db + (gz * g.Y + gy) * g.X;
+#pragma unroll
+    for (int lx = lane; lx < P::PX + 31 - (P::PX + 31) % 32; lx += 32) {
+      if (lx >= P::PX) break;
+      const int64_t gx = x0 + lx;
+      s[r * P::PX + lx] = (rowok && gx >= 0 && gx < g.X) ? __ldg(src + gx) : 0u;
+    }
   }
   __syncthreads();
 
@@ -267,22 +274,22 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
     if (keep) maxd = max(maxd, d);
   }
   __syncthreads();
-  // ---- compaction, stably sorted by D bucket (descending): the dilation's gather stops
-  // scanning a home tile once its remaining balls cannot reach the output tile.  One warp:
-  // histogram -> descending exclusive scan -> stable scatter in element order.
+  // ---- compaction sorted by D bucket (descending; order inside a bucket is arbitrary): the
+  // dilation's gather stops scanning a home tile once its remaining balls cannot reach the
+  // output tile.  All warps: bucket histogram -> warp-0 descending exclusive scan -> scatter.
+  for (int k = tid; k < 128; k += 256) bhist[k] = 0;
+  __syncthreads();
+  for (int row = warp; row < kRows; row += 8) {
+    const uint32_t km = keepmask[row];
+    if (!km) continue;
+    const int ly = row % P::TY, lz = row / P::TY;
+    const bool kept = (km >> lane) & 1u;
+    const int bk = kept ? dbucket(s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::H)]) : -1;
+    const uint32_t grp = __match_any_sync(kFullMask, bk);
+    if (kept && lane == __ffs(grp) - 1) atomicAdd(&bhist[bk], (uint32_t)__popc(grp));
+  }
+  __syncthreads();
   if (warp == 0) {
-    for (int k = lane; k < 128; k += 32) bhist[k] = 0;
-    __syncwarp();
-    for (int row = 0; row < kRows; ++row) {
-      const uint32_t km = keepmask[row];
-      if (!km) continue;
-      const int ly = row % P::TY, lz = row / P::TY;
-      const bool kept = (km >> lane) & 1u;
-      const int bk = kept ? dbucket(s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::H)]) : -1;
-      const uint32_t grp = __match_any_sync(kFullMask, bk);
-      if (kept && lane == __ffs(grp) - 1) bhist[bk] += __popc(grp);
-      __syncwarp();
-    }
     uint32_t h[4], sum = 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -303,9 +310,11 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
       run += h[q];
     }
     if (lane == 31) s_nsurv = inc;  // total kept
-    __syncwarp();
+  }
+  __syncthreads();
+  {
     uint2* out = cent + tile * kTileVol;
-    for (int row = 0; row < kRows; ++row) {
+    for (int row = warp; row < kRows; row += 8) {
       const uint32_t km = keepmask[row];
       if (!km) continue;
       const int ly = row % P::TY, lz = row / P::TY;
@@ -313,11 +322,11 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
       const uint32_t d = kept ? s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::H)] : 0u;
       const int bk = kept ? dbucket(d) : -1;
       const uint32_t grp = __match_any_sync(kFullMask, bk);
-      const uint32_t base = kept ? bhist[bk] : 0u;
+      const int leader = __ffs(grp) - 1;
+      uint32_t base = 0;
+      if (kept && lane == leader) base = atomicAdd(&bhist[bk], (uint32_t)__popc(grp));
+      base = __shfl_sync(kFullMask, base, leader);
       if (kept) out[base + __popc(grp & ((1u << lane) - 1u))] = make_uint2((uint32_t)(row * 32 + lane), d);
-      __syncwarp();
-      if (kept && lane == __ffs(grp) - 1) bhist[bk] = base + __popc(grp);
-      __syncwarp();
     }
   }
   nfg = __reduce_add_sync(kFullMask, nfg);

@@ -20,6 +20,7 @@ BORDER_BACKGROUND = 1
 DETERMINISTIC = 2
 ASYNC = 4
 HOST_IO = 8
+FORCE_FALLBACK = 16  # run the dilation with the atomic sparse-table kernel (cross-check)
 
 STAGES = ("edt_x", "edt_y", "edt_z", "prune", "dilate", "metrics")
 

@@ -60,6 +60,7 @@ def full_check(F, lab, flags, ndim=None, max_label=None, fields=True):
         d2, lt2, sh = oracle.fields(lab, max_label=ml, flags=flags, ndim=ndim)
         np.testing.assert_array_equal(_u32(F.edt_sq(t, ndim=ndim, flags=flags)), d2)
         np.testing.assert_array_equal(_u32(F.local_thickness(t, ndim=ndim, flags=flags)), lt2)
+        np.testing.assert_array_equal(_u32(F.local_thickness(t, ndim=ndim, flags=flags | F.FORCE_FALLBACK)), lt2)
         lt_f = F.local_thickness(t, ndim=ndim, flags=flags, lt2=False, lt=True).cpu().numpy()
         np.testing.assert_array_equal(lt_f, np.sqrt(lt2.astype(np.float64)).astype(np.float32))
     got = F.sphericity_roundness(t, max_label=ml, ndim=ndim, flags=flags, stats=True)
@@ -209,10 +210,15 @@ def test_config_c5_subset(F):
     full_check(F, lab, 1, ndim=2, max_label=info["max_label"], fields=False)
 
 
-def test_config_c4_sampled(F):
+@pytest.fixture(scope="module")
+def c4():
+    return synth.make_config(4)
+
+
+def test_config_c4_sampled(F, c4):
     """C4 at full size in the bench's launch configuration; the oracle evaluates a seeded
     sample of labels one by one (exact by crop exactness)."""
-    lab, info = synth.make_config(4)
+    lab, info = c4
     ml = info["max_label"]
     t = _dev(lab)
     got = F.sphericity_roundness(t, max_label=ml, stats=True)
@@ -255,3 +261,23 @@ def test_diagnostics_counters(F):
     d = F.diagnostics(F.last_workspace(t.device))
     assert d["n_fg"] == 1257 and d["dmax"] == 401
     assert d["n_kept"] <= 9  # 8-neighbourhood alone keeps 9; |s|^2 <= 8 keeps fewer
+
+
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_dilation_cross_check_full_size(F, cfg, c4):
+    """The default exact-order cover dilation and the independent atomic sparse-table kernel
+    (FASTRS_FORCE_FALLBACK) give bit-identical LT^2 on every element of the full-size
+    configs (the oracle itself is checked against both on the sampled/full tests above)."""
+    if cfg == 4:
+        lab, info = c4
+    else:
+        lab, info = synth.make_config(cfg, batch=4) if cfg == 5 else synth.make_config(cfg)
+    ndim = 2 if cfg == 5 else 3
+    t = _dev(lab)
+    a = F.local_thickness(t, ndim=ndim)
+    b = F.local_thickness(t, ndim=ndim, flags=F.BORDER_BACKGROUND | F.FORCE_FALLBACK)
+    assert torch.equal(a, b)
+    d = F.edt_sq(t, ndim=ndim)
+    assert bool((a.view(torch.int32) >= d.view(torch.int32)).all())
+    del a, b, d, t
+    torch.cuda.empty_cache()
