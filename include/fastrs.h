@@ -151,6 +151,63 @@ FASTRS_API double fastrs_ramanujan_perimeter(double a, double b);   /* Eq. 9    
 FASTRS_API double fastrs_sphericity_3d(double V, double mean_lt);   /* Eqs. 1, 8                */
 FASTRS_API double fastrs_sphericity_2d(double A, double mean_lt);   /* Eqs. 2, 10, 11           */
 
+/* ---- multi-GPU z-slab path (north_star "a single large volume is
+ * split into z-slabs") ------------------------------------------------------------------
+ * One 3D volume [Z][Y][X] split into z-slabs, one per rank (batch = 1, ndim = 3).  Every
+ * computation runs in the kernels; the caller performs the three exchanges between the phase
+ * calls (paper_2504_05808_b200/slab.py does them with torch.distributed: NCCL on GPUs, gloo in
+ * the CPU tests).  With h = ceil(sqrt(max D_xy)) and R = isqrt(max D - 1):
+ *   A fastrs_slab_edt_xy   x and y passes of the own slab -> packed words + max D_xy
+ *     exchange 1: allreduce(max) of D_xy; every rank fetches the h packed slices on each side
+ *   B fastrs_slab_edt_z    z pass on the h-extended slab  -> D of the own slab + max D
+ *     exchange 2: allreduce(max) of D; every rank fetches H >= R D-slices on each side
+ *   C fastrs_slab_reduce   K4 on the H-extended slab, K5 + shell + partial per-label sums on the
+ *                          own slab (u64 fixed-point sums, u32 max LT^2: exact integers)
+ *     exchange 3: allreduce(sum) of the u64 partials, allreduce(max) of max LT^2
+ *   D fastrs_metrics_from_partials   closed forms per label
+ * Exactness: the z pass at an own element only looks |dz| <= sqrt(D_xy) <= h away; a ball that
+ * reaches the own slab has its centre within R <= H slices; partial sums are integers, so the
+ * result is bit-identical to fastrs_sphericity_roundness on the whole volume.
+ * All pointers are device pointers; each phase synchronises once unless FASTRS_ASYNC. */
+
+/* Workspace for the slab phases, sized by the extended slab dims {nz_ext, Y, X}. */
+FASTRS_API int fastrs_slab_workspace_bytes(const int64_t* dims_ext, size_t* bytes);
+
+/* A: labels = own slab [nz][Y][X] (dims = {nz, Y, X}); labels_below = the slice z0-1 of the
+ * rank below ([Y][X]), NULL at the bottom of the volume.  packed_out: [nz][Y][X] u32 words
+ * (partial squared distance + z-run-start flag); dxy_max (nullable): device u32 <- max partial
+ * distance over the slab.  Validates labels (EINVAL). */
+FASTRS_API int fastrs_slab_edt_xy(const int32_t* labels, const int32_t* labels_below, const int64_t* dims,
+                                  int32_t max_label, uint32_t flags, uint32_t* packed_out, uint32_t* dxy_max,
+                                  void* ws, size_t ws_bytes, void* stream);
+
+/* B: packed_ext = packed words of global slices [z_ext0, z_ext0 + nz_ext) (dims_ext = {nz_ext, Y,
+ * X}); the own slab is local [own_lo, own_hi).  d_out: [own_hi-own_lo][Y][X] squared distances;
+ * dmax_out (nullable): device u32 <- max D over the own slab.  ENOSITE as fastrs_edt_sq. */
+FASTRS_API int fastrs_slab_edt_z(const uint32_t* packed_ext, const int64_t* dims_ext, int64_t own_lo,
+                                 int64_t own_hi, int64_t z_ext0, int64_t Z, uint32_t flags, uint32_t* d_out,
+                                 uint32_t* dmax_out, void* ws, size_t ws_bytes, void* stream);
+
+/* C: labels = own slab; d_ext = D of the extended slab (dims_ext), own slab local [own_lo,
+ * own_hi), own_lo a multiple of 8 and own_hi a multiple of 8 or nz_ext; Z = global depth;
+ * dmax_global = max D over the whole volume.  Writes the own slab's partial per-label sums to
+ * vol, n_shell, sum_lt, sum_shell_lt (u64, fixed point 2^s with s from (Z*Y*X, dmax_global))
+ * and max_lt2 (u32), each max_label long (zeroed by the call). */
+FASTRS_API int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64_t* dims_ext,
+                                  int64_t own_lo, int64_t own_hi, int64_t Z, uint32_t dmax_global,
+                                  int32_t max_label, uint32_t flags, uint64_t* vol, uint64_t* n_shell,
+                                  uint64_t* sum_lt, uint64_t* sum_shell_lt, uint32_t* max_lt2, void* ws,
+                                  size_t ws_bytes, void* stream);
+
+/* D: closed forms from (reduced) partials: n_labels entries, nscale = elements per item used
+ * for the fixed-point scale, dmax_global as in C.  Outputs as fastrs_sphericity_roundness. */
+FASTRS_API int fastrs_metrics_from_partials(const uint64_t* vol, const uint64_t* n_shell, const uint64_t* sum_lt,
+                                            const uint64_t* sum_shell_lt, const uint32_t* max_lt2,
+                                            int64_t n_labels, int ndim, int64_t nscale, uint32_t dmax_global,
+                                            double* sphericity, double* roundness,
+                                            const fastrs_object_stats* stats, void* ws, size_t ws_bytes,
+                                            void* stream);
+
 FASTRS_API const char* fastrs_last_error(void);  /* thread-local message of the last failure */
 FASTRS_API void fastrs_release(void);            /* free the per-device caches                */
 

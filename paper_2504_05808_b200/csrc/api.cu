@@ -48,6 +48,9 @@ int make_geom(const int64_t* dims, int ndim, int64_t batch, Geom& g) {
   g.nty = (g.Y + g.TY - 1) / g.TY;
   g.ntz = (g.Z + g.TZ - 1) / g.TZ;
   g.ntiles = g.B * g.ntz * g.nty * g.ntx;
+  g.tz_lo = 0;
+  g.tz_hi = g.ntz;
+  g.nscale = g.Z * g.Y * g.X;
   if (g.ntiles >= (1ll << 32)) return fail(FASTRS_EINVAL, "grid too large");
   return FASTRS_OK;
 }
@@ -179,7 +182,7 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
   if (lt_out) cudaMemsetAsync(lt_out, 0, (size_t)g.N * 4, st);
 
   // K1..K3: EDT
-  launch_edt_x(labels, A, g, stage == kFull ? max_label : INT32_MAX, border, hdr, st);
+  launch_edt_x(labels, nullptr, A, g, stage == kFull ? max_label : INT32_MAX, border, hdr, st);
   tm.mark(0);
   uint32_t* D;
   if (g.ndim == 2) {
@@ -218,6 +221,69 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
   if (status & kStInternal) return fail(FASTRS_EINTERNAL, "device invariant violated: LT^2 < D");
   if (status & kStShell) return fail(FASTRS_EINTERNAL, "device invariant violated: shell mean LT > max LT or empty shell");
   return FASTRS_OK;
+}
+
+__global__ void k_set_dmax(WsHeader* hdr, uint32_t v) { hdr->dmax = v; }
+
+// copy one u32 of the header to a caller-owned device word
+int header_word_out(const WsHeader* hdr, const uint32_t* field, uint32_t* dst, cudaStream_t st) {
+  if (!dst) return FASTRS_OK;
+  (void)hdr;
+  cudaError_t e = cudaMemcpyAsync(dst, field, 4, cudaMemcpyDeviceToDevice, st);
+  return e == cudaSuccess ? FASTRS_OK : cuda_fail(e, "header copy");
+}
+
+// end of a call: optional sync + status mapping (shared by the slab phases)
+int finish_call(WsHeader* hdr, uint32_t flags, cudaStream_t st) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  if (flags & kFlagAsync) return FASTRS_OK;
+  uint32_t status = 0;
+  e = cudaMemcpyAsync(&status, &hdr->status, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "status read");
+  if (status & kStBadLabel) return fail(FASTRS_EINVAL, "a label is < 0 or > max_label");
+  if (status & kStNoSite)
+    return fail(FASTRS_ENOSITE, "an object element has no site (no other label and the border is not background)");
+  if (status & kStInternal) return fail(FASTRS_EINTERNAL, "device invariant violated: LT^2 < D");
+  if (status & kStShell) return fail(FASTRS_EINTERNAL, "device invariant violated: shell mean LT > max LT or empty shell");
+  return FASTRS_OK;
+}
+
+struct SlabLayout {
+  size_t hdr, P, meta, cent, total;
+};
+SlabLayout make_slab_layout(const Geom& g) {
+  SlabLayout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  L.hdr = take(256);
+  L.P = take((size_t)g.N * 4);
+  L.meta = take((size_t)g.ntiles * sizeof(TileMeta));
+  L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
+  L.total = off;
+  return L;
+}
+
+int slab_prologue(const int64_t* dims, Geom& g, SlabLayout& L, void* ws, size_t ws_bytes, WsHeader*& hdr,
+                  cudaStream_t st) {
+  int rc = make_geom(dims, 3, 1, g);
+  if (rc) return rc;
+  if (!ws) return fail(FASTRS_EINVAL, "workspace is NULL");
+  if (((uintptr_t)ws & 255) != 0) return fail(FASTRS_EINVAL, "workspace must be 256-byte aligned");
+  L = make_slab_layout(g);
+  if (ws_bytes < L.total) return fail(FASTRS_ENOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = ensure_mtables(dev);
+  if (e != cudaSuccess) return cuda_fail(e, "per-device setup");
+  hdr = (WsHeader*)((char*)ws + L.hdr);
+  e = cudaMemsetAsync(hdr, 0, 256, st);
+  return e == cudaSuccess ? FASTRS_OK : cuda_fail(e, "cudaMemsetAsync");
 }
 
 }  // namespace
@@ -349,5 +415,135 @@ int fastrs_profile_read(double* ms_out, int64_t* calls_out, int n_stages) {
 const char* fastrs_last_error(void) { return t_err.c_str(); }
 
 void fastrs_release(void) { release_mtables(); }
+
+// ---- z-slab multi-GPU path -----------------------------------------------------------------
+int fastrs_slab_workspace_bytes(const int64_t* dims_ext, size_t* bytes) {
+  Geom g;
+  int rc = make_geom(dims_ext, 3, 1, g);
+  if (rc) return rc;
+  if (!bytes) return fail(FASTRS_EINVAL, "bytes is NULL");
+  *bytes = make_slab_layout(g).total;
+  return FASTRS_OK;
+}
+
+int fastrs_slab_edt_xy(const int32_t* labels, const int32_t* labels_below, const int64_t* dims, int32_t max_label,
+                       uint32_t flags, uint32_t* packed_out, uint32_t* dxy_max, void* ws, size_t ws_bytes,
+                       void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  Geom g;
+  SlabLayout L;
+  WsHeader* hdr = nullptr;
+  int rc = slab_prologue(dims, g, L, ws, ws_bytes, hdr, st);
+  if (rc) return rc;
+  if (!labels || !packed_out) return fail(FASTRS_EINVAL, "NULL pointer");
+  uint32_t* tmp = (uint32_t*)((char*)ws + L.P);
+  const bool border = (flags & kFlagBorder) != 0;
+  launch_edt_x(labels, labels_below, tmp, g, max_label > 0 ? max_label : INT32_MAX, border, hdr, st);
+  launch_edt_col(tmp, packed_out, g, 1, false, border, hdr, st);
+  rc = header_word_out(hdr, &hdr->dxymax, dxy_max, st);
+  if (rc) return rc;
+  return finish_call(hdr, flags, st);
+}
+
+int fastrs_slab_edt_z(const uint32_t* packed_ext, const int64_t* dims_ext, int64_t own_lo, int64_t own_hi,
+                      int64_t z_ext0, int64_t Z, uint32_t flags, uint32_t* d_out, uint32_t* dmax_out, void* ws,
+                      size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  Geom g;
+  SlabLayout L;
+  WsHeader* hdr = nullptr;
+  int rc = slab_prologue(dims_ext, g, L, ws, ws_bytes, hdr, st);
+  if (rc) return rc;
+  if (!packed_ext || !d_out) return fail(FASTRS_EINVAL, "NULL pointer");
+  if (own_lo < 0 || own_hi > g.Z || own_lo >= own_hi || z_ext0 < 0 || z_ext0 + g.Z > Z)
+    return fail(FASTRS_EINVAL, "slab range outside the extended slab / the grid");
+  launch_edt_col(packed_ext, d_out, g, 2, true, (flags & kFlagBorder) != 0, hdr, st, own_lo, own_hi, z_ext0, Z);
+  rc = header_word_out(hdr, &hdr->dmax, dmax_out, st);
+  if (rc) return rc;
+  return finish_call(hdr, flags, st);
+}
+
+int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64_t* dims_ext, int64_t own_lo,
+                       int64_t own_hi, int64_t Z, uint32_t dmax_global, int32_t max_label, uint32_t flags,
+                       uint64_t* vol, uint64_t* n_shell, uint64_t* sum_lt, uint64_t* sum_shell_lt, uint32_t* max_lt2,
+                       void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  Geom g;
+  SlabLayout L;
+  WsHeader* hdr = nullptr;
+  int rc = slab_prologue(dims_ext, g, L, ws, ws_bytes, hdr, st);
+  if (rc) return rc;
+  if (!labels || !d_ext || !vol || !n_shell || !sum_lt || !sum_shell_lt || !max_lt2 || max_label < 1)
+    return fail(FASTRS_EINVAL, "NULL pointer or max_label < 1");
+  if (own_lo < 0 || own_hi > g.Z || own_lo >= own_hi || (own_lo % kTZ3) != 0 || ((own_hi % kTZ3) != 0 && own_hi != g.Z))
+    return fail(FASTRS_EINVAL, "own slab range must be tile aligned (multiples of 8 slices) inside the extended slab");
+  g.tz_lo = own_lo / kTZ3;
+  g.tz_hi = (own_hi + kTZ3 - 1) / kTZ3;
+  g.nscale = Z * g.Y * g.X;
+  const int64_t M = max_label;
+  cudaError_t e = cudaSuccess;
+  for (void* a : {(void*)vol, (void*)n_shell, (void*)sum_lt, (void*)sum_shell_lt})
+    if (e == cudaSuccess) e = cudaMemsetAsync(a, 0, (size_t)M * 8, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(max_lt2, 0, (size_t)M * 4, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  k_set_dmax<<<1, 1, 0, st>>>(hdr, dmax_global);
+  TileMeta* meta = (TileMeta*)((char*)ws + L.meta);
+  uint2* cent = (uint2*)((char*)ws + L.cent);
+  launch_prune(d_ext, g, meta, cent, hdr, st);
+  Accum acc{};
+  acc.vol = (unsigned long long*)vol;
+  acc.nshell = (unsigned long long*)n_shell;
+  acc.sum = (unsigned long long*)sum_lt;
+  acc.sumshell = (unsigned long long*)sum_shell_lt;
+  acc.maxlt2 = max_lt2;
+  acc.M = M;
+  acc.max_label = max_label;
+  // the epilogue indexes labels in the extended layout: shift the own-slab pointer (only own
+  // elements are ever read)
+  const int32_t* lab_ext = labels - own_lo * g.Y * g.X;
+  launch_dilate(lab_ext, d_ext, meta, cent, g, &acc, nullptr, nullptr, (flags & kFlagForceFallback) != 0, hdr, st);
+  return finish_call(hdr, flags, st);
+}
+
+int fastrs_metrics_from_partials(const uint64_t* vol, const uint64_t* n_shell, const uint64_t* sum_lt,
+                                 const uint64_t* sum_shell_lt, const uint32_t* max_lt2, int64_t n_labels, int ndim,
+                                 int64_t nscale, uint32_t dmax_global, double* sphericity, double* roundness,
+                                 const fastrs_object_stats* stats, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!vol || !n_shell || !sum_lt || !sum_shell_lt || !max_lt2 || n_labels < 1 || nscale < 1)
+    return fail(FASTRS_EINVAL, "NULL pointer or empty sizes");
+  if (ndim != 2 && ndim != 3) return fail(FASTRS_EINVAL, "ndim must be 2 or 3");
+  if (!ws || ws_bytes < 256 || ((uintptr_t)ws & 255) != 0) return fail(FASTRS_ENOMEM, "workspace must be >= 256 aligned bytes");
+  WsHeader* hdr = (WsHeader*)ws;
+  cudaError_t e = cudaMemsetAsync(hdr, 0, 256, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  k_set_dmax<<<1, 1, 0, st>>>(hdr, dmax_global);
+  Accum acc{};
+  acc.vol = (unsigned long long*)vol;
+  acc.nshell = (unsigned long long*)n_shell;
+  acc.sum = (unsigned long long*)sum_lt;
+  acc.sumshell = (unsigned long long*)sum_shell_lt;
+  acc.maxlt2 = (uint32_t*)max_lt2;
+  acc.M = n_labels;
+  acc.max_label = (int32_t)n_labels;
+  Outputs o{};
+  o.sphericity = sphericity;
+  o.roundness = roundness;
+  if (stats) {
+    o.volume = stats->volume;
+    o.n_shell = stats->n_shell;
+    o.max_lt2 = stats->max_lt2;
+    o.mean_lt = stats->mean_lt;
+    o.max_lt = stats->max_lt;
+    o.shell_mean_lt = stats->shell_mean_lt;
+    o.axis_a = stats->axis_a;
+    o.axis_cb = stats->axis_cb;
+  }
+  Geom g{};
+  g.ndim = ndim;
+  g.nscale = nscale;
+  launch_metrics(acc, g, o, hdr, st);
+  return finish_call(hdr, 0, st);
+}
 
 }  // extern "C"

@@ -22,6 +22,7 @@ constexpr uint32_t kFlagBorder = 1u, kFlagAsync = 4u, kFlagHostIO = 8u, kFlagFor
 constexpr int kTX = 32;
 constexpr int kTileVol = 2048;
 constexpr int kRows = 64;
+constexpr int kTZ3 = 8;                 // 3D tile extent along z (slab alignment unit)
 constexpr int kLevels = 6;              // sparse-table levels for 32-wide rows: 1..32
 constexpr int kRowStride = kLevels * 32 + 1;  // +1: rows start in different banks
 
@@ -37,6 +38,8 @@ struct Geom {
   int64_t N;           // B*Z*Y*X
   int TY, TZ;          // tile extents (3D: 8,8; 2D: 64,1)
   int64_t ntx, nty, ntz, ntiles;  // tile grid per item: ntz*nty*ntx, ntiles includes B
+  int64_t tz_lo, tz_hi;           // tile layers whose LT / reductions are produced (slab path)
+  int64_t nscale;                 // elements per item for the fixed-point scale (global volume)
 };
 
 struct WsHeader {
@@ -47,7 +50,8 @@ struct WsHeader {
   unsigned long long n_intervals;
   int32_t scale_log2;
   uint32_t n_fallback;  // tile groups handed to the atomic fallback dilation
-  int32_t pad[6];
+  uint32_t dxymax;      // max partial D after the y pass (slab path: the z halo width)
+  int32_t pad[5];
 };
 static_assert(sizeof(WsHeader) <= 256, "header");
 
@@ -120,10 +124,14 @@ __host__ __device__ inline uint32_t dbucket_max(int b) {
 }
 
 // ---- kernel launchers (stream-ordered) -----------------------------------------------
-void launch_edt_x(const int32_t* labels, uint32_t* out, const Geom& g, int32_t max_label,
-                  bool border, WsHeader* hdr, cudaStream_t st);
+void launch_edt_x(const int32_t* labels, const int32_t* labels_below, uint32_t* out, const Geom& g,
+                  int32_t max_label, bool border, WsHeader* hdr, cudaStream_t st);
+// Column pass along axis 1 (y) or 2 (z) of g.  Positions [p_lo, p_hi) of the axis are written,
+// to out + (p - p_lo) * stride; gofs / Lg: global position of local 0 and the global axis length
+// (the border convention applies at global 0 and Lg).  Default: p_lo = 0, p_hi = L, gofs = 0.
 void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, bool final_pass,
-                    bool border, WsHeader* hdr, cudaStream_t st);
+                    bool border, WsHeader* hdr, cudaStream_t st, int64_t p_lo = 0, int64_t p_hi = -1,
+                    int64_t gofs = 0, int64_t Lg = -1);
 cudaError_t ensure_mtables(int device);  // builds the per-device lattice tables (sync, once)
 void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, WsHeader* hdr,
                   cudaStream_t st);

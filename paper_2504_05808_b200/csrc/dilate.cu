@@ -200,7 +200,9 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const int32_t* 
   if (dmax > kU16Max) return;  // k_dilate_atomic handles it
 
   // ---- group / tile coordinates --------------------------------------------------------
-  const int64_t ngx = (g.ntx + P::GX - 1) / P::GX, ngy = (g.nty + P::GY - 1) / P::GY, ngz = (g.ntz + P::GZ - 1) / P::GZ;
+  // groups tile the layers [tz_lo, tz_hi) (all layers except on the slab path)
+  const int64_t ngx = (g.ntx + P::GX - 1) / P::GX, ngy = (g.nty + P::GY - 1) / P::GY;
+  const int64_t ngz = (g.tz_hi - g.tz_lo + P::GZ - 1) / P::GZ;
   int64_t t = blockIdx.x;
   const int64_t gxi = t % ngx;
   t /= ngx;
@@ -208,11 +210,11 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const int32_t* 
   t /= ngy;
   const int64_t gzi = t % ngz;
   const int64_t b = t / ngz;
-  const int64_t tx0 = gxi * P::GX, ty0 = gyi * P::GY, tz0 = gzi * P::GZ;
+  const int64_t tx0 = gxi * P::GX, ty0 = gyi * P::GY, tz0 = g.tz_lo + gzi * P::GZ;
   const int64_t rox = tx0 * kTX, roy = ty0 * TY, roz = tz0 * TZ;  // group origin
   const int wx = warp % P::GX, wy = (warp / P::GX) % P::GY, wz = warp / (P::GX * P::GY);
   const int64_t mtx = tx0 + wx, mty = ty0 + wy, mtz = tz0 + wz;
-  const bool have_tile = mtx < g.ntx && mty < g.nty && mtz < g.ntz;
+  const bool have_tile = mtx < g.ntx && mty < g.nty && mtz < g.tz_hi;
   const int64_t mtile = have_tile ? ((b * g.ntz + mtz) * g.nty + mty) * g.ntx + mtx : 0;
   const int mox = wx * kTX, moy = wy * TY, moz = wz * TZ;  // my tile origin within the group
   const bool active = have_tile && meta[mtile].nfg != 0;
@@ -546,7 +548,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const int32_t* 
   if (!active) return;
 
   // ---- epilogue: my tile ------------------------------------------------------------------
-  const int scale_log2 = sum_scale_log2(g.Z * g.Y * g.X, dmax);
+  const int scale_log2 = sum_scale_log2(g.nscale, dmax);
   const double scale = ldexp(1.0, scale_log2);
   uint32_t bad = 0;
   for (int row = 0; row < kRows; ++row) {
@@ -570,7 +572,8 @@ void launch_dilate_cover(const int32_t* labels, const uint32_t* D, TileMeta* met
                          const Geom& g, const Accum& a, int do_reduce, int force_fallback, uint32_t* lt2_out,
                          float* lt_out, WsHeader* hdr, cudaStream_t st) {
   const int GX = g.ndim == 3 ? 1 : 2, GY = 2, GZ = g.ndim == 3 ? 2 : 1;
-  const int64_t ngroups = g.B * ((g.ntx + GX - 1) / GX) * ((g.nty + GY - 1) / GY) * ((g.ntz + GZ - 1) / GZ);
+  const int64_t ngroups = g.B * ((g.ntx + GX - 1) / GX) * ((g.nty + GY - 1) / GY) * ((g.tz_hi - g.tz_lo + GZ - 1) / GZ);
+  if (ngroups <= 0) return;
   const size_t smem = sizeof(Smem);
   if (g.ndim == 3)
     k_dilate_cover<true><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(labels, D, meta, centres, g, a, do_reduce, force_fallback,

@@ -25,7 +25,8 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
-__global__ void __launch_bounds__(256) k_edt_x(const int32_t* __restrict__ lab, uint32_t* __restrict__ out,
+__global__ void __launch_bounds__(256) k_edt_x(const int32_t* __restrict__ lab,
+                                               const int32_t* __restrict__ below, uint32_t* __restrict__ out,
                                                int64_t nrows, int X, int64_t Y, int64_t Z,
                                                int32_t max_label, int border, int is3d,
                                                WsHeader* __restrict__ hdr) {
@@ -39,7 +40,8 @@ __global__ void __launch_bounds__(256) k_edt_x(const int32_t* __restrict__ lab, 
   const int64_t z = (row / Y) % Z;
   const int32_t* L = lab + row * X;
   const int32_t* Ly = y > 0 ? L - X : nullptr;
-  const int32_t* Lz = (is3d && z > 0) ? L - X * Y : nullptr;
+  // z-1 neighbour: the previous slice, or (slab path) the caller's slice just below the slab
+  const int32_t* Lz = is3d ? (z > 0 ? L - X * Y : (below ? below + y * X : nullptr)) : nullptr;
   uint32_t* O = out + row * X;
   const int nchunk = (X + 31) >> 5;
 
@@ -105,7 +107,8 @@ template <bool FINAL>
 __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                                                  int64_t L, int64_t astride, int X, int nxb, int nseg,
                                                  int64_t n_inner, int64_t inner_mult, int64_t outer_mult,
-                                                 uint32_t chbit, int border, WsHeader* __restrict__ hdr) {
+                                                 uint32_t chbit, int border, int64_t p_lo, int64_t p_hi,
+                                                 int64_t gofs, int64_t Lg, WsHeader* __restrict__ hdr) {
   __shared__ uint32_t tile[kColRows * 32];
   int64_t bid = blockIdx.x;
   const int xb = (int)(bid % nxb);
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t base = (outer / n_inner) * outer_mult + (outer % n_inner) * inner_mult + (int64_t)xb * 32 + lane;
   const bool xin = xb * 32 + lane < X;
-  const int64_t s0 = (int64_t)seg * kColS;
+  const int64_t s0 = p_lo + (int64_t)seg * kColS;
   const int64_t lo = s0 - kColH > 0 ? s0 - kColH : 0;
   const int64_t hi = s0 + kColS + kColH < L ? s0 + kColS + kColH : L;
   for (int64_t r = lo + warp; r < hi; r += kColWarps)
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
   __syncthreads();
 
   uint32_t dmax = 0, nfg = 0, nosite = 0;
-  const int64_t pend = s0 + kColS < L ? s0 + kColS : L;
+  const int64_t pend = s0 + kColS < p_hi ? s0 + kColS : p_hi;
   for (int64_t p = s0 + warp; p < pend; p += kColWarps) {
     const uint32_t v = tile[(p - lo) * 32 + lane];
     const uint32_t g = v & kMask;
@@ -135,8 +138,8 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
         uint32_t dq = 1, dq2 = 1;
         int64_t q = p + 1;
         while (dq2 < best) {
-          if (q >= L) {
-            if (border) best = min(best, dq2);
+          if (q >= L) {  // end of the staged axis: the grid end (slab path: h^2 >= D guarantees it)
+            if (border && gofs + q >= Lg) best = min(best, dq2);
             break;
           }
           const uint32_t w = q < hi ? tile[(q - lo) * 32 + lane] : __ldg(in + base + q * astride);
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
         int64_t q = p - 1;
         while (dq2 < best) {
           if (chk) {
-            if (q >= 0 || border) best = min(best, dq2);
+            if (gofs + q >= 0 || border) best = min(best, dq2);
             break;
           }
           const uint32_t w = q >= lo ? tile[(q - lo) * 32 + lane] : __ldg(in + base + q * astride);
@@ -167,18 +170,21 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
           --q;
         }
       }
+      dmax = max(dmax, best);
       if (FINAL) {
         res = best;
-        dmax = max(dmax, best);
         nfg += 1;
         nosite |= best >= kInf;
       } else {
         res = best | (v & (kBitY | kBitZ));
       }
     }
-    if (xin) out[base + p * astride] = res;
+    if (xin) out[base + (p - p_lo) * astride] = res;
   }
-  if (FINAL) {
+  if (!FINAL) {  // the max partial distance bounds the next pass's window (slab z halo)
+    dmax = __reduce_max_sync(kFull, dmax);
+    if (lane == 0 && dmax) atomicMax(&hdr->dxymax, dmax);
+  } else {
     dmax = __reduce_max_sync(kFull, dmax);
     nfg = __reduce_add_sync(kFull, nfg);
     nosite = __any_sync(kFull, nosite);
@@ -192,20 +198,20 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
 
 }  // namespace
 
-void launch_edt_x(const int32_t* labels, uint32_t* out, const Geom& g, int32_t max_label, bool border,
-                  WsHeader* hdr, cudaStream_t st) {
+void launch_edt_x(const int32_t* labels, const int32_t* labels_below, uint32_t* out, const Geom& g,
+                  int32_t max_label, bool border, WsHeader* hdr, cudaStream_t st) {
   const int64_t nrows = g.B * g.Z * g.Y;
   int warps = (int)(49152 / (2 * g.X));
   warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
   const size_t smem = (size_t)warps * g.X * sizeof(uint16_t);
   const int64_t blocks = (nrows + warps - 1) / warps;
-  k_edt_x<<<(unsigned)blocks, warps * 32, smem, st>>>(labels, out, nrows, (int)g.X, g.Y, g.Z, max_label,
+  k_edt_x<<<(unsigned)blocks, warps * 32, smem, st>>>(labels, labels_below, out, nrows, (int)g.X, g.Y, g.Z, max_label,
                                                       border ? 1 : 0, g.ndim == 3 ? 1 : 0, hdr);
 }
 
 // axis 1 = y, axis 2 = z.
 void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, bool final_pass, bool border,
-                    WsHeader* hdr, cudaStream_t st) {
+                    WsHeader* hdr, cudaStream_t st, int64_t p_lo, int64_t p_hi, int64_t gofs, int64_t Lg) {
   int64_t L, astride, n_outer, n_inner, inner_mult, outer_mult;
   uint32_t chbit;
   if (axis == 1) {
@@ -225,15 +231,18 @@ void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, 
     outer_mult = g.Z * g.Y * g.X;
     chbit = kBitZ;
   }
+  if (p_hi < 0) p_hi = L;
+  if (Lg < 0) Lg = L;
   const int nxb = (int)((g.X + 31) / 32);
-  const int nseg = (int)((L + kColS - 1) / kColS);
+  const int nseg = (int)((p_hi - p_lo + kColS - 1) / kColS);
+  if (nseg <= 0) return;
   const int64_t blocks = (int64_t)nxb * nseg * n_outer;
   if (final_pass)
     k_edt_col<true><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(in, out, L, astride, (int)g.X, nxb, nseg, n_inner,
-                                                                  inner_mult, outer_mult, chbit, border ? 1 : 0, hdr);
+                                                                  inner_mult, outer_mult, chbit, border ? 1 : 0, p_lo, p_hi, gofs, Lg, hdr);
   else
     k_edt_col<false><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(in, out, L, astride, (int)g.X, nxb, nseg, n_inner,
-                                                                   inner_mult, outer_mult, chbit, border ? 1 : 0, hdr);
+                                                                   inner_mult, outer_mult, chbit, border ? 1 : 0, p_lo, p_hi, gofs, Lg, hdr);
 }
 
 }  // namespace fastrs

@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(256) k_dilate_atomic(const int32_t* __restrict
   t /= g.nty;
   const int64_t tz = t % g.ntz;
   const int64_t b = t / g.ntz;
+  if (tz < g.tz_lo || tz >= g.tz_hi) return;  // slab path: halo tiles only feed the gather
   const int64_t ox = tx * kTX, oy = ty * TY, oz = tz * TZ;
 
   for (int i = tid; i < kRows * kRowStride; i += 256) T[i] = 0;
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(256) k_dilate_atomic(const int32_t* __restrict
   }
 
   // push-down + epilogue, one warp per row
-  const int scale_log2 = sum_scale_log2(g.Z * g.Y * g.X, dmax);
+  const int scale_log2 = sum_scale_log2(g.nscale, dmax);
   const double scale = ldexp(1.0, scale_log2);
   const int64_t item = b * g.Z * g.Y * g.X;
   uint32_t bad = 0;

@@ -58,7 +58,7 @@ __global__ void k_metrics(Accum acc, Outputs o, int ndim, int64_t Nb, WsHeader* 
 
 void launch_metrics(const Accum& acc, const Geom& g, const Outputs& o, WsHeader* hdr, cudaStream_t st) {
   const int64_t blocks = (acc.M + 255) / 256;
-  k_metrics<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(acc, o, g.ndim, g.Z * g.Y * g.X, hdr);
+  k_metrics<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(acc, o, g.ndim, g.nscale, hdr);
 }
 
 }  // namespace fastrs

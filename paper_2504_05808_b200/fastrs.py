@@ -75,8 +75,16 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
                 f = getattr(lib, "fastrs_" + n)
                 f.argtypes = [cd, cd]
                 f.restype = cd
+            lib.fastrs_slab_workspace_bytes.argtypes = [vp, ctypes.POINTER(sz)]
+            lib.fastrs_slab_edt_xy.argtypes = [vp, vp, vp, i32, u32, vp, vp, vp, sz, vp]
+            lib.fastrs_slab_edt_z.argtypes = [vp, vp, i64, i64, i64, i64, u32, vp, vp, vp, sz, vp]
+            lib.fastrs_slab_reduce.argtypes = [vp, vp, vp, i64, i64, i64, u32, i32, u32, vp, vp, vp, vp, vp, vp,
+                                               sz, vp]
+            lib.fastrs_metrics_from_partials.argtypes = [vp, vp, vp, vp, vp, i64, ci, i64, u32, vp, vp, vp, vp,
+                                                         sz, vp]
             for n in ("workspace_bytes", "edt_sq", "local_thickness", "sphericity_roundness",
-                      "sphericity_roundness_host", "read_diagnostics", "profile_read"):
+                      "sphericity_roundness_host", "read_diagnostics", "profile_read", "slab_workspace_bytes",
+                      "slab_edt_xy", "slab_edt_z", "slab_reduce", "metrics_from_partials"):
                 getattr(lib, "fastrs_" + n).restype = ci
             _lib = lib
     return _lib
@@ -245,6 +253,92 @@ def profile_read() -> tuple[dict, int]:
     calls = ctypes.c_int64(0)
     load().fastrs_profile_read(ms, ctypes.byref(calls), len(STAGES))
     return {s: ms[i] for i, s in enumerate(STAGES)}, calls.value
+
+
+# ------------------------------------------------------------------------------------------
+# z-slab phases (include/fastrs.h "multi-GPU z-slab path"); slab.py orchestrates them
+# ------------------------------------------------------------------------------------------
+
+PARTIAL_KEYS = ("vol", "n_shell", "sum_lt", "sum_shell_lt", "max_lt2")
+
+
+def _dims3(shape):
+    return (ctypes.c_int64 * 3)(*[int(v) for v in shape])
+
+
+def slab_workspace(dims_ext, device) -> torch.Tensor:
+    out = ctypes.c_size_t(0)
+    _check(load().fastrs_slab_workspace_bytes(_dims3(dims_ext), ctypes.byref(out)))
+    return workspace(out.value, device)
+
+
+def _ptr_or_none(t):
+    return None if t is None else t.data_ptr()
+
+
+def slab_edt_xy(labels: torch.Tensor, labels_below, max_label: int, flags=BORDER_BACKGROUND, ws=None):
+    """Phase A: x/y passes of the own slab.  Returns (packed int32 [nz,Y,X], dxy_max int32[1])."""
+    labels = _labels_arg(labels)
+    packed = torch.empty_like(labels)
+    dxy = torch.zeros(1, dtype=torch.int32, device=labels.device)
+    ws = slab_workspace(labels.shape, labels.device) if ws is None else ws
+    below = None if labels_below is None else _labels_arg(labels_below)
+    _check(load().fastrs_slab_edt_xy(labels.data_ptr(), _ptr_or_none(below), _dims3(labels.shape), int(max_label),
+                                     flags, packed.data_ptr(), dxy.data_ptr(), ws.data_ptr(), ws.numel(),
+                                     _stream(labels.device)))
+    return packed, dxy
+
+
+def slab_edt_z(packed_ext: torch.Tensor, own_lo: int, own_hi: int, z_ext0: int, Z: int, flags=BORDER_BACKGROUND,
+               out=None, ws=None):
+    """Phase B: z pass over the h-extended slab.  Returns (D int32 [own_hi-own_lo,Y,X], dmax int32[1])."""
+    packed_ext = packed_ext.contiguous()
+    _, Y, X = packed_ext.shape
+    d = torch.empty((own_hi - own_lo, Y, X), dtype=torch.int32, device=packed_ext.device) if out is None else out
+    dmax = torch.zeros(1, dtype=torch.int32, device=packed_ext.device)
+    ws = slab_workspace(packed_ext.shape, packed_ext.device) if ws is None else ws
+    _check(load().fastrs_slab_edt_z(packed_ext.data_ptr(), _dims3(packed_ext.shape), own_lo, own_hi, z_ext0, Z,
+                                    flags, d.data_ptr(), dmax.data_ptr(), ws.data_ptr(), ws.numel(),
+                                    _stream(packed_ext.device)))
+    return d, dmax
+
+
+def slab_reduce(labels: torch.Tensor, d_ext: torch.Tensor, own_lo: int, own_hi: int, Z: int, dmax_global: int,
+                max_label: int, flags=BORDER_BACKGROUND, ws=None) -> dict:
+    """Phase C: prune + dilation + shell + partial per-label sums of the own slab.  Returns
+    int64 tensors vol, n_shell, sum_lt, sum_shell_lt (u64 bit patterns) and int32 max_lt2."""
+    labels = _labels_arg(labels)
+    d_ext = d_ext.contiguous()
+    dev = labels.device
+    part = {k: torch.empty(max_label, dtype=torch.int64, device=dev) for k in PARTIAL_KEYS[:4]}
+    part["max_lt2"] = torch.empty(max_label, dtype=torch.int32, device=dev)
+    ws = slab_workspace(d_ext.shape, dev) if ws is None else ws
+    _check(load().fastrs_slab_reduce(labels.data_ptr(), d_ext.data_ptr(), _dims3(d_ext.shape), own_lo, own_hi, Z,
+                                     int(dmax_global), int(max_label), flags,
+                                     *[part[k].data_ptr() for k in PARTIAL_KEYS], ws.data_ptr(), ws.numel(),
+                                     _stream(dev)))
+    return part
+
+
+def metrics_from_partials(part: dict, ndim: int, nscale: int, dmax_global: int, stats=False, ws=None) -> dict:
+    """Phase D: closed forms per label from (reduced) partials."""
+    dev = part["vol"].device
+    M = part["vol"].numel()
+    res = {"sphericity": torch.empty(M, dtype=torch.float64, device=dev),
+           "roundness": torch.empty(M, dtype=torch.float64, device=dev)}
+    st = None
+    if stats:
+        for k, dt in (("volume", torch.int64), ("n_shell", torch.int64), ("max_lt2", torch.int32),
+                      ("mean_lt", torch.float64), ("max_lt", torch.float64), ("shell_mean_lt", torch.float64),
+                      ("axis_a", torch.float64), ("axis_cb", torch.float64)):
+            res[k] = torch.empty(M, dtype=dt, device=dev)
+        st = _Stats(*[res[n].data_ptr() for n, _ in _Stats._fields_])
+    ws = workspace(256, dev) if ws is None else ws
+    _check(load().fastrs_metrics_from_partials(*[part[k].contiguous().data_ptr() for k in PARTIAL_KEYS], M, ndim,
+                                               int(nscale), int(dmax_global), res["sphericity"].data_ptr(),
+                                               res["roundness"].data_ptr(), None if st is None else ctypes.byref(st),
+                                               ws.data_ptr(), ws.numel(), _stream(dev)))
+    return res
 
 
 def spheroid_area(a, c):
