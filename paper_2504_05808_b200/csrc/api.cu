@@ -199,8 +199,9 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
   if (stage != kEdtOnly) {
     launch_prune(D, g, meta, cent, hdr, st);  // K4
     tm.mark(3);
+    uint32_t* ltp = D == A ? B : A;  // the plane the EDT no longer needs holds LT^2
     launch_dilate(labels, D, meta, cent, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out,
-                  (flags & kFlagForceFallback) != 0, hdr, st);  // K5
+                  (flags & kFlagForceFallback) != 0, ltp, hdr, st);  // K5
     tm.mark(4);
     if (stage == kFull) {
       launch_metrics(acc, g, *outs, hdr, st);  // K6
@@ -501,7 +502,8 @@ int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64
   // the epilogue indexes labels in the extended layout: shift the own-slab pointer (only own
   // elements are ever read)
   const int32_t* lab_ext = labels - own_lo * g.Y * g.X;
-  launch_dilate(lab_ext, d_ext, meta, cent, g, &acc, nullptr, nullptr, (flags & kFlagForceFallback) != 0, hdr, st);
+  uint32_t* ltp = (uint32_t*)((char*)ws + L.P);
+  launch_dilate(lab_ext, d_ext, meta, cent, g, &acc, nullptr, nullptr, (flags & kFlagForceFallback) != 0, ltp, hdr, st);
   return finish_call(hdr, flags, st);
 }
 

@@ -137,7 +137,7 @@ void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centr
                   cudaStream_t st);
 void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta,
                    const uint2* centres, const Geom& g, const Accum* acc, uint32_t* lt2_out,
-                   float* lt_out, bool force_fallback, WsHeader* hdr, cudaStream_t st);
+                   float* lt_out, bool force_fallback, uint32_t* ltp, WsHeader* hdr, cudaStream_t st);
 void launch_metrics(const Accum& acc, const Geom& g, const Outputs& o, WsHeader* hdr,
                     cudaStream_t st);
 void release_mtables();

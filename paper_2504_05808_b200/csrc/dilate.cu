@@ -24,6 +24,8 @@
 // The pathological case (a single bucket exceeding the list or the sort range) hands the
 // group to the atomic sparse-table kernel k_dilate_atomic (lt.cu), which also handles
 // Dmax > 65535 (FASTRS_FORCE_FALLBACK sends every tile there: a GPU-internal cross-check).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "dilate_common.cuh"
 
@@ -184,13 +186,11 @@ __device__ __forceinline__ unsigned long long row_box(int ya, int yb, int za, in
 }
 
 template <bool IS3D>
-__global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const int32_t* __restrict__ lab,
-                                                             const uint32_t* __restrict__ Dg,
-                                                             TileMeta* __restrict__ meta,
-                                                             const uint2* __restrict__ cent, Geom g, Accum acc,
-                                                             int do_reduce, int force_fallback,
-                                                             uint32_t* __restrict__ lt2_out,
-                                                             float* __restrict__ lt_out, WsHeader* __restrict__ hdr) {
+__global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t* __restrict__ Dg,
+                                                                TileMeta* __restrict__ meta,
+                                                                const uint2* __restrict__ cent, Geom g,
+                                                                int force_fallback, int point_at,
+                                                                uint32_t* __restrict__ ltp, WsHeader* __restrict__ hdr) {
   using P = Shape<IS3D>;
   constexpr int TY = P::TY, TZ = P::TZ;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -265,6 +265,18 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const int32_t* 
   int nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(fgw[lane]) + __popc(fgw[lane + 32])));
   bool pmode = false;
   uint16_t* ulist = S.ulist[warp];
+  int ub[6] = {0, kTX - 1, 0, TY - 1, 0, TZ - 1};  // bounding box of the uncovered cells (point mode)
+  auto ubox_refresh = [&]() {
+    int x0 = 1 << 20, x1 = -1, y0 = 1 << 20, y1 = -1, z0 = 1 << 20, z1 = -1;
+    for (int q = lane; q < nu; q += 32) {
+      const int e = ulist[q], x = e & 31, row = e >> 5;
+      const int ly = IS3D ? (row & 7) : row, lz = IS3D ? (row >> 3) : 0;
+      x0 = min(x0, x); x1 = max(x1, x); y0 = min(y0, ly); y1 = max(y1, ly); z0 = min(z0, lz); z1 = max(z1, lz);
+    }
+    ub[0] = __reduce_min_sync(kFull, x0); ub[1] = __reduce_max_sync(kFull, x1);
+    ub[2] = __reduce_min_sync(kFull, y0); ub[3] = __reduce_max_sync(kFull, y1);
+    ub[4] = __reduce_min_sync(kFull, z0); ub[5] = __reduce_max_sync(kFull, z1);
+  };
 
   const int rmax = dmax > 0 ? isqrt16((int)(dmax - 1)) : 0;
   const int nrx = (rmax + kTX - 1) / kTX, nry = (rmax + TY - 1) / TY, nrz = IS3D ? (rmax + TZ - 1) / TZ : 0;
@@ -400,7 +412,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const int32_t* 
     // final value: each cell is written once and coverage is updated immediately.
     for (uint32_t i0 = 0; i0 < total && nu != 0; i0 += 32) {
       const uint32_t i = i0 + lane;
-      if (!pmode && nu <= kPoint) {
+      if (!pmode && nu <= point_at) {
         // switch to point mode: list the still-uncovered cells
         uint32_t left[2];
 #pragma unroll
@@ -424,6 +436,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const int32_t* 
         }
         pmode = true;
         __syncwarp();
+        ubox_refresh();
       }
       if (pmode) {
         // point tests: lanes = the next 32 balls (descending D), loop over the uncovered cells;
@@ -435,7 +448,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const int32_t* 
           cx = (int)((e >> 16) & 0xFFFFu) - kOff - mox;
           cy = (int)((e >> 32) & 0xFFFFu) - kOff - moy;
           cz = (int)((e >> 48) & 0xFFFFu) - kOff - moz;
-          const int ddx = gap(0, kTX - 1, cx), ddy = gap(0, TY - 1, cy), ddz = gap(0, TZ - 1, cz);
+          // the ball must reach the bounding box of the still-uncovered cells
+          const int ddx = gap(ub[0], ub[1], cx), ddy = gap(ub[2], ub[3], cy), ddz = gap(ub[4], ub[5], cz);
           if (ddx * ddx + ddy * ddy + ddz * ddz > D - 1) D = 0;
         }
         if (__ballot_sync(kFull, D != 0) == 0) continue;
@@ -469,6 +483,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const int32_t* 
             __syncwarp();
           }
           nu = (int)newn;
+          __syncwarp();
+          ubox_refresh();
         }
         continue;
       }
@@ -547,40 +563,39 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const int32_t* 
   }
   if (!active) return;
 
-  // ---- epilogue: my tile ------------------------------------------------------------------
-  const int scale_log2 = sum_scale_log2(g.nscale, dmax);
-  const double scale = ldexp(1.0, scale_log2);
-  uint32_t bad = 0;
+  // ---- my tile's LT^2 -> the LT plane (coalesced rows); shell and reductions run in the
+  // streaming epilogue kernel (lt.cu), at full occupancy
+  const int64_t gx = rox + mox + lane;
   for (int row = 0; row < kRows; ++row) {
     const int ly = row % TY, lz = row / TY;
-    const int64_t gz = roz + moz + lz, gy = roy + moy + ly, gx = rox + mox + lane;
-    if (gz >= g.Z || gy >= g.Y) continue;  // warp-uniform
-    const uint32_t c = val[row * 32 + lane];
-    bad |= row_epilogue(c, lane, gx < g.X, item + (gz * g.Y + gy) * g.X + gx, b, lab, Dg, acc, do_reduce, scale,
-                        lt2_out, lt_out);
+    const int64_t gz = roz + moz + lz, gy = roy + moy + ly;
+    if (gz < g.Z && gy < g.Y && gx < g.X) ltp[item + (gz * g.Y + gy) * g.X + gx] = val[row * 32 + lane];
   }
   n_rows = __reduce_add_sync(kFull, n_rows);
   if (lane == 0 && n_rows) atomicAdd(&hdr->n_intervals, (unsigned long long)n_rows);
-  if (bad) atomicOr(&hdr->status, kStInternal);
 }
 
 }  // namespace
 
 size_t dilate_cover_smem() { return sizeof(Smem); }
 
-void launch_dilate_cover(const int32_t* labels, const uint32_t* D, TileMeta* meta, const uint2* centres,
-                         const Geom& g, const Accum& a, int do_reduce, int force_fallback, uint32_t* lt2_out,
-                         float* lt_out, WsHeader* hdr, cudaStream_t st) {
+void launch_dilate_cover(const uint32_t* D, TileMeta* meta, const uint2* centres, const Geom& g, int force_fallback,
+                         uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
   const int GX = g.ndim == 3 ? 1 : 2, GY = 2, GZ = g.ndim == 3 ? 2 : 1;
   const int64_t ngroups = g.B * ((g.ntx + GX - 1) / GX) * ((g.nty + GY - 1) / GY) * ((g.tz_hi - g.tz_lo + GZ - 1) / GZ);
   if (ngroups <= 0) return;
   const size_t smem = sizeof(Smem);
+  static const int point_at = [] {
+    const char* v = getenv("FASTRS_POINT_AT");  // development knob (default 128 = kPoint)
+    const int p = v ? atoi(v) : kPoint;
+    return p < 0 ? 0 : (p > kPoint ? kPoint : p);
+  }();
   if (g.ndim == 3)
-    k_dilate_cover<true><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(labels, D, meta, centres, g, a, do_reduce, force_fallback,
-                                                                        lt2_out, lt_out, hdr);
+    k_dilate_cover<true><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(D, meta, centres, g, force_fallback, point_at,
+                                                                        ltp, hdr);
   else
-    k_dilate_cover<false><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(labels, D, meta, centres, g, a, do_reduce, force_fallback,
-                                                                         lt2_out, lt_out, hdr);
+    k_dilate_cover<false><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(D, meta, centres, g, force_fallback,
+                                                                         point_at, ltp, hdr);
 }
 
 cudaError_t dilate_cover_setup() {

@@ -8,26 +8,21 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr uint32_t kU16Max = 65535u;
 
 // Shell + per-label reductions + optional LT writes for one 32-wide row held in a warp
-// (lane = x), given each lane's LT^2 `c`.  Returns 1 if the invariant LT^2 >= D failed.
-static __device__ __forceinline__ uint32_t row_epilogue(uint32_t c, int lane, bool valid, int64_t gi, int64_t b,
-                                                 const int32_t* __restrict__ lab, const uint32_t* __restrict__ Dg,
-                                                 const Accum& acc, int do_reduce, double scale,
-                                                 uint32_t* __restrict__ lt2_out, float* __restrict__ lt_out) {
+// (lane = x), given each lane's LT^2 `c`, label L and squared distance d (L = 0 outside the
+// grid).  Returns 1 if the invariant LT^2 >= D failed.
+static __device__ __forceinline__ uint32_t row_epilogue_v(uint32_t c, int32_t L, uint32_t d, int lane, int64_t gi,
+                                                   int64_t b, const Accum& acc, int do_reduce, double scale,
+                                                   uint32_t* __restrict__ lt2_out, float* __restrict__ lt_out) {
   uint32_t bad = 0;
-  int32_t L = 0;
   bool shell = false;
   unsigned long long fx = 0;
-  if (valid) {
-    L = __ldg(lab + gi);
-    if (L != 0) {
-      const uint32_t d = __ldg(Dg + gi);
-      if (c < d) bad = 1;
-      shell = d == 1;
-      const double lt = sqrt((double)c);
-      fx = (unsigned long long)__double2ull_rn(lt * scale);
-      if (lt2_out) lt2_out[gi] = c;
-      if (lt_out) lt_out[gi] = (float)lt;
-    }
+  if (L != 0) {
+    if (c < d) bad = 1;
+    shell = d == 1;
+    const double lt = sqrt((double)c);
+    fx = (unsigned long long)__double2ull_rn(lt * scale);
+    if (lt2_out) lt2_out[gi] = c;
+    if (lt_out) lt_out[gi] = (float)lt;
   }
   if (do_reduce) {
     if (L < 0 || L > acc.max_label) L = 0;
@@ -58,11 +53,20 @@ static __device__ __forceinline__ uint32_t row_epilogue(uint32_t c, int lane, bo
   return bad;
 }
 
+// Same, loading the label and D of the row itself.
+static __device__ __forceinline__ uint32_t row_epilogue(uint32_t c, int lane, bool valid, int64_t gi, int64_t b,
+                                                 const int32_t* __restrict__ lab, const uint32_t* __restrict__ Dg,
+                                                 const Accum& acc, int do_reduce, double scale,
+                                                 uint32_t* __restrict__ lt2_out, float* __restrict__ lt_out) {
+  const int32_t L = valid ? __ldg(lab + gi) : 0;
+  const uint32_t d = (valid && L != 0) ? __ldg(Dg + gi) : 0u;
+  return row_epilogue_v(c, L, d, lane, gi, b, acc, do_reduce, scale, lt2_out, lt_out);
+}
+
 
 size_t dilate_cover_smem();
 cudaError_t dilate_cover_setup();
-void launch_dilate_cover(const int32_t* labels, const uint32_t* D, TileMeta* meta, const uint2* centres,
-                         const Geom& g, const Accum& a, int do_reduce, int force_fallback, uint32_t* lt2_out,
-                         float* lt_out, WsHeader* hdr, cudaStream_t st);
+void launch_dilate_cover(const uint32_t* D, TileMeta* meta, const uint2* centres, const Geom& g, int force_fallback,
+                         uint32_t* ltp, WsHeader* hdr, cudaStream_t st);
 
 }  // namespace fastrs

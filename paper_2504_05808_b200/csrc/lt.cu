@@ -27,10 +27,8 @@ __device__ __forceinline__ int isqrt_i(int h) {
 constexpr int kRcap = 1024;
 
 template <bool IS3D>
-__global__ void __launch_bounds__(256) k_dilate_atomic(const int32_t* __restrict__ lab, const uint32_t* __restrict__ Dg,
-                                                const TileMeta* __restrict__ meta, const uint2* __restrict__ cent,
-                                                Geom g, Accum acc, int do_reduce, uint32_t* __restrict__ lt2_out,
-                                                float* __restrict__ lt_out, WsHeader* __restrict__ hdr) {
+__global__ void __launch_bounds__(256) k_dilate_atomic(const TileMeta* __restrict__ meta, const uint2* __restrict__ cent,
+                                                Geom g, uint32_t* __restrict__ ltp, WsHeader* __restrict__ hdr) {
   constexpr int TY = IS3D ? 8 : 64, TZ = IS3D ? 8 : 1;
   extern __shared__ uint32_t T[];  // kRows * kRowStride
   __shared__ uint32_t s_rt[kRcap];
@@ -165,11 +163,8 @@ __global__ void __launch_bounds__(256) k_dilate_atomic(const int32_t* __restrict
     }
   }
 
-  // push-down + epilogue, one warp per row
-  const int scale_log2 = sum_scale_log2(g.nscale, dmax);
-  const double scale = ldexp(1.0, scale_log2);
+  // push-down, one warp per row -> the LT plane
   const int64_t item = b * g.Z * g.Y * g.X;
-  uint32_t bad = 0;
   for (int row = warp; row < kRows; row += 8) {
     const int ly = row % TY, lz = row / TY;
     const int64_t gz = oz + lz, gy = oy + ly, gx = ox + lane;
@@ -182,12 +177,48 @@ __global__ void __launch_bounds__(256) k_dilate_atomic(const int32_t* __restrict
       if (lane < (1 << k)) upv = 0;
       c = max(Tr[k * 32 + lane], max(c, upv));
     }
-    bad |= row_epilogue(c, lane, valid, item + (gz * g.Y + gy) * g.X + gx, b, lab, Dg, acc, do_reduce, scale,
-                        lt2_out, lt_out);
+    if (valid) ltp[item + (gz * g.Y + gy) * g.X + gx] = c;
   }
   n_int = __reduce_add_sync(kFull, (uint32_t)n_int);
   if (lane == 0 && n_int) atomicAdd(&hdr->n_intervals, n_int);
-  if (bad) atomicOr(&hdr->status, kStInternal);
+}
+
+// ---------------------------------------------------------------------------------------
+// K5 epilogue (streaming, full occupancy): per element LT^2 from the LT plane, shell (D == 1),
+// LT outputs and the per-label reductions (a7); one warp per x-row of the produced z range,
+// 4 chunks of 32 elements in flight.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_epilogue(const int32_t* __restrict__ lab, const uint32_t* __restrict__ Dg,
+                                                  const uint32_t* __restrict__ ltp, Geom g, int64_t z_lo, int64_t nz,
+                                                  Accum acc, int do_reduce, uint32_t* __restrict__ lt2_out,
+                                                  float* __restrict__ lt_out, WsHeader* __restrict__ hdr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= g.B * nz * g.Y) return;
+  const int64_t y = row % g.Y, zb = row / g.Y, z = z_lo + zb % nz, b = zb / nz;
+  const int64_t base = ((b * g.Z + z) * g.Y + y) * g.X;
+  const double scale = ldexp(1.0, sum_scale_log2(g.nscale, hdr->dmax));
+  const int X = (int)g.X;
+  uint32_t bad = 0;
+  for (int x0 = 0; x0 < X; x0 += 128) {
+    int32_t L[4];
+    uint32_t d[4], c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int x = x0 + 32 * k + lane;
+      const bool in = x < X;
+      L[k] = in ? __ldg(lab + base + x) : 0;
+      d[k] = in ? __ldg(Dg + base + x) : 0u;
+      c[k] = (in && L[k] != 0) ? __ldg(ltp + base + x) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (x0 + 32 * k >= X) break;  // warp-uniform
+      bad |= row_epilogue_v(c[k], L[k], d[k], lane, base + x0 + 32 * k + lane, b, acc, do_reduce, scale, lt2_out,
+                            lt_out);
+    }
+  }
+  if (__any_sync(kFull, bad) && lane == 0) atomicOr(&hdr->status, kStInternal);
 }
 
 
@@ -203,19 +234,24 @@ cudaError_t dilate_atomic_setup() {
 
 void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta, const uint2* centres,
                    const Geom& g, const Accum* acc, uint32_t* lt2_out, float* lt_out, bool force_fallback,
-                   WsHeader* hdr, cudaStream_t st) {
+                   uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
   Accum a{};
   if (acc) a = *acc;
-  // both kernels read Dmax / the per-tile fallback flag on the device; the atomic kernel only
-  // processes tiles the sorted-cover kernel left to it
-  launch_dilate_cover(labels, D, meta, centres, g, a, acc ? 1 : 0, force_fallback ? 1 : 0, lt2_out, lt_out, hdr, st);
+  // both dilation kernels read Dmax / the per-tile fallback flag on the device; the atomic
+  // kernel only processes tiles the exact-order kernel left to it.  Both write LT^2 to ltp.
+  launch_dilate_cover(D, meta, centres, g, force_fallback ? 1 : 0, ltp, hdr, st);
   const size_t smem = (size_t)kRows * kRowStride * 4;
   if (g.ndim == 3)
-    k_dilate_atomic<true><<<(unsigned)g.ntiles, 256, smem, st>>>(labels, D, meta, centres, g, a, acc ? 1 : 0, lt2_out,
-                                                                  lt_out, hdr);
+    k_dilate_atomic<true><<<(unsigned)g.ntiles, 256, smem, st>>>(meta, centres, g, ltp, hdr);
   else
-    k_dilate_atomic<false><<<(unsigned)g.ntiles, 256, smem, st>>>(labels, D, meta, centres, g, a, acc ? 1 : 0,
-                                                                   lt2_out, lt_out, hdr);
+    k_dilate_atomic<false><<<(unsigned)g.ntiles, 256, smem, st>>>(meta, centres, g, ltp, hdr);
+  // epilogue over the produced layers
+  const int TZ = g.ndim == 3 ? kTZ3 : 1;
+  const int64_t z_lo = g.tz_lo * TZ, z_hi = g.tz_hi * TZ < g.Z ? g.tz_hi * TZ : g.Z;
+  const int64_t rows = g.B * (z_hi - z_lo) * g.Y;
+  if (rows > 0)
+    k_epilogue<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(labels, D, ltp, g, z_lo, z_hi - z_lo, a, acc ? 1 : 0,
+                                                          lt2_out, lt_out, hdr);
 }
 
 }  // namespace fastrs

@@ -101,6 +101,12 @@ struct DeviceTables {
 std::mutex g_mu;
 DeviceTables g_tables[64];
 
+// 4-byte asynchronous global->shared copy; writes zero when !valid
+__device__ __forceinline__ void cp_async4_zfill(uint32_t* smem, const uint32_t* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 4 : 0) : "memory");
+}
+
 template <bool IS3D>
 struct PruneTile {
   static constexpr int H = IS3D ? 3 : 2;  // halo: |s_i| <= 3 (3D, |s|^2 <= 12) / 2 (2D, |s|^2 <= 8)
@@ -135,19 +141,27 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
   const int64_t b = t / g.ntz;
   const int64_t z0 = tz * P::TZ - P::HZ, y0 = ty * P::TY - P::H, x0 = tx * kTX - P::H;
   const uint32_t* Db = D + b * g.Z * g.Y * g.X;
-  // halo staging, one warp per (z, y) row of the padded tile (lanes over x: no per-element
-  // index division)
-  for (int r = warp; r < P::PZ * P::PY; r += 8) {
-    const int lz = r / P::PY, ly = r - lz * P::PY;
-    const int64_t gz = z0 + lz, gy = y0 + ly;
-    const bool rowok = gz >= 0 && gz < g.Z && gy >= 0 && gy < g.Y;
-    const uint32_t* src = Db + (gz * g.Y + gy) * g.X;
+  // halo staging with cp.async (zero-fill outside the grid): one warp per (z, y) row of the
+  // padded tile, every element's copy in flight at once
+  {
+    const int Zi = (int)g.Z, Yi = (int)g.Y, Xi = (int)g.X;
+    for (int r = warp; r < P::PZ * P::PY; r += 8) {
+      const int lz = r / P::PY, ly = r - lz * P::PY;
+      const int gz = (int)z0 + lz, gy = (int)y0 + ly;
+      const bool rowok = (unsigned)gz < (unsigned)Zi && (unsigned)gy < (unsigned)Yi;
+      const uint32_t* src = Db + ((int64_t)(rowok ? gz : 0) * Yi + (rowok ? gy : 0)) * Xi;
 #pragma unroll
-    for (int lx = lane; lx < P::PX + 31 - (P::PX + 31) % 32; lx += 32) {
-      if (lx >= P::PX) break;
-      const int64_t gx = x0 + lx;
-      s[r * P::PX + lx] = (rowok && gx >= 0 && gx < g.X) ? __ldg(src + gx) : 0u;
+      for (int k = 0; k < (P::PX + 31) / 32; ++k) {
+        const int lx = lane + 32 * k;
+        if (lx < P::PX) {
+          const int gx = (int)x0 + lx;
+          const bool ok = rowok && (unsigned)gx < (unsigned)Xi;
+          cp_async4_zfill(&s[r * P::PX + lx], ok ? src + gx : Db, ok);
+        }
+      }
     }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   }
   __syncthreads();
 
