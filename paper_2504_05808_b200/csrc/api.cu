@@ -58,7 +58,7 @@ int make_geom(const int64_t* dims, int ndim, int64_t batch, Geom& g) {
 inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t hdr, A, B, meta, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd, total;
+  size_t hdr, A, B, meta, fgm, oct, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd, total;
 };
 
 Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
@@ -74,6 +74,8 @@ Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
   L.A = take((size_t)g.N * 4);
   L.B = take((size_t)g.N * 4);
   L.meta = take((size_t)g.ntiles * sizeof(TileMeta));
+  L.fgm = take((size_t)g.ntiles * kRows * 4);
+  L.oct = take((size_t)g.ntiles * 16 * 2);
   L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
   L.vol = take(M * 8);
   L.nsh = take(M * 8);
@@ -197,10 +199,12 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
     tm.mark(2);
   }
   if (stage != kEdtOnly) {
-    launch_prune(D, g, meta, cent, hdr, st);  // K4
+    uint32_t* fgm = (uint32_t*)(w + L.fgm);
+    uint16_t* oct = (uint16_t*)(w + L.oct);
+    launch_prune(D, g, meta, cent, fgm, oct, hdr, st);  // K4
     tm.mark(3);
     uint32_t* ltp = D == A ? B : A;  // the plane the EDT no longer needs holds LT^2
-    launch_dilate(labels, D, meta, cent, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out,
+    launch_dilate(labels, D, meta, cent, fgm, oct, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out,
                   (flags & kFlagForceFallback) != 0, ltp, hdr, st);  // K5
     tm.mark(4);
     if (stage == kFull) {
@@ -252,7 +256,7 @@ int finish_call(WsHeader* hdr, uint32_t flags, cudaStream_t st) {
 }
 
 struct SlabLayout {
-  size_t hdr, P, meta, cent, total;
+  size_t hdr, P, meta, fgm, oct, cent, total;
 };
 SlabLayout make_slab_layout(const Geom& g) {
   SlabLayout L{};
@@ -265,6 +269,8 @@ SlabLayout make_slab_layout(const Geom& g) {
   L.hdr = take(256);
   L.P = take((size_t)g.N * 4);
   L.meta = take((size_t)g.ntiles * sizeof(TileMeta));
+  L.fgm = take((size_t)g.ntiles * kRows * 4);
+  L.oct = take((size_t)g.ntiles * 16 * 2);
   L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
   L.total = off;
   return L;
@@ -490,7 +496,9 @@ int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64
   k_set_dmax<<<1, 1, 0, st>>>(hdr, dmax_global);
   TileMeta* meta = (TileMeta*)((char*)ws + L.meta);
   uint2* cent = (uint2*)((char*)ws + L.cent);
-  launch_prune(d_ext, g, meta, cent, hdr, st);
+  uint32_t* fgm = (uint32_t*)((char*)ws + L.fgm);
+  uint16_t* oct = (uint16_t*)((char*)ws + L.oct);
+  launch_prune(d_ext, g, meta, cent, fgm, oct, hdr, st);
   Accum acc{};
   acc.vol = (unsigned long long*)vol;
   acc.nshell = (unsigned long long*)n_shell;
@@ -503,7 +511,8 @@ int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64
   // elements are ever read)
   const int32_t* lab_ext = labels - own_lo * g.Y * g.X;
   uint32_t* ltp = (uint32_t*)((char*)ws + L.P);
-  launch_dilate(lab_ext, d_ext, meta, cent, g, &acc, nullptr, nullptr, (flags & kFlagForceFallback) != 0, ltp, hdr, st);
+  launch_dilate(lab_ext, d_ext, meta, cent, fgm, oct, g, &acc, nullptr, nullptr, (flags & kFlagForceFallback) != 0, ltp,
+                hdr, st);
   return finish_call(hdr, flags, st);
 }
 

@@ -133,11 +133,14 @@ void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, 
                     bool border, WsHeader* hdr, cudaStream_t st, int64_t p_lo = 0, int64_t p_hi = -1,
                     int64_t gofs = 0, int64_t Lg = -1);
 cudaError_t ensure_mtables(int device);  // builds the per-device lattice tables (sync, once)
-void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, WsHeader* hdr,
-                  cudaStream_t st);
+// K4; also writes per tile the foreground row masks (fgm: kRows u32) and the number of kept
+// entries with D bucket >= 8o for o = 0..15 (oct: 16 u16) used by K5's gather
+void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, uint32_t* fgm, uint16_t* oct,
+                  WsHeader* hdr, cudaStream_t st);
 void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta,
-                   const uint2* centres, const Geom& g, const Accum* acc, uint32_t* lt2_out,
-                   float* lt_out, bool force_fallback, uint32_t* ltp, WsHeader* hdr, cudaStream_t st);
+                   const uint2* centres, const uint32_t* fgm, const uint16_t* oct, const Geom& g,
+                   const Accum* acc, uint32_t* lt2_out, float* lt_out, bool force_fallback, uint32_t* ltp,
+                   WsHeader* hdr, cudaStream_t st);
 void launch_metrics(const Accum& acc, const Geom& g, const Outputs& o, WsHeader* hdr,
                     cudaStream_t st);
 void release_mtables();

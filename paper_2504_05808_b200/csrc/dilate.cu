@@ -39,6 +39,9 @@ constexpr int kHist = 1536;  // exact-D counting-sort bins per round
 constexpr int kPoint = 128;  // uncovered cells at which a warp switches to point tests
 constexpr int kOff = 16384;  // coordinate bias of packed candidates
 
+struct Smem;
+static_assert(2 * 640 <= 1536 && 641 * 2 <= 3072, "gather scratch fits S.hist / S.idx");
+
 struct Smem {
   unsigned long long list[kCap];     // gathered candidates (centre relative to the group), gather order
   uint16_t val[kWarps][kRows * 32];  // LT^2 per element of each warp's tile (D <= 65535 here)
@@ -49,7 +52,7 @@ struct Smem {
   uint16_t ulist[kWarps][kPoint];    // point mode: the still-uncovered cells (row*32 + x)
   uint32_t bhist[kBuckets];
   uint32_t wsum[kWarps];
-  uint32_t count, total;
+  uint32_t count, total, nrec;
   int round_lo, round_hi, round_top, next_hi, fallback, rounds;
 };
 
@@ -79,84 +82,125 @@ __device__ __forceinline__ uint32_t range_mask(int l, int r) {  // bits l..r (0 
 }
 
 // Gather the candidates reaching the group box with bucket in [blo, bhi] into S.list.
-// HIST: also histogram them (the first pass of a round).
+// HIST: also histogram them (the first pass of a round).  Flattened: the CTA first lists the
+// home tiles whose balls can reach the group (records: neighbour index, first entry, count),
+// reading per home tile only the prefix of its bucket-sorted list that can reach the group and
+// lies in the bucket range (K4's octave counts), then every thread takes entries of any record
+// (binary search over the record prefix sums), so all the entry loads are in flight at once.
+// S.hist and S.idx serve as scratch (they are rebuilt by the sort afterwards).
+constexpr int kRecCap = 640;
+
 template <bool IS3D, bool HIST>
 __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ meta, const uint2* __restrict__ cent,
-                                       const Geom& g, int64_t b, int64_t tx0, int64_t ty0, int64_t tz0, int nrx,
-                                       int nry, int nrz, int blo, int bhi) {
+                                       const uint16_t* __restrict__ oct, const Geom& g, int64_t b, int64_t tx0,
+                                       int64_t ty0, int64_t tz0, int nrx, int nry, int nrz, int blo, int bhi) {
   using P = Shape<IS3D>;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nx = P::GX + 2 * nrx, ny = P::GY + 2 * nry, nz = P::GZ + 2 * nrz;
   const int nneigh = nx * ny * nz;
-  for (int nb0 = 0; nb0 < nneigh; nb0 += kWarps * 32) {
-    const int n = nb0 + tid;
-    bool reach = false;
-    int64_t ht = 0;
-    uint32_t hcount = 0;
-    int hox = 0, hoy = 0, hoz = 0, hg2 = 0;
-    if (n < nneigh) {
+  uint32_t* rec = S.hist;                                  // 2 words per record
+  uint32_t* pre = reinterpret_cast<uint32_t*>(S.idx);      // kRecCap + 1 prefix sums
+  const int o_start = (bhi + 1 + 7) >> 3;                  // entries with bucket > bhi come first
+  for (int nb0 = 0; nb0 < nneigh; nb0 += kRecCap) {
+    __syncthreads();
+    if (tid == 0) S.nrec = 0;
+    __syncthreads();
+    const int nb1 = min(nneigh, nb0 + kRecCap);
+    for (int n = nb0 + tid; n < nb1; n += kWarps * 32) {
       const int ix = n % nx, iy = (n / nx) % ny, iz = n / (nx * ny);
       const int64_t hx = tx0 + ix - nrx, hy = ty0 + iy - nry, hz = tz0 + iz - nrz;
-      if (hx >= 0 && hx < g.ntx && hy >= 0 && hy < g.nty && hz >= 0 && hz < g.ntz) {
-        ht = ((b * g.ntz + hz) * g.nty + hy) * g.ntx + hx;
-        const TileMeta hm = meta[ht];
-        hox = (ix - nrx) * kTX;
-        hoy = (iy - nry) * P::TY;
-        hoz = (iz - nrz) * P::TZ;
-        // gap between the home tile box and the group box
-        const int gx = hox < 0 ? -(hox + kTX - 1) : (hox > P::RX - 1 ? hox - (P::RX - 1) : 0);
-        const int gy = hoy < 0 ? -(hoy + P::TY - 1) : (hoy > P::RY - 1 ? hoy - (P::RY - 1) : 0);
-        const int gz = hoz < 0 ? -(hoz + P::TZ - 1) : (hoz > P::RZ - 1 ? hoz - (P::RZ - 1) : 0);
-        hg2 = gx * gx + gy * gy + gz * gz;
-        reach = hm.count && hg2 <= (int)hm.maxD - 1 && dbucket(hm.maxD) >= blo;
-        hcount = hm.count;
-      }
+      if (hx < 0 || hx >= g.ntx || hy < 0 || hy >= g.nty || hz < 0 || hz >= g.ntz) continue;
+      const int64_t ht = ((b * g.ntz + hz) * g.nty + hy) * g.ntx + hx;
+      const TileMeta hm = meta[ht];
+      if (!hm.count) continue;
+      const int hox = (ix - nrx) * kTX, hoy = (iy - nry) * P::TY, hoz = (iz - nrz) * P::TZ;
+      const int gx = hox < 0 ? -(hox + kTX - 1) : (hox > P::RX - 1 ? hox - (P::RX - 1) : 0);
+      const int gy = hoy < 0 ? -(hoy + P::TY - 1) : (hoy > P::RY - 1 ? hoy - (P::RY - 1) : 0);
+      const int gz = hoz < 0 ? -(hoz + P::TZ - 1) : (hoz > P::RZ - 1 ? hoz - (P::RZ - 1) : 0);
+      const int g2 = gx * gx + gy * gy + gz * gz;
+      if (g2 > (int)hm.maxD - 1 || dbucket(hm.maxD) < blo) continue;
+      // lowest bucket whose largest D can still reach the gap: D - 1 >= g2 <=> D >= g2 + 1
+      const int bmin = max(dbucket((uint32_t)g2 + 1u), blo);
+      const uint16_t* oc = oct + ht * 16;
+      const uint32_t end = oc[bmin >> 3];
+      const uint32_t start = o_start >= 16 ? 0u : oc[o_start];
+      if (end <= start) continue;
+      const uint32_t slot = atomicAdd(&S.nrec, 1u);
+      rec[2 * slot] = (uint32_t)n;
+      rec[2 * slot + 1] = start | ((end - start) << 16);
     }
-    uint32_t rm = __ballot_sync(kFull, reach);
-    while (rm) {
-      const int j = __ffs(rm) - 1;
-      rm &= rm - 1;
-      const int64_t hts = __shfl_sync(kFull, ht, j);
-      const uint32_t cnt = __shfl_sync(kFull, hcount, j);
-      const int bx = __shfl_sync(kFull, hox, j), by = __shfl_sync(kFull, hoy, j), bz = __shfl_sync(kFull, hoz, j);
-      const int g2 = __shfl_sync(kFull, hg2, j);
-      const uint2* src = cent + (size_t)hts * kTileVol;
-      // the home tile's list is sorted by D bucket, descending: stop once the remaining balls
-      // are too small to reach the group, or below the round's bucket range
-      for (uint32_t e0 = 0; e0 < cnt; e0 += 32) {
-        bool take = false;
-        int bk = -1;
-        unsigned long long pe = 0;
-        if (e0 + lane < cnt) {
-          const uint2 e = __ldg(src + e0 + lane);
-          const int v = (int)e.x;
-          const int cx = bx + (v & 31), cy = by + ((v >> 5) % P::TY), cz = bz + v / (32 * P::TY);
-          const int ddx = gap(0, P::RX - 1, cx), ddy = gap(0, P::RY - 1, cy), ddz = gap(0, P::RZ - 1, cz);
-          bk = dbucket(e.y);
-          if (ddx * ddx + ddy * ddy + ddz * ddz <= (int)e.y - 1) {
-            take = bk >= blo && bk <= bhi;
-            pe = pack(cx, cy, cz, e.y);
-          }
+    __syncthreads();
+    const int nrec = (int)S.nrec;
+    {  // exclusive prefix of the record counts (kRecCap / 128 = 5 records per thread)
+      constexpr int kPer = (kRecCap + kWarps * 32 - 1) / (kWarps * 32);
+      uint32_t loc[kPer], sum = 0;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int r = tid * kPer + j;
+        loc[j] = r < nrec ? rec[2 * r + 1] >> 16 : 0u;
+        sum += loc[j];
+      }
+      uint32_t inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += v;
+      }
+      if (lane == 31) S.wsum[warp] = inc;
+      __syncthreads();
+      uint32_t run = inc - sum;
+      for (int w = 0; w < warp; ++w) run += S.wsum[w];
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int r = tid * kPer + j;
+        if (r < nrec) pre[r] = run;
+        run += loc[j];
+      }
+      if (tid == kWarps * 32 - 1) pre[nrec] = run;
+    }
+    __syncthreads();
+    const uint32_t total = pre[nrec];
+    for (uint32_t e0 = warp * 32; e0 < total; e0 += kWarps * 32) {
+      const uint32_t e = e0 + lane;
+      bool take = false;
+      int bk = -1;
+      unsigned long long pe = 0;
+      if (e < total) {
+        int lo = 0, hi = nrec;  // pre[lo] <= e < pre[hi]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (pre[mid] <= e) lo = mid; else hi = mid;
         }
-        const int last = (int)min(cnt - e0, 32u) - 1;
-        const int bk_last = __shfl_sync(kFull, bk, last);
-        const bool more = (int)dbucket_max(bk_last) - 1 >= g2 && bk_last >= blo;
-        const uint32_t tm = __ballot_sync(kFull, take);
-        if (tm) {
-          if (HIST) {
-            const uint32_t grp = __match_any_sync(kFull, take ? bk : -1);
-            if (take && lane == __ffs(grp) - 1) atomicAdd(&S.bhist[bk], (uint32_t)__popc(grp));
-          }
-          uint32_t base = 0;
-          if (lane == 0) base = atomicAdd(&S.count, (uint32_t)__popc(tm));
-          base = __shfl_sync(kFull, base, 0);
-          const uint32_t pos = base + __popc(tm & ((1u << lane) - 1u));
-          if (take && pos < kCap) S.list[pos] = pe;
+        const int n = (int)rec[2 * lo];
+        const uint32_t k = (rec[2 * lo + 1] & 0xFFFFu) + (e - pre[lo]);
+        const int ix = n % nx, iy = (n / nx) % ny, iz = n / (nx * ny);
+        const int64_t ht = ((b * g.ntz + (tz0 + iz - nrz)) * g.nty + (ty0 + iy - nry)) * g.ntx + (tx0 + ix - nrx);
+        const uint2 en = __ldg(cent + (size_t)ht * kTileVol + k);
+        const int v = (int)en.x;
+        const int cx = (ix - nrx) * kTX + (v & 31), cy = (iy - nry) * P::TY + ((v >> 5) % P::TY),
+                  cz = (iz - nrz) * P::TZ + v / (32 * P::TY);
+        const int ddx = gap(0, P::RX - 1, cx), ddy = gap(0, P::RY - 1, cy), ddz = gap(0, P::RZ - 1, cz);
+        bk = dbucket(en.y);
+        if (ddx * ddx + ddy * ddy + ddz * ddz <= (int)en.y - 1 && bk >= blo && bk <= bhi) {
+          take = true;
+          pe = pack(cx, cy, cz, en.y);
         }
-        if (!more) break;
+      }
+      const uint32_t tm = __ballot_sync(kFull, take);
+      if (tm) {
+        if (HIST) {
+          const uint32_t grp = __match_any_sync(kFull, take ? bk : -1);
+          if (take && lane == __ffs(grp) - 1) atomicAdd(&S.bhist[bk], (uint32_t)__popc(grp));
+        }
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&S.count, (uint32_t)__popc(tm));
+        base = __shfl_sync(kFull, base, 0);
+        const uint32_t pos = base + __popc(tm & ((1u << lane) - 1u));
+        if (take && pos < kCap) S.list[pos] = pe;
       }
     }
   }
+  __syncthreads();
 }
 
 // position of the n-th (0-based) set bit of m (requires popc(m) > n)
@@ -186,9 +230,10 @@ __device__ __forceinline__ unsigned long long row_box(int ya, int yb, int za, in
 }
 
 template <bool IS3D>
-__global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t* __restrict__ Dg,
+__global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t* __restrict__ fgm,
                                                                 TileMeta* __restrict__ meta,
-                                                                const uint2* __restrict__ cent, Geom g,
+                                                                const uint2* __restrict__ cent,
+                                                                const uint16_t* __restrict__ oct, Geom g,
                                                                 int force_fallback, int point_at,
                                                                 uint32_t* __restrict__ ltp, WsHeader* __restrict__ hdr) {
   using P = Shape<IS3D>;
@@ -234,31 +279,21 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
 #pragma unroll 4
     for (int i = lane; i < kRows * 32 / 8; i += 32) v4[i] = make_uint4(0u, 0u, 0u, 0u);
   }
-  // rows of my tile that still hold uncovered foreground, per 8-column chunk of x
+  // rows of my tile that still hold uncovered foreground, per 8-column chunk of x (K4 wrote
+  // the tile's foreground row masks)
   unsigned long long Uc[4] = {0, 0, 0, 0};
   {
-    const int64_t gx = rox + mox + lane;
+    uint32_t f[2];
 #pragma unroll
-    for (int r0 = 0; r0 < kRows; r0 += 16) {
-      uint32_t dv[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int row = r0 + k, ly = row % TY, lz = row / TY;
-        const int64_t gz = roz + moz + lz, gy = roy + moy + ly;
-        dv[k] = (active && gz < g.Z && gy < g.Y && gx < g.X) ? __ldg(Dg + item + (gz * g.Y + gy) * g.X + gx) : 0u;
-      }
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const uint32_t m = __ballot_sync(kFull, dv[k] != 0);
-        if (lane == ((r0 + k) & 31)) {
-          fgw[r0 + k] = m;
-          covw[r0 + k] = 0;
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if ((m >> (8 * c)) & 0xFFu) Uc[c] |= 1ull << (r0 + k);
-      }
+    for (int k = 0; k < 2; ++k) {
+      f[k] = active ? fgm[mtile * kRows + lane + 32 * k] : 0u;
+      fgw[lane + 32 * k] = f[k];
+      covw[lane + 32 * k] = 0;
     }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      Uc[c] = (unsigned long long)__ballot_sync(kFull, (f[0] >> (8 * c)) & 0xFFu) |
+              ((unsigned long long)__ballot_sync(kFull, (f[1] >> (8 * c)) & 0xFFu) << 32);
   }
   __syncwarp();
   // uncovered foreground cells of my tile (warp-uniform); point mode once it is small
@@ -296,7 +331,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
     for (int i = tid; i < kBuckets; i += kWarps * 32) S.bhist[i] = 0;
     if (tid == 0) S.count = 0;
     __syncthreads();
-    gather<IS3D, true>(S, meta, cent, g, b, tx0, ty0, tz0, nrx, nry, nrz, 0, rhi);
+    gather<IS3D, true>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, 0, rhi);
     __syncthreads();
     // --- this round's bucket range [rlo, rhi]: as many buckets as fit the list and the sort
     // range (warp 0: descending inclusive scan of the histogram, 4 buckets per lane)
@@ -355,7 +390,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
       __syncthreads();
       if (tid == 0) S.count = 0;
       __syncthreads();
-      gather<IS3D, false>(S, meta, cent, g, b, tx0, ty0, tz0, nrx, nry, nrz, rlo, rhi);
+      gather<IS3D, false>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, rlo, rhi);
       __syncthreads();
     }
     // --- exact counting sort of the list indices by D (descending), D in [dlo, dhi]
@@ -579,8 +614,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
 
 size_t dilate_cover_smem() { return sizeof(Smem); }
 
-void launch_dilate_cover(const uint32_t* D, TileMeta* meta, const uint2* centres, const Geom& g, int force_fallback,
-                         uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
+void launch_dilate_cover(const uint32_t* fgm, TileMeta* meta, const uint2* centres, const uint16_t* oct, const Geom& g,
+                         int force_fallback, uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
   const int GX = g.ndim == 3 ? 1 : 2, GY = 2, GZ = g.ndim == 3 ? 2 : 1;
   const int64_t ngroups = g.B * ((g.ntx + GX - 1) / GX) * ((g.nty + GY - 1) / GY) * ((g.tz_hi - g.tz_lo + GZ - 1) / GZ);
   if (ngroups <= 0) return;
@@ -591,10 +626,10 @@ void launch_dilate_cover(const uint32_t* D, TileMeta* meta, const uint2* centres
     return p < 0 ? 0 : (p > kPoint ? kPoint : p);
   }();
   if (g.ndim == 3)
-    k_dilate_cover<true><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(D, meta, centres, g, force_fallback, point_at,
-                                                                        ltp, hdr);
+    k_dilate_cover<true><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(fgm, meta, centres, oct, g, force_fallback,
+                                                                        point_at, ltp, hdr);
   else
-    k_dilate_cover<false><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(D, meta, centres, g, force_fallback,
+    k_dilate_cover<false><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(fgm, meta, centres, oct, g, force_fallback,
                                                                          point_at, ltp, hdr);
 }
 

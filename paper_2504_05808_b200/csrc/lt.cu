@@ -233,13 +233,13 @@ cudaError_t dilate_atomic_setup() {
 }
 
 void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta, const uint2* centres,
-                   const Geom& g, const Accum* acc, uint32_t* lt2_out, float* lt_out, bool force_fallback,
-                   uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
+                   const uint32_t* fgm, const uint16_t* oct, const Geom& g, const Accum* acc, uint32_t* lt2_out,
+                   float* lt_out, bool force_fallback, uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
   Accum a{};
   if (acc) a = *acc;
   // both dilation kernels read Dmax / the per-tile fallback flag on the device; the atomic
   // kernel only processes tiles the exact-order kernel left to it.  Both write LT^2 to ltp.
-  launch_dilate_cover(D, meta, centres, g, force_fallback ? 1 : 0, ltp, hdr, st);
+  launch_dilate_cover(fgm, meta, centres, oct, g, force_fallback ? 1 : 0, ltp, hdr, st);
   const size_t smem = (size_t)kRows * kRowStride * 4;
   if (g.ndim == 3)
     k_dilate_atomic<true><<<(unsigned)g.ntiles, 256, smem, st>>>(meta, centres, g, ltp, hdr);

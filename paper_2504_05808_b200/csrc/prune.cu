@@ -120,7 +120,8 @@ struct PruneTile {
 
 template <bool IS3D>
 __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, Geom g, TileMeta* __restrict__ meta,
-                                               uint2* __restrict__ cent, const uint32_t* __restrict__ M,
+                                               uint2* __restrict__ cent, uint32_t* __restrict__ fgm,
+                                               uint16_t* __restrict__ oct, const uint32_t* __restrict__ M,
                                                WsHeader* __restrict__ hdr) {
   using P = PruneTile<IS3D>;
   __shared__ uint32_t s[P::PZ * P::PY * P::PX];
@@ -220,7 +221,11 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
       }
     }
     const uint32_t bal = __ballot_sync(kFullMask, keep);
-    if (lane == 0) keepmask[row] = bal;
+    const uint32_t fgb = __ballot_sync(kFullMask, fg);
+    if (lane == 0) {
+      keepmask[row] = bal;
+      fgm[tile * kRows + row] = fgb;  // foreground mask per row, for the dilation's coverage
+    }
     nfg += fg;
   }
   __syncthreads();
@@ -318,6 +323,9 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
     }
     uint32_t run = inc - sum;
     __syncwarp();
+    // entries with bucket >= 8o (o = 1..15) = the exclusive prefix at bucket 8o-1 (lane 32-2o, q 0)
+    if ((lane & 1) == 0 && lane >= 2) oct[tile * 16 + ((32 - lane) >> 1)] = (uint16_t)run;
+    if (lane == 31) oct[tile * 16] = (uint16_t)inc;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       bhist[127 - 4 * lane - q] = run;  // now: next free slot of each bucket
@@ -405,13 +413,14 @@ void release_mtables() {
   }
 }
 
-void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, WsHeader* hdr, cudaStream_t st) {
+void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, uint32_t* fgm, uint16_t* oct,
+                  WsHeader* hdr, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (g.ndim == 3)
-    k_prune<true><<<(unsigned)g.ntiles, 256, 0, st>>>(D, g, meta, centres, g_tables[dev].m3, hdr);
+    k_prune<true><<<(unsigned)g.ntiles, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m3, hdr);
   else
-    k_prune<false><<<(unsigned)g.ntiles, 256, 0, st>>>(D, g, meta, centres, g_tables[dev].m2, hdr);
+    k_prune<false><<<(unsigned)g.ntiles, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m2, hdr);
 }
 
 }  // namespace fastrs
