@@ -40,7 +40,7 @@ constexpr int kPoint = 128;  // uncovered cells at which a warp switches to poin
 constexpr int kOff = 16384;  // coordinate bias of packed candidates
 
 struct Smem;
-static_assert(2 * 640 <= 1536 && 641 * 2 <= 3072, "gather scratch fits S.hist / S.idx");
+static_assert(3 * 512 <= 1536 && 2 * (512 + 8) + 512 <= 3072, "gather scratch fits S.hist / S.idx");
 
 struct Smem {
   unsigned long long list[kCap];     // gathered candidates (centre relative to the group), gather order
@@ -88,7 +88,7 @@ __device__ __forceinline__ uint32_t range_mask(int l, int r) {  // bits l..r (0 
 // lies in the bucket range (K4's octave counts), then every thread takes entries of any record
 // (binary search over the record prefix sums), so all the entry loads are in flight at once.
 // S.hist and S.idx serve as scratch (they are rebuilt by the sort afterwards).
-constexpr int kRecCap = 640;
+constexpr int kRecCap = 512;  // records per chunk: 3 words each in S.hist, prefix sums in S.idx
 
 template <bool IS3D, bool HIST>
 __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ meta, const uint2* __restrict__ cent,
@@ -98,8 +98,9 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nx = P::GX + 2 * nrx, ny = P::GY + 2 * nry, nz = P::GZ + 2 * nrz;
   const int nneigh = nx * ny * nz;
-  uint32_t* rec = S.hist;                                  // 2 words per record
+  uint32_t* rec = S.hist;                                  // 3 words per record
   uint32_t* pre = reinterpret_cast<uint32_t*>(S.idx);      // kRecCap + 1 prefix sums
+  int16_t* recz = reinterpret_cast<int16_t*>(S.idx) + 2 * (kRecCap + 8);  // home tile z offsets
   const int o_start = (bhi + 1 + 7) >> 3;                  // entries with bucket > bhi come first
   for (int nb0 = 0; nb0 < nneigh; nb0 += kRecCap) {
     __syncthreads();
@@ -126,8 +127,11 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
       const uint32_t start = o_start >= 16 ? 0u : oc[o_start];
       if (end <= start) continue;
       const uint32_t slot = atomicAdd(&S.nrec, 1u);
-      rec[2 * slot] = (uint32_t)n;
-      rec[2 * slot + 1] = start | ((end - start) << 16);
+      rec[3 * slot] = (uint32_t)ht;  // tile index (< 2^32, checked in make_geom)
+      rec[3 * slot + 1] = start | ((end - start) << 16);
+      // home tile origin relative to the group, biased to stay non-negative (|offset| < 2^15)
+      rec[3 * slot + 2] = (uint32_t)(hox + kOff) | ((uint32_t)(hoy + kOff) << 16);
+      recz[slot] = (int16_t)hoz;
     }
     __syncthreads();
     const int nrec = (int)S.nrec;
@@ -137,7 +141,7 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
 #pragma unroll
       for (int j = 0; j < kPer; ++j) {
         const int r = tid * kPer + j;
-        loc[j] = r < nrec ? rec[2 * r + 1] >> 16 : 0u;
+        loc[j] = r < nrec ? rec[3 * r + 1] >> 16 : 0u;
         sum += loc[j];
       }
       uint32_t inc = sum;
@@ -171,14 +175,13 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
           const int mid = (lo + hi) >> 1;
           if (pre[mid] <= e) lo = mid; else hi = mid;
         }
-        const int n = (int)rec[2 * lo];
-        const uint32_t k = (rec[2 * lo + 1] & 0xFFFFu) + (e - pre[lo]);
-        const int ix = n % nx, iy = (n / nx) % ny, iz = n / (nx * ny);
-        const int64_t ht = ((b * g.ntz + (tz0 + iz - nrz)) * g.nty + (ty0 + iy - nry)) * g.ntx + (tx0 + ix - nrx);
+        const uint32_t ht = rec[3 * lo];
+        const uint32_t k = (rec[3 * lo + 1] & 0xFFFFu) + (e - pre[lo]);
+        const uint32_t o = rec[3 * lo + 2];
         const uint2 en = __ldg(cent + (size_t)ht * kTileVol + k);
         const int v = (int)en.x;
-        const int cx = (ix - nrx) * kTX + (v & 31), cy = (iy - nry) * P::TY + ((v >> 5) % P::TY),
-                  cz = (iz - nrz) * P::TZ + v / (32 * P::TY);
+        const int cx = (int)(o & 0xFFFFu) - kOff + (v & 31), cy = (int)(o >> 16) - kOff + ((v >> 5) % P::TY),
+                  cz = (int)recz[lo] + v / (32 * P::TY);
         const int ddx = gap(0, P::RX - 1, cx), ddy = gap(0, P::RY - 1, cy), ddz = gap(0, P::RZ - 1, cz);
         bk = dbucket(en.y);
         if (ddx * ddx + ddy * ddy + ddz * ddz <= (int)en.y - 1 && bk >= blo && bk <= bhi) {
