@@ -107,11 +107,18 @@ __device__ __forceinline__ void cp_async4_zfill(uint32_t* smem, const uint32_t* 
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 4 : 0) : "memory");
 }
 
+// 16-byte asynchronous global->shared copy (both 16-byte aligned); zeros when !valid
+__device__ __forceinline__ void cp_async16_zfill(uint32_t* smem, const uint32_t* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
+}
+
 template <bool IS3D>
 struct PruneTile {
   static constexpr int H = IS3D ? 3 : 2;  // halo: |s_i| <= 3 (3D, |s|^2 <= 12) / 2 (2D, |s|^2 <= 8)
   static constexpr int TY = IS3D ? 8 : 64, TZ = IS3D ? 8 : 1;
-  static constexpr int PX = kTX + 2 * H, PY = TY + 2 * H, PZ = IS3D ? TZ + 2 * H : 1;
+  static constexpr int HX = 4;  // x halo of the staged rows: 4 (>= H) keeps rows 16-byte aligned
+  static constexpr int PX = kTX + 2 * HX, PY = TY + 2 * H, PZ = IS3D ? TZ + 2 * H : 1;
   static constexpr int HZ = IS3D ? H : 0;
   static constexpr int NC = IS3D ? kClasses3 : kClasses2;   // classes
   static constexpr int C1 = IS3D ? 3 : 2;                   // stage-1 classes
@@ -124,7 +131,7 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
                                                uint16_t* __restrict__ oct, const uint32_t* __restrict__ M,
                                                WsHeader* __restrict__ hdr) {
   using P = PruneTile<IS3D>;
-  __shared__ uint32_t s[P::PZ * P::PY * P::PX];
+  __shared__ __align__(16) uint32_t s[P::PZ * P::PY * P::PX];
   __shared__ uint32_t keepmask[kRows];
   __shared__ uint32_t pre[kRows];
   __shared__ uint32_t red_cnt[8], red_max[8];
@@ -140,24 +147,37 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
   t /= g.nty;
   const int64_t tz = t % g.ntz;
   const int64_t b = t / g.ntz;
-  const int64_t z0 = tz * P::TZ - P::HZ, y0 = ty * P::TY - P::H, x0 = tx * kTX - P::H;
+  const int64_t z0 = tz * P::TZ - P::HZ, y0 = ty * P::TY - P::H, x0 = tx * kTX - P::HX;
   const uint32_t* Db = D + b * g.Z * g.Y * g.X;
-  // halo staging with cp.async (zero-fill outside the grid): one warp per (z, y) row of the
-  // padded tile, every element's copy in flight at once
+  // halo staging with cp.async (zero-fill outside the grid), one warp per (z, y) row of the
+  // padded tile.  Rows are 40 words starting at a multiple of 4, so when X % 4 == 0 every
+  // 16-byte chunk lies entirely inside or outside the grid: 10 chunk copies per row.
   {
     const int Zi = (int)g.Z, Yi = (int)g.Y, Xi = (int)g.X;
-    for (int r = warp; r < P::PZ * P::PY; r += 8) {
-      const int lz = r / P::PY, ly = r - lz * P::PY;
-      const int gz = (int)z0 + lz, gy = (int)y0 + ly;
-      const bool rowok = (unsigned)gz < (unsigned)Zi && (unsigned)gy < (unsigned)Yi;
-      const uint32_t* src = Db + ((int64_t)(rowok ? gz : 0) * Yi + (rowok ? gy : 0)) * Xi;
+    constexpr int kRowsPZ = P::PZ * P::PY;
+    if ((Xi & 3) == 0) {
+      for (int i = tid; i < kRowsPZ * (P::PX / 4); i += 256) {
+        const int r = i / (P::PX / 4), j = i - r * (P::PX / 4);
+        const int lz = r / P::PY, ly = r - lz * P::PY;
+        const int gz = (int)z0 + lz, gy = (int)y0 + ly, gx = (int)x0 + 4 * j;
+        const bool ok = (unsigned)gz < (unsigned)Zi && (unsigned)gy < (unsigned)Yi && (unsigned)gx < (unsigned)Xi;
+        const uint32_t* src = ok ? Db + ((int64_t)gz * Yi + gy) * Xi + gx : Db;
+        cp_async16_zfill(&s[r * P::PX + 4 * j], src, ok);
+      }
+    } else {
+      for (int r = warp; r < kRowsPZ; r += 8) {
+        const int lz = r / P::PY, ly = r - lz * P::PY;
+        const int gz = (int)z0 + lz, gy = (int)y0 + ly;
+        const bool rowok = (unsigned)gz < (unsigned)Zi && (unsigned)gy < (unsigned)Yi;
+        const uint32_t* src = Db + ((int64_t)(rowok ? gz : 0) * Yi + (rowok ? gy : 0)) * Xi;
 #pragma unroll
-      for (int k = 0; k < (P::PX + 31) / 32; ++k) {
-        const int lx = lane + 32 * k;
-        if (lx < P::PX) {
-          const int gx = (int)x0 + lx;
-          const bool ok = rowok && (unsigned)gx < (unsigned)Xi;
-          cp_async4_zfill(&s[r * P::PX + lx], ok ? src + gx : Db, ok);
+        for (int k = 0; k < (P::PX + 31) / 32; ++k) {
+          const int lx = lane + 32 * k;
+          if (lx < P::PX) {
+            const int gx = (int)x0 + lx;
+            const bool ok = rowok && (unsigned)gx < (unsigned)Xi;
+            cp_async4_zfill(&s[r * P::PX + lx], ok ? src + gx : Db, ok);
+          }
         }
       }
     }
@@ -179,7 +199,7 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
     const int row = warp + 8 * k;
     const int ly = row % P::TY, lz = row / P::TY;
     const int64_t gz = tz * P::TZ + lz, gy = ty * P::TY + ly;
-    const int c = ((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::H);
+    const int c = ((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::HX);
     const uint32_t d = s[c];
     fgr[k] = d != 0 && gz < g.Z && gy < g.Y && gx < g.X;
     dr[k] = d;
@@ -192,7 +212,7 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
   for (int k = 0; k < kRowsPerWarp; ++k) {
     const int row = warp + 8 * k;
     const int ly = row % P::TY, lz = row / P::TY;
-    const int c = ((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::H);
+    const int c = ((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::HX);
     const bool fg = fgr[k];
     bool keep = fg;
     if (__any_sync(kFullMask, fg)) {
@@ -261,7 +281,7 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
     if (i < nsurv) {
       v = surv[i];
       const int lx = v & 31, ly = (v >> 5) % P::TY, lz = v / (32 * P::TY);
-      c = ((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lx + P::H);
+      c = ((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lx + P::HX);
       d = s[c];
       keep = true;
     }
@@ -303,7 +323,7 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
     if (!km) continue;
     const int ly = row % P::TY, lz = row / P::TY;
     const bool kept = (km >> lane) & 1u;
-    const int bk = kept ? dbucket(s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::H)]) : -1;
+    const int bk = kept ? dbucket(s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::HX)]) : -1;
     const uint32_t grp = __match_any_sync(kFullMask, bk);
     if (kept && lane == __ffs(grp) - 1) atomicAdd(&bhist[bk], (uint32_t)__popc(grp));
   }
@@ -341,7 +361,7 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
       if (!km) continue;
       const int ly = row % P::TY, lz = row / P::TY;
       const bool kept = (km >> lane) & 1u;
-      const uint32_t d = kept ? s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::H)] : 0u;
+      const uint32_t d = kept ? s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::HX)] : 0u;
       const int bk = kept ? dbucket(d) : -1;
       const uint32_t grp = __match_any_sync(kFullMask, bk);
       const int leader = __ffs(grp) - 1;
