@@ -34,9 +34,14 @@ sys.path.insert(0, ROOT)
 METRIC = "Gvoxels/s end-to-end (EDT+LT+sphericity+roundness); % of HBM roofline"
 UNIT = "Gvoxels/s"
 
-# algorithmic HBM bytes per grid element of each stage, 3D path
-STAGE_BYTES_PER_ELEM = {"edt_x": 8.0, "edt_y": 8.0, "edt_z": 8.0, "prune": 4.0, "dilate": 8.0, "metrics": 0.0}
+# algorithmic HBM bytes per grid element of each stage (DESIGN.md §6 "Algorithmic bytes"), 3D path
+STAGE_BYTES_PER_ELEM = {"edt_x": 8.0, "edt_y": 8.0, "edt_z": 8.0, "prune": 4.0, "dilate": 4.0, "epilogue": 12.0,
+                        "metrics": 0.0}
 STAGE_BYTES_PER_KEPT = {"prune": 8.0, "dilate": 8.0}  # centre entries written / read once
+# the kernel behind each stage (names in the ncu summaries under profiles/)
+STAGE_KERNEL = {"edt_x": "k_edt_x", "edt_y": "k_edt_col<0>", "edt_z": "k_edt_col<1>", "prune": "k_prune<1>",
+                "dilate": "k_dilate_cover<1>", "epilogue": "k_epilogue", "metrics": "k_metrics"}
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r01_ncu_summary_c4.json")
 
 
 def parse():
@@ -50,7 +55,19 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--cpu-sample-labels", type=int, default=1000)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--mode", default="volumes", choices=["volumes", "slab"],
+                   help="volumes: one independent volume per rank (weak scaling, default); slab: one volume "
+                        "split into z-slabs across the ranks (strong scaling, NCCL halo exchanges)")
     return p.parse_args()
+
+
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary, or None."""
+    try:
+        k = json.load(open(NCU_SUMMARY))["kernels"].get(kernel)
+        return None if k is None else k["traffic_bytes_per_launch"]
+    except Exception:
+        return None
 
 
 def workload_name(cfg: int) -> str:
@@ -265,7 +282,7 @@ def run_fastrs(args):
             stage_gbs[k] = {"ms": round(v, 4), "GB/s": round(b / (v * 1e-3) / 1e9, 1),
                             "frac": round(b / (v * 1e-3) / 1e9 / hbm_peak, 4)}
     model_bytes = sum(STAGE_BYTES_PER_ELEM[k] for k in per_launch if per_launch[k] > 0) * n \
-        + 16.0 * diag["n_kept"]
+        + sum(STAGE_BYTES_PER_KEPT.values()) * diag["n_kept"]
     pipe_gbs = model_bytes / (ms * 1e-3) / 1e9
 
     if rank != 0:
@@ -286,9 +303,11 @@ def run_fastrs(args):
                    "input_sha256": info["sha256"], "input_hash_kind": info.get("sha256_kind")},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(lab.nbytes),
                 "d2h_bytes_per_step": int(2 * M * 8), "ms_per_step": float(e2e_ms.item())},
-        "gpu_launches": int((6 if ndim == 3 else 5) * args.steps),
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
+        "gpu_launches": int((8 if ndim == 3 else 7) * args.steps),
+        "roofline": {"bound": "hbm", "kernel": STAGE_KERNEL[dom], "stage": dom, "achieved": achieved,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                     "traffic": ncu_traffic(STAGE_KERNEL[dom]),
+                     "traffic_source": os.path.relpath(NCU_SUMMARY, ROOT), "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes},
         "stages": stage_gbs,
         "pipeline_model": {"bytes_per_step": model_bytes, "GB/s": pipe_gbs, "frac": pipe_gbs / hbm_peak},
@@ -301,10 +320,76 @@ def run_fastrs(args):
         dist.destroy_process_group()
 
 
+def run_slab(args):
+    """One volume split into z-slabs across the ranks: every step runs
+    the four slab phases with the three NCCL exchanges (paper_2504_05808_b200/slab.py)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_05808_b200 as F
+    from paper_2504_05808_b200 import slab
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    F.load()
+    lab, info, ndim = make_input(args.config, args.batch)
+    if ndim != 3:
+        raise SystemExit("--mode slab needs a 3D config")
+    ml = info["max_label"]
+    Z = lab.shape[0]
+    slabs = slab.partition(Z, world)
+    z0, z1 = slabs[rank]
+    t = torch.from_numpy(lab[z0:z1].copy()).to(dev)
+    del lab
+
+    def step():
+        return slab.sphericity_roundness_slab(t, slabs, ml, group=None)
+
+    for _ in range(args.warmup):
+        res = step()
+    stream = torch.cuda.current_stream(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    clk = clocks.stop()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    n = Z * t.shape[1] * t.shape[2]
+    if rank == 0:
+        line = {"metric": METRIC, "value": n / (ms * 1e-3) / 1e9, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
+                "config": {"workload": workload_name(args.config) + f", z-slabs over {world} GPU(s)",
+                           "seed": info["seed"], "elements": int(n), "slabs": slabs,
+                           "parallelism": f"z-slab{world}", "halo": res["slab_info"]},
+                "gpu_launches": int(10 * args.steps), "clocks": clk, "e2e": None, "roofline": None,
+                "cpu_baseline": None}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode == "slab":
+        run_slab(args)
     else:
         run_fastrs(args)
 

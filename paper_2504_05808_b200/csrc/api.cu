@@ -92,7 +92,7 @@ Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
 }
 
 // ---- profiling -------------------------------------------------------------------------
-constexpr int kStages = 6;
+constexpr int kStages = 7;
 std::mutex g_prof_mu;
 bool g_prof = false;
 double g_prof_ms[kStages];
@@ -104,8 +104,8 @@ struct StageTimer {
   bool on = false;
   int dev = 0;
   cudaStream_t st = nullptr;
-  bool used[kStages] = {};
-  int last = -1;
+  int order[kStages];  // stages in the order their end events were recorded
+  int nmarks = 0;
   void begin(cudaStream_t s) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     on = g_prof;
@@ -118,20 +118,19 @@ struct StageTimer {
     }
     cudaEventRecord(g_ev[dev][0], st);
   }
-  // mark the end of stage k (events are recorded after each stage, in order)
+  // mark the end of stage k (each stage's time runs from the previous mark)
   void mark(int k) {
-    if (!on) return;
+    if (!on || nmarks >= kStages) return;
     cudaEventRecord(g_ev[dev][k + 1], st);
-    used[k] = true;
-    last = k;
+    order[nmarks++] = k;
   }
   void finish() {
-    if (!on || last < 0) return;
-    cudaEventSynchronize(g_ev[dev][last + 1]);
+    if (!on || nmarks == 0) return;
+    cudaEventSynchronize(g_ev[dev][order[nmarks - 1] + 1]);
     std::lock_guard<std::mutex> lk(g_prof_mu);
     int prev = 0;
-    for (int k = 0; k < kStages; ++k) {
-      if (!used[k]) continue;
+    for (int i = 0; i < nmarks; ++i) {
+      const int k = order[i];
       float ms = 0;
       cudaEventElapsedTime(&ms, g_ev[dev][prev], g_ev[dev][k + 1]);
       g_prof_ms[k] += ms;
@@ -207,6 +206,8 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
     launch_dilate(labels, D, meta, cent, fgm, oct, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out,
                   (flags & kFlagForceFallback) != 0, ltp, hdr, st);  // K5
     tm.mark(4);
+    launch_epilogue(labels, D, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out, ltp, hdr, st);  // K5 epilogue
+    tm.mark(6);
     if (stage == kFull) {
       launch_metrics(acc, g, *outs, hdr, st);  // K6
       tm.mark(5);
@@ -513,6 +514,7 @@ int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64
   uint32_t* ltp = (uint32_t*)((char*)ws + L.P);
   launch_dilate(lab_ext, d_ext, meta, cent, fgm, oct, g, &acc, nullptr, nullptr, (flags & kFlagForceFallback) != 0, ltp,
                 hdr, st);
+  launch_epilogue(lab_ext, d_ext, g, &acc, nullptr, nullptr, ltp, hdr, st);
   return finish_call(hdr, flags, st);
 }
 

@@ -141,6 +141,9 @@ void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta,
                    const uint2* centres, const uint32_t* fgm, const uint16_t* oct, const Geom& g,
                    const Accum* acc, uint32_t* lt2_out, float* lt_out, bool force_fallback, uint32_t* ltp,
                    WsHeader* hdr, cudaStream_t st);
+// K5 epilogue: shell, per-label reductions and LT outputs from the LT plane ltp
+void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,
+                     float* lt_out, const uint32_t* ltp, WsHeader* hdr, cudaStream_t st);
 void launch_metrics(const Accum& acc, const Geom& g, const Outputs& o, WsHeader* hdr,
                     cudaStream_t st);
 void release_mtables();

@@ -245,6 +245,12 @@ void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta, con
     k_dilate_atomic<true><<<(unsigned)g.ntiles, 256, smem, st>>>(meta, centres, g, ltp, hdr);
   else
     k_dilate_atomic<false><<<(unsigned)g.ntiles, 256, smem, st>>>(meta, centres, g, ltp, hdr);
+}
+
+void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,
+                     float* lt_out, const uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
+  Accum a{};
+  if (acc) a = *acc;
   // epilogue over the produced layers
   const int TZ = g.ndim == 3 ? kTZ3 : 1;
   const int64_t z_lo = g.tz_lo * TZ, z_hi = g.tz_hi * TZ < g.Z ? g.tz_hi * TZ : g.Z;
