@@ -58,7 +58,7 @@ int make_geom(const int64_t* dims, int ndim, int64_t batch, Geom& g) {
 inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t hdr, A, B, meta, fgm, oct, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd, total;
+  size_t hdr, A, B, meta, fgm, oct, fbl, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd, total;
 };
 
 Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
@@ -76,6 +76,7 @@ Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
   L.meta = take((size_t)g.ntiles * sizeof(TileMeta));
   L.fgm = take((size_t)g.ntiles * kRows * 4);
   L.oct = take((size_t)g.ntiles * 16 * 2);
+  L.fbl = take((size_t)g.ntiles * 4);
   L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
   L.vol = take(M * 8);
   L.nsh = take(M * 8);
@@ -203,7 +204,8 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
     launch_prune(D, g, meta, cent, fgm, oct, hdr, st);  // K4
     tm.mark(3);
     uint32_t* ltp = D == A ? B : A;  // the plane the EDT no longer needs holds LT^2
-    launch_dilate(labels, D, meta, cent, fgm, oct, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out,
+    uint32_t* fbl = (uint32_t*)(w + L.fbl);
+    launch_dilate(labels, D, meta, cent, fgm, oct, fbl, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out,
                   (flags & kFlagForceFallback) != 0, ltp, hdr, st);  // K5
     tm.mark(4);
     launch_epilogue(labels, D, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out, ltp, hdr, st);  // K5 epilogue
@@ -257,7 +259,7 @@ int finish_call(WsHeader* hdr, uint32_t flags, cudaStream_t st) {
 }
 
 struct SlabLayout {
-  size_t hdr, P, meta, fgm, oct, cent, total;
+  size_t hdr, P, meta, fgm, oct, fbl, cent, total;
 };
 SlabLayout make_slab_layout(const Geom& g) {
   SlabLayout L{};
@@ -272,6 +274,7 @@ SlabLayout make_slab_layout(const Geom& g) {
   L.meta = take((size_t)g.ntiles * sizeof(TileMeta));
   L.fgm = take((size_t)g.ntiles * kRows * 4);
   L.oct = take((size_t)g.ntiles * 16 * 2);
+  L.fbl = take((size_t)g.ntiles * 4);
   L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
   L.total = off;
   return L;
@@ -512,8 +515,9 @@ int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64
   // elements are ever read)
   const int32_t* lab_ext = labels - own_lo * g.Y * g.X;
   uint32_t* ltp = (uint32_t*)((char*)ws + L.P);
-  launch_dilate(lab_ext, d_ext, meta, cent, fgm, oct, g, &acc, nullptr, nullptr, (flags & kFlagForceFallback) != 0, ltp,
-                hdr, st);
+  uint32_t* fbl = (uint32_t*)((char*)ws + L.fbl);
+  launch_dilate(lab_ext, d_ext, meta, cent, fgm, oct, fbl, g, &acc, nullptr, nullptr, (flags & kFlagForceFallback) != 0,
+                ltp, hdr, st);
   launch_epilogue(lab_ext, d_ext, g, &acc, nullptr, nullptr, ltp, hdr, st);
   return finish_call(hdr, flags, st);
 }

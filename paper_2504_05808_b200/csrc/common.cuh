@@ -51,7 +51,8 @@ struct WsHeader {
   int32_t scale_log2;
   uint32_t n_fallback;  // tile groups handed to the atomic fallback dilation
   uint32_t dxymax;      // max partial D after the y pass (slab path: the z halo width)
-  int32_t pad[5];
+  uint32_t n_fb;        // tiles listed for the atomic fallback dilation
+  int32_t pad[4];
 };
 static_assert(sizeof(WsHeader) <= 256, "header");
 
@@ -60,7 +61,7 @@ struct TileMeta {
   uint32_t count;  // kept centres
   uint32_t maxD;   // max D over kept centres
   uint32_t nfg;    // foreground elements of the tile
-  uint32_t pad;    // set by the sorted-cover dilation when it leaves the tile to the fallback
+  uint32_t pad;
 };
 
 // per-label accumulators (SoA)
@@ -138,9 +139,9 @@ cudaError_t ensure_mtables(int device);  // builds the per-device lattice tables
 void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, uint32_t* fgm, uint16_t* oct,
                   WsHeader* hdr, cudaStream_t st);
 void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta,
-                   const uint2* centres, const uint32_t* fgm, const uint16_t* oct, const Geom& g,
-                   const Accum* acc, uint32_t* lt2_out, float* lt_out, bool force_fallback, uint32_t* ltp,
-                   WsHeader* hdr, cudaStream_t st);
+                   const uint2* centres, const uint32_t* fgm, const uint16_t* oct, uint32_t* fbl,
+                   const Geom& g, const Accum* acc, uint32_t* lt2_out, float* lt_out, bool force_fallback,
+                   uint32_t* ltp, WsHeader* hdr, cudaStream_t st);
 // K5 epilogue: shell, per-label reductions and LT outputs from the LT plane ltp
 void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,
                      float* lt_out, const uint32_t* ltp, WsHeader* hdr, cudaStream_t st);

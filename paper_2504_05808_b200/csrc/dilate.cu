@@ -236,7 +236,8 @@ template <bool IS3D>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t* __restrict__ fgm,
                                                                 TileMeta* __restrict__ meta,
                                                                 const uint2* __restrict__ cent,
-                                                                const uint16_t* __restrict__ oct, Geom g,
+                                                                const uint16_t* __restrict__ oct,
+                                                                uint32_t* __restrict__ fbl, Geom g,
                                                                 int force_fallback, int point_at,
                                                                 uint32_t* __restrict__ ltp, WsHeader* __restrict__ hdr) {
   using P = Shape<IS3D>;
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
   const bool active = have_tile && meta[mtile].nfg != 0;
   if (__syncthreads_or(active) == 0) return;  // the whole group is background
   if (force_fallback) {
-    if (lane == 0 && have_tile) meta[mtile].pad = 1u;
+    if (lane == 0 && have_tile) fbl[atomicAdd(&hdr->n_fb, 1u)] = (uint32_t)mtile;
     return;
   }
   const int64_t item = b * g.Z * g.Y * g.X;
@@ -595,7 +596,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
   }
 
   if (S.fallback) {  // leave this group to k_dilate_atomic
-    if (lane == 0 && have_tile) meta[mtile].pad = 1u;
+    if (lane == 0 && have_tile) fbl[atomicAdd(&hdr->n_fb, 1u)] = (uint32_t)mtile;
     if (tid == 0) atomicAdd(&hdr->n_fallback, 1u);
     return;
   }
@@ -617,8 +618,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
 
 size_t dilate_cover_smem() { return sizeof(Smem); }
 
-void launch_dilate_cover(const uint32_t* fgm, TileMeta* meta, const uint2* centres, const uint16_t* oct, const Geom& g,
-                         int force_fallback, uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
+void launch_dilate_cover(const uint32_t* fgm, TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
+                         const Geom& g, int force_fallback, uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
   const int GX = g.ndim == 3 ? 1 : 2, GY = 2, GZ = g.ndim == 3 ? 2 : 1;
   const int64_t ngroups = g.B * ((g.ntx + GX - 1) / GX) * ((g.nty + GY - 1) / GY) * ((g.tz_hi - g.tz_lo + GZ - 1) / GZ);
   if (ngroups <= 0) return;
@@ -629,10 +630,10 @@ void launch_dilate_cover(const uint32_t* fgm, TileMeta* meta, const uint2* centr
     return p < 0 ? 0 : (p > kPoint ? kPoint : p);
   }();
   if (g.ndim == 3)
-    k_dilate_cover<true><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(fgm, meta, centres, oct, g, force_fallback,
+    k_dilate_cover<true><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(fgm, meta, centres, oct, fbl, g, force_fallback,
                                                                         point_at, ltp, hdr);
   else
-    k_dilate_cover<false><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(fgm, meta, centres, oct, g, force_fallback,
+    k_dilate_cover<false><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(fgm, meta, centres, oct, fbl, g, force_fallback,
                                                                          point_at, ltp, hdr);
 }
 

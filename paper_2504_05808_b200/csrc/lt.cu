@@ -27,18 +27,12 @@ __device__ __forceinline__ int isqrt_i(int h) {
 constexpr int kRcap = 1024;
 
 template <bool IS3D>
-__global__ void __launch_bounds__(256) k_dilate_atomic(const TileMeta* __restrict__ meta, const uint2* __restrict__ cent,
-                                                Geom g, uint32_t* __restrict__ ltp, WsHeader* __restrict__ hdr) {
+__device__ __forceinline__ void dilate_tile_atomic(int64_t tile, const TileMeta* __restrict__ meta,
+                                                   const uint2* __restrict__ cent, const Geom& g,
+                                                   uint32_t* __restrict__ ltp, WsHeader* __restrict__ hdr, uint32_t* T,
+                                                   uint32_t* s_rt, uint32_t* s_rpre, int& s_nr) {
   constexpr int TY = IS3D ? 8 : 64, TZ = IS3D ? 8 : 1;
-  extern __shared__ uint32_t T[];  // kRows * kRowStride
-  __shared__ uint32_t s_rt[kRcap];
-  __shared__ uint32_t s_rpre[kRcap + 1];
-  __shared__ int s_nr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t tile = blockIdx.x;
-  const TileMeta mt = meta[tile];
-  // the sorted-cover kernel (dilate.cu) handles every tile unless Dmax > 65535 or it flagged the tile
-  if (mt.nfg == 0 || (hdr->dmax <= kU16Max && mt.pad == 0)) return;
   int64_t t = tile;
   const int64_t tx = t % g.ntx;
   t /= g.ntx;
@@ -46,7 +40,7 @@ __global__ void __launch_bounds__(256) k_dilate_atomic(const TileMeta* __restric
   t /= g.nty;
   const int64_t tz = t % g.ntz;
   const int64_t b = t / g.ntz;
-  if (tz < g.tz_lo || tz >= g.tz_hi) return;  // slab path: halo tiles only feed the gather
+  if (tz < g.tz_lo || tz >= g.tz_hi) return;  // slab path: halo tiles only feed the gather (uniform)
   const int64_t ox = tx * kTX, oy = ty * TY, oz = tz * TZ;
 
   for (int i = tid; i < kRows * kRowStride; i += 256) T[i] = 0;
@@ -183,6 +177,26 @@ __global__ void __launch_bounds__(256) k_dilate_atomic(const TileMeta* __restric
   if (lane == 0 && n_int) atomicAdd(&hdr->n_intervals, n_int);
 }
 
+// Grid-stride over the work: every tile when Dmax > 65535 (the exact-order kernel stores u16
+// values and leaves everything here), else the tiles it listed in fbl (hdr->n_fb of them).
+template <bool IS3D>
+__global__ void __launch_bounds__(256) k_dilate_atomic(const TileMeta* __restrict__ meta, const uint2* __restrict__ cent,
+                                                Geom g, const uint32_t* __restrict__ fbl, uint32_t* __restrict__ ltp,
+                                                WsHeader* __restrict__ hdr) {
+  extern __shared__ uint32_t T[];  // kRows * kRowStride
+  __shared__ uint32_t s_rt[kRcap];
+  __shared__ uint32_t s_rpre[kRcap + 1];
+  __shared__ int s_nr;
+  const bool all = hdr->dmax > kU16Max;
+  const int64_t nitems = all ? g.ntiles : (int64_t)hdr->n_fb;
+  for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int64_t tile = all ? it : (int64_t)fbl[it];
+    if (meta[tile].nfg != 0) dilate_tile_atomic<IS3D>(tile, meta, cent, g, ltp, hdr, T, s_rt, s_rpre, s_nr);
+    __syncthreads();  // shared memory is reused by the next tile
+  }
+}
+
+
 // ---------------------------------------------------------------------------------------
 // K5 epilogue (streaming, full occupancy): per element LT^2 from the LT plane, shell (D == 1),
 // LT outputs and the per-label reductions (a7); one warp per x-row of the produced z range,
@@ -233,18 +247,23 @@ cudaError_t dilate_atomic_setup() {
 }
 
 void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta, const uint2* centres,
-                   const uint32_t* fgm, const uint16_t* oct, const Geom& g, const Accum* acc, uint32_t* lt2_out,
-                   float* lt_out, bool force_fallback, uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
+                   const uint32_t* fgm, const uint16_t* oct, uint32_t* fbl, const Geom& g, const Accum* acc,
+                   uint32_t* lt2_out, float* lt_out, bool force_fallback, uint32_t* ltp, WsHeader* hdr,
+                   cudaStream_t st) {
   Accum a{};
   if (acc) a = *acc;
   // both dilation kernels read Dmax / the per-tile fallback flag on the device; the atomic
   // kernel only processes tiles the exact-order kernel left to it.  Both write LT^2 to ltp.
-  launch_dilate_cover(fgm, meta, centres, oct, g, force_fallback ? 1 : 0, ltp, hdr, st);
+  launch_dilate_cover(fgm, meta, centres, oct, fbl, g, force_fallback ? 1 : 0, ltp, hdr, st);
   const size_t smem = (size_t)kRows * kRowStride * 4;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)(g.ntiles < (int64_t)nsm * 4 ? g.ntiles : (int64_t)nsm * 4);
   if (g.ndim == 3)
-    k_dilate_atomic<true><<<(unsigned)g.ntiles, 256, smem, st>>>(meta, centres, g, ltp, hdr);
+    k_dilate_atomic<true><<<grid, 256, smem, st>>>(meta, centres, g, fbl, ltp, hdr);
   else
-    k_dilate_atomic<false><<<(unsigned)g.ntiles, 256, smem, st>>>(meta, centres, g, ltp, hdr);
+    k_dilate_atomic<false><<<grid, 256, smem, st>>>(meta, centres, g, fbl, ltp, hdr);
 }
 
 void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,
