@@ -96,6 +96,8 @@ typedef struct {
   uint64_t n_intervals;   /* (ball, row) intervals emitted by the dilation (K5)          */
   int32_t sum_scale_log2; /* fixed-point scale of the LT sums (2^s)                      */
   uint32_t n_fallback;   /* tile groups handed to the atomic fallback dilation         */
+  uint32_t n_rounds_extra; /* K5: candidate-list rounds beyond the first, summed over groups */
+  uint32_t n_regathers;  /* K5: list overflows that needed a second gather pass         */
 } fastrs_diagnostics;
 
 /* Bytes of device workspace needed by every entry point below for this geometry.

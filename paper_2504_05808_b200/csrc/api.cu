@@ -404,6 +404,8 @@ int fastrs_read_diagnostics(const void* ws, fastrs_diagnostics* out, void* strea
   out->n_intervals = h.n_intervals;
   out->sum_scale_log2 = h.scale_log2;
   out->n_fallback = h.n_fallback;
+  out->n_rounds_extra = h.n_rounds_extra;
+  out->n_regathers = h.n_regathers;
   return FASTRS_OK;
 }
 

@@ -52,7 +52,9 @@ struct WsHeader {
   uint32_t n_fallback;  // tile groups handed to the atomic fallback dilation
   uint32_t dxymax;      // max partial D after the y pass (slab path: the z halo width)
   uint32_t n_fb;        // tiles listed for the atomic fallback dilation
-  int32_t pad[4];
+  uint32_t n_rounds_extra;  // K5 groups x rounds beyond the first
+  uint32_t n_regathers;     // K5 list overflows that needed a second gather pass
+  int32_t pad[2];
 };
 static_assert(sizeof(WsHeader) <= 256, "header");
 

@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
     if (S.fallback) break;
     const int rlo = S.round_lo;
     if (S.count > kCap) {  // the list overflowed: gather again, keeping [rlo, rhi] only (they fit)
+      if (tid == 0) atomicAdd(&hdr->n_regathers, 1u);
       __syncthreads();
       if (tid == 0) S.count = 0;
       __syncthreads();
@@ -591,7 +592,10 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
     }
     if (last_round) break;
     __syncthreads();
-    if (tid == 0) S.round_hi = S.next_hi;
+    if (tid == 0) {
+      S.round_hi = S.next_hi;
+      atomicAdd(&hdr->n_rounds_extra, 1u);
+    }
     __syncthreads();
   }
 

@@ -45,4 +45,4 @@ F.profile(False)
 d = F.diagnostics(F.last_workspace())
 print(json.dumps({"env": {k: v for k, v in os.environ.items() if k.startswith("FASTRS_")},
                   "ms": {k: round(v / calls, 3) for k, v in ms.items()}, "total_ms": round(sum(ms.values()) / calls, 3),
-                  "n_intervals": d["n_intervals"], "n_fallback": d["n_fallback"]}))
+                  "diag": d}))
