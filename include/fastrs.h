@@ -98,6 +98,8 @@ typedef struct {
   uint32_t n_fallback;   /* tile groups handed to the atomic fallback dilation         */
   uint32_t n_rounds_extra; /* K5: candidate-list rounds beyond the first, summed over groups */
   uint32_t n_regathers;  /* K5: list overflows that needed a second gather pass         */
+  uint32_t max_group_list; /* K5: longest per-group candidate list                      */
+  uint64_t sum_group_list; /* K5: candidates summed over tile groups                    */
 } fastrs_diagnostics;
 
 /* Bytes of device workspace needed by every entry point below for this geometry.

@@ -58,7 +58,7 @@ int make_geom(const int64_t* dims, int ndim, int64_t batch, Geom& g) {
 inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t hdr, A, B, meta, fgm, oct, fbl, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd, total;
+  size_t hdr, A, B, meta, fgm, oct, fbl, gcount, goff, pool, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd, total;
 };
 
 Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
@@ -77,6 +77,9 @@ Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
   L.fgm = take((size_t)g.ntiles * kRows * 4);
   L.oct = take((size_t)g.ntiles * 16 * 2);
   L.fbl = take((size_t)g.ntiles * 4);
+  L.gcount = take((size_t)dilate_groups(g) * 4);
+  L.goff = take((size_t)dilate_groups(g) * 4);
+  L.pool = take((size_t)dilate_pool_entries(g) * 8);
   L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
   L.vol = take(M * 8);
   L.nsh = take(M * 8);
@@ -205,7 +208,8 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
     tm.mark(3);
     uint32_t* ltp = D == A ? B : A;  // the plane the EDT no longer needs holds LT^2
     uint32_t* fbl = (uint32_t*)(w + L.fbl);
-    launch_dilate(labels, D, meta, cent, fgm, oct, fbl, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out,
+    launch_dilate(labels, D, meta, cent, fgm, oct, fbl, (unsigned long long*)(w + L.pool), (uint32_t*)(w + L.gcount),
+                  (uint32_t*)(w + L.goff), g, stage == kFull ? &acc : nullptr, lt2_out, lt_out,
                   (flags & kFlagForceFallback) != 0, ltp, hdr, st);  // K5
     tm.mark(4);
     launch_epilogue(labels, D, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out, ltp, hdr, st);  // K5 epilogue
@@ -259,7 +263,7 @@ int finish_call(WsHeader* hdr, uint32_t flags, cudaStream_t st) {
 }
 
 struct SlabLayout {
-  size_t hdr, P, meta, fgm, oct, fbl, cent, total;
+  size_t hdr, P, meta, fgm, oct, fbl, gcount, goff, pool, cent, total;
 };
 SlabLayout make_slab_layout(const Geom& g) {
   SlabLayout L{};
@@ -275,6 +279,9 @@ SlabLayout make_slab_layout(const Geom& g) {
   L.fgm = take((size_t)g.ntiles * kRows * 4);
   L.oct = take((size_t)g.ntiles * 16 * 2);
   L.fbl = take((size_t)g.ntiles * 4);
+  L.gcount = take((size_t)dilate_groups(g) * 4);
+  L.goff = take((size_t)dilate_groups(g) * 4);
+  L.pool = take((size_t)dilate_pool_entries(g) * 8);
   L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
   L.total = off;
   return L;
@@ -406,6 +413,8 @@ int fastrs_read_diagnostics(const void* ws, fastrs_diagnostics* out, void* strea
   out->n_fallback = h.n_fallback;
   out->n_rounds_extra = h.n_rounds_extra;
   out->n_regathers = h.n_regathers;
+  out->max_group_list = h.max_group_list;
+  out->sum_group_list = h.sum_group_list;
   return FASTRS_OK;
 }
 
@@ -518,8 +527,9 @@ int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64
   const int32_t* lab_ext = labels - own_lo * g.Y * g.X;
   uint32_t* ltp = (uint32_t*)((char*)ws + L.P);
   uint32_t* fbl = (uint32_t*)((char*)ws + L.fbl);
-  launch_dilate(lab_ext, d_ext, meta, cent, fgm, oct, fbl, g, &acc, nullptr, nullptr, (flags & kFlagForceFallback) != 0,
-                ltp, hdr, st);
+  launch_dilate(lab_ext, d_ext, meta, cent, fgm, oct, fbl, (unsigned long long*)((char*)ws + L.pool),
+                (uint32_t*)((char*)ws + L.gcount), (uint32_t*)((char*)ws + L.goff), g, &acc, nullptr, nullptr, (flags & kFlagForceFallback) != 0, ltp,
+                hdr, st);
   launch_epilogue(lab_ext, d_ext, g, &acc, nullptr, nullptr, ltp, hdr, st);
   return finish_call(hdr, flags, st);
 }

@@ -54,7 +54,10 @@ struct WsHeader {
   uint32_t n_fb;        // tiles listed for the atomic fallback dilation
   uint32_t n_rounds_extra;  // K5 groups x rounds beyond the first
   uint32_t n_regathers;     // K5 list overflows that needed a second gather pass
-  int32_t pad[2];
+  uint32_t max_group_list;  // K5 longest per-group candidate list
+  uint32_t pad[1];
+  unsigned long long sum_group_list;  // K5 candidates summed over groups
+  unsigned long long pool_used;       // K5 candidate pool entries allocated
 };
 static_assert(sizeof(WsHeader) <= 256, "header");
 
@@ -142,8 +145,11 @@ void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centr
                   WsHeader* hdr, cudaStream_t st);
 void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta,
                    const uint2* centres, const uint32_t* fgm, const uint16_t* oct, uint32_t* fbl,
-                   const Geom& g, const Accum* acc, uint32_t* lt2_out, float* lt_out, bool force_fallback,
-                   uint32_t* ltp, WsHeader* hdr, cudaStream_t st);
+                   unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, const Accum* acc,
+                   uint32_t* lt2_out, float* lt_out, bool force_fallback, uint32_t* ltp, WsHeader* hdr,
+                   cudaStream_t st);
+int64_t dilate_groups(const Geom& g);        // K5 tile groups (gcount / goff entries)
+int64_t dilate_pool_entries(const Geom& g);  // K5 candidate pool (sorted per-group lists), u64 entries
 // K5 epilogue: shell, per-label reductions and LT outputs from the LT plane ltp
 void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,
                      float* lt_out, const uint32_t* ltp, WsHeader* hdr, cudaStream_t st);

@@ -36,24 +36,30 @@ constexpr int kWarps = 4;  // warps per CTA = tiles per group
 constexpr int kCap = 3072;   // candidate list capacity per round
 constexpr int kBuckets = 128;
 constexpr int kHist = 1536;  // exact-D counting-sort bins per round
-constexpr int kPoint = 128;  // uncovered cells at which a warp switches to point tests
+constexpr int kPoint = 128;
+constexpr uint32_t kGroupFallback = 0xFFFFFFFFu;  // uncovered cells at which a warp switches to point tests
 constexpr int kOff = 16384;  // coordinate bias of packed candidates
 
 struct Smem;
 static_assert(3 * 512 <= 1536 && 2 * (512 + 8) + 512 <= 3072, "gather scratch fits S.hist / S.idx");
 
-struct Smem {
+struct Smem {  // K5a (gather + sort)
   unsigned long long list[kCap];     // gathered candidates (centre relative to the group), gather order
-  uint16_t val[kWarps][kRows * 32];  // LT^2 per element of each warp's tile (D <= 65535 here)
-  uint32_t hist[kHist];              // exact-D counting sort: bin Dhi - D
+  uint32_t hist[kHist];              // exact-D counting sort: bin Dhi - D (rounds path; gather scratch)
   uint16_t idx[kCap];                // indices into list, sorted by D (descending)
-  uint32_t fg[kWarps][kRows];        // foreground mask per row
-  uint32_t cov[kWarps][kRows];       // covered (final value written)
-  uint16_t ulist[kWarps][kPoint];    // point mode: the still-uncovered cells (row*32 + x)
+  uint32_t dh[kHist];                // exact-D histogram / cursors of the single-pass path
   uint32_t bhist[kBuckets];
+  unsigned long long base;           // the group's offset in the global candidate pool
   uint32_t wsum[kWarps];
   uint32_t count, total, nrec;
   int round_lo, round_hi, round_top, next_hi, fallback, rounds;
+};
+
+struct PaintSmem {  // K5b (one tile per warp)
+  uint16_t val[kWarps][kRows * 32];  // LT^2 per element of each warp's tile (D <= 65535 here)
+  uint32_t fg[kWarps][kRows];        // foreground mask per row
+  uint32_t cov[kWarps][kRows];       // covered (final value written)
+  uint16_t ulist[kWarps][kPoint];    // point mode: the still-uncovered cells (row*32 + x)
 };
 
 template <bool IS3D>
@@ -90,10 +96,51 @@ __device__ __forceinline__ uint32_t range_mask(int l, int r) {  // bits l..r (0 
 // S.hist and S.idx serve as scratch (they are rebuilt by the sort afterwards).
 constexpr int kRecCap = 512;  // records per chunk: 3 words each in S.hist, prefix sums in S.idx
 
-template <bool IS3D, bool HIST>
+// Exclusive prefix sum of a[0..n) (n <= kHist) in place by the whole CTA; returns the total.
+// Ends with a barrier.
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t* a, int n, uint32_t* wsum) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kPer = kHist / (kWarps * 32);
+  const int base = tid * kPer;
+  uint32_t loc[kPer], sum = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    loc[j] = base + j < n ? a[base + j] : 0u;
+    sum += loc[j];
+  }
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  uint32_t run = inc - sum, total = 0;
+  for (int w = 0; w < kWarps; ++w) {
+    if (w < warp) run += wsum[w];
+    total += wsum[w];
+  }
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    if (base + j < n) a[base + j] = run;
+    run += loc[j];
+  }
+  __syncthreads();
+  return total;
+}
+
+// gather modes: what happens to each candidate that reaches the group
+enum { kListBucketHist = 0,  // append to S.list (up to kCap) and count its D bucket in S.bhist
+       kListOnly = 1,        // append to S.list
+       kListExactHist = 2,   // append to S.list and count its exact D in S.dh (bin dtop - D)
+       kScatter = 3 };       // store it at out[S.dh[dtop - D]++] (S.dh holds the sorted cursors)
+
+template <bool IS3D, int MODE>
 __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ meta, const uint2* __restrict__ cent,
                                        const uint16_t* __restrict__ oct, const Geom& g, int64_t b, int64_t tx0,
-                                       int64_t ty0, int64_t tz0, int nrx, int nry, int nrz, int blo, int bhi) {
+                                       int64_t ty0, int64_t tz0, int nrx, int nry, int nrz, int blo, int bhi,
+                                       uint32_t dtop = 0, unsigned long long* out = nullptr) {
   using P = Shape<IS3D>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nx = P::GX + 2 * nrx, ny = P::GY + 2 * nry, nz = P::GZ + 2 * nrz;
@@ -191,15 +238,20 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
       }
       const uint32_t tm = __ballot_sync(kFull, take);
       if (tm) {
-        if (HIST) {
-          const uint32_t grp = __match_any_sync(kFull, take ? bk : -1);
-          if (take && lane == __ffs(grp) - 1) atomicAdd(&S.bhist[bk], (uint32_t)__popc(grp));
+        if (MODE == kScatter) {
+          if (take) out[atomicAdd(&S.dh[dtop - (uint32_t)(pe & 0xFFFFu)], 1u)] = pe;
+        } else {
+          if (MODE == kListBucketHist) {
+            const uint32_t grp = __match_any_sync(kFull, take ? bk : -1);
+            if (take && lane == __ffs(grp) - 1) atomicAdd(&S.bhist[bk], (uint32_t)__popc(grp));
+          }
+          if (MODE == kListExactHist && take) atomicAdd(&S.dh[dtop - (uint32_t)(pe & 0xFFFFu)], 1u);
+          uint32_t base = 0;
+          if (lane == 0) base = atomicAdd(&S.count, (uint32_t)__popc(tm));
+          base = __shfl_sync(kFull, base, 0);
+          const uint32_t pos = base + __popc(tm & ((1u << lane) - 1u));
+          if (take && pos < kCap) S.list[pos] = pe;
         }
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&S.count, (uint32_t)__popc(tm));
-        base = __shfl_sync(kFull, base, 0);
-        const uint32_t pos = base + __popc(tm & ((1u << lane) - 1u));
-        if (take && pos < kCap) S.list[pos] = pe;
       }
     }
   }
@@ -233,13 +285,15 @@ __device__ __forceinline__ unsigned long long row_box(int ya, int yb, int za, in
 }
 
 template <bool IS3D>
-__global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t* __restrict__ fgm,
-                                                                TileMeta* __restrict__ meta,
-                                                                const uint2* __restrict__ cent,
-                                                                const uint16_t* __restrict__ oct,
-                                                                uint32_t* __restrict__ fbl, Geom g,
-                                                                int force_fallback, int point_at,
-                                                                uint32_t* __restrict__ ltp, WsHeader* __restrict__ hdr) {
+__global__ void __launch_bounds__(kWarps * 32, 5) k_dilate_gather(const TileMeta* __restrict__ meta,
+                                                               const uint2* __restrict__ cent,
+                                                               const uint16_t* __restrict__ oct,
+                                                               uint32_t* __restrict__ fbl, Geom g, int force_fallback,
+                                                               unsigned long long* __restrict__ pool,
+                                                               unsigned long long pool_cap,
+                                                               uint32_t* __restrict__ gcount,
+                                                               uint32_t* __restrict__ goff,
+                                                               WsHeader* __restrict__ hdr) {
   using P = Shape<IS3D>;
   constexpr int TY = P::TY, TZ = P::TZ;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -267,75 +321,68 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
   const int64_t mtile = have_tile ? ((b * g.ntz + mtz) * g.nty + mty) * g.ntx + mtx : 0;
   const int mox = wx * kTX, moy = wy * TY, moz = wz * TZ;  // my tile origin within the group
   const bool active = have_tile && meta[mtile].nfg != 0;
-  if (__syncthreads_or(active) == 0) return;  // the whole group is background
-  if (force_fallback) {
-    if (lane == 0 && have_tile) fbl[atomicAdd(&hdr->n_fb, 1u)] = (uint32_t)mtile;
+  const int64_t group = blockIdx.x;
+  if (__syncthreads_or(active) == 0) {  // the whole group is background
+    if (tid == 0) gcount[group] = 0;
     return;
   }
-  const int64_t item = b * g.Z * g.Y * g.X;
-
-  // ---- per-warp init: values, foreground masks, coverage ----------------------------------
-  uint16_t* val = S.val[warp];
-  uint32_t* fgw = S.fg[warp];
-  uint32_t* covw = S.cov[warp];
-  {
-    uint4* v4 = reinterpret_cast<uint4*>(val);
-#pragma unroll 4
-    for (int i = lane; i < kRows * 32 / 8; i += 32) v4[i] = make_uint4(0u, 0u, 0u, 0u);
+  if (force_fallback) {
+    if (lane == 0 && have_tile) fbl[atomicAdd(&hdr->n_fb, 1u)] = (uint32_t)mtile;
+    if (tid == 0) gcount[group] = kGroupFallback;
+    return;
   }
-  // rows of my tile that still hold uncovered foreground, per 8-column chunk of x (K4 wrote
-  // the tile's foreground row masks)
-  unsigned long long Uc[4] = {0, 0, 0, 0};
-  {
-    uint32_t f[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      f[k] = active ? fgm[mtile * kRows + lane + 32 * k] : 0u;
-      fgw[lane + 32 * k] = f[k];
-      covw[lane + 32 * k] = 0;
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      Uc[c] = (unsigned long long)__ballot_sync(kFull, (f[0] >> (8 * c)) & 0xFFu) |
-              ((unsigned long long)__ballot_sync(kFull, (f[1] >> (8 * c)) & 0xFFu) << 32);
-  }
-  __syncwarp();
-  // uncovered foreground cells of my tile (warp-uniform); point mode once it is small
-  int nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(fgw[lane]) + __popc(fgw[lane + 32])));
-  bool pmode = false;
-  uint16_t* ulist = S.ulist[warp];
-  int ub[6] = {0, kTX - 1, 0, TY - 1, 0, TZ - 1};  // bounding box of the uncovered cells (point mode)
-  auto ubox_refresh = [&]() {
-    int x0 = 1 << 20, x1 = -1, y0 = 1 << 20, y1 = -1, z0 = 1 << 20, z1 = -1;
-    for (int q = lane; q < nu; q += 32) {
-      const int e = ulist[q], x = e & 31, row = e >> 5;
-      const int ly = IS3D ? (row & 7) : row, lz = IS3D ? (row >> 3) : 0;
-      x0 = min(x0, x); x1 = max(x1, x); y0 = min(y0, ly); y1 = max(y1, ly); z0 = min(z0, lz); z1 = max(z1, lz);
-    }
-    ub[0] = __reduce_min_sync(kFull, x0); ub[1] = __reduce_max_sync(kFull, x1);
-    ub[2] = __reduce_min_sync(kFull, y0); ub[3] = __reduce_max_sync(kFull, y1);
-    ub[4] = __reduce_min_sync(kFull, z0); ub[5] = __reduce_max_sync(kFull, z1);
-  };
-
   const int rmax = dmax > 0 ? isqrt16((int)(dmax - 1)) : 0;
   const int nrx = (rmax + kTX - 1) / kTX, nry = (rmax + TY - 1) / TY, nrz = IS3D ? (rmax + TZ - 1) / TZ : 0;
-  uint32_t n_rows = 0;
-
-  // ---- rounds over D-bucket ranges (normally exactly one) --------------------------------
+  uint32_t written = 0;
+  if (tid == 0) {
+    S.fallback = 0;
+    S.base = 0;
+  }
+  __syncthreads();
+  if (dmax <= (uint32_t)kHist) {
+    // ---- single pass: the exact-D histogram is built while gathering, the group's slice of
+    // the global pool is allocated, and the list is scattered to its sorted (descending D)
+    // positions; a list that overflowed the shared buffer is regathered straight to the pool
+    const uint32_t dtop = dmax;
+    for (int k = tid; k < (int)dtop; k += kWarps * 32) S.dh[k] = 0;
+    if (tid == 0) S.count = 0;
+    __syncthreads();
+    gather<IS3D, kListExactHist>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, 0, kBuckets - 1, dtop);
+    const uint32_t total = S.count;
+    if (tid == 0) {
+      const unsigned long long b0 = atomicAdd(&hdr->pool_used, (unsigned long long)total);
+      S.base = b0;
+      if (b0 + total > pool_cap) S.fallback = 1;
+    }
+    block_exclusive_scan(S.dh, (int)dtop, S.wsum);
+    if (!S.fallback) {
+      unsigned long long* out = pool + S.base;
+      if (total <= (uint32_t)kCap) {
+        for (uint32_t i = tid; i < total; i += kWarps * 32) {
+          const unsigned long long pe = S.list[i];
+          out[atomicAdd(&S.dh[dtop - (uint32_t)(pe & 0xFFFFu)], 1u)] = pe;
+        }
+      } else {
+        if (tid == 0) atomicAdd(&hdr->n_regathers, 1u);
+        gather<IS3D, kScatter>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, 0, kBuckets - 1, dtop, out);
+      }
+      written = total;
+    }
+    __syncthreads();
+  } else {
+  // ---- rounds over D-bucket ranges (Dmax > kHist): each round an exactly sorted chunk
+  unsigned long long* out = nullptr;
   if (tid == 0) {
     S.round_hi = kBuckets - 1;
-    S.fallback = 0;
     S.rounds = 0;
   }
   __syncthreads();
   for (;;) {
-    // every tile of the group fully covered: nothing left to gather
-    if (__syncthreads_or(nu != 0) == 0) break;
     const int rhi = S.round_hi;
     for (int i = tid; i < kBuckets; i += kWarps * 32) S.bhist[i] = 0;
     if (tid == 0) S.count = 0;
     __syncthreads();
-    gather<IS3D, true>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, 0, rhi);
+    gather<IS3D, kListBucketHist>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, 0, rhi);
     __syncthreads();
     // --- this round's bucket range [rlo, rhi]: as many buckets as fit the list and the sort
     // range (warp 0: descending inclusive scan of the histogram, 4 buckets per lane)
@@ -379,9 +426,15 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
         if (k <= lo) below += h[q];
       }
       below = __reduce_add_sync(kFull, below);
+      if (lane == 31 && S.rounds == 0) {  // first round: the histogram covers every candidate
+        const unsigned long long b0 = atomicAdd(&hdr->pool_used, (unsigned long long)inc);
+        S.base = b0;
+        if (b0 + inc > pool_cap) S.fallback = 1;
+      }
+      __syncwarp();
       if (lane == 0) {
         // a single bucket exceeds the list / range, or (defensive) too many rounds
-        S.fallback = ((lo == top && lo >= 0) || ++S.rounds > kBuckets) ? 1 : 0;
+        S.fallback = (S.fallback || (lo == top && lo >= 0) || ++S.rounds > kBuckets) ? 1 : 0;
         S.round_lo = lo + 1;
         S.round_top = top;
         S.next_hi = below ? lo : -1;
@@ -395,7 +448,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
       __syncthreads();
       if (tid == 0) S.count = 0;
       __syncthreads();
-      gather<IS3D, false>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, rlo, rhi);
+      gather<IS3D, kListOnly>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, rlo, rhi);
       __syncthreads();
     }
     // --- exact counting sort of the list indices by D (descending), D in [dlo, dhi]
@@ -445,6 +498,120 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
     const uint32_t total = S.total;
     const bool last_round = S.next_hi < 0;
 
+    // --- append the round (exactly descending D) to the group's slice of the pool
+    out = pool + S.base;
+    for (uint32_t i = tid; i < total; i += kWarps * 32) out[written + i] = S.list[S.idx[i]];
+    written += total;
+    if (last_round) break;
+    __syncthreads();
+    if (tid == 0) {
+      S.round_hi = S.next_hi;
+      atomicAdd(&hdr->n_rounds_extra, 1u);
+    }
+    __syncthreads();
+  }
+
+  }
+  if (S.fallback) {  // leave this group to k_dilate_atomic
+    if (lane == 0 && active) fbl[atomicAdd(&hdr->n_fb, 1u)] = (uint32_t)mtile;
+    if (tid == 0) {
+      atomicAdd(&hdr->n_fallback, 1u);
+      gcount[group] = kGroupFallback;
+    }
+    return;
+  }
+  if (tid == 0) {
+    gcount[group] = written;
+    goff[group] = (uint32_t)S.base;
+    atomicMax(&hdr->max_group_list, written);
+    atomicAdd(&hdr->sum_group_list, (unsigned long long)written);
+  }
+}
+
+template <bool IS3D>
+__global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __restrict__ fgm,
+                                                              const TileMeta* __restrict__ meta, Geom g,
+                                                              const unsigned long long* __restrict__ pool,
+                                                              const uint32_t* __restrict__ gcount,
+                                                              const uint32_t* __restrict__ goff, int point_at,
+                                                              uint32_t* __restrict__ ltp, WsHeader* __restrict__ hdr) {
+  using P = Shape<IS3D>;
+  constexpr int TY = P::TY, TZ = P::TZ;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PaintSmem& S = *reinterpret_cast<PaintSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (hdr->dmax > kU16Max) return;  // k_dilate_atomic handles it
+
+  // ---- group / tile coordinates --------------------------------------------------------
+  // groups tile the layers [tz_lo, tz_hi) (all layers except on the slab path)
+  const int64_t ngx = (g.ntx + P::GX - 1) / P::GX, ngy = (g.nty + P::GY - 1) / P::GY;
+  const int64_t ngz = (g.tz_hi - g.tz_lo + P::GZ - 1) / P::GZ;
+  int64_t t = blockIdx.x;
+  const int64_t gxi = t % ngx;
+  t /= ngx;
+  const int64_t gyi = t % ngy;
+  t /= ngy;
+  const int64_t gzi = t % ngz;
+  const int64_t b = t / ngz;
+  const int64_t tx0 = gxi * P::GX, ty0 = gyi * P::GY, tz0 = g.tz_lo + gzi * P::GZ;
+  const int64_t rox = tx0 * kTX, roy = ty0 * TY, roz = tz0 * TZ;  // group origin
+  const int wx = warp % P::GX, wy = (warp / P::GX) % P::GY, wz = warp / (P::GX * P::GY);
+  const int64_t mtx = tx0 + wx, mty = ty0 + wy, mtz = tz0 + wz;
+  const bool have_tile = mtx < g.ntx && mty < g.nty && mtz < g.tz_hi;
+  const int64_t mtile = have_tile ? ((b * g.ntz + mtz) * g.nty + mty) * g.ntx + mtx : 0;
+  const int mox = wx * kTX, moy = wy * TY, moz = wz * TZ;  // my tile origin within the group
+  const bool active = have_tile && meta[mtile].nfg != 0;
+  const int64_t group = blockIdx.x;
+  const uint32_t total = gcount[group];
+  if (!active || total == kGroupFallback) return;  // background, or left to k_dilate_atomic
+  const unsigned long long* list = pool + goff[group];
+  const int64_t item = b * g.Z * g.Y * g.X;
+
+  // ---- per-warp init: values, foreground masks, coverage ----------------------------------
+  uint16_t* val = S.val[warp];
+  uint32_t* fgw = S.fg[warp];
+  uint32_t* covw = S.cov[warp];
+  {
+    uint4* v4 = reinterpret_cast<uint4*>(val);
+#pragma unroll 4
+    for (int i = lane; i < kRows * 32 / 8; i += 32) v4[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  // rows of my tile that still hold uncovered foreground, per 8-column chunk of x (K4 wrote
+  // the tile's foreground row masks)
+  unsigned long long Uc[4] = {0, 0, 0, 0};
+  {
+    uint32_t f[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      f[k] = active ? fgm[mtile * kRows + lane + 32 * k] : 0u;
+      fgw[lane + 32 * k] = f[k];
+      covw[lane + 32 * k] = 0;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      Uc[c] = (unsigned long long)__ballot_sync(kFull, (f[0] >> (8 * c)) & 0xFFu) |
+              ((unsigned long long)__ballot_sync(kFull, (f[1] >> (8 * c)) & 0xFFu) << 32);
+  }
+  __syncwarp();
+  // uncovered foreground cells of my tile (warp-uniform); point mode once it is small
+  int nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(fgw[lane]) + __popc(fgw[lane + 32])));
+  bool pmode = false;
+  uint16_t* ulist = S.ulist[warp];
+  int ub[6] = {0, kTX - 1, 0, TY - 1, 0, TZ - 1};  // bounding box of the uncovered cells (point mode)
+  auto ubox_refresh = [&]() {
+    int x0 = 1 << 20, x1 = -1, y0 = 1 << 20, y1 = -1, z0 = 1 << 20, z1 = -1;
+    for (int q = lane; q < nu; q += 32) {
+      const int e = ulist[q], x = e & 31, row = e >> 5;
+      const int ly = IS3D ? (row & 7) : row, lz = IS3D ? (row >> 3) : 0;
+      x0 = min(x0, x); x1 = max(x1, x); y0 = min(y0, ly); y1 = max(y1, ly); z0 = min(z0, lz); z1 = max(z1, lz);
+    }
+    ub[0] = __reduce_min_sync(kFull, x0); ub[1] = __reduce_max_sync(kFull, x1);
+    ub[2] = __reduce_min_sync(kFull, y0); ub[3] = __reduce_max_sync(kFull, y1);
+    ub[4] = __reduce_min_sync(kFull, z0); ub[5] = __reduce_max_sync(kFull, z1);
+  };
+
+  uint32_t n_rows = 0;
+  {
     // --- cover: my tile, balls in descending D.  Lanes first screen 32 balls at a time (reach
     // + rows with uncovered foreground inside the ball's x-extent); the surviving balls are
     // then painted one by one with the lanes over the tile's rows (lane = row, row + 32).
@@ -483,7 +650,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
         // a cell takes the D of the first (largest) ball containing it
         int cx = 0, cy = 0, cz = 0, D = 0;
         if (i < total) {
-          const unsigned long long e = S.list[S.idx[i]];
+          const unsigned long long e = list[i];
           D = (int)(e & 0xFFFFu);
           cx = (int)((e >> 16) & 0xFFFFu) - kOff - mox;
           cy = (int)((e >> 32) & 0xFFFFu) - kOff - moy;
@@ -531,7 +698,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
       unsigned long long cand = 0;
       int cx = 0, cy = 0, cz = 0, D = 0;
       if (i < total) {
-        const unsigned long long e = S.list[S.idx[i]];
+        const unsigned long long e = list[i];
         D = (int)(e & 0xFFFFu);
         cx = (int)((e >> 16) & 0xFFFFu) - kOff - mox;
         cy = (int)((e >> 32) & 0xFFFFu) - kOff - moy;
@@ -590,21 +757,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
                 ((unsigned long long)__ballot_sync(kFull, (left[1] >> (8 * c)) & 0xFFu) << 32);
       nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(left[0]) + __popc(left[1])));
     }
-    if (last_round) break;
-    __syncthreads();
-    if (tid == 0) {
-      S.round_hi = S.next_hi;
-      atomicAdd(&hdr->n_rounds_extra, 1u);
-    }
-    __syncthreads();
   }
 
-  if (S.fallback) {  // leave this group to k_dilate_atomic
-    if (lane == 0 && have_tile) fbl[atomicAdd(&hdr->n_fb, 1u)] = (uint32_t)mtile;
-    if (tid == 0) atomicAdd(&hdr->n_fallback, 1u);
-    return;
-  }
-  if (!active) return;
 
   // ---- my tile's LT^2 -> the LT plane (coalesced rows); shell and reductions run in the
   // streaming epilogue kernel (lt.cu), at full occupancy
@@ -620,32 +774,49 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_dilate_cover(const uint32_t*
 
 }  // namespace
 
-size_t dilate_cover_smem() { return sizeof(Smem); }
+int64_t dilate_groups(const Geom& g) {
+  const int GX = g.ndim == 3 ? 1 : 2, GY = 2, GZ = g.ndim == 3 ? 2 : 1;
+  return g.B * ((g.ntx + GX - 1) / GX) * ((g.nty + GY - 1) / GY) * ((g.ntz + GZ - 1) / GZ);
+}
+// candidate pool: N/2 entries (C4: 4.3 GB; measured demand 0.16 entries per element); a group
+// that does not fit is left to the fallback kernel
+int64_t dilate_pool_entries(const Geom& g) {
+  const int64_t n = g.N / 2 > (1 << 20) ? g.N / 2 : (1 << 20);
+  return n < 0xFFFFFFFFll ? n : 0xFFFFFFFFll;  // offsets are u32
+}
 
 void launch_dilate_cover(const uint32_t* fgm, TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
-                         const Geom& g, int force_fallback, uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
+                         unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int force_fallback,
+                         uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
+  const unsigned long long pool_cap = (unsigned long long)dilate_pool_entries(g);
   const int GX = g.ndim == 3 ? 1 : 2, GY = 2, GZ = g.ndim == 3 ? 2 : 1;
   const int64_t ngroups = g.B * ((g.ntx + GX - 1) / GX) * ((g.nty + GY - 1) / GY) * ((g.tz_hi - g.tz_lo + GZ - 1) / GZ);
   if (ngroups <= 0) return;
-  const size_t smem = sizeof(Smem);
   static const int point_at = [] {
     const char* v = getenv("FASTRS_POINT_AT");  // development knob (default 128 = kPoint)
     const int p = v ? atoi(v) : kPoint;
     return p < 0 ? 0 : (p > kPoint ? kPoint : p);
   }();
-  if (g.ndim == 3)
-    k_dilate_cover<true><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(fgm, meta, centres, oct, fbl, g, force_fallback,
-                                                                        point_at, ltp, hdr);
-  else
-    k_dilate_cover<false><<<(unsigned)ngroups, kWarps * 32, smem, st>>>(fgm, meta, centres, oct, fbl, g, force_fallback,
-                                                                         point_at, ltp, hdr);
+  if (g.ndim == 3) {
+    k_dilate_gather<true><<<(unsigned)ngroups, kWarps * 32, sizeof(Smem), st>>>(meta, centres, oct, fbl, g,
+                                                                                 force_fallback, pool, pool_cap, gcount,
+                                                                                 goff, hdr);
+    k_dilate_paint<true><<<(unsigned)ngroups, kWarps * 32, sizeof(PaintSmem), st>>>(fgm, meta, g, pool, gcount,
+                                                                                     goff, point_at, ltp, hdr);
+  } else {
+    k_dilate_gather<false><<<(unsigned)ngroups, kWarps * 32, sizeof(Smem), st>>>(meta, centres, oct, fbl, g,
+                                                                                  force_fallback, pool, pool_cap, gcount,
+                                                                                  goff, hdr);
+    k_dilate_paint<false><<<(unsigned)ngroups, kWarps * 32, sizeof(PaintSmem), st>>>(fgm, meta, g, pool, gcount,
+                                                                                      goff, point_at, ltp, hdr);
+  }
 }
 
 cudaError_t dilate_cover_setup() {
-  cudaError_t e = cudaFuncSetAttribute(k_dilate_cover<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k_dilate_gather<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sizeof(Smem));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_dilate_cover<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+    e = cudaFuncSetAttribute(k_dilate_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
   return e;
 }
 

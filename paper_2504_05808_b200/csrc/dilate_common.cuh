@@ -64,9 +64,9 @@ static __device__ __forceinline__ uint32_t row_epilogue(uint32_t c, int lane, bo
 }
 
 
-size_t dilate_cover_smem();
 cudaError_t dilate_cover_setup();
 void launch_dilate_cover(const uint32_t* fgm, TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
-                         const Geom& g, int force_fallback, uint32_t* ltp, WsHeader* hdr, cudaStream_t st);
+                         unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int force_fallback,
+                         uint32_t* ltp, WsHeader* hdr, cudaStream_t st);
 
 }  // namespace fastrs

@@ -247,14 +247,14 @@ cudaError_t dilate_atomic_setup() {
 }
 
 void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta, const uint2* centres,
-                   const uint32_t* fgm, const uint16_t* oct, uint32_t* fbl, const Geom& g, const Accum* acc,
-                   uint32_t* lt2_out, float* lt_out, bool force_fallback, uint32_t* ltp, WsHeader* hdr,
-                   cudaStream_t st) {
+                   const uint32_t* fgm, const uint16_t* oct, uint32_t* fbl, unsigned long long* pool,
+                   uint32_t* gcount, uint32_t* goff, const Geom& g, const Accum* acc, uint32_t* lt2_out, float* lt_out,
+                   bool force_fallback, uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
   Accum a{};
   if (acc) a = *acc;
   // both dilation kernels read Dmax / the per-tile fallback flag on the device; the atomic
   // kernel only processes tiles the exact-order kernel left to it.  Both write LT^2 to ltp.
-  launch_dilate_cover(fgm, meta, centres, oct, fbl, g, force_fallback ? 1 : 0, ltp, hdr, st);
+  launch_dilate_cover(fgm, meta, centres, oct, fbl, pool, gcount, goff, g, force_fallback ? 1 : 0, ltp, hdr, st);
   const size_t smem = (size_t)kRows * kRowStride * 4;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);

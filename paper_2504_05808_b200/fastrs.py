@@ -46,7 +46,8 @@ class _Diag(ctypes.Structure):
     _fields_ = [("status_bits", ctypes.c_uint32), ("dmax", ctypes.c_uint32), ("n_fg", ctypes.c_uint64),
                 ("n_kept", ctypes.c_uint64), ("n_intervals", ctypes.c_uint64),
                 ("sum_scale_log2", ctypes.c_int32), ("n_fallback", ctypes.c_uint32),
-                ("n_rounds_extra", ctypes.c_uint32), ("n_regathers", ctypes.c_uint32)]
+                ("n_rounds_extra", ctypes.c_uint32), ("n_regathers", ctypes.c_uint32),
+                ("max_group_list", ctypes.c_uint32), ("sum_group_list", ctypes.c_uint64)]
 
 
 def load(build_if_missing: bool = True) -> ctypes.CDLL:
