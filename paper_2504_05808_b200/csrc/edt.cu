@@ -99,9 +99,53 @@ __global__ void __launch_bounds__(256) k_edt_x(const int32_t* __restrict__ lab,
 }
 
 constexpr int kColS = 256;  // positions per CTA
-constexpr int kColH = 32;   // staged halo on each side
+constexpr int kColH = 48;   // staged halo on each side
 constexpr int kColRows = kColS + 2 * kColH;
 constexpr int kColWarps = 8;
+
+// Slow path of the column scan for an element whose window leaves the staged rows: the same
+// exact scan, reading beyond the window from global memory (L2).
+__device__ __noinline__ uint32_t scan_global(const uint32_t* __restrict__ in, int64_t base, int64_t astride, int64_t p,
+                                             int64_t L, int64_t lo, int64_t hi, const uint32_t* tile, int lane,
+                                             uint32_t v, uint32_t chbit, int border, int64_t gofs, int64_t Lg) {
+  uint32_t best = v & kMask;
+  {
+    uint32_t dq = 1, dq2 = 1;
+    int64_t q = p + 1;
+    while (dq2 < best) {
+      if (q >= L) {  // end of the staged axis: the grid end (slab path: h^2 >= D guarantees it)
+        if (border && gofs + q >= Lg) best = min(best, dq2);
+        break;
+      }
+      const uint32_t w = q < hi ? tile[(q - lo) * 32 + lane] : __ldg(in + base + q * astride);
+      if (w & chbit) {
+        best = min(best, dq2);
+        break;
+      }
+      best = min(best, (w & kMask) + dq2);
+      dq2 += 2 * dq + 1;
+      ++dq;
+      ++q;
+    }
+  }
+  {
+    uint32_t dq = 1, dq2 = 1, chk = v & chbit;
+    int64_t q = p - 1;
+    while (dq2 < best) {
+      if (chk) {
+        if (gofs + q >= 0 || border) best = min(best, dq2);
+        break;
+      }
+      const uint32_t w = q >= lo ? tile[(q - lo) * 32 + lane] : __ldg(in + base + q * astride);
+      best = min(best, (w & kMask) + dq2);
+      chk = w & chbit;
+      dq2 += 2 * dq + 1;
+      ++dq;
+      --q;
+    }
+  }
+  return best;
+}
 
 template <bool FINAL>
 __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
@@ -133,43 +177,54 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
     uint32_t res = FINAL ? 0u : v;
     if (xin && g != 0) {
       uint32_t best = g;
-      // up side: p+1, p+2, ... until a run end (the element there is a site) or dq^2 >= best
+      // Fast path: pure shared-memory scan in 32-bit indices.  up side: rows p+1, p+2, ... until a
+      // run end (the element there is a site) or dq^2 >= best; leaving the staged rows before
+      // that hands the element to the slow path below.
+      const int i = (int)(p - lo), nt = (int)(hi - lo);
+      bool slow = false;
       {
-        uint32_t dq = 1, dq2 = 1;
-        int64_t q = p + 1;
+        uint32_t dq2 = 1, inc = 3;
+        const uint32_t* w_ptr = tile + (i + 1) * 32 + lane;
+        const uint32_t* w_end = tile + nt * 32 + lane;
         while (dq2 < best) {
-          if (q >= L) {  // end of the staged axis: the grid end (slab path: h^2 >= D guarantees it)
-            if (border && gofs + q >= Lg) best = min(best, dq2);
+          if (w_ptr >= w_end) {
+            if (hi < L) slow = true;  // more rows exist beyond the staged window
+            else if (border && gofs + L >= Lg) best = min(best, dq2);  // the grid end
             break;
           }
-          const uint32_t w = q < hi ? tile[(q - lo) * 32 + lane] : __ldg(in + base + q * astride);
+          const uint32_t w = *w_ptr;
           if (w & chbit) {
             best = min(best, dq2);
             break;
           }
           best = min(best, (w & kMask) + dq2);
-          dq2 += 2 * dq + 1;
-          ++dq;
-          ++q;
+          dq2 += inc;
+          inc += 2;
+          w_ptr += 32;
         }
       }
-      // down side: p-1, p-2, ...; element p-dq lies outside the run iff p-dq+1 starts the run
+      // down side: rows p-1, p-2, ...; element p-dq lies outside the run iff p-dq+1 starts it
       {
-        uint32_t dq = 1, dq2 = 1, chk = v & chbit;
-        int64_t q = p - 1;
+        uint32_t dq2 = 1, inc = 3, chk = v & chbit;
+        int r = i - 1;
         while (dq2 < best) {
           if (chk) {
-            if (gofs + q >= 0 || border) best = min(best, dq2);
+            if (gofs + lo + r >= 0 || border) best = min(best, dq2);
             break;
           }
-          const uint32_t w = q >= lo ? tile[(q - lo) * 32 + lane] : __ldg(in + base + q * astride);
+          if (r < 0) {  // lo > 0 here (element 0 of the axis always starts a run)
+            slow = true;
+            break;
+          }
+          const uint32_t w = tile[r * 32 + lane];
           best = min(best, (w & kMask) + dq2);
           chk = w & chbit;
-          dq2 += 2 * dq + 1;
-          ++dq;
-          --q;
+          dq2 += inc;
+          inc += 2;
+          --r;
         }
       }
+      if (slow) best = scan_global(in, base, astride, p, L, lo, hi, tile, lane, v, chbit, border, gofs, Lg);
       dmax = max(dmax, best);
       if (FINAL) {
         res = best;
