@@ -35,12 +35,14 @@ METRIC = "Gvoxels/s end-to-end (EDT+LT+sphericity+roundness); % of HBM roofline"
 UNIT = "Gvoxels/s"
 
 # algorithmic HBM bytes per grid element of each stage (DESIGN.md §6 "Algorithmic bytes"), 3D path
-STAGE_BYTES_PER_ELEM = {"edt_x": 8.0, "edt_y": 8.0, "edt_z": 8.0, "prune": 4.0, "dilate": 4.0, "epilogue": 12.0,
-                        "metrics": 0.0}
-STAGE_BYTES_PER_KEPT = {"prune": 8.0, "dilate": 8.0}  # centre entries written / read once
+STAGE_BYTES_PER_ELEM = {"edt_x": 8.0, "edt_y": 8.0, "edt_z": 8.0, "prune": 4.0, "gather": 0.0, "dilate": 4.0,
+                        "epilogue": 12.0, "metrics": 0.0}
+STAGE_BYTES_PER_KEPT = {"prune": 8.0, "gather": 8.0}  # centre entries written by K4 / read once by K5a
+STAGE_BYTES_PER_CAND = {"gather": 8.0, "dilate": 8.0}  # sorted per-group candidates: written by K5a, read by K5b
 # the kernel behind each stage (names in the ncu summaries under profiles/)
 STAGE_KERNEL = {"edt_x": "k_edt_x", "edt_y": "k_edt_col<0>", "edt_z": "k_edt_col<1>", "prune": "k_prune<1>",
-                "dilate": "k_dilate_cover<1>", "epilogue": "k_epilogue", "metrics": "k_metrics"}
+                "gather": "k_dilate_gather<1>", "dilate": "k_dilate_paint<1>", "epilogue": "k_epilogue",
+                "metrics": "k_metrics"}
 NCU_SUMMARY = os.path.join(ROOT, "profiles", "r01_ncu_summary_c4.json")
 
 
@@ -273,16 +275,20 @@ def run_fastrs(args):
     per_launch = {k: v / max(calls, 1) for k, v in stage_ms.items()}
     dom = max(per_launch, key=lambda k: per_launch[k])
     n = lab.size
-    alg_bytes = STAGE_BYTES_PER_ELEM[dom] * n + STAGE_BYTES_PER_KEPT.get(dom, 0.0) * diag["n_kept"]
+
+    def stage_bytes(k):
+        return (STAGE_BYTES_PER_ELEM[k] * n + STAGE_BYTES_PER_KEPT.get(k, 0.0) * diag["n_kept"]
+                + STAGE_BYTES_PER_CAND.get(k, 0.0) * diag["sum_group_list"])
+
+    alg_bytes = stage_bytes(dom)
     achieved = alg_bytes / (per_launch[dom] * 1e-3) / 1e9
     stage_gbs = {}
     for k, v in per_launch.items():
         if v > 0:
-            b = STAGE_BYTES_PER_ELEM[k] * n + STAGE_BYTES_PER_KEPT.get(k, 0.0) * diag["n_kept"]
+            b = stage_bytes(k)
             stage_gbs[k] = {"ms": round(v, 4), "GB/s": round(b / (v * 1e-3) / 1e9, 1),
                             "frac": round(b / (v * 1e-3) / 1e9 / hbm_peak, 4)}
-    model_bytes = sum(STAGE_BYTES_PER_ELEM[k] for k in per_launch if per_launch[k] > 0) * n \
-        + sum(STAGE_BYTES_PER_KEPT.values()) * diag["n_kept"]
+    model_bytes = sum(stage_bytes(k) for k in per_launch if per_launch[k] > 0)
     pipe_gbs = model_bytes / (ms * 1e-3) / 1e9
 
     if rank != 0:
@@ -303,7 +309,7 @@ def run_fastrs(args):
                    "input_sha256": info["sha256"], "input_hash_kind": info.get("sha256_kind")},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(lab.nbytes),
                 "d2h_bytes_per_step": int(2 * M * 8), "ms_per_step": float(e2e_ms.item())},
-        "gpu_launches": int((8 if ndim == 3 else 7) * args.steps),
+        "gpu_launches": int((9 if ndim == 3 else 8) * args.steps),
         "roofline": {"bound": "hbm", "kernel": STAGE_KERNEL[dom], "stage": dom, "achieved": achieved,
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                      "traffic": ncu_traffic(STAGE_KERNEL[dom]),

@@ -144,7 +144,8 @@ FASTRS_API int fastrs_sphericity_roundness_host(const int32_t* labels_host, cons
 FASTRS_API int fastrs_read_diagnostics(const void* ws, fastrs_diagnostics* out, void* stream);
 
 /* Per-stage device time (ms) accumulated over calls while profiling is on: stages are
- * 0 edt_x, 1 edt_y, 2 edt_z, 3 prune, 4 dilate, 5 metrics, 6 epilogue (K5 shell + reductions).
+ * 0 edt_x, 1 edt_y, 2 edt_z, 3 prune, 4 dilate (K5b paint + fallback), 5 metrics, 6 epilogue
+ * (K5 shell + reductions), 7 gather (K5a candidate gather + sort).
  * Events are recorded on the
  * call's stream.  fastrs_profile(1) enables and resets; fastrs_profile(0) disables. */
 FASTRS_API void fastrs_profile(int enable);

@@ -109,8 +109,10 @@ __host__ __device__ inline int sum_scale_log2(int64_t Nb, uint32_t dmax) {
   return s < 0 ? 0 : (s > 32 ? 32 : s);
 }
 
-// Monotone bucket of a squared radius D: 8 buckets per octave (0..127 for D < 65536).
-// Kept-centre lists are sorted by it (descending) and the dilation walks it downwards.
+// Monotone bucket of a squared radius D: 8 buckets per octave, 0..126 for D < 65536; every
+// D >= 65536 shares the saturated bucket 127 (K4's 128-entry histograms stay in range).
+// Kept-centre lists are sorted by it (descending) and K5 walks it downwards.
+constexpr int kBucketTop = 127;
 __host__ __device__ inline int dbucket(uint32_t D) {
   int msb = 31;
   while (msb > 0 && !((D >> msb) & 1u)) --msb;
@@ -118,10 +120,12 @@ __host__ __device__ inline int dbucket(uint32_t D) {
   msb = 31 - __clz(D);
 #endif
   const int frac = msb >= 3 ? (int)((D >> (msb - 3)) & 7u) : (int)((D << (3 - msb)) & 7u);
-  return msb * 8 + frac;
+  const int b = msb * 8 + frac;
+  return b < kBucketTop ? b : kBucketTop;
 }
 // Largest D with dbucket(D) <= b (D >= 1): one less than the smallest D of bucket b+1 or above.
 __host__ __device__ inline uint32_t dbucket_max(int b) {
+  if (b >= kBucketTop) return 0xFFFFFFFFu;  // the saturated bucket is unbounded
   const int b1 = b + 1;
   if (b1 >= 24) return ((uint32_t)(8 + (b1 & 7)) << ((b1 >> 3) - 3)) - 1u;
   // smallest D with dbucket(D) >= b1 for b1 < 24 (dbucket: 1->0, 2->8, 3->12, 4->16, 5->18, 6->20, 7->22, 8->24)
@@ -149,6 +153,11 @@ void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta,
                    uint32_t* lt2_out, float* lt_out, bool force_fallback, uint32_t* ltp, WsHeader* hdr,
                    cudaStream_t st);
 int64_t dilate_groups(const Geom& g);        // K5 tile groups (gcount / goff entries)
+// K5a: per tile group, gather the kept balls that reach it and write them sorted by D
+// (descending) to the candidate pool; groups that cannot be handled are listed in fbl
+void launch_dilate_gather(TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
+                          unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int force_fallback,
+                          WsHeader* hdr, cudaStream_t st);
 int64_t dilate_pool_entries(const Geom& g);  // K5 candidate pool (sorted per-group lists), u64 entries
 // K5 epilogue: shell, per-label reductions and LT outputs from the LT plane ltp
 void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,

@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kWarps * 32, 5) k_dilate_gather(const TileMeta
         if (h[q] && k <= rhi) top_l = k;
       }
       const int top = __reduce_max_sync(kFull, top_l);
-      const uint32_t dtop = dbucket_max(top < 0 ? 0 : top);
+      const uint32_t dtop = min(dbucket_max(top < 0 ? 0 : top), dmax);  // bucket 127 is unbounded
       int lo_l = -1;  // the highest bucket that no longer fits (count or D range)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(kWarps * 32, 5) k_dilate_gather(const TileMeta
     }
     // --- exact counting sort of the list indices by D (descending), D in [dlo, dhi]
     const int rtop = S.round_top;
-    const uint32_t dhi = dbucket_max(rtop < 0 ? 0 : rtop), dlo = rlo == 0 ? 1u : dbucket_max(rlo - 1) + 1u;
+    const uint32_t dhi = min(dbucket_max(rtop < 0 ? 0 : rtop), dmax), dlo = rlo == 0 ? 1u : dbucket_max(rlo - 1) + 1u;
     const int nb = (int)(dhi - dlo) + 1;
     const uint32_t n = min(S.count, (uint32_t)kCap);
     for (int k = tid; k < nb; k += kWarps * 32) S.hist[k] = 0;
@@ -785,31 +785,48 @@ int64_t dilate_pool_entries(const Geom& g) {
   return n < 0xFFFFFFFFll ? n : 0xFFFFFFFFll;  // offsets are u32
 }
 
-void launch_dilate_cover(const uint32_t* fgm, TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
-                         unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int force_fallback,
-                         uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
-  const unsigned long long pool_cap = (unsigned long long)dilate_pool_entries(g);
-  const int GX = g.ndim == 3 ? 1 : 2, GY = 2, GZ = g.ndim == 3 ? 2 : 1;
-  const int64_t ngroups = g.B * ((g.ntx + GX - 1) / GX) * ((g.nty + GY - 1) / GY) * ((g.tz_hi - g.tz_lo + GZ - 1) / GZ);
-  if (ngroups <= 0) return;
+namespace {
+int point_at_knob() {
   static const int point_at = [] {
-    const char* v = getenv("FASTRS_POINT_AT");  // development knob (default 128 = kPoint)
+    const char* v = getenv("FASTRS_POINT_AT");  // development knob (default kPoint)
     const int p = v ? atoi(v) : kPoint;
     return p < 0 ? 0 : (p > kPoint ? kPoint : p);
   }();
-  if (g.ndim == 3) {
+  return point_at;
+}
+int64_t launched_groups(const Geom& g) {
+  const int GX = g.ndim == 3 ? 1 : 2, GY = 2, GZ = g.ndim == 3 ? 2 : 1;
+  return g.B * ((g.ntx + GX - 1) / GX) * ((g.nty + GY - 1) / GY) * ((g.tz_hi - g.tz_lo + GZ - 1) / GZ);
+}
+}  // namespace
+
+void launch_dilate_gather(TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
+                          unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int force_fallback,
+                          WsHeader* hdr, cudaStream_t st) {
+  const int64_t ngroups = launched_groups(g);
+  if (ngroups <= 0) return;
+  const unsigned long long pool_cap = (unsigned long long)dilate_pool_entries(g);
+  if (g.ndim == 3)
     k_dilate_gather<true><<<(unsigned)ngroups, kWarps * 32, sizeof(Smem), st>>>(meta, centres, oct, fbl, g,
                                                                                  force_fallback, pool, pool_cap, gcount,
                                                                                  goff, hdr);
-    k_dilate_paint<true><<<(unsigned)ngroups, kWarps * 32, sizeof(PaintSmem), st>>>(fgm, meta, g, pool, gcount,
-                                                                                     goff, point_at, ltp, hdr);
-  } else {
+  else
     k_dilate_gather<false><<<(unsigned)ngroups, kWarps * 32, sizeof(Smem), st>>>(meta, centres, oct, fbl, g,
                                                                                   force_fallback, pool, pool_cap, gcount,
                                                                                   goff, hdr);
-    k_dilate_paint<false><<<(unsigned)ngroups, kWarps * 32, sizeof(PaintSmem), st>>>(fgm, meta, g, pool, gcount,
-                                                                                      goff, point_at, ltp, hdr);
-  }
+}
+
+void launch_dilate_paint(const uint32_t* fgm, const TileMeta* meta, const unsigned long long* pool,
+                         const uint32_t* gcount, const uint32_t* goff, const Geom& g, uint32_t* ltp, WsHeader* hdr,
+                         cudaStream_t st) {
+  const int64_t ngroups = launched_groups(g);
+  if (ngroups <= 0) return;
+  if (g.ndim == 3)
+    k_dilate_paint<true><<<(unsigned)ngroups, kWarps * 32, sizeof(PaintSmem), st>>>(fgm, meta, g, pool, gcount, goff,
+                                                                                     point_at_knob(), ltp, hdr);
+  else
+    k_dilate_paint<false><<<(unsigned)ngroups, kWarps * 32, sizeof(PaintSmem), st>>>(fgm, meta, g, pool, gcount, goff,
+                                                                                      point_at_knob(), ltp, hdr);
 }
 
 cudaError_t dilate_cover_setup() {

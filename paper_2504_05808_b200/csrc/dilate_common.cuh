@@ -65,8 +65,8 @@ static __device__ __forceinline__ uint32_t row_epilogue(uint32_t c, int lane, bo
 
 
 cudaError_t dilate_cover_setup();
-void launch_dilate_cover(const uint32_t* fgm, TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
-                         unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int force_fallback,
-                         uint32_t* ltp, WsHeader* hdr, cudaStream_t st);
+void launch_dilate_paint(const uint32_t* fgm, const TileMeta* meta, const unsigned long long* pool,
+                         const uint32_t* gcount, const uint32_t* goff, const Geom& g, uint32_t* ltp, WsHeader* hdr,
+                         cudaStream_t st);
 
 }  // namespace fastrs

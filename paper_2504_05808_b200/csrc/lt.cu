@@ -254,7 +254,9 @@ void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta, con
   if (acc) a = *acc;
   // both dilation kernels read Dmax / the per-tile fallback flag on the device; the atomic
   // kernel only processes tiles the exact-order kernel left to it.  Both write LT^2 to ltp.
-  launch_dilate_cover(fgm, meta, centres, oct, fbl, pool, gcount, goff, g, force_fallback ? 1 : 0, ltp, hdr, st);
+  (void)oct;
+  (void)force_fallback;
+  launch_dilate_paint(fgm, meta, pool, gcount, goff, g, ltp, hdr, st);  // K5b (after K5a launch_dilate_gather)
   const size_t smem = (size_t)kRows * kRowStride * 4;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);

@@ -22,7 +22,7 @@ ASYNC = 4
 HOST_IO = 8
 FORCE_FALLBACK = 16  # run the dilation with the atomic sparse-table kernel (cross-check)
 
-STAGES = ("edt_x", "edt_y", "edt_z", "prune", "dilate", "metrics", "epilogue")
+STAGES = ("edt_x", "edt_y", "edt_z", "prune", "dilate", "metrics", "epilogue", "gather")
 
 _STATUS = {0: "OK", 1: "EINVAL", 2: "ENOSITE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "EINTERNAL"}
 

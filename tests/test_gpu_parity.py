@@ -136,7 +136,9 @@ def test_large_balls_beyond_table_and_halo(F):
     radius r centred on an element has D(centre) = r^2 + 1 and LT^2 = r^2 + 1 everywhere
     (the centre ball covers the whole object)."""
     import scipy.ndimage
-    for lab, r in ((synth.disk(150, canvas=311), 150), (synth.sphere(95, canvas=193), 95)):
+    # r = 300: D = 90001 > 65535 sends every tile to the atomic sparse-table kernel (u32 values)
+    for lab, r in ((synth.disk(150, canvas=311), 150), (synth.sphere(95, canvas=193), 95),
+                   (synth.disk(300, canvas=605), 300)):
         t = _dev(lab)
         ref = np.rint(scipy.ndimage.distance_transform_edt(np.pad(lab > 0, 1)) ** 2).astype(np.uint32)
         ref = ref[(slice(1, -1),) * lab.ndim]
