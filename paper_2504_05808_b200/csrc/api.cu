@@ -58,7 +58,7 @@ int make_geom(const int64_t* dims, int ndim, int64_t batch, Geom& g) {
 inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t hdr, A, B, meta, fgm, oct, fbl, gcount, goff, pool, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd, total;
+  size_t hdr, A, B, meta, fgm, oct, fbl, gcount, goff, pool, fxl, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd, total;
 };
 
 Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
@@ -80,6 +80,7 @@ Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
   L.gcount = take((size_t)dilate_groups(g) * 4);
   L.goff = take((size_t)dilate_groups(g) * 4);
   L.pool = take((size_t)dilate_pool_entries(g) * 8);
+  L.fxl = take(kFxLutBytes);
   L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
   L.vol = take(M * 8);
   L.nsh = take(M * 8);
@@ -215,7 +216,8 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
                   (uint32_t*)(w + L.goff), g, stage == kFull ? &acc : nullptr, lt2_out, lt_out,
                   (flags & kFlagForceFallback) != 0, ltp, hdr, st);  // K5
     tm.mark(4);
-    launch_epilogue(labels, D, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out, ltp, hdr, st);  // K5 epilogue
+    launch_epilogue(labels, D, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out, ltp,
+                    (unsigned long long*)(w + L.fxl), hdr, st);  // K5 epilogue
     tm.mark(6);
     if (stage == kFull) {
       launch_metrics(acc, g, *outs, hdr, st);  // K6
@@ -266,7 +268,7 @@ int finish_call(WsHeader* hdr, uint32_t flags, cudaStream_t st) {
 }
 
 struct SlabLayout {
-  size_t hdr, P, meta, fgm, oct, fbl, gcount, goff, pool, cent, total;
+  size_t hdr, P, meta, fgm, oct, fbl, gcount, goff, pool, fxl, cent, total;
 };
 SlabLayout make_slab_layout(const Geom& g) {
   SlabLayout L{};
@@ -285,6 +287,7 @@ SlabLayout make_slab_layout(const Geom& g) {
   L.gcount = take((size_t)dilate_groups(g) * 4);
   L.goff = take((size_t)dilate_groups(g) * 4);
   L.pool = take((size_t)dilate_pool_entries(g) * 8);
+  L.fxl = take(kFxLutBytes);
   L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
   L.total = off;
   return L;
@@ -535,7 +538,7 @@ int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64
   launch_dilate(lab_ext, d_ext, meta, cent, fgm, oct, fbl, (unsigned long long*)((char*)ws + L.pool),
                 (uint32_t*)((char*)ws + L.gcount), (uint32_t*)((char*)ws + L.goff), g, &acc, nullptr, nullptr, (flags & kFlagForceFallback) != 0, ltp,
                 hdr, st);
-  launch_epilogue(lab_ext, d_ext, g, &acc, nullptr, nullptr, ltp, hdr, st);
+  launch_epilogue(lab_ext, d_ext, g, &acc, nullptr, nullptr, ltp, (unsigned long long*)((char*)ws + L.fxl), hdr, st);
   return finish_call(hdr, flags, st);
 }
 

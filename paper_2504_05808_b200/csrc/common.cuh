@@ -161,7 +161,8 @@ void launch_dilate_gather(TileMeta* meta, const uint2* centres, const uint16_t* 
 int64_t dilate_pool_entries(const Geom& g);  // K5 candidate pool (sorted per-group lists), u64 entries
 // K5 epilogue: shell, per-label reductions and LT outputs from the LT plane ltp
 void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,
-                     float* lt_out, const uint32_t* ltp, WsHeader* hdr, cudaStream_t st);
+                     float* lt_out, const uint32_t* ltp, unsigned long long* fxlut, WsHeader* hdr, cudaStream_t st);
+constexpr size_t kFxLutBytes = 65536 * 8;  // workspace for the epilogue's fixed-point sqrt table
 void launch_metrics(const Accum& acc, const Geom& g, const Outputs& o, WsHeader* hdr,
                     cudaStream_t st);
 void release_mtables();

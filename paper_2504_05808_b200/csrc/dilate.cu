@@ -766,7 +766,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
   for (int row = 0; row < kRows; ++row) {
     const int ly = row % TY, lz = row / TY;
     const int64_t gz = roz + moz + lz, gy = roy + moy + ly;
-    if (gz < g.Z && gy < g.Y && gx < g.X) ltp[item + (gz * g.Y + gy) * g.X + gx] = val[row * 32 + lane];
+    // the LT plane holds u16 values whenever Dmax <= 65535 (always the case here)
+    if (gz < g.Z && gy < g.Y && gx < g.X)
+      reinterpret_cast<uint16_t*>(ltp)[item + (gz * g.Y + gy) * g.X + gx] = val[row * 32 + lane];
   }
   n_rows = __reduce_add_sync(kFull, n_rows);
   if (lane == 0 && n_rows) atomicAdd(&hdr->n_intervals, (unsigned long long)n_rows);

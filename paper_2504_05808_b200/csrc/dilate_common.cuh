@@ -5,6 +5,7 @@
 namespace fastrs {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr uint32_t kFxLut = 65536;  // entries of the fixed-point sqrt table
 constexpr uint32_t kU16Max = 65535u;
 
 // Shell + per-label reductions + optional LT writes for one 32-wide row held in a warp
@@ -12,17 +13,23 @@ constexpr uint32_t kU16Max = 65535u;
 // grid).  Returns 1 if the invariant LT^2 >= D failed.
 static __device__ __forceinline__ uint32_t row_epilogue_v(uint32_t c, int32_t L, uint32_t d, int lane, int64_t gi,
                                                    int64_t b, const Accum& acc, int do_reduce, double scale,
-                                                   uint32_t* __restrict__ lt2_out, float* __restrict__ lt_out) {
+                                                   uint32_t* __restrict__ lt2_out, float* __restrict__ lt_out,
+                                                   const unsigned long long* __restrict__ fxlut = nullptr) {
   uint32_t bad = 0;
   bool shell = false;
   unsigned long long fx = 0;
   if (L != 0) {
     if (c < d) bad = 1;
     shell = d == 1;
-    const double lt = sqrt((double)c);
-    fx = (unsigned long long)__double2ull_rn(lt * scale);
+    // fixed-point sqrt(LT^2) * 2^s: from the per-call table when LT^2 < 65536 (bit-identical:
+    // the table holds the same correctly rounded values)
+    if (fxlut && c < kFxLut) {
+      fx = __ldg(fxlut + c);
+    } else {
+      fx = (unsigned long long)__double2ull_rn(sqrt((double)c) * scale);
+    }
     if (lt2_out) lt2_out[gi] = c;
-    if (lt_out) lt_out[gi] = (float)lt;
+    if (lt_out) lt_out[gi] = (float)sqrt((double)c);
   }
   if (do_reduce) {
     if (L < 0 || L > acc.max_label) L = 0;

@@ -171,7 +171,10 @@ __device__ __forceinline__ void dilate_tile_atomic(int64_t tile, const TileMeta*
       if (lane < (1 << k)) upv = 0;
       c = max(Tr[k * 32 + lane], max(c, upv));
     }
-    if (valid) ltp[item + (gz * g.Y + gy) * g.X + gx] = c;
+    if (valid) {  // the LT plane is u16 when Dmax <= 65535 (K5b writes it too), else u32
+      const int64_t gi = item + (gz * g.Y + gy) * g.X + gx;
+      if (hdr->dmax > kU16Max) ltp[gi] = c; else reinterpret_cast<uint16_t*>(ltp)[gi] = (uint16_t)c;
+    }
   }
   n_int = __reduce_add_sync(kFull, (uint32_t)n_int);
   if (lane == 0 && n_int) atomicAdd(&hdr->n_intervals, n_int);
@@ -202,16 +205,27 @@ __global__ void __launch_bounds__(256) k_dilate_atomic(const TileMeta* __restric
 // LT outputs and the per-label reductions (a7); one warp per x-row of the produced z range,
 // 4 chunks of 32 elements in flight.
 // ---------------------------------------------------------------------------------------
+// fxlut[c] = round(sqrt(c) * 2^s) for c < kFxLut: the fixed-point LT terms of the sums
+__global__ void k_fxlut(unsigned long long* __restrict__ fxlut, int64_t nscale, const WsHeader* __restrict__ hdr) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= kFxLut) return;
+  const double scale = ldexp(1.0, sum_scale_log2(nscale, hdr->dmax));
+  fxlut[c] = (unsigned long long)__double2ull_rn(sqrt((double)c) * scale);
+}
+
 __global__ void __launch_bounds__(256) k_epilogue(const int32_t* __restrict__ lab, const uint32_t* __restrict__ Dg,
                                                   const uint32_t* __restrict__ ltp, Geom g, int64_t z_lo, int64_t nz,
                                                   Accum acc, int do_reduce, uint32_t* __restrict__ lt2_out,
-                                                  float* __restrict__ lt_out, WsHeader* __restrict__ hdr) {
+                                                  float* __restrict__ lt_out, const unsigned long long* __restrict__ fxlut,
+                                                  WsHeader* __restrict__ hdr) {
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= g.B * nz * g.Y) return;
   const int64_t y = row % g.Y, zb = row / g.Y, z = z_lo + zb % nz, b = zb / nz;
   const int64_t base = ((b * g.Z + z) * g.Y + y) * g.X;
   const double scale = ldexp(1.0, sum_scale_log2(g.nscale, hdr->dmax));
+  const bool wide = hdr->dmax > kU16Max;  // LT plane element type: u32 if wide, else u16
+  const uint16_t* ltp16 = reinterpret_cast<const uint16_t*>(ltp);
   const int X = (int)g.X;
   uint32_t bad = 0;
   for (int x0 = 0; x0 < X; x0 += 128) {
@@ -223,13 +237,13 @@ __global__ void __launch_bounds__(256) k_epilogue(const int32_t* __restrict__ la
       const bool in = x < X;
       L[k] = in ? __ldg(lab + base + x) : 0;
       d[k] = in ? __ldg(Dg + base + x) : 0u;
-      c[k] = (in && L[k] != 0) ? __ldg(ltp + base + x) : 0u;
+      c[k] = (in && L[k] != 0) ? (wide ? __ldg(ltp + base + x) : (uint32_t)__ldg(ltp16 + base + x)) : 0u;
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (x0 + 32 * k >= X) break;  // warp-uniform
       bad |= row_epilogue_v(c[k], L[k], d[k], lane, base + x0 + 32 * k + lane, b, acc, do_reduce, scale, lt2_out,
-                            lt_out);
+                            lt_out, fxlut);
     }
   }
   if (__any_sync(kFull, bad) && lane == 0) atomicOr(&hdr->status, kStInternal);
@@ -269,16 +283,17 @@ void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta, con
 }
 
 void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,
-                     float* lt_out, const uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
+                     float* lt_out, const uint32_t* ltp, unsigned long long* fxlut, WsHeader* hdr, cudaStream_t st) {
   Accum a{};
   if (acc) a = *acc;
   // epilogue over the produced layers
   const int TZ = g.ndim == 3 ? kTZ3 : 1;
   const int64_t z_lo = g.tz_lo * TZ, z_hi = g.tz_hi * TZ < g.Z ? g.tz_hi * TZ : g.Z;
   const int64_t rows = g.B * (z_hi - z_lo) * g.Y;
+  if (acc) k_fxlut<<<kFxLut / 256, 256, 0, st>>>(fxlut, g.nscale, hdr);
   if (rows > 0)
     k_epilogue<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(labels, D, ltp, g, z_lo, z_hi - z_lo, a, acc ? 1 : 0,
-                                                          lt2_out, lt_out, hdr);
+                                                          lt2_out, lt_out, acc ? fxlut : nullptr, hdr);
 }
 
 }  // namespace fastrs
