@@ -33,7 +33,7 @@ namespace fastrs {
 namespace {
 
 constexpr int kWarps = 4;  // warps per CTA = tiles per group
-constexpr int kCap = 3072;   // candidate list capacity per round
+constexpr int kCap = 2048;   // candidate list capacity per round
 constexpr int kBuckets = 128;
 constexpr int kHist = 1536;  // exact-D counting-sort bins per round
 constexpr int kPoint = 128;
@@ -41,7 +41,7 @@ constexpr uint32_t kGroupFallback = 0xFFFFFFFFu;  // uncovered cells at which a 
 constexpr int kOff = 16384;  // coordinate bias of packed candidates
 
 struct Smem;
-static_assert(3 * 512 <= 1536 && 2 * (512 + 8) + 512 <= 3072, "gather scratch fits S.hist / S.idx");
+static_assert(3 * 512 <= 1536 && 2 * (512 + 8) + 512 <= 2048, "gather scratch fits S.hist / S.idx");
 
 struct Smem {  // K5a (gather + sort)
   unsigned long long list[kCap];     // gathered candidates (centre relative to the group), gather order
@@ -285,7 +285,7 @@ __device__ __forceinline__ unsigned long long row_box(int ya, int yb, int za, in
 }
 
 template <bool IS3D>
-__global__ void __launch_bounds__(kWarps * 32, 5) k_dilate_gather(const TileMeta* __restrict__ meta,
+__global__ void __launch_bounds__(kWarps * 32, 6) k_dilate_gather(const TileMeta* __restrict__ meta,
                                                                const uint2* __restrict__ cent,
                                                                const uint16_t* __restrict__ oct,
                                                                uint32_t* __restrict__ fbl, Geom g, int force_fallback,
