@@ -209,7 +209,7 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
     tm.mark(3);
     uint32_t* ltp = D == A ? B : A;  // the plane the EDT no longer needs holds LT^2
     uint32_t* fbl = (uint32_t*)(w + L.fbl);
-    launch_dilate_gather(meta, cent, oct, fbl, (unsigned long long*)(w + L.pool), (uint32_t*)(w + L.gcount),
+    launch_dilate_gather(fgm, meta, cent, oct, fbl, (unsigned long long*)(w + L.pool), (uint32_t*)(w + L.gcount),
                          (uint32_t*)(w + L.goff), g, (flags & kFlagForceFallback) != 0 ? 1 : 0, hdr, st);  // K5a
     tm.mark(7);
     launch_dilate(labels, D, meta, cent, fgm, oct, fbl, (unsigned long long*)(w + L.pool), (uint32_t*)(w + L.gcount),
@@ -533,7 +533,7 @@ int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64
   const int32_t* lab_ext = labels - own_lo * g.Y * g.X;
   uint32_t* ltp = (uint32_t*)((char*)ws + L.P);
   uint32_t* fbl = (uint32_t*)((char*)ws + L.fbl);
-  launch_dilate_gather(meta, cent, oct, fbl, (unsigned long long*)((char*)ws + L.pool), (uint32_t*)((char*)ws + L.gcount),
+  launch_dilate_gather(fgm, meta, cent, oct, fbl, (unsigned long long*)((char*)ws + L.pool), (uint32_t*)((char*)ws + L.gcount),
                        (uint32_t*)((char*)ws + L.goff), g, (flags & kFlagForceFallback) != 0 ? 1 : 0, hdr, st);
   launch_dilate(lab_ext, d_ext, meta, cent, fgm, oct, fbl, (unsigned long long*)((char*)ws + L.pool),
                 (uint32_t*)((char*)ws + L.gcount), (uint32_t*)((char*)ws + L.goff), g, &acc, nullptr, nullptr, (flags & kFlagForceFallback) != 0, ltp,

@@ -155,7 +155,7 @@ void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta,
 int64_t dilate_groups(const Geom& g);        // K5 tile groups (gcount / goff entries)
 // K5a: per tile group, gather the kept balls that reach it and write them sorted by D
 // (descending) to the candidate pool; groups that cannot be handled are listed in fbl
-void launch_dilate_gather(TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
+void launch_dilate_gather(const uint32_t* fgm, TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
                           unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int force_fallback,
                           WsHeader* hdr, cudaStream_t st);
 int64_t dilate_pool_entries(const Geom& g);  // K5 candidate pool (sorted per-group lists), u64 entries

@@ -24,8 +24,6 @@
 // The pathological case (a single bucket exceeding the list or the sort range) hands the
 // group to the atomic sparse-table kernel k_dilate_atomic (lt.cu), which also handles
 // Dmax > 65535 (FASTRS_FORCE_FALLBACK sends every tile there: a GPU-internal cross-check).
-#include <cstdlib>
-
 #include "common.cuh"
 #include "dilate_common.cuh"
 
@@ -53,6 +51,7 @@ struct Smem {  // K5a (gather + sort)
   uint32_t wsum[kWarps];
   uint32_t count, total, nrec;
   int round_lo, round_hi, round_top, next_hi, fallback, rounds;
+  int bb[6];                         // bounding box of the group's foreground (group coordinates)
 };
 
 struct PaintSmem {  // K5b (one tile per warp)
@@ -162,9 +161,10 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
       const TileMeta hm = meta[ht];
       if (!hm.count) continue;
       const int hox = (ix - nrx) * kTX, hoy = (iy - nry) * P::TY, hoz = (iz - nrz) * P::TZ;
-      const int gx = hox < 0 ? -(hox + kTX - 1) : (hox > P::RX - 1 ? hox - (P::RX - 1) : 0);
-      const int gy = hoy < 0 ? -(hoy + P::TY - 1) : (hoy > P::RY - 1 ? hoy - (P::RY - 1) : 0);
-      const int gz = hoz < 0 ? -(hoz + P::TZ - 1) : (hoz > P::RZ - 1 ? hoz - (P::RZ - 1) : 0);
+      // gap between the home tile box and the bounding box of the group's foreground
+      const int gx = max(0, max(hox - S.bb[1], S.bb[0] - (hox + kTX - 1)));
+      const int gy = max(0, max(hoy - S.bb[3], S.bb[2] - (hoy + P::TY - 1)));
+      const int gz = max(0, max(hoz - S.bb[5], S.bb[4] - (hoz + P::TZ - 1)));
       const int g2 = gx * gx + gy * gy + gz * gz;
       if (g2 > (int)hm.maxD - 1 || dbucket(hm.maxD) < blo) continue;
       // lowest bucket whose largest D can still reach the gap: D - 1 >= g2 <=> D >= g2 + 1
@@ -229,7 +229,7 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
         const int v = (int)en.x;
         const int cx = (int)(o & 0xFFFFu) - kOff + (v & 31), cy = (int)(o >> 16) - kOff + ((v >> 5) % P::TY),
                   cz = (int)recz[lo] + v / (32 * P::TY);
-        const int ddx = gap(0, P::RX - 1, cx), ddy = gap(0, P::RY - 1, cy), ddz = gap(0, P::RZ - 1, cz);
+        const int ddx = gap(S.bb[0], S.bb[1], cx), ddy = gap(S.bb[2], S.bb[3], cy), ddz = gap(S.bb[4], S.bb[5], cz);
         bk = dbucket(en.y);
         if (ddx * ddx + ddy * ddy + ddz * ddz <= (int)en.y - 1 && bk >= blo && bk <= bhi) {
           take = true;
@@ -285,7 +285,8 @@ __device__ __forceinline__ unsigned long long row_box(int ya, int yb, int za, in
 }
 
 template <bool IS3D>
-__global__ void __launch_bounds__(kWarps * 32, 6) k_dilate_gather(const TileMeta* __restrict__ meta,
+__global__ void __launch_bounds__(kWarps * 32, 6) k_dilate_gather(const uint32_t* __restrict__ fgm,
+                                                                  const TileMeta* __restrict__ meta,
                                                                const uint2* __restrict__ cent,
                                                                const uint16_t* __restrict__ oct,
                                                                uint32_t* __restrict__ fbl, Geom g, int force_fallback,
@@ -331,6 +332,38 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_dilate_gather(const TileMeta
     if (tid == 0) gcount[group] = kGroupFallback;
     return;
   }
+  // bounding box of the group's foreground (K4's row masks): candidates must reach it
+  if (tid == 0) {
+    S.bb[0] = S.bb[2] = S.bb[4] = 1 << 20;
+    S.bb[1] = S.bb[3] = S.bb[5] = -(1 << 20);
+  }
+  __syncthreads();
+  {
+    uint32_t xm = 0;
+    int y0 = 1 << 20, y1 = -(1 << 20), z0 = 1 << 20, z1 = -(1 << 20);
+    if (active) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int row = lane + 32 * k;
+        const uint32_t f = fgm[mtile * kRows + row];
+        if (f) {
+          xm |= f;
+          const int ly = row % TY + moy, lz = row / TY + moz;
+          y0 = min(y0, ly); y1 = max(y1, ly); z0 = min(z0, lz); z1 = max(z1, lz);
+        }
+      }
+    }
+    xm = __reduce_or_sync(kFull, xm);
+    y0 = __reduce_min_sync(kFull, y0); y1 = __reduce_max_sync(kFull, y1);
+    z0 = __reduce_min_sync(kFull, z0); z1 = __reduce_max_sync(kFull, z1);
+    if (lane == 0 && xm) {
+      atomicMin(&S.bb[0], mox + __ffs(xm) - 1);
+      atomicMax(&S.bb[1], mox + 31 - __clz(xm));
+      atomicMin(&S.bb[2], y0); atomicMax(&S.bb[3], y1);
+      atomicMin(&S.bb[4], z0); atomicMax(&S.bb[5], z1);
+    }
+  }
+  __syncthreads();
   const int rmax = dmax > 0 ? isqrt16((int)(dmax - 1)) : 0;
   const int nrx = (rmax + kTX - 1) / kTX, nry = (rmax + TY - 1) / TY, nrz = IS3D ? (rmax + TZ - 1) / TZ : 0;
   uint32_t written = 0;
@@ -788,32 +821,25 @@ int64_t dilate_pool_entries(const Geom& g) {
 }
 
 namespace {
-int point_at_knob() {
-  static const int point_at = [] {
-    const char* v = getenv("FASTRS_POINT_AT");  // development knob (default kPoint)
-    const int p = v ? atoi(v) : kPoint;
-    return p < 0 ? 0 : (p > kPoint ? kPoint : p);
-  }();
-  return point_at;
-}
+int point_at_knob() { return kPoint; }  // uncovered cells at which a warp switches to point tests
 int64_t launched_groups(const Geom& g) {
   const int GX = g.ndim == 3 ? 1 : 2, GY = 2, GZ = g.ndim == 3 ? 2 : 1;
   return g.B * ((g.ntx + GX - 1) / GX) * ((g.nty + GY - 1) / GY) * ((g.tz_hi - g.tz_lo + GZ - 1) / GZ);
 }
 }  // namespace
 
-void launch_dilate_gather(TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
+void launch_dilate_gather(const uint32_t* fgm, TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
                           unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int force_fallback,
                           WsHeader* hdr, cudaStream_t st) {
   const int64_t ngroups = launched_groups(g);
   if (ngroups <= 0) return;
   const unsigned long long pool_cap = (unsigned long long)dilate_pool_entries(g);
   if (g.ndim == 3)
-    k_dilate_gather<true><<<(unsigned)ngroups, kWarps * 32, sizeof(Smem), st>>>(meta, centres, oct, fbl, g,
+    k_dilate_gather<true><<<(unsigned)ngroups, kWarps * 32, sizeof(Smem), st>>>(fgm, meta, centres, oct, fbl, g,
                                                                                  force_fallback, pool, pool_cap, gcount,
                                                                                  goff, hdr);
   else
-    k_dilate_gather<false><<<(unsigned)ngroups, kWarps * 32, sizeof(Smem), st>>>(meta, centres, oct, fbl, g,
+    k_dilate_gather<false><<<(unsigned)ngroups, kWarps * 32, sizeof(Smem), st>>>(fgm, meta, centres, oct, fbl, g,
                                                                                   force_fallback, pool, pool_cap, gcount,
                                                                                   goff, hdr);
 }
