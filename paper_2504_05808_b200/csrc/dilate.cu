@@ -55,10 +55,10 @@ struct Smem {  // K5a (gather + sort)
 };
 
 struct PaintSmem {  // K5b (one tile per warp)
-  uint16_t val[kWarps][kRows * 32];  // LT^2 per element of each warp's tile (D <= 65535 here)
-  uint32_t fg[kWarps][kRows];        // foreground mask per row
-  uint32_t cov[kWarps][kRows];       // covered (final value written)
-  uint16_t ulist[kWarps][kPoint];    // point mode: the still-uncovered cells (row*32 + x)
+  uint16_t val[kWarps][kRows * 32];   // LT^2 per element of each warp's tile (D <= 65535 here)
+  int4 sball[kWarps][32];             // survivors of a screened batch: centre (tile coords), D
+  unsigned long long scand[kWarps][32];  // their candidate rows
+  uint16_t ulist[kWarps][kPoint];     // point mode: the still-uncovered cells (row*32 + x)
 };
 
 template <bool IS3D>
@@ -602,32 +602,27 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
 
   // ---- per-warp init: values, foreground masks, coverage ----------------------------------
   uint16_t* val = S.val[warp];
-  uint32_t* fgw = S.fg[warp];
-  uint32_t* covw = S.cov[warp];
   {
     uint4* v4 = reinterpret_cast<uint4*>(val);
 #pragma unroll 4
     for (int i = lane; i < kRows * 32 / 8; i += 32) v4[i] = make_uint4(0u, 0u, 0u, 0u);
   }
-  // rows of my tile that still hold uncovered foreground, per 8-column chunk of x (K4 wrote
-  // the tile's foreground row masks)
-  unsigned long long Uc[4] = {0, 0, 0, 0};
-  {
-    uint32_t f[2];
+  // lane owns rows `lane` (0) and `lane + 32` (1): foreground and covered masks in registers
+  const uint32_t f0 = active ? fgm[mtile * kRows + lane] : 0u, f1 = active ? fgm[mtile * kRows + lane + 32] : 0u;
+  uint32_t c0 = 0, c1 = 0;
+  const int ly0 = IS3D ? (lane & 7) : lane, lz0 = IS3D ? (lane >> 3) : 0;
+  const int ly1 = IS3D ? ly0 : lane + 32, lz1 = IS3D ? lz0 + 4 : 0;
+  // rows of my tile that still hold uncovered foreground, per 8-column chunk of x
+  unsigned long long Uc[4];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      f[k] = active ? fgm[mtile * kRows + lane + 32 * k] : 0u;
-      fgw[lane + 32 * k] = f[k];
-      covw[lane + 32 * k] = 0;
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      Uc[c] = (unsigned long long)__ballot_sync(kFull, (f[0] >> (8 * c)) & 0xFFu) |
-              ((unsigned long long)__ballot_sync(kFull, (f[1] >> (8 * c)) & 0xFFu) << 32);
-  }
+  for (int c = 0; c < 4; ++c)
+    Uc[c] = (unsigned long long)__ballot_sync(kFull, (f0 >> (8 * c)) & 0xFFu) |
+            ((unsigned long long)__ballot_sync(kFull, (f1 >> (8 * c)) & 0xFFu) << 32);
   __syncwarp();
   // uncovered foreground cells of my tile (warp-uniform); point mode once it is small
-  int nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(fgw[lane]) + __popc(fgw[lane + 32])));
+  int nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(f0) + __popc(f1)));
+  int4* sball = S.sball[warp];                 // survivors of a screened batch (cx, cy, cz, D)
+  unsigned long long* scand = S.scand[warp];   // their candidate rows
   bool pmode = false;
   uint16_t* ulist = S.ulist[warp];
   int ub[6] = {0, kTX - 1, 0, TY - 1, 0, TZ - 1};  // bounding box of the uncovered cells (point mode)
@@ -654,9 +649,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
       const uint32_t i = i0 + lane;
       if (!pmode && nu <= point_at) {
         // switch to point mode: list the still-uncovered cells
-        uint32_t left[2];
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) left[kk] = fgw[lane + 32 * kk] & ~covw[lane + 32 * kk];
+        const uint32_t left[2] = {f0 & ~c0, f1 & ~c1};
         const uint32_t cnt = __popc(left[0]) + __popc(left[1]);
         uint32_t inc = cnt;
 #pragma unroll
@@ -748,42 +741,47 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
           cand = row_box<IS3D>(max(cy - rho, 0), min(cy + rho, TY - 1), max(cz - rho, 0), min(cz + rho, TZ - 1)) & ux;
         }
       }
-      uint32_t act = __ballot_sync(kFull, cand != 0);
-      while (act) {
-        const int j = __ffs(act) - 1;
-        act &= act - 1;
-        const int jx = __shfl_sync(kFull, cx, j), jy = __shfl_sync(kFull, cy, j), jz = __shfl_sync(kFull, cz, j);
-        const int jD = __shfl_sync(kFull, D, j), jR2 = jD - 1;
-        const uint32_t jm[2] = {__shfl_sync(kFull, (uint32_t)cand, j), __shfl_sync(kFull, (uint32_t)(cand >> 32), j)};
-        const uint16_t dv = (uint16_t)jD;
+      // survivors, compacted in lane order (= descending D) into the warp's buffer, then painted
+      // one by one: every lane reads the ball (broadcast) and handles its own two rows
+      const uint32_t act = __ballot_sync(kFull, cand != 0);
+      if (act) {
+        if (cand) {
+          const int slot = __popc(act & ((1u << lane) - 1u));
+          sball[slot] = make_int4(cx, cy, cz, D);
+          scand[slot] = cand;
+        }
+        __syncwarp();
+        const int ns = __popc(act);
+        for (int j = 0; j < ns; ++j) {
+          const int4 bp = sball[j];
+          const unsigned long long jc = scand[j];
+          const int jR2 = bp.w - 1;
+          const uint16_t dv = (uint16_t)bp.w;
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          if (!((jm[half] >> lane) & 1u)) continue;
-          const int row = 32 * half + lane;
-          const int ly = IS3D ? (row & 7) : row, lz = IS3D ? (row >> 3) : 0;
-          const int dy = ly - jy, dz = lz - jz;
-          const int hrem = jR2 - dy * dy - dz * dz;
-          if (hrem < 0) continue;
-          const int w = isqrt16(hrem);
-          const int l = max(jx - w, 0), rr = min(jx + w, kTX - 1);
-          if (l > rr) continue;
-          ++n_rows;
-          uint32_t m = fgw[row] & ~covw[row] & range_mask(l, rr);
-          if (!m) continue;
-          covw[row] |= m;
-          uint16_t* vr = val + row * 32;
-          do {
-            const int c = __ffs(m) - 1;
-            m &= m - 1;
-            vr[c] = dv;
-          } while (m);
+          for (int hf = 0; hf < 2; ++hf) {
+            if (!((jc >> (32 * hf + lane)) & 1ull)) continue;
+            const int dy = (hf ? ly1 : ly0) - bp.y, dz = (hf ? lz1 : lz0) - bp.z;
+            const int hrem = jR2 - dy * dy - dz * dz;
+            if (hrem < 0) continue;
+            const int w = isqrt16(hrem);
+            const int l = max(bp.x - w, 0), rr = min(bp.x + w, kTX - 1);
+            if (l > rr) continue;
+            ++n_rows;
+            uint32_t m = (hf ? (f1 & ~c1) : (f0 & ~c0)) & range_mask(l, rr);
+            if (!m) continue;
+            if (hf) c1 |= m; else c0 |= m;
+            uint16_t* vr = val + (32 * hf + lane) * 32;
+            do {
+              const int c = __ffs(m) - 1;
+              m &= m - 1;
+              vr[c] = dv;
+            } while (m);
+          }
         }
         __syncwarp();
       }
       // refresh the uncovered-row masks
-      uint32_t left[2];
-#pragma unroll
-      for (int kk = 0; kk < 2; ++kk) left[kk] = fgw[lane + 32 * kk] & ~covw[lane + 32 * kk];
+      const uint32_t left[2] = {f0 & ~c0, f1 & ~c1};
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         Uc[c] = (unsigned long long)__ballot_sync(kFull, (left[0] >> (8 * c)) & 0xFFu) |
