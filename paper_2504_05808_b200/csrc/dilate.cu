@@ -637,6 +637,52 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
     ub[2] = __reduce_min_sync(kFull, y0); ub[3] = __reduce_max_sync(kFull, y1);
     ub[4] = __reduce_min_sync(kFull, z0); ub[5] = __reduce_max_sync(kFull, z1);
   };
+  int nq = 0;  // point mode: queued balls in sball (warp-uniform)
+  auto point_flush = [&]() {
+    int cx = 0, cy = 0, cz = 0, D = 0;
+    if (lane < nq) {
+      const int4 bp = sball[lane];
+      cx = bp.x;
+      cy = bp.y;
+      cz = bp.z;
+      D = bp.w;
+    }
+    nq = 0;
+    bool hit = false;
+    for (int q = 0; q < nu; ++q) {
+      const uint32_t e = ulist[q];
+      const int x = (int)(e & 31u), row = (int)(e >> 5);
+      const int ly = IS3D ? (row & 7) : row, lz = IS3D ? (row >> 3) : 0;
+      const int dx = x - cx, dy = ly - cy, dz = lz - cz;
+      const uint32_t bm = __ballot_sync(kFull, dx * dx + dy * dy + dz * dz < D);
+      if (bm) {
+        const int wD = __shfl_sync(kFull, D, __ffs(bm) - 1);
+        if (lane == 0) {
+          val[e] = (uint16_t)wD;
+          ulist[q] = (uint16_t)(e | 0x8000u);
+        }
+        hit = true;
+      }
+    }
+    if (hit) {  // drop the covered cells from the list
+      __syncwarp();
+      uint32_t newn = 0;
+      for (int q0 = 0; q0 < nu; q0 += 32) {
+        const int q = q0 + lane;
+        const uint32_t e = q < nu ? ulist[q] : 0x8000u;
+        const bool keep = !(e & 0x8000u);
+        const uint32_t km = __ballot_sync(kFull, keep);
+        __syncwarp();
+        if (keep) ulist[newn + __popc(km & ((1u << lane) - 1u))] = (uint16_t)e;
+        newn += __popc(km);
+        __syncwarp();
+      }
+      nu = (int)newn;
+      __syncwarp();
+      ubox_refresh();
+    }
+    __syncwarp();
+  };
 
   uint32_t n_rows = 0;
   {
@@ -672,8 +718,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
         ubox_refresh();
       }
       if (pmode) {
-        // point tests: lanes = the next 32 balls (descending D), loop over the uncovered cells;
-        // a cell takes the D of the first (largest) ball containing it
+        // point tests.  The next 32 balls are screened against the bounding box of the
+        // still-uncovered cells and the survivors queued (order kept = descending D); a full
+        // queue is flushed: lanes = queued balls, loop over the uncovered cells, a cell takes
+        // the D of the first (largest) ball containing it.
         int cx = 0, cy = 0, cz = 0, D = 0;
         if (i < total) {
           const unsigned long long e = list[i];
@@ -681,44 +729,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
           cx = (int)((e >> 16) & 0xFFFFu) - kOff - mox;
           cy = (int)((e >> 32) & 0xFFFFu) - kOff - moy;
           cz = (int)((e >> 48) & 0xFFFFu) - kOff - moz;
-          // the ball must reach the bounding box of the still-uncovered cells
           const int ddx = gap(ub[0], ub[1], cx), ddy = gap(ub[2], ub[3], cy), ddz = gap(ub[4], ub[5], cz);
           if (ddx * ddx + ddy * ddy + ddz * ddz > D - 1) D = 0;
         }
-        if (__ballot_sync(kFull, D != 0) == 0) continue;
-        bool hit = false;
-        for (int q = 0; q < nu; ++q) {
-          const uint32_t e = ulist[q];
-          const int x = (int)(e & 31u), row = (int)(e >> 5);
-          const int ly = IS3D ? (row & 7) : row, lz = IS3D ? (row >> 3) : 0;
-          const int dx = x - cx, dy = ly - cy, dz = lz - cz;
-          const uint32_t bm = __ballot_sync(kFull, dx * dx + dy * dy + dz * dz < D);
-          if (bm) {
-            const int wD = __shfl_sync(kFull, D, __ffs(bm) - 1);
-            if (lane == 0) {
-              val[e] = (uint16_t)wD;
-              ulist[q] = (uint16_t)(e | 0x8000u);
-            }
-            hit = true;
-          }
-        }
-        if (hit) {  // drop the covered cells from the list
-          __syncwarp();
-          uint32_t newn = 0;
-          for (int q0 = 0; q0 < nu; q0 += 32) {
-            const int q = q0 + lane;
-            const uint32_t e = q < nu ? ulist[q] : 0x8000u;
-            const bool keep = !(e & 0x8000u);
-            const uint32_t km = __ballot_sync(kFull, keep);
-            __syncwarp();
-            if (keep) ulist[newn + __popc(km & ((1u << lane) - 1u))] = (uint16_t)e;
-            newn += __popc(km);
-            __syncwarp();
-          }
-          nu = (int)newn;
-          __syncwarp();
-          ubox_refresh();
-        }
+        const uint32_t sv = __ballot_sync(kFull, D != 0);
+        if (nq + __popc(sv) > 32) point_flush();
+        if (nu == 0) break;
+        if (D != 0) sball[nq + __popc(sv & ((1u << lane) - 1u))] = make_int4(cx, cy, cz, D);
+        nq += __popc(sv);
+        __syncwarp();
         continue;
       }
       unsigned long long cand = 0;
@@ -788,6 +807,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
                 ((unsigned long long)__ballot_sync(kFull, (left[1] >> (8 * c)) & 0xFFu) << 32);
       nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(left[0]) + __popc(left[1])));
     }
+    if (pmode && nq > 0 && nu > 0) point_flush();  // the queue's last balls
   }
 
 
