@@ -5,6 +5,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "fastrs.h"
@@ -310,6 +311,128 @@ int slab_prologue(const int64_t* dims, Geom& g, SlabLayout& L, void* ws, size_t 
   return e == cudaSuccess ? FASTRS_OK : cuda_fail(e, "cudaMemsetAsync");
 }
 
+// ---- host entry point: the host->device copy overlapped with the computation -------------
+// The label volume is copied in z-chunks of kChunkZ slices on a copy stream; the compute stream
+// runs each stage on a chunk as soon as the chunks it depends on are in: K1+K2 on chunk c
+// (per-slice work), K3 on chunk c-1 (reads up to h = ceil(sqrt(max D_xy)) slices away), K4 on
+// chunk c-2 (3-voxel halo), K5a+K5b on chunk c-3 (balls of radius R = isqrt(Dmax-1)); K5's
+// fallback tiles, the epilogue (it needs the final Dmax for the fixed-point scale) and K6 run
+// after the last chunk.  Exact whenever h <= kChunkZ and R <= kChunkZ, which is checked at the
+// end; otherwise the call recomputes everything with the plain path from the resident labels.
+constexpr int64_t kChunkZ = 128;  // a multiple of the 16-slice K5 tile group
+
+std::mutex g_cs_mu;
+cudaStream_t g_copy_stream[64];
+
+cudaStream_t copy_stream(int dev) {
+  std::lock_guard<std::mutex> lk(g_cs_mu);
+  if (!g_copy_stream[dev]) cudaStreamCreateWithFlags(&g_copy_stream[dev], cudaStreamNonBlocking);
+  return g_copy_stream[dev];
+}
+
+// returns FASTRS_OK with *exact = false when the halo check failed (the caller reruns)
+int run_host_pipelined(const int32_t* labels_host, int32_t* dlab, const Geom& g, int32_t max_label, uint32_t flags,
+                       const Outputs& outs, void* ws, cudaStream_t st, bool* exact) {
+  *exact = false;
+  const Layout L = make_layout(g, max_label, 0);
+  char* w = (char*)ws;
+  WsHeader* hdr = (WsHeader*)(w + L.hdr);
+  uint32_t* A = (uint32_t*)(w + L.A);
+  uint32_t* B = (uint32_t*)(w + L.B);
+  TileMeta* meta = (TileMeta*)(w + L.meta);
+  uint2* cent = (uint2*)(w + L.cent);
+  uint32_t* fgm = (uint32_t*)(w + L.fgm);
+  uint16_t* oct = (uint16_t*)(w + L.oct);
+  uint32_t* fbl = (uint32_t*)(w + L.fbl);
+  unsigned long long* pool = (unsigned long long*)(w + L.pool);
+  uint32_t* gcount = (uint32_t*)(w + L.gcount);
+  uint32_t* goff = (uint32_t*)(w + L.goff);
+  const bool border = (flags & kFlagBorder) != 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = ensure_mtables(dev);
+  if (e != cudaSuccess) return cuda_fail(e, "per-device setup");
+  Accum acc{};
+  acc.vol = (unsigned long long*)(w + L.vol);
+  acc.nshell = (unsigned long long*)(w + L.nsh);
+  acc.sum = (unsigned long long*)(w + L.sum);
+  acc.sumshell = (unsigned long long*)(w + L.sumsh);
+  acc.maxlt2 = (uint32_t*)(w + L.mx);
+  acc.M = (int64_t)max_label;
+  acc.max_label = max_label;
+  cudaMemsetAsync(hdr, 0, 256, st);
+  cudaMemsetAsync(w + L.vol, 0, (L.mx - L.vol) + align256((size_t)acc.M * 4), st);
+  cudaMemsetAsync(meta, 0, (size_t)g.ntiles * sizeof(TileMeta), st);  // unpruned tiles read as empty
+  const int64_t YX = g.Y * g.X, Z = g.Z;
+  const int nc = (int)((Z + kChunkZ - 1) / kChunkZ);
+  cudaStream_t cs = copy_stream(dev);
+  std::vector<cudaEvent_t> ev(nc + 1);
+  for (auto& x : ev) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  cudaEventRecord(ev[nc], st);  // the copies wait for earlier work on the caller's stream
+  cudaStreamWaitEvent(cs, ev[nc], 0);
+  for (int c = 0; c < nc; ++c) {
+    const int64_t z0 = c * kChunkZ, nz = (z0 + kChunkZ < Z ? kChunkZ : Z - z0);
+    e = cudaMemcpyAsync(dlab + z0 * YX, labels_host + z0 * YX, (size_t)(nz * YX) * 4, cudaMemcpyHostToDevice, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D labels chunk");
+    cudaEventRecord(ev[c], cs);
+  }
+  auto zr = [&](int c, int64_t& z0, int64_t& z1) {
+    z0 = c * kChunkZ;
+    z1 = z0 + kChunkZ < Z ? z0 + kChunkZ : Z;
+  };
+  for (int step = 0; step < nc + 3; ++step) {
+    int64_t z0, z1;
+    if (step < nc) {  // K1 + K2 on chunk `step`
+      zr(step, z0, z1);
+      cudaStreamWaitEvent(st, ev[step], 0);
+      const int64_t cd[3] = {z1 - z0, g.Y, g.X};
+      Geom gc;
+      make_geom(cd, 3, 1, gc);
+      launch_edt_x(dlab + z0 * YX, z0 > 0 ? dlab + (z0 - 1) * YX : nullptr, A + z0 * YX, gc, max_label, border, hdr,
+                   st);
+      launch_edt_col(A + z0 * YX, B + z0 * YX, gc, 1, false, border, hdr, st);
+    }
+    if (step >= 1 && step - 1 < nc) {  // K3 on chunk step-1: D into A
+      zr(step - 1, z0, z1);
+      launch_edt_col(B, A + z0 * YX, g, 2, true, border, hdr, st, z0, z1);
+    }
+    if (step >= 2 && step - 2 < nc) {  // K4 on chunk step-2
+      zr(step - 2, z0, z1);
+      launch_prune(A, g, meta, cent, fgm, oct, hdr, st, z0 / kTZ3, (z1 + kTZ3 - 1) / kTZ3);
+    }
+    if (step >= 3 && step - 3 < nc) {  // K5a + K5b on chunk step-3 (LT^2 into B: its y-pass words are consumed)
+      zr(step - 3, z0, z1);
+      Geom gg = g;
+      gg.tz_lo = z0 / kTZ3;
+      gg.tz_hi = (z1 + kTZ3 - 1) / kTZ3;
+      launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, gg, 0, hdr, st);
+      launch_dilate_paint(fgm, meta, pool, gcount, goff, gg, B, hdr, st);
+    }
+  }
+  launch_dilate_fallback(meta, cent, fbl, g, B, hdr, st);
+  // halo check: the chunked z pass and dilation were exact iff both halos fit in one chunk
+  WsHeader h;
+  e = cudaMemcpyAsync(&h, hdr, sizeof h, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  for (auto& x : ev) cudaEventDestroy(x);
+  if (e != cudaSuccess) return cuda_fail(e, "pipelined pass");
+  if (h.status & (kStBadLabel | kStNoSite)) {  // report through the caller's status read
+    *exact = true;
+    return FASTRS_OK;
+  }
+  uint64_t hz = 0;
+  while (hz * hz < h.dxymax && hz <= (uint64_t)kChunkZ) ++hz;
+  uint64_t rr = 0;
+  while ((rr + 1) * (rr + 1) <= (h.dmax ? h.dmax - 1 : 0) && rr <= (uint64_t)kChunkZ) ++rr;
+  if (hz > (uint64_t)kChunkZ || rr > (uint64_t)kChunkZ || h.dxymax >= kInf) return FASTRS_OK;  // not exact: rerun
+  launch_epilogue(dlab, A, g, &acc, nullptr, nullptr, B, (unsigned long long*)(w + L.fxl), hdr, st);
+  launch_metrics(acc, g, outs, hdr, st);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  *exact = true;
+  return FASTRS_OK;
+}
+
 }  // namespace
 }  // namespace fastrs
 
@@ -384,13 +507,22 @@ int fastrs_sphericity_roundness_host(const int32_t* labels_host, const int64_t* 
   int32_t* dlab = (int32_t*)(w + L.h_labels);
   double* dsph = (double*)(w + L.h_sph);
   double* drnd = (double*)(w + L.h_rnd);
-  cudaError_t e = cudaMemcpyAsync(dlab, labels_host, (size_t)g.N * 4, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return cuda_fail(e, "H2D labels");
   Outputs o{};
   o.sphericity = dsph;
   o.roundness = drnd;
-  rc = run(dlab, g, max_label, flags | kFlagAsync, kFull, nullptr, nullptr, nullptr, &o, ws, ws_bytes, st);
-  if (rc) return rc;
+  bool done = false;
+  if (g.ndim == 3 && g.B == 1 && g.Z >= 4 * kChunkZ && !(flags & kFlagForceFallback)) {
+    rc = run_host_pipelined(labels_host, dlab, g, max_label, flags, o, ws, st, &done);
+    if (rc) return rc;
+  } else {
+    cudaError_t e0 = cudaMemcpyAsync(dlab, labels_host, (size_t)g.N * 4, cudaMemcpyHostToDevice, st);
+    if (e0 != cudaSuccess) return cuda_fail(e0, "H2D labels");
+  }
+  if (!done) {  // plain path (labels resident in dlab)
+    rc = run(dlab, g, max_label, flags | kFlagAsync, kFull, nullptr, nullptr, nullptr, &o, ws, ws_bytes, st);
+    if (rc) return rc;
+  }
+  cudaError_t e = cudaSuccess;
   const size_t M = (size_t)g.B * max_label;
   uint32_t status = 0;
   e = cudaMemcpyAsync(&status, w + make_layout(g, max_label, 0).hdr, 4, cudaMemcpyDeviceToHost, st);

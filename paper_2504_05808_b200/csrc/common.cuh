@@ -146,13 +146,18 @@ cudaError_t ensure_mtables(int device);  // builds the per-device lattice tables
 // K4; also writes per tile the foreground row masks (fgm: kRows u32) and the number of kept
 // entries with D bucket >= 8o for o = 0..15 (oct: 16 u16) used by K5's gather
 void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, uint32_t* fgm, uint16_t* oct,
-                  WsHeader* hdr, cudaStream_t st);
+                  WsHeader* hdr, cudaStream_t st, int64_t tz_lo = 0, int64_t tz_hi = 0);
 void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta,
                    const uint2* centres, const uint32_t* fgm, const uint16_t* oct, uint32_t* fbl,
                    unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, const Accum* acc,
                    uint32_t* lt2_out, float* lt_out, bool force_fallback, uint32_t* ltp, WsHeader* hdr,
                    cudaStream_t st);
 int64_t dilate_groups(const Geom& g);        // K5 tile groups (gcount / goff entries)
+void launch_dilate_paint(const uint32_t* fgm, const TileMeta* meta, const unsigned long long* pool,
+                         const uint32_t* gcount, const uint32_t* goff, const Geom& g, uint32_t* ltp, WsHeader* hdr,
+                         cudaStream_t st);
+void launch_dilate_fallback(TileMeta* meta, const uint2* centres, const uint32_t* fbl, const Geom& g, uint32_t* ltp,
+                            WsHeader* hdr, cudaStream_t st);
 // K5a: per tile group, gather the kept balls that reach it and write them sorted by D
 // (descending) to the candidate pool; groups that cannot be handled are listed in fbl
 void launch_dilate_gather(const uint32_t* fgm, TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,

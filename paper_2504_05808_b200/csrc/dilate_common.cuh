@@ -72,8 +72,6 @@ static __device__ __forceinline__ uint32_t row_epilogue(uint32_t c, int lane, bo
 
 
 cudaError_t dilate_cover_setup();
-void launch_dilate_paint(const uint32_t* fgm, const TileMeta* meta, const unsigned long long* pool,
-                         const uint32_t* gcount, const uint32_t* goff, const Geom& g, uint32_t* ltp, WsHeader* hdr,
-                         cudaStream_t st);
+
 
 }  // namespace fastrs

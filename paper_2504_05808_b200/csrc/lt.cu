@@ -260,17 +260,8 @@ cudaError_t dilate_atomic_setup() {
   return e;
 }
 
-void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta, const uint2* centres,
-                   const uint32_t* fgm, const uint16_t* oct, uint32_t* fbl, unsigned long long* pool,
-                   uint32_t* gcount, uint32_t* goff, const Geom& g, const Accum* acc, uint32_t* lt2_out, float* lt_out,
-                   bool force_fallback, uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
-  Accum a{};
-  if (acc) a = *acc;
-  // both dilation kernels read Dmax / the per-tile fallback flag on the device; the atomic
-  // kernel only processes tiles the exact-order kernel left to it.  Both write LT^2 to ltp.
-  (void)oct;
-  (void)force_fallback;
-  launch_dilate_paint(fgm, meta, pool, gcount, goff, g, ltp, hdr, st);  // K5b (after K5a launch_dilate_gather)
+void launch_dilate_fallback(TileMeta* meta, const uint2* centres, const uint32_t* fbl, const Geom& g, uint32_t* ltp,
+                            WsHeader* hdr, cudaStream_t st) {
   const size_t smem = (size_t)kRows * kRowStride * 4;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -280,6 +271,23 @@ void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta, con
     k_dilate_atomic<true><<<grid, 256, smem, st>>>(meta, centres, g, fbl, ltp, hdr);
   else
     k_dilate_atomic<false><<<grid, 256, smem, st>>>(meta, centres, g, fbl, ltp, hdr);
+}
+
+void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta, const uint2* centres,
+                   const uint32_t* fgm, const uint16_t* oct, uint32_t* fbl, unsigned long long* pool,
+                   uint32_t* gcount, uint32_t* goff, const Geom& g, const Accum* acc, uint32_t* lt2_out, float* lt_out,
+                   bool force_fallback, uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
+  (void)labels;
+  (void)D;
+  (void)acc;
+  (void)lt2_out;
+  (void)lt_out;
+  (void)oct;
+  (void)force_fallback;
+  // K5b paints the groups K5a sorted; the atomic kernel takes the tiles K5a listed (or every
+  // tile when Dmax > 65535).  Both write LT^2 to ltp.
+  launch_dilate_paint(fgm, meta, pool, gcount, goff, g, ltp, hdr, st);
+  launch_dilate_fallback(meta, centres, fbl, g, ltp, hdr, st);
 }
 
 void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,

@@ -129,7 +129,7 @@ template <bool IS3D>
 __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, Geom g, TileMeta* __restrict__ meta,
                                                uint2* __restrict__ cent, uint32_t* __restrict__ fgm,
                                                uint16_t* __restrict__ oct, const uint32_t* __restrict__ M,
-                                               WsHeader* __restrict__ hdr) {
+                                               int64_t tile0, WsHeader* __restrict__ hdr) {
   using P = PruneTile<IS3D>;
   __shared__ __align__(16) uint32_t s[P::PZ * P::PY * P::PX];
   __shared__ uint32_t keepmask[kRows];
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
   __shared__ uint32_t s_nsurv;
   __shared__ uint32_t bhist[128];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t tile = blockIdx.x;
+  const int64_t tile = tile0 + blockIdx.x;
   int64_t t = tile;
   const int64_t tx = t % g.ntx;
   t /= g.ntx;
@@ -434,13 +434,18 @@ void release_mtables() {
 }
 
 void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, uint32_t* fgm, uint16_t* oct,
-                  WsHeader* hdr, cudaStream_t st) {
+                  WsHeader* hdr, cudaStream_t st, int64_t tz_lo, int64_t tz_hi) {
   int dev = 0;
   cudaGetDevice(&dev);
+  // tile layers [tz_lo, tz_hi) of item 0 (batch 1), or every tile
+  const bool part = tz_hi > tz_lo && g.B == 1;
+  const int64_t tile0 = part ? tz_lo * g.nty * g.ntx : 0;
+  const int64_t n = part ? (tz_hi - tz_lo) * g.nty * g.ntx : g.ntiles;
+  if (n <= 0) return;
   if (g.ndim == 3)
-    k_prune<true><<<(unsigned)g.ntiles, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m3, hdr);
+    k_prune<true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m3, tile0, hdr);
   else
-    k_prune<false><<<(unsigned)g.ntiles, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m2, hdr);
+    k_prune<false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m2, tile0, hdr);
 }
 
 }  // namespace fastrs

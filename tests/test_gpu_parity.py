@@ -283,3 +283,23 @@ def test_dilation_cross_check_full_size(F, cfg, c4):
     assert bool((a.view(torch.int32) >= d.view(torch.int32)).all())
     del a, b, d, t
     torch.cuda.empty_cache()
+
+
+def test_host_entry_point_pipelined_matches_device_call(F):
+    """fastrs_sphericity_roundness_host on a volume deep enough for the chunked copy/compute
+    pipeline (Z >= 512) gives results bit-identical to the device call; with a ball too big for
+    one chunk (R > 128) the pipeline's halo check fails and the call recomputes: still exact."""
+    lab, info = synth.make_config(3)
+    ml = info["max_label"]
+    want = F.sphericity_roundness(_dev(lab), max_label=ml)
+    s, r = F.sphericity_roundness_host(lab, max_label=ml)
+    np.testing.assert_array_equal(s, want["sphericity"].cpu().numpy())
+    np.testing.assert_array_equal(r, want["roundness"].cpu().numpy())
+    big = np.zeros((520, 310, 310), np.int32)
+    big[5:306, 5:306, 5:306] = synth.sphere(150, canvas=301)
+    big[400:440, 100:120, 100:130] = 2
+    want = F.sphericity_roundness(_dev(big), max_label=2)
+    s, r = F.sphericity_roundness_host(big, max_label=2)
+    np.testing.assert_array_equal(s, want["sphericity"].cpu().numpy())
+    np.testing.assert_array_equal(r, want["roundness"].cpu().numpy())
+    assert r[0] == 1.0
