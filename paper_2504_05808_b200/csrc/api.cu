@@ -319,7 +319,7 @@ int slab_prologue(const int64_t* dims, Geom& g, SlabLayout& L, void* ws, size_t 
 // fallback tiles, the epilogue (it needs the final Dmax for the fixed-point scale) and K6 run
 // after the last chunk.  Exact whenever h <= kChunkZ and R <= kChunkZ, which is checked at the
 // end; otherwise the call recomputes everything with the plain path from the resident labels.
-constexpr int64_t kChunkZ = 128;  // a multiple of the 16-slice K5 tile group
+constexpr int64_t kChunkZ = 64;  // a multiple of the 16-slice K5 tile group
 
 std::mutex g_cs_mu;
 cudaStream_t g_copy_stream[64];
