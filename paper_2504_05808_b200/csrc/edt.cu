@@ -182,46 +182,79 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
       // that hands the element to the slow path below.
       const int i = (int)(p - lo), nt = (int)(hi - lo);
       bool slow = false;
+      // dq^2 < best <= g bounds the scan: when isqrt(g-1) rows exist on a side, that side's loop
+      // needs no window-end check (the common case)
+      const int reach = (int)sqrtf((float)(g - 1)) + 1;  // >= isqrt(g - 1)
       {
         uint32_t dq2 = 1, inc = 3;
         const uint32_t* w_ptr = tile + (i + 1) * 32 + lane;
-        const uint32_t* w_end = tile + nt * 32 + lane;
-        while (dq2 < best) {
-          if (w_ptr >= w_end) {
-            if (hi < L) slow = true;  // more rows exist beyond the staged window
-            else if (border && gofs + L >= Lg) best = min(best, dq2);  // the grid end
-            break;
+        if (reach <= nt - 1 - i) {
+          while (dq2 < best) {
+            const uint32_t w = *w_ptr;
+            if (w & chbit) {
+              best = min(best, dq2);
+              break;
+            }
+            best = min(best, (w & kMask) + dq2);
+            dq2 += inc;
+            inc += 2;
+            w_ptr += 32;
           }
-          const uint32_t w = *w_ptr;
-          if (w & chbit) {
-            best = min(best, dq2);
-            break;
+        } else {
+          const uint32_t* w_end = tile + nt * 32 + lane;
+          while (dq2 < best) {
+            if (w_ptr >= w_end) {
+              if (hi < L) slow = true;  // more rows exist beyond the staged window
+              else if (border && gofs + L >= Lg) best = min(best, dq2);  // the grid end
+              break;
+            }
+            const uint32_t w = *w_ptr;
+            if (w & chbit) {
+              best = min(best, dq2);
+              break;
+            }
+            best = min(best, (w & kMask) + dq2);
+            dq2 += inc;
+            inc += 2;
+            w_ptr += 32;
           }
-          best = min(best, (w & kMask) + dq2);
-          dq2 += inc;
-          inc += 2;
-          w_ptr += 32;
         }
       }
       // down side: rows p-1, p-2, ...; element p-dq lies outside the run iff p-dq+1 starts it
       {
         uint32_t dq2 = 1, inc = 3, chk = v & chbit;
-        int r = i - 1;
-        while (dq2 < best) {
-          if (chk) {
-            if (gofs + lo + r >= 0 || border) best = min(best, dq2);
-            break;
+        const uint32_t* w_ptr = tile + (i - 1) * 32 + lane;
+        if (reach <= i) {
+          while (dq2 < best) {
+            if (chk) {  // the element at p-dq is inside the staged window: a real site
+              best = min(best, dq2);
+              break;
+            }
+            const uint32_t w = *w_ptr;
+            best = min(best, (w & kMask) + dq2);
+            chk = w & chbit;
+            dq2 += inc;
+            inc += 2;
+            w_ptr -= 32;
           }
-          if (r < 0) {  // lo > 0 here (element 0 of the axis always starts a run)
-            slow = true;
-            break;
+        } else {
+          int r = i - 1;
+          while (dq2 < best) {
+            if (chk) {
+              if (gofs + lo + r >= 0 || border) best = min(best, dq2);
+              break;
+            }
+            if (r < 0) {  // lo > 0 here (element 0 of the axis always starts a run)
+              slow = true;
+              break;
+            }
+            const uint32_t w = tile[r * 32 + lane];
+            best = min(best, (w & kMask) + dq2);
+            chk = w & chbit;
+            dq2 += inc;
+            inc += 2;
+            --r;
           }
-          const uint32_t w = tile[r * 32 + lane];
-          best = min(best, (w & kMask) + dq2);
-          chk = w & chbit;
-          dq2 += inc;
-          inc += 2;
-          --r;
         }
       }
       if (slow) best = scan_global(in, base, astride, p, L, lo, hi, tile, lane, v, chbit, border, gofs, Lg);
