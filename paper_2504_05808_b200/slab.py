@@ -136,6 +136,11 @@ def sphericity_roundness_slab(labels_slab: torch.Tensor, slabs, max_label: int, 
     if nz != z1 - z0:
         raise ValueError("labels_slab does not match slabs[rank]")
     info = {}
+    # one collective before the first point-to-point batch: every rank joins the communicator
+    chk = torch.tensor([nz], dtype=torch.int64, device=labels_slab.device)
+    dist.all_reduce(chk, op=dist.ReduceOp.SUM, group=group)
+    if int(chk.item()) != Z:
+        raise ValueError("the ranks' slabs do not add up to the volume depth")
     # labels of the slice just below the slab (z-run flags of the first slice)
     lo_lab, _ = exchange_halo(labels_slab, slabs, rank, 1, Z, group)
     below = lo_lab[0] if lo_lab.shape[0] else None

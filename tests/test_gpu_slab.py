@@ -55,3 +55,23 @@ def test_halo_spans_several_slabs():
     lab[80:90, 10:60, 20:30] = 2
     info = _check(lab, 6)
     assert info["h"] > 16 and info["H"] > 16
+
+
+def test_c4_four_slabs_full_size():
+    """The slab phases at the bench's full size (1024^3, 20 000 grains, 4 slabs of 256)."""
+    lab, _ = synth.make_config(4)
+    info = _check(lab, 4)
+    assert info["h"] <= 256 and info["H"] <= 256
+
+
+def test_slab_phase_argument_errors():
+    lab = torch.zeros((32, 16, 16), dtype=torch.int32, device="cuda")
+    lab[4:20, 4:12, 4:12] = 1
+    packed, _ = fastrs.slab_edt_xy(lab, None, 1)
+    d, _ = fastrs.slab_edt_z(packed, 0, 32, 0, 32)
+    with pytest.raises(fastrs.FastrsError) as e:  # own range not tile aligned
+        fastrs.slab_reduce(lab[3:29].contiguous(), d, 3, 29, 32, 82, 1)
+    assert e.value.name == "EINVAL"
+    with pytest.raises(fastrs.FastrsError) as e:  # extended slab outside the grid
+        fastrs.slab_edt_z(packed, 0, 32, 8, 32)
+    assert e.value.name == "EINVAL"
