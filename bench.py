@@ -35,8 +35,9 @@ METRIC = "Gvoxels/s end-to-end (EDT+LT+sphericity+roundness); % of HBM roofline"
 UNIT = "Gvoxels/s"
 
 # algorithmic HBM bytes per grid element of each stage (DESIGN.md §6 "Algorithmic bytes"), 3D path
-STAGE_BYTES_PER_ELEM = {"edt_x": 8.0, "edt_y": 8.0, "edt_z": 8.0, "prune": 4.0, "gather": 0.0, "dilate": 4.0,
-                        "epilogue": 12.0, "metrics": 0.0}
+# K5b writes LT^2 as u16 (Dmax <= 65535) and K5e reads labels, D and that u16 plane
+STAGE_BYTES_PER_ELEM = {"edt_x": 8.0, "edt_y": 8.0, "edt_z": 8.0, "prune": 4.0, "gather": 0.0, "dilate": 2.0,
+                        "epilogue": 10.0, "metrics": 0.0}
 STAGE_BYTES_PER_KEPT = {"prune": 8.0, "gather": 8.0}  # centre entries written by K4 / read once by K5a
 STAGE_BYTES_PER_CAND = {"gather": 8.0, "dilate": 8.0}  # sorted per-group candidates: written by K5a, read by K5b
 # the kernel behind each stage (names in the ncu summaries under profiles/)
