@@ -83,7 +83,9 @@ __device__ __forceinline__ int isqrt16(int h) {
 }
 
 __device__ __forceinline__ uint32_t range_mask(int l, int r) {  // bits l..r (0 <= l <= r <= 31)
-  return (r == 31 ? 0xFFFFFFFFu : ((1u << (r + 1)) - 1u)) & (0xFFFFFFFFu << l);
+  uint32_t m;
+  asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(m) : "r"(l), "r"(r - l + 1));  // r-l+1 bits from bit l
+  return m;
 }
 
 // Gather the candidates reaching the group box with bucket in [blo, bhi] into S.list.
@@ -773,12 +775,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
         const int ns = __popc(act);
         for (int j = 0; j < ns; ++j) {
           const int4 bp = sball[j];
-          const unsigned long long jc = scand[j];
+          const uint2 jc2 = reinterpret_cast<const uint2*>(scand)[j];  // candidate rows 0-31 | 32-63
           const int jR2 = bp.w - 1;
           const uint16_t dv = (uint16_t)bp.w;
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {
-            if (!((jc >> (32 * hf + lane)) & 1ull)) continue;
+            if (!(((hf ? jc2.y : jc2.x) >> lane) & 1u)) continue;
             const int dy = (hf ? ly1 : ly0) - bp.y, dz = (hf ? lz1 : lz0) - bp.z;
             const int hrem = jR2 - dy * dy - dz * dz;
             if (hrem < 0) continue;
