@@ -815,13 +815,22 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
 
   // ---- my tile's LT^2 -> the LT plane (coalesced rows); shell and reductions run in the
   // streaming epilogue kernel (lt.cu), at full occupancy
+  // the LT plane holds u16 values whenever Dmax <= 65535 (always the case here)
   const int64_t gx = rox + mox + lane;
-  for (int row = 0; row < kRows; ++row) {
-    const int ly = row % TY, lz = row / TY;
-    const int64_t gz = roz + moz + lz, gy = roy + moy + ly;
-    // the LT plane holds u16 values whenever Dmax <= 65535 (always the case here)
-    if (gz < g.Z && gy < g.Y && gx < g.X)
-      reinterpret_cast<uint16_t*>(ltp)[item + (gz * g.Y + gy) * g.X + gx] = val[row * 32 + lane];
+  const int64_t gy0 = roy + moy, gz0 = roz + moz;
+  const bool full = gz0 + TZ <= g.Z && gy0 + TY <= g.Y && gx < g.X;  // interior tile: no bounds tests
+  uint16_t* lt16 = reinterpret_cast<uint16_t*>(ltp) + item + (gz0 * g.Y + gy0) * g.X + gx;
+  if (full) {
+#pragma unroll 8
+    for (int row = 0; row < kRows; ++row) {
+      const int ly = row % TY, lz = row / TY;
+      lt16[((int64_t)lz * g.Y + ly) * g.X] = val[row * 32 + lane];
+    }
+  } else {
+    for (int row = 0; row < kRows; ++row) {
+      const int ly = row % TY, lz = row / TY;
+      if (gz0 + lz < g.Z && gy0 + ly < g.Y && gx < g.X) lt16[((int64_t)lz * g.Y + ly) * g.X] = val[row * 32 + lane];
+    }
   }
   n_rows = __reduce_add_sync(kFull, n_rows);
   if (lane == 0 && n_rows) atomicAdd(&hdr->n_intervals, (unsigned long long)n_rows);
