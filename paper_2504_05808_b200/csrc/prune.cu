@@ -14,6 +14,8 @@
 // K4 is row-vectorised: one warp per tile row, lane = x, every lane tests the same offset
 // (warp-uniform, shared-memory reads conflict-free); survivors are compacted per home tile
 // in element order with the tile's count / max D / #foreground (TileMeta).
+#include <cuda.h>
+
 #include <mutex>
 
 #include "common.cuh"
@@ -125,13 +127,15 @@ struct PruneTile {
 };
 
 
-template <bool IS3D>
+template <bool IS3D, bool TMA>
 __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, Geom g, TileMeta* __restrict__ meta,
                                                uint2* __restrict__ cent, uint32_t* __restrict__ fgm,
                                                uint16_t* __restrict__ oct, const uint32_t* __restrict__ M,
-                                               int64_t tile0, WsHeader* __restrict__ hdr) {
+                                               int64_t tile0, WsHeader* __restrict__ hdr,
+                                               const __grid_constant__ CUtensorMap tmap) {
   using P = PruneTile<IS3D>;
-  __shared__ __align__(16) uint32_t s[P::PZ * P::PY * P::PX];
+  __shared__ __align__(128) uint32_t s[P::PZ * P::PY * P::PX];
+  __shared__ __align__(8) uint64_t s_bar;
   __shared__ uint32_t keepmask[kRows];
   __shared__ uint32_t pre[kRows];
   __shared__ uint32_t red_cnt[8], red_max[8];
@@ -152,7 +156,36 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
   // halo staging with cp.async (zero-fill outside the grid), one warp per (z, y) row of the
   // padded tile.  Rows are 40 words starting at a multiple of 4, so when X % 4 == 0 every
   // 16-byte chunk lies entirely inside or outside the grid: 10 chunk copies per row.
-  {
+  if constexpr (TMA) {
+    // one tensor-memory-accelerator copy of the whole padded box; elements outside the grid
+    // arrive as zeros (the tensor map's out-of-bounds fill), same as the cp.async path
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                   "r"((unsigned)sizeof(s))
+                   : "memory");
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(s);
+      if constexpr (IS3D)
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+            "%4, %5}], [%6];\n" ::"r"(dst),
+            "l"(&tmap), "r"((int)x0), "r"((int)y0), "r"((int)z0), "r"((int)b), "r"(bar)
+            : "memory");
+      else
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+            "%4}], [%5];\n" ::"r"(dst),
+            "l"(&tmap), "r"((int)x0), "r"((int)y0), "r"((int)b), "r"(bar)
+            : "memory");
+    }
+    __syncthreads();  // the barrier is initialised before anyone polls it
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            bar)
+        : "memory");
+  } else {
     const int Zi = (int)g.Z, Yi = (int)g.Y, Xi = (int)g.X;
     constexpr int kRowsPZ = P::PZ * P::PY;
     if ((Xi & 3) == 0) {
@@ -433,6 +466,50 @@ void release_mtables() {
   }
 }
 
+// Tiled tensor map over D ([B][Z][Y][X] u32, x fastest) whose box is the padded K4 tile; false
+// (-> cp.async staging) when the driver entry point is missing or the layout does not meet the
+// copy engine's rules (16-byte aligned base and row pitch, coordinates and extents in int32).
+static bool prune_tensor_map(CUtensorMap* m, const uint32_t* D, const Geom& g) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<Encode>(fn);
+  }();
+  memset(m, 0, sizeof(*m));
+  if (!encode || (g.X & 3) != 0 || (reinterpret_cast<uintptr_t>(D) & 15) != 0) return false;
+  if (g.X > INT32_MAX / 2 || g.Y > INT32_MAX / 2 || g.Z > INT32_MAX / 2 || g.B > INT32_MAX) return false;
+  const bool is3 = g.ndim == 3;
+  const cuuint32_t rank = is3 ? 4 : 3;
+  cuuint64_t dims[4], strides[3];
+  cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
+  dims[0] = (cuuint64_t)g.X;
+  dims[1] = (cuuint64_t)g.Y;
+  strides[0] = (cuuint64_t)g.X * 4;
+  if (is3) {
+    dims[2] = (cuuint64_t)g.Z;
+    dims[3] = (cuuint64_t)g.B;
+    strides[1] = strides[0] * (cuuint64_t)g.Y;
+    strides[2] = strides[1] * (cuuint64_t)g.Z;
+    box[0] = PruneTile<true>::PX, box[1] = PruneTile<true>::PY, box[2] = PruneTile<true>::PZ, box[3] = 1;
+  } else {
+    dims[2] = (cuuint64_t)g.B;
+    strides[1] = strides[0] * (cuuint64_t)g.Y;
+    box[0] = PruneTile<false>::PX, box[1] = PruneTile<false>::PY, box[2] = 1;
+  }
+  for (cuuint32_t i = 0; i + 1 < rank; ++i)
+    if (strides[i] >= (1ull << 40)) return false;
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, rank, const_cast<uint32_t*>(D), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, uint32_t* fgm, uint16_t* oct,
                   WsHeader* hdr, cudaStream_t st, int64_t tz_lo, int64_t tz_hi) {
   int dev = 0;
@@ -442,10 +519,19 @@ void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centr
   const int64_t tile0 = part ? tz_lo * g.nty * g.ntx : 0;
   const int64_t n = part ? (tz_hi - tz_lo) * g.nty * g.ntx : g.ntiles;
   if (n <= 0) return;
-  if (g.ndim == 3)
-    k_prune<true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m3, tile0, hdr);
-  else
-    k_prune<false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m2, tile0, hdr);
+  CUtensorMap tmap;
+  const bool tma = prune_tensor_map(&tmap, D, g);
+  if (g.ndim == 3) {
+    if (tma)
+      k_prune<true, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m3, tile0, hdr, tmap);
+    else
+      k_prune<true, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m3, tile0, hdr, tmap);
+  } else {
+    if (tma)
+      k_prune<false, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m2, tile0, hdr, tmap);
+    else
+      k_prune<false, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m2, tile0, hdr, tmap);
+  }
 }
 
 }  // namespace fastrs
