@@ -693,8 +693,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
     // then painted one by one with the lanes over the tile's rows (lane = row, row + 32).
     // Because the order is exactly descending, the first ball that covers a cell carries its
     // final value: each cell is written once and coverage is updated immediately.
+    // the next batch's entries are loaded one iteration ahead (their latency overlaps the
+    // current batch's screening and painting)
+    unsigned long long e_next = lane < total ? list[lane] : 0ull;
     for (uint32_t i0 = 0; i0 < total && nu != 0; i0 += 32) {
       const uint32_t i = i0 + lane;
+      const unsigned long long e_cur = e_next;
+      if (i0 + 32 < total) e_next = i + 32 < total ? list[i + 32] : 0ull;
       if (!pmode && nu <= point_at) {
         // switch to point mode: list the still-uncovered cells
         const uint32_t left[2] = {f0 & ~c0, f1 & ~c1};
@@ -726,7 +731,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
         // the D of the first (largest) ball containing it.
         int cx = 0, cy = 0, cz = 0, D = 0;
         if (i < total) {
-          const unsigned long long e = list[i];
+          const unsigned long long e = e_cur;
           D = (int)(e & 0xFFFFu);
           cx = (int)((e >> 16) & 0xFFFFu) - kOff - mox;
           cy = (int)((e >> 32) & 0xFFFFu) - kOff - moy;
@@ -745,7 +750,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
       unsigned long long cand = 0;
       int cx = 0, cy = 0, cz = 0, D = 0;
       if (i < total) {
-        const unsigned long long e = list[i];
+        const unsigned long long e = e_cur;
         D = (int)(e & 0xFFFFu);
         cx = (int)((e >> 16) & 0xFFFFu) - kOff - mox;
         cy = (int)((e >> 32) & 0xFFFFu) - kOff - moy;
