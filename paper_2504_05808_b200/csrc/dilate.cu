@@ -54,11 +54,15 @@ struct Smem {  // K5a (gather + sort)
   int bb[6];                         // bounding box of the group's foreground (group coordinates)
 };
 
+// K5b CTAs hold kPaintWarps of a group's kWarps tiles (one warp each).  The warps share
+// nothing, so one warp per CTA lets every tile retire on its own: no warp slot idles while a
+// sibling tile of the same CTA is still painting.
+constexpr int kPaintWarps = 1;
 struct PaintSmem {  // K5b (one tile per warp)
-  uint16_t val[kWarps][kRows * 32];   // LT^2 per element of each warp's tile (D <= 65535 here)
-  int4 sball[kWarps][32];             // survivors of a screened batch: centre (tile coords), D
-  unsigned long long scand[kWarps][32];  // their candidate rows
-  uint16_t ulist[kWarps][kPoint];     // point mode: the still-uncovered cells (row*32 + x)
+  uint16_t val[kPaintWarps][kRows * 32];   // LT^2 per element of each warp's tile (D <= 65535 here)
+  int4 sball[kPaintWarps][32];             // survivors of a screened batch: centre (tile coords), D
+  unsigned long long scand[kPaintWarps][32];  // their candidate rows
+  uint16_t ulist[kPaintWarps][kPoint];     // point mode: the still-uncovered cells (row*32 + x)
 };
 
 template <bool IS3D>
@@ -564,7 +568,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_dilate_gather(const uint32_t
 }
 
 template <bool IS3D>
-__global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __restrict__ fgm,
+__global__ void __launch_bounds__(kPaintWarps * 32) k_dilate_paint(const uint32_t* __restrict__ fgm,
                                                               const TileMeta* __restrict__ meta, Geom g,
                                                               const unsigned long long* __restrict__ pool,
                                                               const uint32_t* __restrict__ gcount,
@@ -574,14 +578,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
   constexpr int TY = P::TY, TZ = P::TZ;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PaintSmem& S = *reinterpret_cast<PaintSmem*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kSplit = kWarps / kPaintWarps;  // CTAs per group
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int warp = (int)(blockIdx.x % kSplit) * kPaintWarps + wl;  // my tile within the group
+  const int64_t group = blockIdx.x / kSplit;
   if (hdr->dmax > kU16Max) return;  // k_dilate_atomic handles it
 
   // ---- group / tile coordinates --------------------------------------------------------
   // groups tile the layers [tz_lo, tz_hi) (all layers except on the slab path)
   const int64_t ngx = (g.ntx + P::GX - 1) / P::GX, ngy = (g.nty + P::GY - 1) / P::GY;
   const int64_t ngz = (g.tz_hi - g.tz_lo + P::GZ - 1) / P::GZ;
-  int64_t t = blockIdx.x;
+  int64_t t = group;
   const int64_t gxi = t % ngx;
   t /= ngx;
   const int64_t gyi = t % ngy;
@@ -596,14 +603,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
   const int64_t mtile = have_tile ? ((b * g.ntz + mtz) * g.nty + mty) * g.ntx + mtx : 0;
   const int mox = wx * kTX, moy = wy * TY, moz = wz * TZ;  // my tile origin within the group
   const bool active = have_tile && meta[mtile].nfg != 0;
-  const int64_t group = blockIdx.x;
   const uint32_t total = gcount[group];
   if (!active || total == kGroupFallback) return;  // background, or left to k_dilate_atomic
   const unsigned long long* list = pool + goff[group];
   const int64_t item = b * g.Z * g.Y * g.X;
 
   // ---- per-warp init: values, foreground masks, coverage ----------------------------------
-  uint16_t* val = S.val[warp];
+  uint16_t* val = S.val[wl];
   {
     uint4* v4 = reinterpret_cast<uint4*>(val);
 #pragma unroll 4
@@ -623,10 +629,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_dilate_paint(const uint32_t* __
   __syncwarp();
   // uncovered foreground cells of my tile (warp-uniform); point mode once it is small
   int nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(f0) + __popc(f1)));
-  int4* sball = S.sball[warp];                 // survivors of a screened batch (cx, cy, cz, D)
-  unsigned long long* scand = S.scand[warp];   // their candidate rows
+  int4* sball = S.sball[wl];                 // survivors of a screened batch (cx, cy, cz, D)
+  unsigned long long* scand = S.scand[wl];   // their candidate rows
   bool pmode = false;
-  uint16_t* ulist = S.ulist[warp];
+  uint16_t* ulist = S.ulist[wl];
   int ub[6] = {0, kTX - 1, 0, TY - 1, 0, TZ - 1};  // bounding box of the uncovered cells (point mode)
   auto ubox_refresh = [&]() {
     int x0 = 1 << 20, x1 = -1, y0 = 1 << 20, y1 = -1, z0 = 1 << 20, z1 = -1;
@@ -884,10 +890,10 @@ void launch_dilate_paint(const uint32_t* fgm, const TileMeta* meta, const unsign
   const int64_t ngroups = launched_groups(g);
   if (ngroups <= 0) return;
   if (g.ndim == 3)
-    k_dilate_paint<true><<<(unsigned)ngroups, kWarps * 32, sizeof(PaintSmem), st>>>(fgm, meta, g, pool, gcount, goff,
+    k_dilate_paint<true><<<(unsigned)(ngroups * (kWarps / kPaintWarps)), kPaintWarps * 32, sizeof(PaintSmem), st>>>(fgm, meta, g, pool, gcount, goff,
                                                                                      point_at_knob(), ltp, hdr);
   else
-    k_dilate_paint<false><<<(unsigned)ngroups, kWarps * 32, sizeof(PaintSmem), st>>>(fgm, meta, g, pool, gcount, goff,
+    k_dilate_paint<false><<<(unsigned)(ngroups * (kWarps / kPaintWarps)), kPaintWarps * 32, sizeof(PaintSmem), st>>>(fgm, meta, g, pool, gcount, goff,
                                                                                       point_at_knob(), ltp, hdr);
 }
 
