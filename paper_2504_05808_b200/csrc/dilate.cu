@@ -54,15 +54,15 @@ struct Smem {  // K5a (gather + sort)
   int bb[6];                         // bounding box of the group's foreground (group coordinates)
 };
 
-// K5b CTAs hold kPaintWarps of a group's kWarps tiles (one warp each).  The warps share
+// K5b CTAs hold NW of a group's kWarps tiles (one warp each).  The warps share
 // nothing, so one warp per CTA lets every tile retire on its own: no warp slot idles while a
 // sibling tile of the same CTA is still painting.
-constexpr int kPaintWarps = 1;
+template <int NW>
 struct PaintSmem {  // K5b (one tile per warp)
-  uint16_t val[kPaintWarps][kRows * 32];   // LT^2 per element of each warp's tile (D <= 65535 here)
-  int4 sball[kPaintWarps][32];             // survivors of a screened batch: centre (tile coords), D
-  unsigned long long scand[kPaintWarps][32];  // their candidate rows
-  uint16_t ulist[kPaintWarps][kPoint];     // point mode: the still-uncovered cells (row*32 + x)
+  uint16_t val[NW][kRows * 32];   // LT^2 per element of each warp's tile (D <= 65535 here)
+  int4 sball[NW][32];             // survivors of a screened batch: centre (tile coords), D
+  unsigned long long scand[NW][32];  // their candidate rows
+  uint16_t ulist[NW][kPoint];     // point mode: the still-uncovered cells (row*32 + x)
 };
 
 template <bool IS3D>
@@ -567,8 +567,8 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_dilate_gather(const uint32_t
   }
 }
 
-template <bool IS3D>
-__global__ void __launch_bounds__(kPaintWarps * 32) k_dilate_paint(const uint32_t* __restrict__ fgm,
+template <bool IS3D, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* __restrict__ fgm,
                                                               const TileMeta* __restrict__ meta, Geom g,
                                                               const unsigned long long* __restrict__ pool,
                                                               const uint32_t* __restrict__ gcount,
@@ -577,10 +577,10 @@ __global__ void __launch_bounds__(kPaintWarps * 32) k_dilate_paint(const uint32_
   using P = Shape<IS3D>;
   constexpr int TY = P::TY, TZ = P::TZ;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  PaintSmem& S = *reinterpret_cast<PaintSmem*>(smem_raw);
-  constexpr int kSplit = kWarps / kPaintWarps;  // CTAs per group
+  PaintSmem<NW>& S = *reinterpret_cast<PaintSmem<NW>*>(smem_raw);
+  constexpr int kSplit = kWarps / NW;  // CTAs per group
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int warp = (int)(blockIdx.x % kSplit) * kPaintWarps + wl;  // my tile within the group
+  const int warp = (int)(blockIdx.x % kSplit) * NW + wl;  // my tile within the group
   const int64_t group = blockIdx.x / kSplit;
   if (hdr->dmax > kU16Max) return;  // k_dilate_atomic handles it
 
@@ -884,17 +884,29 @@ void launch_dilate_gather(const uint32_t* fgm, TileMeta* meta, const uint2* cent
                                                                                   goff, hdr);
 }
 
+namespace {
+// K5b launch shape: one warp (tile) per CTA, registers capped for 32 resident CTAs per SM (the
+// CTA limit).  Measured on C4: 2 warps per CTA at 48 / 40 registers (42 / 51 resident warps),
+// 4 warps at 48, or no register cap were all slower (13.9-16.4 ms vs 13.7).
+template <bool IS3D>
+void paint_variant(int64_t ngroups, const uint32_t* fgm, const TileMeta* meta, const Geom& g,
+                   const unsigned long long* pool, const uint32_t* gcount, const uint32_t* goff, uint32_t* ltp,
+                   WsHeader* hdr, cudaStream_t st) {
+  constexpr int NW = 1;
+  k_dilate_paint<IS3D, NW, 32><<<(unsigned)(ngroups * (kWarps / NW)), NW * 32, sizeof(PaintSmem<NW>), st>>>(
+      fgm, meta, g, pool, gcount, goff, point_at_knob(), ltp, hdr);
+}
+}  // namespace
+
 void launch_dilate_paint(const uint32_t* fgm, const TileMeta* meta, const unsigned long long* pool,
                          const uint32_t* gcount, const uint32_t* goff, const Geom& g, uint32_t* ltp, WsHeader* hdr,
                          cudaStream_t st) {
   const int64_t ngroups = launched_groups(g);
   if (ngroups <= 0) return;
   if (g.ndim == 3)
-    k_dilate_paint<true><<<(unsigned)(ngroups * (kWarps / kPaintWarps)), kPaintWarps * 32, sizeof(PaintSmem), st>>>(fgm, meta, g, pool, gcount, goff,
-                                                                                     point_at_knob(), ltp, hdr);
+    paint_variant<true>(ngroups, fgm, meta, g, pool, gcount, goff, ltp, hdr, st);
   else
-    k_dilate_paint<false><<<(unsigned)(ngroups * (kWarps / kPaintWarps)), kPaintWarps * 32, sizeof(PaintSmem), st>>>(fgm, meta, g, pool, gcount, goff,
-                                                                                      point_at_knob(), ltp, hdr);
+    paint_variant<false>(ngroups, fgm, meta, g, pool, gcount, goff, ltp, hdr, st);
 }
 
 cudaError_t dilate_cover_setup() {
