@@ -217,17 +217,30 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
     }
     __syncthreads();
     const uint32_t total = pre[nrec];
-    for (uint32_t e0 = warp * 32; e0 < total; e0 += kWarps * 32) {
+    // every warp walks a contiguous quarter of the entries in batches of 32.  Records hold >= 1
+    // entry, so at most 32 record starts fall in (e0, e0 + 32]: one load of the next 32 prefix
+    // sums places every lane's entry in its record (no per-entry search)
+    const uint32_t chunk = (total + kWarps * 32 - 1) / (kWarps * 32) * 32;
+    const uint32_t wbeg = min(total, (uint32_t)warp * chunk), wend = min(total, wbeg + chunk);
+    int cur = 0;  // record holding entry e0 (warp-uniform): pre[cur] <= e0 < pre[cur + 1]
+    if (wbeg < wend) {
+      int hi = nrec;
+      while (hi - cur > 1) {
+        const int mid = (cur + hi) >> 1;
+        if (pre[mid] <= wbeg) cur = mid; else hi = mid;
+      }
+    }
+    for (uint32_t e0 = wbeg; e0 < wend; e0 += 32) {
       const uint32_t e = e0 + lane;
+      const int j = cur + 1 + lane;
+      const uint32_t off = (j <= nrec ? pre[j] : 0xFFFFFFFFu) - e0;  // record j starts at e0 + off
+      const uint32_t starts = __reduce_or_sync(kFull, off - 1u < 31u ? 1u << off : 0u);
+      const int lo = cur + __popc(starts & ((2u << lane) - 1u));
+      cur += __popc(__ballot_sync(kFull, off - 1u < 32u));
       bool take = false;
       int bk = -1;
       unsigned long long pe = 0;
-      if (e < total) {
-        int lo = 0, hi = nrec;  // pre[lo] <= e < pre[hi]
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (pre[mid] <= e) lo = mid; else hi = mid;
-        }
+      if (e < wend) {
         const uint32_t ht = rec[3 * lo];
         const uint32_t k = (rec[3 * lo + 1] & 0xFFFFu) + (e - pre[lo]);
         const uint32_t o = rec[3 * lo + 2];
