@@ -206,11 +206,13 @@ __global__ void __launch_bounds__(256) k_dilate_atomic(const TileMeta* __restric
 // 4 chunks of 32 elements in flight.
 // ---------------------------------------------------------------------------------------
 // fxlut[c] = round(sqrt(c) * 2^s) for c < kFxLut: the fixed-point LT terms of the sums
-__global__ void k_fxlut(unsigned long long* __restrict__ fxlut, int64_t nscale, const WsHeader* __restrict__ hdr) {
+// (and the scale exponent s in the header, for the epilogue's terms beyond the table)
+__global__ void k_fxlut(unsigned long long* __restrict__ fxlut, int64_t nscale, WsHeader* __restrict__ hdr) {
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= kFxLut) return;
-  const double scale = ldexp(1.0, sum_scale_log2(nscale, hdr->dmax));
-  fxlut[c] = (unsigned long long)__double2ull_rn(sqrt((double)c) * scale);
+  const int s = sum_scale_log2(nscale, hdr->dmax);
+  fxlut[c] = (unsigned long long)__double2ull_rn(sqrt((double)c) * ldexp(1.0, s));
+  if (c == 0) hdr->scale_log2 = s;
 }
 
 __global__ void __launch_bounds__(256) k_epilogue(const int32_t* __restrict__ lab, const uint32_t* __restrict__ Dg,
@@ -223,7 +225,8 @@ __global__ void __launch_bounds__(256) k_epilogue(const int32_t* __restrict__ la
   if (row >= g.B * nz * g.Y) return;
   const int64_t y = row % g.Y, zb = row / g.Y, z = z_lo + zb % nz, b = zb / nz;
   const int64_t base = ((b * g.Z + z) * g.Y + y) * g.X;
-  const double scale = ldexp(1.0, sum_scale_log2(g.nscale, hdr->dmax));
+  // the sums' fixed-point scale: k_fxlut ran before this kernel whenever do_reduce is set
+  const double scale = do_reduce ? ldexp(1.0, hdr->scale_log2) : 1.0;
   const bool wide = hdr->dmax > kU16Max;  // LT plane element type: u32 if wide, else u16
   const uint16_t* ltp16 = reinterpret_cast<const uint16_t*>(ltp);
   const int X = (int)g.X;
