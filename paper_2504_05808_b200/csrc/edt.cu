@@ -25,6 +25,7 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
+template <int U>
 __global__ void __launch_bounds__(256) k_edt_x(const int32_t* __restrict__ lab,
                                                const int32_t* __restrict__ below, uint32_t* __restrict__ out,
                                                int64_t nrows, int X, int64_t Y, int64_t Z,
@@ -48,7 +49,7 @@ __global__ void __launch_bounds__(256) k_edt_x(const int32_t* __restrict__ lab,
   // sweep 1 (right to left): end of the run containing x
   int carry_end = X - 1;
   int32_t right_next = 0;
-#pragma unroll 4
+#pragma unroll U
   for (int c = nchunk - 1; c >= 0; --c) {
     const int x = (c << 5) + lane;
     const int32_t v = x < X ? __ldg(L + x) : 0;
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(256) k_edt_x(const int32_t* __restrict__ lab,
   int carry_start = 0;
   int32_t left_prev = 0;
   uint32_t bad = 0;
-#pragma unroll 4
+#pragma unroll U
   for (int c = 0; c < nchunk; ++c) {
     const int x = (c << 5) + lane;
     const int32_t v = x < X ? __ldg(L + x) : 0;
@@ -293,8 +294,9 @@ void launch_edt_x(const int32_t* labels, const int32_t* labels_below, uint32_t* 
   warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
   const size_t smem = (size_t)warps * g.X * sizeof(uint16_t);
   const int64_t blocks = (nrows + warps - 1) / warps;
-  k_edt_x<<<(unsigned)blocks, warps * 32, smem, st>>>(labels, labels_below, out, nrows, (int)g.X, g.Y, g.Z, max_label,
-                                                      border ? 1 : 0, g.ndim == 3 ? 1 : 0, hdr);
+  // sweep unroll 2: measured on C4 4.13 ms vs 4.46 (4), 4.35 (8), 4.26 (16)
+  k_edt_x<2><<<(unsigned)blocks, warps * 32, smem, st>>>(labels, labels_below, out, nrows, (int)g.X, g.Y, g.Z, max_label,
+                                                         border ? 1 : 0, g.ndim == 3 ? 1 : 0, hdr);
 }
 
 // axis 1 = y, axis 2 = z.
