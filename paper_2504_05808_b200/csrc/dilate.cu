@@ -42,7 +42,10 @@ struct Smem;
 static_assert(3 * 512 <= 1536 && 2 * (512 + 8) + 512 <= 2048, "gather scratch fits S.hist / S.idx");
 
 struct Smem {  // K5a (gather + sort)
-  unsigned long long list[kCap];     // gathered candidates (centre relative to the group), gather order
+  union {
+    unsigned long long list[kCap];   // gathered candidates (centre relative to the group), gather order
+    uint32_t list32[2 * kCap];       // the same, compact (3D single-pass path, see pack32)
+  };
   uint32_t hist[kHist];              // exact-D counting sort: bin Dhi - D (rounds path; gather scratch)
   uint16_t idx[kCap];                // indices into list, sorted by D (descending)
   uint32_t dh[kHist];                // exact-D histogram / cursors of the single-pass path
@@ -75,6 +78,17 @@ struct Shape {
 __device__ __forceinline__ unsigned long long pack(int x, int y, int z, uint32_t D) {
   return (unsigned long long)D | ((unsigned long long)(uint16_t)(x + kOff) << 16) |
          ((unsigned long long)(uint16_t)(y + kOff) << 32) | ((unsigned long long)(uint16_t)(z + kOff) << 48);
+}
+// Compact 32-bit candidate of the 3D single-pass gather (Dmax <= kHist, so r <= 39): a centre
+// that reaches the group lies within r of its 32x16x16 box, i.e. x in [-39, 70], y, z in
+// [-39, 54]; biased by 40 they fit 7 bits each, D <= 1536 fits 11.  Twice the entries of the
+// shared list in the same bytes, so fewer groups overflow into the regather.
+constexpr int kB32 = 40;
+__device__ __forceinline__ uint32_t pack32(int x, int y, int z, uint32_t D) {
+  return (uint32_t)(x + kB32) | ((uint32_t)(y + kB32) << 7) | ((uint32_t)(z + kB32) << 14) | (D << 21);
+}
+__device__ __forceinline__ unsigned long long unpack32(uint32_t e) {
+  return pack((int)(e & 127u) - kB32, (int)((e >> 7) & 127u) - kB32, (int)((e >> 14) & 127u) - kB32, e >> 21);
 }
 
 __device__ __forceinline__ int gap(int lo, int hi, int c) { return c < lo ? lo - c : (c > hi ? c - hi : 0); }
@@ -141,7 +155,7 @@ enum { kListBucketHist = 0,  // append to S.list (up to kCap) and count its D bu
        kListExactHist = 2,   // append to S.list and count its exact D in S.dh (bin dtop - D)
        kScatter = 3 };       // store it at out[S.dh[dtop - D]++] (S.dh holds the sorted cursors)
 
-template <bool IS3D, int MODE>
+template <bool IS3D, int MODE, bool COMPACT = false>
 __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ meta, const uint2* __restrict__ cent,
                                        const uint16_t* __restrict__ oct, const Geom& g, int64_t b, int64_t tx0,
                                        int64_t ty0, int64_t tz0, int nrx, int nry, int nrz, int blo, int bhi,
@@ -240,6 +254,7 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
       bool take = false;
       int bk = -1;
       unsigned long long pe = 0;
+      uint32_t pe32 = 0;
       if (e < wend) {
         const uint32_t ht = rec[3 * lo];
         const uint32_t k = (rec[3 * lo + 1] & 0xFFFFu) + (e - pre[lo]);
@@ -253,6 +268,7 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
         if (ddx * ddx + ddy * ddy + ddz * ddz <= (int)en.y - 1 && bk >= blo && bk <= bhi) {
           take = true;
           pe = pack(cx, cy, cz, en.y);
+          if (COMPACT) pe32 = pack32(cx, cy, cz, en.y);
         }
       }
       const uint32_t tm = __ballot_sync(kFull, take);
@@ -269,7 +285,11 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
           if (lane == 0) base = atomicAdd(&S.count, (uint32_t)__popc(tm));
           base = __shfl_sync(kFull, base, 0);
           const uint32_t pos = base + __popc(tm & ((1u << lane) - 1u));
-          if (take && pos < kCap) S.list[pos] = pe;
+          if (COMPACT) {
+            if (take && pos < 2 * kCap) S.list32[pos] = pe32;
+          } else {
+            if (take && pos < kCap) S.list[pos] = pe;
+          }
         }
       }
     }
@@ -399,8 +419,9 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_dilate_gather(const uint32_t
     for (int k = tid; k < (int)dtop; k += kWarps * 32) S.dh[k] = 0;
     if (tid == 0) S.count = 0;
     __syncthreads();
-    gather<IS3D, kListExactHist>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, 0, kBuckets - 1, dtop);
+    gather<IS3D, kListExactHist, IS3D>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, 0, kBuckets - 1, dtop);
     const uint32_t total = S.count;
+    constexpr uint32_t kListCap = IS3D ? 2 * kCap : kCap;  // 3D keeps compact entries
     if (tid == 0) {
       const unsigned long long b0 = atomicAdd(&hdr->pool_used, (unsigned long long)total);
       S.base = b0;
@@ -409,9 +430,9 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_dilate_gather(const uint32_t
     block_exclusive_scan(S.dh, (int)dtop, S.wsum);
     if (!S.fallback) {
       unsigned long long* out = pool + S.base;
-      if (total <= (uint32_t)kCap) {
+      if (total <= kListCap) {
         for (uint32_t i = tid; i < total; i += kWarps * 32) {
-          const unsigned long long pe = S.list[i];
+          const unsigned long long pe = IS3D ? unpack32(S.list32[i]) : S.list[i];
           out[atomicAdd(&S.dh[dtop - (uint32_t)(pe & 0xFFFFu)], 1u)] = pe;
         }
       } else {
