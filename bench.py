@@ -64,13 +64,29 @@ def parse():
     return p.parse_args()
 
 
+def _kernel_key(name: str):
+    """(base name, first template argument or None): 'k_prune<1, 1>' -> ('k_prune', '1')."""
+    base, _, args = name.partition("<")
+    return base.strip(), (args.split(",")[0].strip(" >") or None) if args else None
+
+
 def ncu_traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary, or None."""
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary, or None.
+    Names match on the base name and the first template argument (the 2D/3D instance), so a
+    kernel that gained template parameters still finds its summary line."""
     try:
-        k = json.load(open(NCU_SUMMARY))["kernels"].get(kernel)
-        return None if k is None else k["traffic_bytes_per_launch"]
+        kernels = json.load(open(NCU_SUMMARY))["kernels"]
     except Exception:
         return None
+    k = kernels.get(kernel)
+    if k is None:
+        want = _kernel_key(kernel)
+        for name, rec in kernels.items():
+            got = _kernel_key(name)
+            if got[0] == want[0] and (want[1] is None or got[1] == want[1]):
+                k = rec
+                break
+    return None if k is None else k["traffic_bytes_per_launch"]
 
 
 def workload_name(cfg: int) -> str:
