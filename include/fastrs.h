@@ -93,7 +93,7 @@ typedef struct {
   uint32_t dmax;          /* max squared distance over the grid                          */
   uint64_t n_fg;          /* foreground elements                                         */
   uint64_t n_kept;        /* maximal-ball centres kept by the lattice pruning (K4)       */
-  uint64_t n_intervals;   /* (ball, row) intervals emitted by the dilation (K5)          */
+  uint64_t n_intervals;   /* (ball, row) chords the dilation (K5) evaluated exactly       */
   int32_t sum_scale_log2; /* fixed-point scale of the LT sums (2^s)                      */
   uint32_t n_fallback;   /* tile groups handed to the atomic fallback dilation         */
   uint32_t n_rounds_extra; /* K5: candidate-list rounds beyond the first, summed over groups */

@@ -297,6 +297,12 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
   __syncthreads();
 }
 
+// [lo, hi] = x range of the set bits of a row mask; an empty mask gives a range no ball reaches
+__device__ __forceinline__ void uncovered_range(uint32_t u, int& lo, int& hi) {
+  lo = u ? __ffs(u) - 1 : 1 << 14;
+  hi = u ? 31 - __clz(u) : -(1 << 14);
+}
+
 // position of the n-th (0-based) set bit of m (requires popc(m) > n)
 __device__ __forceinline__ int nth_bit(uint32_t m, int n) {
   int pos = 0, c = __popc(m & 0xFFFFu);
@@ -652,6 +658,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* 
   // lane owns rows `lane` (0) and `lane + 32` (1): foreground and covered masks in registers
   const uint32_t f0 = active ? fgm[mtile * kRows + lane] : 0u, f1 = active ? fgm[mtile * kRows + lane + 32] : 0u;
   uint32_t c0 = 0, c1 = 0;
+  int ul0, uh0, ul1, uh1;  // x range of the uncovered foreground of rows lane / lane + 32
+  uncovered_range(f0, ul0, uh0);
+  uncovered_range(f1, ul1, uh1);
   const int ly0 = IS3D ? (lane & 7) : lane, lz0 = IS3D ? (lane >> 3) : 0;
   const int ly1 = IS3D ? ly0 : lane + 32, lz1 = IS3D ? lz0 + 4 : 0;
   // rows of my tile that still hold uncovered foreground, per 8-column chunk of x
@@ -829,13 +838,23 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* 
             const int dy = (hf ? ly1 : ly0) - bp.y, dz = (hf ? lz1 : lz0) - bp.z;
             const int hrem = jR2 - dy * dy - dz * dz;
             if (hrem < 0) continue;
+            // cheap reject: the row's uncovered cells all lie in [ul, uh]; the ball's chord
+            // reaches none of them when the nearest point of that range is outside it
+            const int ddx = max(max((hf ? ul1 : ul0) - bp.x, bp.x - (hf ? uh1 : uh0)), 0);
+            if (ddx * ddx > hrem) continue;
             const int w = isqrt16(hrem);
             const int l = max(bp.x - w, 0), rr = min(bp.x + w, kTX - 1);
             if (l > rr) continue;
             ++n_rows;
             uint32_t m = (hf ? (f1 & ~c1) : (f0 & ~c0)) & range_mask(l, rr);
             if (!m) continue;
-            if (hf) c1 |= m; else c0 |= m;
+            if (hf) {
+              c1 |= m;
+              uncovered_range(f1 & ~c1, ul1, uh1);
+            } else {
+              c0 |= m;
+              uncovered_range(f0 & ~c0, ul0, uh0);
+            }
             uint16_t* vr = val + (32 * hf + lane) * 32;
             do {
               const int c = __ffs(m) - 1;
