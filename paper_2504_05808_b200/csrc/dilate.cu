@@ -34,7 +34,7 @@ constexpr int kWarps = 4;  // warps per CTA = tiles per group
 constexpr int kCap = 2048;   // candidate list capacity per round
 constexpr int kBuckets = 128;
 constexpr int kHist = 1536;  // exact-D counting-sort bins per round
-constexpr int kPoint = 128;
+constexpr int kPoint = 96;  // C4 sweep: 128 -> 11.98 ms, 96 -> 11.75, 64 -> 11.92, 32 -> 12.59, 0 -> 15.38
 constexpr uint32_t kGroupFallback = 0xFFFFFFFFu;  // uncovered cells at which a warp switches to point tests
 constexpr int kOff = 16384;  // coordinate bias of packed candidates
 
