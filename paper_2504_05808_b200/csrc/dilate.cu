@@ -168,13 +168,20 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
   uint32_t* pre = reinterpret_cast<uint32_t*>(S.idx);      // kRecCap + 1 prefix sums
   int16_t* recz = reinterpret_cast<int16_t*>(S.idx) + 2 * (kRecCap + 8);  // home tile z offsets
   const int o_start = (bhi + 1 + 7) >> 3;                  // entries with bucket > bhi come first
+  // n -> (ix, iy, iz) without integer divides: umulhi(n, floor((2^32-1)/d) + 1) = n / d
+  // exactly whenever n * d < 2^32 (here n < 10^5, d < 100); d = 1 (the reciprocal would be
+  // 2^32) is taken apart
+  const uint32_t rx = 0xFFFFFFFFu / (uint32_t)nx + 1u, ry = 0xFFFFFFFFu / (uint32_t)ny + 1u;
+  const int bb0 = S.bb[0], bb1 = S.bb[1], bb2 = S.bb[2], bb3 = S.bb[3], bb4 = S.bb[4], bb5 = S.bb[5];
   for (int nb0 = 0; nb0 < nneigh; nb0 += kRecCap) {
     __syncthreads();
     if (tid == 0) S.nrec = 0;
     __syncthreads();
     const int nb1 = min(nneigh, nb0 + kRecCap);
     for (int n = nb0 + tid; n < nb1; n += kWarps * 32) {
-      const int ix = n % nx, iy = (n / nx) % ny, iz = n / (nx * ny);
+      const int q1 = nx == 1 ? n : (int)__umulhi((uint32_t)n, rx);
+      const int iz = ny == 1 ? q1 : (int)__umulhi((uint32_t)q1, ry);
+      const int ix = n - q1 * nx, iy = q1 - iz * ny;
       const int64_t hx = tx0 + ix - nrx, hy = ty0 + iy - nry, hz = tz0 + iz - nrz;
       if (hx < 0 || hx >= g.ntx || hy < 0 || hy >= g.nty || hz < 0 || hz >= g.ntz) continue;
       const int64_t ht = ((b * g.ntz + hz) * g.nty + hy) * g.ntx + hx;
@@ -182,9 +189,9 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
       if (!hm.count) continue;
       const int hox = (ix - nrx) * kTX, hoy = (iy - nry) * P::TY, hoz = (iz - nrz) * P::TZ;
       // gap between the home tile box and the bounding box of the group's foreground
-      const int gx = max(0, max(hox - S.bb[1], S.bb[0] - (hox + kTX - 1)));
-      const int gy = max(0, max(hoy - S.bb[3], S.bb[2] - (hoy + P::TY - 1)));
-      const int gz = max(0, max(hoz - S.bb[5], S.bb[4] - (hoz + P::TZ - 1)));
+      const int gx = max(0, max(hox - bb1, bb0 - (hox + kTX - 1)));
+      const int gy = max(0, max(hoy - bb3, bb2 - (hoy + P::TY - 1)));
+      const int gz = max(0, max(hoz - bb5, bb4 - (hoz + P::TZ - 1)));
       const int g2 = gx * gx + gy * gy + gz * gz;
       if (g2 > (int)hm.maxD - 1 || dbucket(hm.maxD) < blo) continue;
       // lowest bucket whose largest D can still reach the gap: D - 1 >= g2 <=> D >= g2 + 1
@@ -263,7 +270,7 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
         const int v = (int)en.x;
         const int cx = (int)(o & 0xFFFFu) - kOff + (v & 31), cy = (int)(o >> 16) - kOff + ((v >> 5) % P::TY),
                   cz = (int)recz[lo] + v / (32 * P::TY);
-        const int ddx = gap(S.bb[0], S.bb[1], cx), ddy = gap(S.bb[2], S.bb[3], cy), ddz = gap(S.bb[4], S.bb[5], cz);
+        const int ddx = gap(bb0, bb1, cx), ddy = gap(bb2, bb3, cy), ddz = gap(bb4, bb5, cz);
         bk = dbucket(en.y);
         if (ddx * ddx + ddy * ddy + ddz * ddz <= (int)en.y - 1 && bk >= blo && bk <= bhi) {
           take = true;
