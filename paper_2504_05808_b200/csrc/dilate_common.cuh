@@ -11,6 +11,9 @@ constexpr uint32_t kU16Max = 65535u;
 // Shell + per-label reductions + optional LT writes for one 32-wide row held in a warp
 // (lane = x), given each lane's LT^2 `c`, label L and squared distance d (L = 0 outside the
 // grid).  Returns 1 if the invariant LT^2 >= D failed.
+// FAST: reductions only, with the fixed-point table (no LT outputs): the per-element option
+// tests fold away.
+template <bool FAST = false>
 static __device__ __forceinline__ uint32_t row_epilogue_v(uint32_t c, int32_t L, uint32_t d, int lane, int64_t gi,
                                                    int64_t b, const Accum& acc, int do_reduce, double scale,
                                                    uint32_t* __restrict__ lt2_out, float* __restrict__ lt_out,
@@ -23,16 +26,16 @@ static __device__ __forceinline__ uint32_t row_epilogue_v(uint32_t c, int32_t L,
     shell = d == 1;
     // fixed-point sqrt(LT^2) * 2^s: from the per-call table when LT^2 < 65536 (bit-identical:
     // the table holds the same correctly rounded values)
-    if (fxlut && c < kFxLut) {
+    if ((FAST || fxlut) && c < kFxLut) {
       fx = __ldg(fxlut + c);
     } else {
       fx = (unsigned long long)__double2ull_rn(sqrt((double)c) * scale);
     }
-    if (lt2_out) lt2_out[gi] = c;
-    if (lt_out) lt_out[gi] = (float)sqrt((double)c);
+    if (!FAST && lt2_out) lt2_out[gi] = c;
+    if (!FAST && lt_out) lt_out[gi] = (float)sqrt((double)c);
   }
-  if (do_reduce) {
-    if (L < 0 || L > acc.max_label) L = 0;
+  if (FAST || do_reduce) {
+    if ((uint32_t)L > (uint32_t)acc.max_label) L = 0;  // also catches L < 0
     uint32_t act = __ballot_sync(kFull, L != 0);
     while (act) {
       const int leader = __ffs(act) - 1;
@@ -59,17 +62,6 @@ static __device__ __forceinline__ uint32_t row_epilogue_v(uint32_t c, int32_t L,
   }
   return bad;
 }
-
-// Same, loading the label and D of the row itself.
-static __device__ __forceinline__ uint32_t row_epilogue(uint32_t c, int lane, bool valid, int64_t gi, int64_t b,
-                                                 const int32_t* __restrict__ lab, const uint32_t* __restrict__ Dg,
-                                                 const Accum& acc, int do_reduce, double scale,
-                                                 uint32_t* __restrict__ lt2_out, float* __restrict__ lt_out) {
-  const int32_t L = valid ? __ldg(lab + gi) : 0;
-  const uint32_t d = (valid && L != 0) ? __ldg(Dg + gi) : 0u;
-  return row_epilogue_v(c, L, d, lane, gi, b, acc, do_reduce, scale, lt2_out, lt_out);
-}
-
 
 cudaError_t dilate_cover_setup();
 

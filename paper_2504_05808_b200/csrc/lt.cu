@@ -215,6 +215,7 @@ __global__ void k_fxlut(unsigned long long* __restrict__ fxlut, int64_t nscale, 
   if (c == 0) hdr->scale_log2 = s;
 }
 
+template <bool FAST>
 __global__ void __launch_bounds__(256) k_epilogue(const int32_t* __restrict__ lab, const uint32_t* __restrict__ Dg,
                                                   const uint32_t* __restrict__ ltp, Geom g, int64_t z_lo, int64_t nz,
                                                   Accum acc, int do_reduce, uint32_t* __restrict__ lt2_out,
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(256) k_epilogue(const int32_t* __restrict__ la
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (x0 + 32 * k >= X) break;  // warp-uniform
-      bad |= row_epilogue_v(c[k], L[k], d[k], lane, base + x0 + 32 * k + lane, b, acc, do_reduce, scale, lt2_out,
+      bad |= row_epilogue_v<FAST>(c[k], L[k], d[k], lane, base + x0 + 32 * k + lane, b, acc, do_reduce, scale, lt2_out,
                             lt_out, fxlut);
     }
   }
@@ -302,9 +303,14 @@ void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, co
   const int64_t z_lo = g.tz_lo * TZ, z_hi = g.tz_hi * TZ < g.Z ? g.tz_hi * TZ : g.Z;
   const int64_t rows = g.B * (z_hi - z_lo) * g.Y;
   if (acc) k_fxlut<<<kFxLut / 256, 256, 0, st>>>(fxlut, g.nscale, hdr);
-  if (rows > 0)
-    k_epilogue<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(labels, D, ltp, g, z_lo, z_hi - z_lo, a, acc ? 1 : 0,
-                                                          lt2_out, lt_out, acc ? fxlut : nullptr, hdr);
+  if (rows > 0) {
+    if (acc && !lt2_out && !lt_out)
+      k_epilogue<true><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(labels, D, ltp, g, z_lo, z_hi - z_lo, a, 1, nullptr,
+                                                                  nullptr, fxlut, hdr);
+    else
+      k_epilogue<false><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(labels, D, ltp, g, z_lo, z_hi - z_lo, a, acc ? 1 : 0,
+                                                                   lt2_out, lt_out, acc ? fxlut : nullptr, hdr);
+  }
 }
 
 }  // namespace fastrs
