@@ -189,17 +189,25 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
       {
         uint32_t dq2 = 1, inc = 3;
         const uint32_t* w_ptr = tile + (i + 1) * 32 + lane;
-        if (reach <= nt - 1 - i) {
+        if (reach + 1 <= nt - 1 - i) {
+          // two rows per iteration (one more row is staged than the scan can need): the second
+          // row's terms are exact candidates even when the first made dq^2 >= best
           while (dq2 < best) {
-            const uint32_t w = *w_ptr;
+            const uint32_t w = w_ptr[0], w2 = w_ptr[32];
             if (w & chbit) {
               best = min(best, dq2);
               break;
             }
             best = min(best, (w & kMask) + dq2);
-            dq2 += inc;
-            inc += 2;
-            w_ptr += 32;
+            const uint32_t dq2b = dq2 + inc;
+            if (w2 & chbit) {
+              best = min(best, dq2b);
+              break;
+            }
+            best = min(best, (w2 & kMask) + dq2b);
+            dq2 = dq2b + inc + 2;
+            inc += 4;
+            w_ptr += 64;
           }
         } else {
           const uint32_t* w_end = tile + nt * 32 + lane;
@@ -225,18 +233,24 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
       {
         uint32_t dq2 = 1, inc = 3, chk = v & chbit;
         const uint32_t* w_ptr = tile + (i - 1) * 32 + lane;
-        if (reach <= i) {
+        if (reach + 1 <= i) {
           while (dq2 < best) {
             if (chk) {  // the element at p-dq is inside the staged window: a real site
               best = min(best, dq2);
               break;
             }
-            const uint32_t w = *w_ptr;
+            const uint32_t w = w_ptr[0], w2 = w_ptr[-32];
             best = min(best, (w & kMask) + dq2);
-            chk = w & chbit;
-            dq2 += inc;
-            inc += 2;
-            w_ptr -= 32;
+            const uint32_t dq2b = dq2 + inc;
+            if (w & chbit) {
+              best = min(best, dq2b);
+              break;
+            }
+            best = min(best, (w2 & kMask) + dq2b);
+            chk = w2 & chbit;
+            dq2 = dq2b + inc + 2;
+            inc += 4;
+            w_ptr -= 64;
           }
         } else {
           int r = i - 1;
