@@ -103,6 +103,7 @@ constexpr int kColS = 256;  // positions per CTA
 constexpr int kColH = 48;   // staged halo on each side
 constexpr int kColRows = kColS + 2 * kColH;
 constexpr int kColWarps = 8;
+constexpr int kScanU = 4;  // rows per iteration of the hoisted scan loops
 
 // Slow path of the column scan for an element whose window leaves the staged rows: the same
 // exact scan, reading beyond the window from global memory (L2).
@@ -189,25 +190,27 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
       {
         uint32_t dq2 = 1, inc = 3;
         const uint32_t* w_ptr = tile + (i + 1) * 32 + lane;
-        if (reach + 1 <= nt - 1 - i) {
-          // two rows per iteration (one more row is staged than the scan can need): the second
-          // row's terms are exact candidates even when the first made dq^2 >= best
+        if (reach + kScanU - 1 <= nt - 1 - i) {
+          // kScanU rows per iteration (the staged rows suffice): a row's term is an exact
+          // candidate even when an earlier one made dq^2 >= best
           while (dq2 < best) {
-            const uint32_t w = w_ptr[0], w2 = w_ptr[32];
-            if (w & chbit) {
-              best = min(best, dq2);
-              break;
+            uint32_t w[kScanU];
+#pragma unroll
+            for (int u = 0; u < kScanU; ++u) w[u] = w_ptr[32 * u];
+            bool stop = false;
+#pragma unroll
+            for (int u = 0; u < kScanU; ++u) {
+              if (w[u] & chbit) {
+                best = min(best, dq2);
+                stop = true;
+                break;
+              }
+              best = min(best, (w[u] & kMask) + dq2);
+              dq2 += inc;
+              inc += 2;
             }
-            best = min(best, (w & kMask) + dq2);
-            const uint32_t dq2b = dq2 + inc;
-            if (w2 & chbit) {
-              best = min(best, dq2b);
-              break;
-            }
-            best = min(best, (w2 & kMask) + dq2b);
-            dq2 = dq2b + inc + 2;
-            inc += 4;
-            w_ptr += 64;
+            if (stop) break;
+            w_ptr += 32 * kScanU;
           }
         } else {
           const uint32_t* w_end = tile + nt * 32 + lane;
@@ -233,24 +236,30 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
       {
         uint32_t dq2 = 1, inc = 3, chk = v & chbit;
         const uint32_t* w_ptr = tile + (i - 1) * 32 + lane;
-        if (reach + 1 <= i) {
+        if (reach + kScanU - 1 <= i) {
           while (dq2 < best) {
             if (chk) {  // the element at p-dq is inside the staged window: a real site
               best = min(best, dq2);
               break;
             }
-            const uint32_t w = w_ptr[0], w2 = w_ptr[-32];
-            best = min(best, (w & kMask) + dq2);
-            const uint32_t dq2b = dq2 + inc;
-            if (w & chbit) {
-              best = min(best, dq2b);
-              break;
+            uint32_t w[kScanU];
+#pragma unroll
+            for (int u = 0; u < kScanU; ++u) w[u] = w_ptr[-32 * u];
+            bool stop = false;
+#pragma unroll
+            for (int u = 0; u < kScanU; ++u) {
+              best = min(best, (w[u] & kMask) + dq2);
+              dq2 += inc;
+              inc += 2;
+              chk = w[u] & chbit;
+              if (u + 1 < kScanU && chk) {  // p-dq (now) lies below the run start: a site
+                best = min(best, dq2);
+                stop = true;
+                break;
+              }
             }
-            best = min(best, (w2 & kMask) + dq2b);
-            chk = w2 & chbit;
-            dq2 = dq2b + inc + 2;
-            inc += 4;
-            w_ptr -= 64;
+            if (stop) break;
+            w_ptr -= 32 * kScanU;
           }
         } else {
           int r = i - 1;
