@@ -743,6 +743,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* 
   };
 
   uint32_t n_rows = 0;
+  bool dirty = false;  // my rows' coverage changed since the masks were last refreshed
   {
     // --- cover: my tile, balls in descending D.  Lanes first screen 32 balls at a time (reach
     // + rows with uncovered foreground inside the ball's x-extent); the surviving balls are
@@ -855,6 +856,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* 
             ++n_rows;
             uint32_t m = (hf ? (f1 & ~c1) : (f0 & ~c0)) & range_mask(l, rr);
             if (!m) continue;
+            dirty = true;
             if (hf) {
               c1 |= m;
               uncovered_range(f1 & ~c1, ul1, uh1);
@@ -872,13 +874,16 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* 
         }
         __syncwarp();
       }
-      // refresh the uncovered-row masks
-      const uint32_t left[2] = {f0 & ~c0, f1 & ~c1};
+      // refresh the uncovered-row masks (only when this batch covered something)
+      if (__any_sync(kFull, dirty)) {
+        dirty = false;
+        const uint32_t left[2] = {f0 & ~c0, f1 & ~c1};
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        Uc[c] = (unsigned long long)__ballot_sync(kFull, (left[0] >> (8 * c)) & 0xFFu) |
-                ((unsigned long long)__ballot_sync(kFull, (left[1] >> (8 * c)) & 0xFFu) << 32);
-      nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(left[0]) + __popc(left[1])));
+        for (int c = 0; c < 4; ++c)
+          Uc[c] = (unsigned long long)__ballot_sync(kFull, (left[0] >> (8 * c)) & 0xFFu) |
+                  ((unsigned long long)__ballot_sync(kFull, (left[1] >> (8 * c)) & 0xFFu) << 32);
+        nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(left[0]) + __popc(left[1])));
+      }
     }
     if (pmode && nq > 0 && nu > 0) point_flush();  // the queue's last balls
   }
