@@ -840,11 +840,22 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* 
           const uint2 jc2 = reinterpret_cast<const uint2*>(scand)[j];  // candidate rows 0-31 | 32-63
           const int jR2 = bp.w - 1;
           const uint16_t dv = (uint16_t)bp.w;
+          // 3D: rows lane and lane + 32 share ly, and lie 4 layers apart
+          const int dy0 = ly0 - bp.y, dz0 = lz0 - bp.z;
+          const int base0 = jR2 - dy0 * dy0;
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {
-            if (!(((hf ? jc2.y : jc2.x) >> lane) & 1u)) continue;
-            const int dy = (hf ? ly1 : ly0) - bp.y, dz = (hf ? lz1 : lz0) - bp.z;
-            const int hrem = jR2 - dy * dy - dz * dz;
+            const uint32_t hm = hf ? jc2.y : jc2.x;
+            if (hm == 0u) continue;  // the ball has no candidate row in this half (warp-uniform)
+            if (!((hm >> lane) & 1u)) continue;
+            int hrem;
+            if (IS3D) {
+              const int dz = hf ? dz0 + 4 : dz0;
+              hrem = base0 - dz * dz;
+            } else {
+              const int dy = (hf ? ly1 : ly0) - bp.y;
+              hrem = jR2 - dy * dy;
+            }
             if (hrem < 0) continue;
             // cheap reject: the row's uncovered cells all lie in [ul, uh]; the ball's chord
             // reaches none of them when the nearest point of that range is outside it
