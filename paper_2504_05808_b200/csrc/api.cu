@@ -407,9 +407,13 @@ int run_host_pipelined(const int32_t* labels_host, int32_t* dlab, const Geom& g,
       gg.tz_hi = (z1 + kTZ3 - 1) / kTZ3;
       launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, gg, 0, hdr, st);
       launch_dilate_paint(fgm, meta, pool, gcount, goff, gg, B, hdr, st);
+      // K5e on the chunk's finished layers, with the scale of the Dmax seen so far (checked
+      // against the final Dmax below; fallback tiles make it skip)
+      launch_epilogue(dlab, A, gg, &acc, nullptr, nullptr, B, (unsigned long long*)(w + L.fxl), hdr, st, true);
     }
   }
   launch_dilate_fallback(meta, cent, fbl, g, B, hdr, st);
+  launch_metrics(acc, g, outs, hdr, st);  // speculative: redone below if the chunked epilogue was not exact
   // halo check: the chunked z pass and dilation were exact iff both halos fit in one chunk
   WsHeader h;
   e = cudaMemcpyAsync(&h, hdr, sizeof h, cudaMemcpyDeviceToHost, st);
@@ -425,8 +429,13 @@ int run_host_pipelined(const int32_t* labels_host, int32_t* dlab, const Geom& g,
   uint64_t rr = 0;
   while ((rr + 1) * (rr + 1) <= (h.dmax ? h.dmax - 1 : 0) && rr <= (uint64_t)kChunkZ) ++rr;
   if (hz > (uint64_t)kChunkZ || rr > (uint64_t)kChunkZ || h.dxymax >= kInf) return FASTRS_OK;  // not exact: rerun
-  launch_epilogue(dlab, A, g, &acc, nullptr, nullptr, B, (unsigned long long*)(w + L.fxl), hdr, st);
-  launch_metrics(acc, g, outs, hdr, st);
+  // the per-chunk epilogues are exact when no tile went to the fallback kernel and every chunk
+  // used the scale of the final Dmax; otherwise redo the reductions over the whole volume
+  if (h.n_fb != 0 || h.epi_skipped != 0 || h.scale_set != (uint32_t)sum_scale_log2(g.nscale, h.dmax) + 1u) {
+    cudaMemsetAsync(w + L.vol, 0, (L.mx - L.vol) + align256((size_t)acc.M * 4), st);
+    launch_epilogue(dlab, A, g, &acc, nullptr, nullptr, B, (unsigned long long*)(w + L.fxl), hdr, st);
+    launch_metrics(acc, g, outs, hdr, st);
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   *exact = true;

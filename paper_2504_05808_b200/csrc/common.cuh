@@ -58,6 +58,8 @@ struct WsHeader {
   uint32_t pad[1];
   unsigned long long sum_group_list;  // K5 candidates summed over groups
   unsigned long long pool_used;       // K5 candidate pool entries allocated
+  uint32_t scale_set;    // host pipeline: s + 1 of the per-chunk epilogues (0xFFFFFFFF: they differed)
+  uint32_t epi_skipped;  // host pipeline: a per-chunk epilogue saw fallback tiles and did nothing
 };
 static_assert(sizeof(WsHeader) <= 256, "header");
 
@@ -166,7 +168,7 @@ void launch_dilate_gather(const uint32_t* fgm, TileMeta* meta, const uint2* cent
 int64_t dilate_pool_entries(const Geom& g);  // K5 candidate pool (sorted per-group lists), u64 entries
 // K5 epilogue: shell, per-label reductions and LT outputs from the LT plane ltp
 void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,
-                     float* lt_out, const uint32_t* ltp, unsigned long long* fxlut, WsHeader* hdr, cudaStream_t st);
+                     float* lt_out, const uint32_t* ltp, unsigned long long* fxlut, WsHeader* hdr, cudaStream_t st, bool chunked = false);
 constexpr size_t kFxLutBytes = 65536 * 8;  // workspace for the epilogue's fixed-point sqrt table
 void launch_metrics(const Accum& acc, const Geom& g, const Outputs& o, WsHeader* hdr,
                     cudaStream_t st);

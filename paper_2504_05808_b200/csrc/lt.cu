@@ -207,12 +207,19 @@ __global__ void __launch_bounds__(256) k_dilate_atomic(const TileMeta* __restric
 // ---------------------------------------------------------------------------------------
 // fxlut[c] = round(sqrt(c) * 2^s) for c < kFxLut: the fixed-point LT terms of the sums
 // (and the scale exponent s in the header, for the epilogue's terms beyond the table)
-__global__ void k_fxlut(unsigned long long* __restrict__ fxlut, int64_t nscale, WsHeader* __restrict__ hdr) {
+// track (host pipeline): record s + 1 in scale_set, or 0xFFFFFFFF once two chunks' scales differ
+__global__ void k_fxlut(unsigned long long* __restrict__ fxlut, int64_t nscale, WsHeader* __restrict__ hdr, int track) {
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= kFxLut) return;
   const int s = sum_scale_log2(nscale, hdr->dmax);
   fxlut[c] = (unsigned long long)__double2ull_rn(sqrt((double)c) * ldexp(1.0, s));
-  if (c == 0) hdr->scale_log2 = s;
+  if (c == 0) {
+    hdr->scale_log2 = s;
+    if (track) {
+      const uint32_t prev = hdr->scale_set;
+      hdr->scale_set = (prev == 0u || prev == (uint32_t)s + 1u) ? (uint32_t)s + 1u : 0xFFFFFFFFu;
+    }
+  }
 }
 
 template <bool FAST>
@@ -220,7 +227,13 @@ __global__ void __launch_bounds__(256) k_epilogue(const int32_t* __restrict__ la
                                                   const uint32_t* __restrict__ ltp, Geom g, int64_t z_lo, int64_t nz,
                                                   Accum acc, int do_reduce, uint32_t* __restrict__ lt2_out,
                                                   float* __restrict__ lt_out, const unsigned long long* __restrict__ fxlut,
-                                                  WsHeader* __restrict__ hdr) {
+                                                  WsHeader* __restrict__ hdr, int guard) {
+  // guard (host pipeline, per chunk): tiles left to the fallback kernel have no LT yet; the
+  // call then redoes the whole epilogue at the end
+  if (guard && hdr->n_fb != 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) hdr->epi_skipped = 1u;
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= g.B * nz * g.Y) return;
@@ -295,21 +308,22 @@ void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta, con
 }
 
 void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,
-                     float* lt_out, const uint32_t* ltp, unsigned long long* fxlut, WsHeader* hdr, cudaStream_t st) {
+                     float* lt_out, const uint32_t* ltp, unsigned long long* fxlut, WsHeader* hdr, cudaStream_t st, bool chunked) {
   Accum a{};
   if (acc) a = *acc;
   // epilogue over the produced layers
   const int TZ = g.ndim == 3 ? kTZ3 : 1;
   const int64_t z_lo = g.tz_lo * TZ, z_hi = g.tz_hi * TZ < g.Z ? g.tz_hi * TZ : g.Z;
   const int64_t rows = g.B * (z_hi - z_lo) * g.Y;
-  if (acc) k_fxlut<<<kFxLut / 256, 256, 0, st>>>(fxlut, g.nscale, hdr);
+  if (acc) k_fxlut<<<kFxLut / 256, 256, 0, st>>>(fxlut, g.nscale, hdr, chunked ? 1 : 0);
   if (rows > 0) {
     if (acc && !lt2_out && !lt_out)
       k_epilogue<true><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(labels, D, ltp, g, z_lo, z_hi - z_lo, a, 1, nullptr,
-                                                                  nullptr, fxlut, hdr);
+                                                                  nullptr, fxlut, hdr, chunked ? 1 : 0);
     else
       k_epilogue<false><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(labels, D, ltp, g, z_lo, z_hi - z_lo, a, acc ? 1 : 0,
-                                                                   lt2_out, lt_out, acc ? fxlut : nullptr, hdr);
+                                                                   lt2_out, lt_out, acc ? fxlut : nullptr, hdr,
+                                                                   chunked ? 1 : 0);
   }
 }
 

@@ -295,6 +295,20 @@ def test_host_entry_point_pipelined_matches_device_call(F):
     s, r = F.sphericity_roundness_host(lab, max_label=ml)
     np.testing.assert_array_equal(s, want["sphericity"].cpu().numpy())
     np.testing.assert_array_equal(r, want["roundness"].cpu().numpy())
+    # small grains in the first chunks and a large ball near the end: the per-chunk epilogues
+    # run with the fixed-point scale of a smaller Dmax than the final one, so the call redoes
+    # the reductions; still bit-identical
+    mixed = np.zeros((512, 96, 96), np.int32)
+    k = 0
+    for z in range(8, 300, 12):
+        for y in range(8, 90, 12):
+            k += 1
+            mixed[z - 3:z + 4, y - 3:y + 4, 40:47] = np.where(synth.sphere(3, canvas=7) > 0, k, 0)
+    mixed[380:461, 8:89, 8:89] = np.where(synth.sphere(40, canvas=81) > 0, k + 1, 0)
+    want = F.sphericity_roundness(_dev(mixed), max_label=k + 1)
+    s, r = F.sphericity_roundness_host(mixed, max_label=k + 1)
+    np.testing.assert_array_equal(s, want["sphericity"].cpu().numpy())
+    np.testing.assert_array_equal(r, want["roundness"].cpu().numpy())
     big = np.zeros((520, 310, 310), np.int32)
     big[5:306, 5:306, 5:306] = synth.sphere(150, canvas=301)
     big[400:440, 100:120, 100:130] = 2
