@@ -251,22 +251,34 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
         if (pre[mid] <= wbeg) cur = mid; else hi = mid;
       }
     }
-    for (uint32_t e0 = wbeg; e0 < wend; e0 += 32) {
-      const uint32_t e = e0 + lane;
+    // batch e0: its record lo and centre entry; the next batch's entry is loaded before the
+    // current one is processed (its latency overlaps the tests and list appends)
+    auto locate = [&](uint32_t e0, int& lo, uint2& en) {
       const int j = cur + 1 + lane;
       const uint32_t off = (j <= nrec ? pre[j] : 0xFFFFFFFFu) - e0;  // record j starts at e0 + off
       const uint32_t starts = __reduce_or_sync(kFull, off - 1u < 31u ? 1u << off : 0u);
-      const int lo = cur + __popc(starts & ((2u << lane) - 1u));
+      lo = cur + __popc(starts & ((2u << lane) - 1u));
       cur += __popc(__ballot_sync(kFull, off - 1u < 32u));
+      en = make_uint2(0u, 0u);
+      if (e0 + lane < wend) {
+        const uint32_t k = (rec[3 * lo + 1] & 0xFFFFu) + (e0 + lane - pre[lo]);
+        en = __ldg(cent + (size_t)rec[3 * lo] * kTileVol + k);
+      }
+    };
+    int lo_n = 0;
+    uint2 en_n = make_uint2(0u, 0u);
+    if (wbeg < wend) locate(wbeg, lo_n, en_n);
+    for (uint32_t e0 = wbeg; e0 < wend; e0 += 32) {
+      const uint32_t e = e0 + lane;
+      const int lo = lo_n;
+      const uint2 en = en_n;
+      if (e0 + 32 < wend) locate(e0 + 32, lo_n, en_n);
       bool take = false;
       int bk = -1;
       unsigned long long pe = 0;
       uint32_t pe32 = 0;
       if (e < wend) {
-        const uint32_t ht = rec[3 * lo];
-        const uint32_t k = (rec[3 * lo + 1] & 0xFFFFu) + (e - pre[lo]);
         const uint32_t o = rec[3 * lo + 2];
-        const uint2 en = __ldg(cent + (size_t)ht * kTileVol + k);
         const int v = (int)en.x;
         const int cx = (int)(o & 0xFFFFu) - kOff + (v & 31), cy = (int)(o >> 16) - kOff + ((v >> 5) % P::TY),
                   cz = (int)recz[lo] + v / (32 * P::TY);
