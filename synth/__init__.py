@@ -252,6 +252,28 @@ def make_config(i: int, seed: int | None = None, batch: int | None = None):
     return lab, info
 
 
+def make_count_volume(seed: int = 6, n: int = 15503, dim: int = 400):
+    """Synthetic stand-in for the paper's object-count experiment volume (a 400^3
+    uCT scan with 15 503 objects of 27 to ~130 000 voxels): n
+    spheroids / rough grains, r_eq on a truncated power law p(r) ~ r^-3 between the radii of 27
+    and 130 000 voxel spheres (expected fill ~21 %), aspect U[0.3, 3], half rough; largest
+    placed first, >= 1 voxel gaps.  Objects that do not fit are left out (info["n_objects"])."""
+    rng = np.random.default_rng(seed)
+    k = 3.0
+    r_lo, r_hi = (3 * 27 / (4 * math.pi)) ** (1 / 3), (3 * 130000 / (4 * math.pi)) ** (1 / 3)
+    u = rng.random(n)
+    lo, hi = r_lo ** (1 - k), r_hi ** (1 - k)
+    r_eq = (lo + u * (hi - lo)) ** (1.0 / (1 - k))
+    asp = rng.uniform(0.3, 3.0, n)
+    p = _objects3d(rng, r_eq, asp, 0.5)
+    order = np.argsort(-r_eq, kind="stable")
+    labels = np.arange(1, n + 1, dtype=np.int32)
+    grid, placed, _ = _place((dim, dim, dim), False, p[order], labels, seed, max_tries=2000)
+    info = describe(grid, ndim=3, batch=1, max_label=n)
+    info.update(config="count-volume", seed=seed)
+    return grid, info
+
+
 def describe(lab: np.ndarray, ndim: int, batch: int, max_label: int) -> dict:
     counts = np.bincount(lab.reshape(-1), minlength=max_label + 1)
     fg = int(lab.size - counts[0])

@@ -31,3 +31,15 @@ def test_c5_small_batch_touching():
     # touching allowed: some face-adjacent pairs of different non-zero labels exist
     a, b = lab[0, :, 1:], lab[0, :, :-1]
     assert ((a != b) & (a > 0) & (b > 0)).any()
+
+
+def test_count_volume_matches_the_paper_experiment_shape():
+    """The NEXT-1 stand-in volume (400^3, 15 503 objects of 27 to ~130 000 voxels):
+    every object is placed, sizes span the paper's range (rasterised spheroids and rough grains
+    deviate from the nominal volume by tens of percent at the extremes), fill is moderate."""
+    lab, info = synth.make_count_volume()
+    assert lab.shape == (400, 400, 400) and lab.dtype == np.int32
+    assert info["n_labels_present"] == 15503 and info["max_label"] == 15503
+    v = np.bincount(lab.ravel(), minlength=15504)[1:]
+    assert v.min() >= 10 and 27 * 0.5 <= np.percentile(v, 1) and v.max() <= 2 * 130000
+    assert 0.15 < info["fill"] < 0.30
