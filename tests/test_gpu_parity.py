@@ -317,3 +317,22 @@ def test_host_entry_point_pipelined_matches_device_call(F):
     np.testing.assert_array_equal(s, want["sphericity"].cpu().numpy())
     np.testing.assert_array_equal(r, want["roundness"].cpu().numpy())
     assert r[0] == 1.0
+
+
+def test_count_volume_subsets(F):
+    """NEXT-1 (tools/count_scaling.py): subsets of the 400^3 count volume with the other labels
+    zeroed; the drawn objects' metrics match the oracle (the zeroed ones stay absent)."""
+    lab, info = synth.make_count_volume()
+    ml = info["max_label"]
+    rng = np.random.default_rng(3)
+    for n in (1, 37):
+        sel = np.sort(rng.choice(np.arange(1, ml + 1), n, replace=False))
+        sub = np.where(np.isin(lab, sel), lab, 0).astype(np.int32)
+        got = F.sphericity_roundness(_dev(sub), max_label=ml, stats=True)
+        mask = np.zeros(ml, np.uint8)
+        mask[sel - 1] = 1
+        want = oracle.sphericity_roundness(sub, max_label=ml, label_mask=mask)
+        np.testing.assert_array_equal(got["volume"].cpu().numpy()[sel - 1], want["volume"][sel - 1])
+        for k in ("sphericity", "roundness", "mean_lt"):
+            np.testing.assert_allclose(got[k].cpu().numpy()[sel - 1], want[k][sel - 1], rtol=RTOL, atol=0)
+        assert np.isnan(got["sphericity"].cpu().numpy()[np.setdiff1d(np.arange(ml), sel - 1)]).all()
