@@ -60,6 +60,7 @@ struct WsHeader {
   unsigned long long pool_used;       // K5 candidate pool entries allocated
   uint32_t scale_set;    // host pipeline: s + 1 of the per-chunk epilogues (0xFFFFFFFF: they differed)
   uint32_t epi_skipped;  // host pipeline: a per-chunk epilogue saw fallback tiles and did nothing
+  uint32_t paint_next;   // K5b work counter (reset before each launch)
 };
 static_assert(sizeof(WsHeader) <= 256, "header");
 

@@ -626,22 +626,20 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_dilate_gather(const uint32_t
   }
 }
 
-template <bool IS3D, int NW, int MINB>
-__global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* __restrict__ fgm,
-                                                              const TileMeta* __restrict__ meta, Geom g,
-                                                              const unsigned long long* __restrict__ pool,
-                                                              const uint32_t* __restrict__ gcount,
-                                                              const uint32_t* __restrict__ goff, int point_at,
-                                                              uint32_t* __restrict__ ltp, WsHeader* __restrict__ hdr) {
+template <bool IS3D, int NW>
+__device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* __restrict__ fgm,
+                                           const TileMeta* __restrict__ meta, const Geom& g,
+                                           const unsigned long long* __restrict__ pool,
+                                           const uint32_t* __restrict__ gcount, const uint32_t* __restrict__ goff,
+                                           int point_at, uint32_t* __restrict__ ltp, WsHeader* __restrict__ hdr) {
   using P = Shape<IS3D>;
   constexpr int TY = P::TY, TZ = P::TZ;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PaintSmem<NW>& S = *reinterpret_cast<PaintSmem<NW>*>(smem_raw);
   constexpr int kSplit = kWarps / NW;  // CTAs per group
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int warp = (int)(blockIdx.x % kSplit) * NW + wl;  // my tile within the group
-  const int64_t group = blockIdx.x / kSplit;
-  if (hdr->dmax > kU16Max) return;  // k_dilate_atomic handles it
+  const int warp = (int)(bid % kSplit) * NW + wl;  // my tile within the group
+  const int64_t group = bid / kSplit;
 
   // ---- group / tile coordinates --------------------------------------------------------
   // groups tile the layers [tz_lo, tz_hi) (all layers except on the slab path)
@@ -935,6 +933,29 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* 
   if (lane == 0 && n_rows) atomicAdd(&hdr->n_intervals, (unsigned long long)n_rows);
 }
 
+
+// Persistent K5b: resident one-warp CTAs take tiles from a global counter in launch order (the
+// four tiles of a group one after another), so no CTA slot idles between short tiles.
+template <bool IS3D, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* __restrict__ fgm,
+                                                              const TileMeta* __restrict__ meta, Geom g,
+                                                              const unsigned long long* __restrict__ pool,
+                                                              const uint32_t* __restrict__ gcount,
+                                                              const uint32_t* __restrict__ goff, int point_at,
+                                                              uint32_t* __restrict__ ltp, WsHeader* __restrict__ hdr,
+                                                              uint32_t nbid) {
+  if (hdr->dmax > kU16Max) return;  // k_dilate_atomic handles it
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    uint32_t bid = 0;
+    if (lane == 0) bid = atomicAdd(&hdr->paint_next, 1u);
+    bid = __shfl_sync(kFull, bid, 0);
+    if (bid >= nbid) break;
+    paint_tile<IS3D, NW>(bid, fgm, meta, g, pool, gcount, goff, point_at, ltp, hdr);
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
 int64_t dilate_groups(const Geom& g) {
@@ -981,8 +1002,14 @@ void paint_variant(int64_t ngroups, const uint32_t* fgm, const TileMeta* meta, c
                    const unsigned long long* pool, const uint32_t* gcount, const uint32_t* goff, uint32_t* ltp,
                    WsHeader* hdr, cudaStream_t st) {
   constexpr int NW = 1;
-  k_dilate_paint<IS3D, NW, 32><<<(unsigned)(ngroups * (kWarps / NW)), NW * 32, sizeof(PaintSmem<NW>), st>>>(
-      fgm, meta, g, pool, gcount, goff, point_at_knob(), ltp, hdr);
+  const uint32_t nbid = (uint32_t)(ngroups * (kWarps / NW));
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t grid = nbid < (uint32_t)nsm * 32u ? nbid : (uint32_t)nsm * 32u;
+  cudaMemsetAsync(&hdr->paint_next, 0, sizeof(uint32_t), st);
+  k_dilate_paint<IS3D, NW, 32><<<grid, NW * 32, sizeof(PaintSmem<NW>), st>>>(fgm, meta, g, pool, gcount, goff,
+                                                                           point_at_knob(), ltp, hdr, nbid);
 }
 }  // namespace
 
