@@ -60,6 +60,10 @@ struct Smem {  // K5a (gather + sort)
 // K5b CTAs hold NW of a group's kWarps tiles (one warp each).  The warps share
 // nothing, so one warp per CTA lets every tile retire on its own: no warp slot idles while a
 // sibling tile of the same CTA is still painting.
+// K5b launch shape: warps per CTA and resident CTAs per SM (sets the register cap: 56 here, 36
+// resident warps).  C4 sweep (persistent): (2,16) 10.63 ms, (2,18) 10.58, (2,20) 10.71, (2,24)
+// 10.68, (1,32) 10.76, (4,10) 10.70.
+constexpr int kPaintNW = 2, kPaintMinB = 18;
 template <int NW>
 struct PaintSmem {  // K5b (one tile per warp)
   uint16_t val[NW][kRows * 32];   // LT^2 per element of each warp's tile (D <= 65535 here)
@@ -636,10 +640,10 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
   constexpr int TY = P::TY, TZ = P::TZ;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PaintSmem<NW>& S = *reinterpret_cast<PaintSmem<NW>*>(smem_raw);
-  constexpr int kSplit = kWarps / NW;  // CTAs per group
+  // bid numbers tiles: group bid / kWarps, tile bid % kWarps within it; wl = my warp's smem slot
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int warp = (int)(bid % kSplit) * NW + wl;  // my tile within the group
-  const int64_t group = bid / kSplit;
+  const int warp = (int)(bid % kWarps);  // my tile within the group
+  const int64_t group = bid / kWarps;
 
   // ---- group / tile coordinates --------------------------------------------------------
   // groups tile the layers [tz_lo, tz_hi) (all layers except on the slab path)
@@ -994,22 +998,25 @@ void launch_dilate_gather(const uint32_t* fgm, TileMeta* meta, const uint2* cent
 }
 
 namespace {
-// K5b launch shape: one warp (tile) per CTA, registers capped for 32 resident CTAs per SM (the
-// CTA limit).  Measured on C4: 2 warps per CTA at 48 / 40 registers (42 / 51 resident warps),
-// 4 warps at 48, or no register cap were all slower (13.9-16.4 ms vs 13.7).
+template <bool IS3D, int NW, int MINB>
+void paint_go(int64_t ngroups, const uint32_t* fgm, const TileMeta* meta, const Geom& g,
+              const unsigned long long* pool, const uint32_t* gcount, const uint32_t* goff, uint32_t* ltp,
+              WsHeader* hdr, cudaStream_t st) {
+  const uint32_t nbid = (uint32_t)(ngroups * kWarps);
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t cap = (uint32_t)nsm * MINB * NW;  // resident warps
+  const uint32_t grid = ((nbid < cap ? nbid : cap) + NW - 1) / NW;
+  cudaMemsetAsync(&hdr->paint_next, 0, sizeof(uint32_t), st);
+  k_dilate_paint<IS3D, NW, MINB><<<grid, NW * 32, sizeof(PaintSmem<NW>), st>>>(fgm, meta, g, pool, gcount, goff,
+                                                                             point_at_knob(), ltp, hdr, nbid);
+}
 template <bool IS3D>
 void paint_variant(int64_t ngroups, const uint32_t* fgm, const TileMeta* meta, const Geom& g,
                    const unsigned long long* pool, const uint32_t* gcount, const uint32_t* goff, uint32_t* ltp,
                    WsHeader* hdr, cudaStream_t st) {
-  constexpr int NW = 1;
-  const uint32_t nbid = (uint32_t)(ngroups * (kWarps / NW));
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const uint32_t grid = nbid < (uint32_t)nsm * 32u ? nbid : (uint32_t)nsm * 32u;
-  cudaMemsetAsync(&hdr->paint_next, 0, sizeof(uint32_t), st);
-  k_dilate_paint<IS3D, NW, 32><<<grid, NW * 32, sizeof(PaintSmem<NW>), st>>>(fgm, meta, g, pool, gcount, goff,
-                                                                           point_at_knob(), ltp, hdr, nbid);
+  paint_go<IS3D, kPaintNW, kPaintMinB>(ngroups, fgm, meta, g, pool, gcount, goff, ltp, hdr, st);
 }
 }  // namespace
 
