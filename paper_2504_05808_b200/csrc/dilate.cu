@@ -31,7 +31,8 @@ namespace fastrs {
 namespace {
 
 constexpr int kWarps = 4;  // warps per CTA = tiles per group
-constexpr int kCap = 2048;   // candidate list capacity per round
+constexpr int kCap = 1536;   // candidate list capacity per round (3D single pass: 2 * kCap compact entries)
+constexpr int kIdx = 2048;   // sort indices (rounds path) / gather scratch (record prefix sums and z offsets)
 constexpr int kBuckets = 128;
 constexpr int kHist = 1536;  // exact-D counting-sort bins per round
 constexpr int kPoint = 96;  // C4 sweep: 128 -> 11.98 ms, 96 -> 11.75, 64 -> 11.92, 32 -> 12.59, 0 -> 15.38
@@ -47,7 +48,7 @@ struct Smem {  // K5a (gather + sort)
     uint32_t list32[2 * kCap];       // the same, compact (3D single-pass path, see pack32)
   };
   uint32_t hist[kHist];              // exact-D counting sort: bin Dhi - D (rounds path; gather scratch)
-  uint16_t idx[kCap];                // indices into list, sorted by D (descending)
+  uint16_t idx[kIdx];                // indices into list, sorted by D (descending)
   uint32_t dh[kHist];                // exact-D histogram / cursors of the single-pass path
   uint32_t bhist[kBuckets];
   unsigned long long base;           // the group's offset in the global candidate pool
@@ -353,7 +354,7 @@ __device__ __forceinline__ unsigned long long row_box(int ya, int yb, int za, in
 }
 
 template <bool IS3D>
-__global__ void __launch_bounds__(kWarps * 32, 6) k_dilate_gather(const uint32_t* __restrict__ fgm,
+__global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t* __restrict__ fgm,
                                                                   const TileMeta* __restrict__ meta,
                                                                const uint2* __restrict__ cent,
                                                                const uint16_t* __restrict__ oct,
