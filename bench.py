@@ -70,10 +70,10 @@ def _kernel_key(name: str):
     return base.strip(), (args.split(",")[0].strip(" >") or None) if args else None
 
 
-def ncu_traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary, or None.
-    Names match on the base name and the first template argument (the 2D/3D instance), so a
-    kernel that gained template parameters still finds its summary line."""
+def ncu_record(kernel: str):
+    """The committed ncu --set full summary line of `kernel` (dict), or None.  Names match on the
+    base name and the first template argument (the 2D/3D instance), so a kernel that gained
+    template parameters still finds its summary line."""
     try:
         kernels = json.load(open(NCU_SUMMARY))["kernels"]
     except Exception:
@@ -86,7 +86,29 @@ def ncu_traffic(kernel: str):
             if got[0] == want[0] and (want[1] is None or got[1] == want[1]):
                 k = rec
                 break
+    return k
+
+
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu summary, or None."""
+    k = ncu_record(kernel)
     return None if k is None else k["traffic_bytes_per_launch"]
+
+
+def issue_roofline(per_launch: dict, sm_mhz: float, n_sm: int) -> dict:
+    """Instruction-issue roofline per stage: warp instructions per launch (committed ncu summary)
+    / the live per-launch time, against 4 schedulers x 1 warp instruction per clock per SM at the
+    SM clock sampled during the run.  The kernels of this path are issue-bound, not HBM-bound."""
+    peak = n_sm * 4 * sm_mhz * 1e6
+    out = {}
+    for stage, ms in per_launch.items():
+        rec = ncu_record(STAGE_KERNEL.get(stage, ""))
+        if rec is None or ms <= 0 or not rec.get("warp_instructions"):
+            continue
+        ach = rec["warp_instructions"] / (ms * 1e-3)
+        out[stage] = {"achieved_winst_per_s": ach, "frac": round(ach / peak, 4)}
+    return {"peak_winst_per_s": peak, "sm_mhz": sm_mhz, "sms": n_sm, "source": os.path.relpath(NCU_SUMMARY, ROOT),
+            "stages": out}
 
 
 def workload_name(cfg: int) -> str:
@@ -333,6 +355,8 @@ def run_fastrs(args):
                      "traffic_source": os.path.relpath(NCU_SUMMARY, ROOT), "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes},
         "stages": stage_gbs,
+        "issue_roofline": issue_roofline(per_launch, float(clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0),
+                                         torch.cuda.get_device_properties(dev).multi_processor_count),
         "pipeline_model": {"bytes_per_step": model_bytes, "GB/s": pipe_gbs, "frac": pipe_gbs / hbm_peak},
         "diagnostics": {k: int(v) for k, v in diag.items()},
         "clocks": clk,
