@@ -1,6 +1,6 @@
 """Per-stage device times (library CUDA events) of the hot path on one BASELINE config.
 usage: python tools/stage_times.py [--config 4] [--iters 3] [--cache /tmp/c4.npy]
-Development helper for sweeps (e.g. FASTRS_POINT_AT=64 python tools/stage_times.py)."""
+Development helper for A/B runs of kernel variants (reads the library's per-stage events)."""
 import argparse
 import json
 import os
