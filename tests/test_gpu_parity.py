@@ -181,6 +181,9 @@ def test_batched_items_are_independent(F):
     full_check(F, a, 1, ndim=2)
     b = synth.random_labels((2, 12, 20, 33), nlabels=4, seed=4, fill=0.8, blob=3)
     full_check(F, b, 1, ndim=3)
+    # X % 4 == 0: K4 stages its tiles through the 4D TMA tensor map (batch as the 4th dim)
+    c = synth.random_labels((3, 19, 21, 36), nlabels=5, seed=6, fill=0.8, blob=3)
+    full_check(F, c, 1, ndim=3)
     # a batch equals its items run one by one
     t = _dev(a)
     rb = F.sphericity_roundness(t, max_label=4, ndim=2)["roundness"].cpu().numpy().reshape(3, 4)
