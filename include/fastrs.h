@@ -214,6 +214,24 @@ FASTRS_API int fastrs_metrics_from_partials(const uint64_t* vol, const uint64_t*
                                             const fastrs_object_stats* stats, void* ws, size_t ws_bytes,
                                             void* stream);
 
+/* ---- object filters of the paper's analysis protocol (label level) ----
+ * fastrs_touches_edge: touches_edge[b*max_label + label-1] = 1 if some element of that label
+ * lies on the boundary of its grid item (any face in 3D, any edge in 2D), else 0 (PAPER.md:195
+ * "Edge cells are removed"; SPEC.md:212 remove_edge_objects).  labels as in
+ * fastrs_sphericity_roundness (device); touches_edge: device, batch*max_label bytes, written in
+ * full.  Labels outside 1..max_label are ignored.  Errors: EINVAL (geometry, NULL, max_label < 1),
+ * ECUDA.  Synchronises `stream` at the end unless flags has FASTRS_ASYNC.
+ * fastrs_filter_objects: sets sphericity[i] and roundness[i] (either may be NULL) to NaN where
+ * volume[i] < min_volume ("the smallest objects are filtered out (V < 10^3)";
+ * SPEC.md:219 filter_small) when volume != NULL, or where touches_edge[i] != 0 when touches_edge
+ * != NULL; n_labels entries, all device pointers (volume: the stats output of
+ * fastrs_sphericity_roundness).  Errors: EINVAL (n_labels < 0), ECUDA. */
+FASTRS_API int fastrs_touches_edge(const int32_t* labels, const int64_t* dims, int ndim, int64_t batch,
+                                   int32_t max_label, uint8_t* touches_edge, uint32_t flags, void* stream);
+FASTRS_API int fastrs_filter_objects(double* sphericity, double* roundness, const int64_t* volume,
+                                     const uint8_t* touches_edge, int64_t n_labels, int64_t min_volume,
+                                     uint32_t flags, void* stream);
+
 FASTRS_API const char* fastrs_last_error(void);  /* thread-local message of the last failure */
 FASTRS_API void fastrs_release(void);            /* free the per-device caches                */
 

@@ -142,3 +142,38 @@ def sphericity_3d(V: float, mean_lt: float) -> float:
 
 def sphericity_2d(A: float, mean_lt: float) -> float:
     return _load().fastrs_oracle_sphericity_2d(A, mean_lt)
+
+
+def touches_edge(labels, max_label, ndim=None, batch=None) -> np.ndarray:
+    """Edge objects, the plain definition (SPEC.md:212 remove_edge_objects: "any label whose
+    support touches a grid boundary"; "Edge cells are removed"): uint8 flags,
+    batch*max_label entries, 1 where the label occurs on the first or last index of any axis of
+    its item.  Labels outside 1..max_label are ignored."""
+    labels, ndim, batch, dims = _geom(labels, ndim, batch)
+    items = labels.reshape((batch,) + tuple(int(d) for d in dims))
+    out = np.zeros(batch * int(max_label), np.uint8)
+    for b in range(batch):
+        it = items[b]
+        for ax in range(ndim):
+            for idx in (0, it.shape[ax] - 1):
+                face = np.take(it, idx, axis=ax)
+                for L in np.unique(face):
+                    if 1 <= L <= max_label:
+                        out[b * max_label + L - 1] = 1
+    return out
+
+
+def filter_objects(res: dict, min_volume=None, edge=None) -> dict:
+    """The paper's analysis filters on an oracle result dict (copies): NaN sphericity/roundness
+    where volume < min_volume (PAPER.md:274, SPEC.md:219 filter_small) or edge[i] != 0."""
+    out = dict(res)
+    drop = np.zeros(res["sphericity"].shape, bool)
+    if min_volume is not None:
+        drop |= res["volume"] < min_volume
+    if edge is not None:
+        drop |= np.asarray(edge) != 0
+    for k in ("sphericity", "roundness"):
+        v = np.array(res[k], dtype=np.float64)
+        v[drop] = np.nan
+        out[k] = v
+    return out

@@ -545,6 +545,28 @@ int fastrs_sphericity_roundness_host(const int32_t* labels_host, const int64_t* 
   return FASTRS_OK;
 }
 
+int fastrs_touches_edge(const int32_t* labels, const int64_t* dims, int ndim, int64_t batch, int32_t max_label,
+                        uint8_t* touches_edge, uint32_t flags, void* stream) {
+  Geom g;
+  int rc = make_geom(dims, ndim, batch, g);
+  if (rc) return rc;
+  if (!labels || !touches_edge) return fail(FASTRS_EINVAL, "NULL pointer");
+  if (max_label < 1) return fail(FASTRS_EINVAL, "max_label must be >= 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = launch_touch_edge(labels, g, max_label, touches_edge, st);
+  if (e == cudaSuccess && !(flags & kFlagAsync)) e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? FASTRS_OK : cuda_fail(e, "touches_edge");
+}
+
+int fastrs_filter_objects(double* sphericity, double* roundness, const int64_t* volume, const uint8_t* touches_edge,
+                          int64_t n_labels, int64_t min_volume, uint32_t flags, void* stream) {
+  if (n_labels < 0) return fail(FASTRS_EINVAL, "n_labels < 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = launch_filter(sphericity, roundness, volume, touches_edge, n_labels, min_volume, st);
+  if (e == cudaSuccess && !(flags & kFlagAsync)) e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? FASTRS_OK : cuda_fail(e, "filter_objects");
+}
+
 int fastrs_read_diagnostics(const void* ws, fastrs_diagnostics* out, void* stream) {
   if (!ws || !out) return fail(FASTRS_EINVAL, "NULL pointer");
   WsHeader h;

@@ -171,6 +171,10 @@ int64_t dilate_pool_entries(const Geom& g);  // K5 candidate pool (sorted per-gr
 void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,
                      float* lt_out, const uint32_t* ltp, unsigned long long* fxlut, WsHeader* hdr, cudaStream_t st, bool chunked = false);
 constexpr size_t kFxLutBytes = 65536 * 8;  // workspace for the epilogue's fixed-point sqrt table
+cudaError_t launch_touch_edge(const int32_t* labels, const Geom& g, int32_t max_label, uint8_t* touch,
+                              cudaStream_t st);
+cudaError_t launch_filter(double* sph, double* rnd, const int64_t* vol, const uint8_t* touch, int64_t n,
+                          int64_t min_volume, cudaStream_t st);
 void launch_metrics(const Accum& acc, const Geom& g, const Outputs& o, WsHeader* hdr,
                     cudaStream_t st);
 void release_mtables();

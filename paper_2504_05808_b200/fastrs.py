@@ -84,9 +84,12 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
                                                sz, vp]
             lib.fastrs_metrics_from_partials.argtypes = [vp, vp, vp, vp, vp, i64, ci, i64, u32, vp, vp, vp, vp,
                                                          sz, vp]
+            lib.fastrs_touches_edge.argtypes = [vp, vp, ci, i64, i32, vp, u32, vp]
+            lib.fastrs_filter_objects.argtypes = [vp, vp, vp, vp, i64, i64, u32, vp]
             for n in ("workspace_bytes", "edt_sq", "local_thickness", "sphericity_roundness",
                       "sphericity_roundness_host", "read_diagnostics", "profile_read", "slab_workspace_bytes",
-                      "slab_edt_xy", "slab_edt_z", "slab_reduce", "metrics_from_partials"):
+                      "slab_edt_xy", "slab_edt_z", "slab_reduce", "metrics_from_partials", "touches_edge",
+                      "filter_objects"):
                 getattr(lib, "fastrs_" + n).restype = ci
             _lib = lib
     return _lib
@@ -340,6 +343,33 @@ def metrics_from_partials(part: dict, ndim: int, nscale: int, dmax_global: int, 
                                                int(nscale), int(dmax_global), res["sphericity"].data_ptr(),
                                                res["roundness"].data_ptr(), None if st is None else ctypes.byref(st),
                                                ws.data_ptr(), ws.numel(), _stream(dev)))
+    return res
+
+
+def touches_edge(labels: torch.Tensor, max_label: int, ndim=None) -> torch.Tensor:
+    """uint8 flags (batch*max_label): 1 where a label has an element on its item's grid boundary
+    (fastrs_touches_edge; PAPER.md:195, SPEC.md:212)."""
+    labels = _labels_arg(labels)
+    ndim, b, dims = _geometry(labels.shape, ndim, None)
+    out = torch.empty(b * int(max_label), dtype=torch.uint8, device=labels.device)
+    _check(load().fastrs_touches_edge(labels.data_ptr(), dims, ndim, b, int(max_label), out.data_ptr(), 0,
+                                      _stream(labels.device)))
+    return out
+
+
+def filter_objects(res: dict, min_volume=None, edge=None) -> dict:
+    """The paper's analysis filters, in place on a result dict of sphericity_roundness(stats=True
+    when min_volume is given): NaN metrics for labels with volume < min_volume and,
+    with edge = touches_edge(...), for labels on the grid boundary."""
+    sph, rnd = res["sphericity"], res["roundness"]
+    vol = None
+    if min_volume is not None:
+        if "volume" not in res:
+            raise ValueError("min_volume needs the stats of sphericity_roundness(stats=True)")
+        vol = res["volume"]
+    _check(load().fastrs_filter_objects(sph.data_ptr(), rnd.data_ptr(), None if vol is None else vol.data_ptr(),
+                                        None if edge is None else edge.data_ptr(), sph.numel(),
+                                        int(min_volume or 0), 0, _stream(sph.device)))
     return res
 
 

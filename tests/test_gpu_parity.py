@@ -339,3 +339,30 @@ def test_count_volume_subsets(F):
         for k in ("sphericity", "roundness", "mean_lt"):
             np.testing.assert_allclose(got[k].cpu().numpy()[sel - 1], want[k][sel - 1], rtol=RTOL, atol=0)
         assert np.isnan(got["sphericity"].cpu().numpy()[np.setdiff1d(np.arange(ml), sel - 1)]).all()
+
+
+def test_touches_edge_and_filters_match_oracle(F):
+    """NEXT-4 label-level filters: edge objects are flagged exactly as the oracle's
+    plain definition on 2D, 3D and batched inputs, and the small-object / edge filters
+     blank the same labels."""
+    cases = [(synth.make_config(1)[0], 21, None), (synth.make_config(5, batch=3)[0], 500, 2),
+             (synth.random_labels((2, 12, 20, 36), nlabels=6, seed=8, fill=0.8, blob=3), 6, 3),
+             (synth.random_labels((33, 1, 17), nlabels=3, seed=9, fill=0.9, blob=2), 3, None)]
+    for lab, ml, nd in cases:
+        got = F.touches_edge(_dev(lab), ml, ndim=nd).cpu().numpy()
+        want = oracle.touches_edge(lab, ml, ndim=nd)
+        np.testing.assert_array_equal(got, want)
+    lab, info = synth.make_config(2)
+    ml = info["max_label"]
+    t = _dev(lab)
+    res = F.sphericity_roundness(t, max_label=ml, stats=True)
+    edge = F.touches_edge(t, ml)
+    F.filter_objects(res, min_volume=1000, edge=edge)
+    ref = oracle.filter_objects(oracle.sphericity_roundness(lab, max_label=ml), min_volume=1000,
+                                edge=oracle.touches_edge(lab, ml))
+    for k in ("sphericity", "roundness"):
+        g, w = res[k].cpu().numpy(), ref[k]
+        np.testing.assert_array_equal(np.isnan(g), np.isnan(w))
+        ok = ~np.isnan(w)
+        assert ok.any()
+        np.testing.assert_allclose(g[ok], w[ok], rtol=RTOL, atol=0)

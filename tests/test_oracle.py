@@ -325,3 +325,45 @@ def test_batch_items_independent():
     ra = oracle.sphericity_roundness(a, max_label=21)
     np.testing.assert_array_equal(r["sphericity"][:21], ra["sphericity"])
     assert r["sphericity"][21] == pytest.approx(0.999999085802, rel=1e-11)
+
+
+def test_touches_edge_spec_examples():
+    """SPEC.md:215-218 remove_edge_objects examples, and the same rule on every face in 3D,
+    per batch item."""
+    a = np.zeros((5, 6), np.int32)
+    a[0, 2] = 1  # a single object touching row 0
+    assert oracle.touches_edge(a, 1).tolist() == [1]
+    b = np.zeros((5, 6), np.int32)
+    b[2, 2:4] = 1  # interior object only
+    assert oracle.touches_edge(b, 1).tolist() == [0]
+    c = b.copy()
+    c[3:5, 5] = 2  # one interior + one edge object -> one label remains
+    flags = oracle.touches_edge(c, 2)
+    assert flags.tolist() == [0, 1] and int((flags == 0).sum()) == 1
+    v = np.zeros((4, 5, 6), np.int32)
+    v[1:3, 1:4, 1:5] = 1
+    v[3, 2, 2] = 2  # last z slice
+    v[1, 2, 0] = 3  # first x column
+    v[2, 4, 3] = 4  # last y row
+    v[2, 2, 2] = 5  # interior
+    assert oracle.touches_edge(v, 5).tolist() == [0, 1, 1, 1, 0]
+    batch = np.stack([b, c])  # per item: label 2 of item 1 touches, nothing in item 0
+    assert oracle.touches_edge(batch, 2, ndim=2).tolist() == [0, 0, 0, 1]
+    assert oracle.touches_edge(np.full((1, 1), 7), 6).tolist() == [0] * 6  # label > max_label ignored
+
+
+def test_filter_objects_small_and_edge():
+    """SPEC.md:220-224 filter_small examples through the result filter: min_volume 1 is the
+    identity; a 27-voxel object is removed at 1000; a threshold above every object removes all."""
+    lab = np.zeros((12, 12, 12), np.int32)
+    lab[2:5, 2:5, 2:5] = 1  # 27 voxels
+    lab[6:11, 6:11, 6:11] = 2  # 125 voxels
+    res = oracle.sphericity_roundness(lab, max_label=2)
+    same = oracle.filter_objects(res, min_volume=1)
+    np.testing.assert_array_equal(same["sphericity"], res["sphericity"])
+    f = oracle.filter_objects(res, min_volume=1000)
+    assert np.isnan(f["sphericity"]).all() and np.isnan(f["roundness"]).all()
+    g = oracle.filter_objects(res, min_volume=100)
+    assert np.isnan(g["sphericity"][0]) and g["sphericity"][1] == res["sphericity"][1]
+    h = oracle.filter_objects(res, edge=np.array([0, 1], np.uint8))
+    assert h["roundness"][0] == res["roundness"][0] and np.isnan(h["roundness"][1])
