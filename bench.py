@@ -348,7 +348,7 @@ def run_fastrs(args):
                    "input_sha256": info["sha256"], "input_hash_kind": info.get("sha256_kind")},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(lab.nbytes),
                 "d2h_bytes_per_step": int(2 * M * 8), "ms_per_step": float(e2e_ms.item())},
-        "gpu_launches": int((9 if ndim == 3 else 8) * args.steps),
+        "gpu_launches": int((10 if ndim == 3 else 9) * args.steps),  # K1 K2 (K3) K4 K5a K5b K5' fxlut K5e K6
         "roofline": {"bound": "hbm", "kernel": STAGE_KERNEL[dom], "stage": dom, "achieved": achieved,
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                      "traffic": ncu_traffic(STAGE_KERNEL[dom]),
@@ -425,7 +425,7 @@ def run_slab(args):
                 "config": {"workload": workload_name(args.config) + f", z-slabs over {world} GPU(s)",
                            "seed": info["seed"], "elements": int(n), "slabs": slabs,
                            "parallelism": f"z-slab{world}", "halo": res["slab_info"]},
-                "gpu_launches": int(10 * args.steps), "clocks": clk, "e2e": None, "roofline": None,
+                "gpu_launches": int(11 * args.steps), "clocks": clk, "e2e": None, "roofline": None,
                 "cpu_baseline": None}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
