@@ -71,8 +71,10 @@ enum {
                                     fixed-point integers, bit-identical across runs     */
   FASTRS_ASYNC = 4u,             /* do not synchronise the stream at the end of the call  */
   FASTRS_HOST_IO = 8u,           /* size the workspace for fastrs_sphericity_roundness_host */
-  FASTRS_FORCE_FALLBACK = 16u    /* run K5 with the atomic sparse-table kernel on every tile
+  FASTRS_FORCE_FALLBACK = 16u,   /* run K5 with the atomic sparse-table kernel on every tile
                                     (a GPU-internal cross-check of the default dilation)    */
+  FASTRS_EDGE_SKIP_ZLO = 32u,    /* fastrs_touches_edge on a z-slab (3D): its first slice is  */
+  FASTRS_EDGE_SKIP_ZHI = 64u     /* not a grid face / its last slice is not (slab path)      */
 };
 
 /* Optional per-label statistics (device pointers, each nullable, batch*max_label long). */
@@ -219,8 +221,9 @@ FASTRS_API int fastrs_metrics_from_partials(const uint64_t* vol, const uint64_t*
  * lies on the boundary of its grid item (any face in 3D, any edge in 2D), else 0 (PAPER.md:195
  * "Edge cells are removed"; SPEC.md:212 remove_edge_objects).  labels as in
  * fastrs_sphericity_roundness (device); touches_edge: device, batch*max_label bytes, written in
- * full.  Labels outside 1..max_label are ignored.  Errors: EINVAL (geometry, NULL, max_label < 1),
- * ECUDA.  Synchronises `stream` at the end unless flags has FASTRS_ASYNC.
+ * full.  Labels outside 1..max_label are ignored.  FASTRS_EDGE_SKIP_ZLO / _ZHI leave out the first /
+ * last z slice (a z-slab's inner faces; the slab path ORs the slabs' flags).  Errors: EINVAL
+ * (geometry, NULL, max_label < 1), ECUDA.  Synchronises `stream` at the end unless FASTRS_ASYNC.
  * fastrs_filter_objects: sets sphericity[i] and roundness[i] (either may be NULL) to NaN where
  * volume[i] < min_volume ("the smallest objects are filtered out (V < 10^3)";
  * SPEC.md:219 filter_small) when volume != NULL, or where touches_edge[i] != 0 when touches_edge

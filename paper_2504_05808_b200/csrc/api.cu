@@ -553,7 +553,8 @@ int fastrs_touches_edge(const int32_t* labels, const int64_t* dims, int ndim, in
   if (!labels || !touches_edge) return fail(FASTRS_EINVAL, "NULL pointer");
   if (max_label < 1) return fail(FASTRS_EINVAL, "max_label must be >= 1");
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = launch_touch_edge(labels, g, max_label, touches_edge, st);
+  cudaError_t e = launch_touch_edge(labels, g, max_label, touches_edge, (flags & kFlagEdgeSkipZlo) && g.ndim == 3,
+                                    (flags & kFlagEdgeSkipZhi) && g.ndim == 3, st);
   if (e == cudaSuccess && !(flags & kFlagAsync)) e = cudaStreamSynchronize(st);
   return e == cudaSuccess ? FASTRS_OK : cuda_fail(e, "touches_edge");
 }

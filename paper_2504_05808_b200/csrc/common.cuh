@@ -16,6 +16,7 @@ constexpr uint32_t kBitZ = 0x40000000u;  // element is the first of its z-run
 constexpr uint32_t kStBadLabel = 1u, kStNoSite = 2u, kStInternal = 4u, kStShell = 8u;
 
 constexpr uint32_t kFlagBorder = 1u, kFlagAsync = 4u, kFlagHostIO = 8u, kFlagForceFallback = 16u;
+constexpr uint32_t kFlagEdgeSkipZlo = 32u, kFlagEdgeSkipZhi = 64u;
 
 // ---- dilation / pruning tiles ---------------------------------------------------------
 // 3D tile 32 x 8 x 8 (x fastest), 2D tile 32 x 64; both 64 rows of 32 = 2048 elements.
@@ -172,7 +173,7 @@ void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, co
                      float* lt_out, const uint32_t* ltp, unsigned long long* fxlut, WsHeader* hdr, cudaStream_t st, bool chunked = false);
 constexpr size_t kFxLutBytes = 65536 * 8;  // workspace for the epilogue's fixed-point sqrt table
 cudaError_t launch_touch_edge(const int32_t* labels, const Geom& g, int32_t max_label, uint8_t* touch,
-                              cudaStream_t st);
+                              bool skip_zlo, bool skip_zhi, cudaStream_t st);
 cudaError_t launch_filter(double* sph, double* rnd, const int64_t* vol, const uint8_t* touch, int64_t n,
                           int64_t min_volume, cudaStream_t st);
 void launch_metrics(const Accum& acc, const Geom& g, const Outputs& o, WsHeader* hdr,

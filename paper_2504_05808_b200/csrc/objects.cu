@@ -13,7 +13,7 @@ namespace {
 // (Z*X), x = 0, X-1 (Z*Y); 2D edges y = 0, Y-1 (X each), x = 0, X-1 (Y each).  Elements on
 // several faces are visited more than once (harmless: every write stores 1).
 __global__ void k_touch_edge(const int32_t* __restrict__ lab, Geom g, int32_t max_label, int64_t per_item,
-                             uint8_t* __restrict__ touch) {
+                             int skip_zlo, int skip_zhi, uint8_t* __restrict__ touch) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= per_item * g.B) return;
   const int64_t b = t / per_item;
@@ -23,6 +23,7 @@ __global__ void k_touch_edge(const int32_t* __restrict__ lab, Geom g, int32_t ma
   if (g.ndim == 3) {
     if (r < 2 * Y * X) {
       z = r < Y * X ? 0 : Z - 1;
+      if ((r < Y * X && skip_zlo) || (r >= Y * X && skip_zhi)) return;  // a slab's inner face
       r %= Y * X;
       y = r / X;
       x = r % X;
@@ -67,12 +68,14 @@ __global__ void k_filter(double* __restrict__ sph, double* __restrict__ rnd, con
 }  // namespace
 
 cudaError_t launch_touch_edge(const int32_t* labels, const Geom& g, int32_t max_label, uint8_t* touch,
-                              cudaStream_t st) {
+                              bool skip_zlo, bool skip_zhi, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(touch, 0, (size_t)g.B * (size_t)max_label, st);
   if (e != cudaSuccess) return e;
   const int64_t per_item = g.ndim == 3 ? 2 * (g.Y * g.X + g.Z * g.X + g.Z * g.Y) : 2 * (g.X + g.Y);
   const int64_t n = per_item * g.B;
-  if (n > 0) k_touch_edge<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(labels, g, max_label, per_item, touch);
+  if (n > 0)
+    k_touch_edge<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(labels, g, max_label, per_item, skip_zlo ? 1 : 0,
+                                                             skip_zhi ? 1 : 0, touch);
   return cudaGetLastError();
 }
 

@@ -346,13 +346,17 @@ def metrics_from_partials(part: dict, ndim: int, nscale: int, dmax_global: int, 
     return res
 
 
-def touches_edge(labels: torch.Tensor, max_label: int, ndim=None) -> torch.Tensor:
+EDGE_SKIP_ZLO, EDGE_SKIP_ZHI = 32, 64
+
+
+def touches_edge(labels: torch.Tensor, max_label: int, ndim=None, flags: int = 0) -> torch.Tensor:
     """uint8 flags (batch*max_label): 1 where a label has an element on its item's grid boundary
-    (fastrs_touches_edge; PAPER.md:195, SPEC.md:212)."""
+    (fastrs_touches_edge; PAPER.md:195, SPEC.md:212).  flags: EDGE_SKIP_ZLO / EDGE_SKIP_ZHI for a
+    z-slab whose first / last slice is not a face of the whole volume."""
     labels = _labels_arg(labels)
     ndim, b, dims = _geometry(labels.shape, ndim, None)
     out = torch.empty(b * int(max_label), dtype=torch.uint8, device=labels.device)
-    _check(load().fastrs_touches_edge(labels.data_ptr(), dims, ndim, b, int(max_label), out.data_ptr(), 0,
+    _check(load().fastrs_touches_edge(labels.data_ptr(), dims, ndim, b, int(max_label), out.data_ptr(), int(flags),
                                       _stream(labels.device)))
     return out
 

@@ -122,6 +122,10 @@ class GpuPhases:
     def metrics(self, part, nscale, dmax, stats):
         return self.F.metrics_from_partials(part, 3, nscale, dmax, stats=stats)
 
+    def edge(self, labels, max_label, skip_zlo, skip_zhi):
+        return self.F.touches_edge(labels, max_label, flags=(self.F.EDGE_SKIP_ZLO if skip_zlo else 0)
+                                   | (self.F.EDGE_SKIP_ZHI if skip_zhi else 0))
+
 
 def sphericity_roundness_slab(labels_slab: torch.Tensor, slabs, max_label: int, flags: int = 1, group=None,
                               phases=None, stats: bool = False) -> dict:
@@ -165,6 +169,19 @@ def sphericity_roundness_slab(labels_slab: torch.Tensor, slabs, max_label: int, 
     info.update(h=h, H=H, dmax=dmax, halo_slices=int(lo_p.shape[0] + hi_p.shape[0] + lo_d.shape[0] + hi_d.shape[0]))
     res["slab_info"] = info
     return res
+
+
+def touches_edge_slab(labels_slab: torch.Tensor, slabs, max_label: int, group=None, phases=None) -> torch.Tensor:
+    """Collective: edge-object flags of the whole volume from z-slabs — every rank
+    flags the labels on its slab's faces that are faces of the volume (its first / last slice
+    only on the first / last rank), then allreduce(max).  Returns max_label uint8 flags."""
+    phases = phases or GpuPhases()
+    rank = dist.get_rank(group)
+    z0, z1 = slabs[rank]
+    Z = slabs[-1][1]
+    f = phases.edge(labels_slab, max_label, z0 > 0, z1 < Z).to(torch.int32)
+    dist.all_reduce(f, op=dist.ReduceOp.MAX, group=group)
+    return f.to(torch.uint8)
 
 
 def simulate_slabs(labels: torch.Tensor, nranks: int, max_label: int, flags: int = 1, stats: bool = False,

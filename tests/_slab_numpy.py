@@ -174,3 +174,19 @@ class NumpyPhases:
             res["n_shell"] = torch.from_numpy(nsh.astype(np.int64))
             res["max_lt2"] = part["max_lt2"].clone()
         return res
+
+    def edge(self, labels, max_label, skip_zlo, skip_zhi):
+        """Labels on the slab's faces that are faces of the volume (brute force)."""
+        lab = labels.numpy()
+        out = np.zeros(max_label, np.uint8)
+        faces = [lab[:, 0, :], lab[:, -1, :], lab[:, :, 0], lab[:, :, -1]]
+        if not skip_zlo:
+            faces.append(lab[0])
+        if not skip_zhi:
+            faces.append(lab[-1])
+        for f in faces:
+            for L in np.unique(f):
+                if 1 <= L <= max_label:
+                    out[L - 1] = 1
+        return torch.from_numpy(out)
+

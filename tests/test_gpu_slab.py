@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 import torch
 
+import oracle
 import synth
 from paper_2504_05808_b200 import fastrs, slab
 
@@ -75,3 +76,26 @@ def test_slab_phase_argument_errors():
     with pytest.raises(fastrs.FastrsError) as e:  # extended slab outside the grid
         fastrs.slab_edt_z(packed, 0, 32, 8, 32)
     assert e.value.name == "EINVAL"
+
+
+def test_touches_edge_slabs_or_to_the_volume_flags():
+    """Edge flags from z-slabs (inner slab faces skipped) OR-ed together equal the flags of the
+    whole volume (what slab.touches_edge_slab's allreduce(max) computes across ranks)."""
+    rng = np.random.default_rng(12)
+    lab = np.zeros((64, 40, 48), np.int32)
+    for k in range(1, 81):  # boxes anywhere: some on faces, some across slab boundaries
+        sz = rng.integers(1, 7, 3)
+        lo = [int(rng.integers(0, n - w + 1)) for n, w in zip(lab.shape, sz)]
+        lab[lo[0]:lo[0] + sz[0], lo[1]:lo[1] + sz[1], lo[2]:lo[2] + sz[2]] = k
+    ml = 80
+    t = torch.from_numpy(lab).cuda()
+    want = fastrs.touches_edge(t, ml)
+    assert 0 < int(want.sum()) < ml
+    slabs = slab.partition(lab.shape[0], 5)
+    acc = torch.zeros_like(want)
+    for z0, z1 in slabs:
+        f = fastrs.touches_edge(t[z0:z1].contiguous(), ml,
+                                flags=(fastrs.EDGE_SKIP_ZLO if z0 > 0 else 0) | (fastrs.EDGE_SKIP_ZHI if z1 < lab.shape[0] else 0))
+        acc = torch.maximum(acc, f)
+    np.testing.assert_array_equal(acc.cpu().numpy(), want.cpu().numpy())
+    np.testing.assert_array_equal(want.cpu().numpy(), oracle.touches_edge(lab, ml))

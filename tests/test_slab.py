@@ -99,6 +99,32 @@ def _worker(rank, world, port, lab, max_label, flags, shrink, out_dir):
         dist.destroy_process_group()
 
 
+def _edge_worker(rank, world, port, lab, max_label, out_dir):
+    dist.init_process_group("gloo", rank=rank, world_size=world, init_method=f"tcp://127.0.0.1:{port}")
+    try:
+        slabs = slab.partition(lab.shape[0], world)
+        z0, z1 = slabs[rank]
+        f = slab.touches_edge_slab(torch.from_numpy(lab[z0:z1].copy()), slabs, max_label, phases=NumpyPhases())
+        if rank == 0:
+            np.save(os.path.join(out_dir, "edge.npy"), f.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_touches_edge_slab_gloo_matches_oracle(world, tmp_path):
+    """Edge-object flags from z-slabs (inner slab faces skipped, allreduce max) equal the oracle's
+    flags on the whole volume; labels that touch only an inner slab face stay unflagged."""
+    lab = _volume(seed=world)
+    lab[15, 10, 10] = 9  # interior voxel on the slab boundary region
+    ml = int(lab.max())
+    mp.start_processes(_edge_worker, args=(world, _free_port(), lab, ml, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    got = np.load(os.path.join(tmp_path, "edge.npy"))
+    np.testing.assert_array_equal(got, oracle.touches_edge(lab, ml))
+    assert got[8] == 0
+
+
 def _run(world, lab, max_label, flags, tmp_path, shrink=False):
     mp.start_processes(_worker, args=(world, _free_port(), lab, max_label, flags, shrink, str(tmp_path)),
                        nprocs=world, join=True, start_method="spawn")
