@@ -623,7 +623,7 @@ int fastrs_slab_edt_xy(const int32_t* labels, const int32_t* labels_below, const
                        void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   Geom g;
-  SlabLayout L;
+  SlabLayout L{};
   WsHeader* hdr = nullptr;
   int rc = slab_prologue(dims, g, L, ws, ws_bytes, hdr, st);
   if (rc) return rc;
@@ -642,7 +642,7 @@ int fastrs_slab_edt_z(const uint32_t* packed_ext, const int64_t* dims_ext, int64
                       size_t ws_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   Geom g;
-  SlabLayout L;
+  SlabLayout L{};
   WsHeader* hdr = nullptr;
   int rc = slab_prologue(dims_ext, g, L, ws, ws_bytes, hdr, st);
   if (rc) return rc;
@@ -661,7 +661,7 @@ int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64
                        void* ws, size_t ws_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   Geom g;
-  SlabLayout L;
+  SlabLayout L{};
   WsHeader* hdr = nullptr;
   int rc = slab_prologue(dims_ext, g, L, ws, ws_bytes, hdr, st);
   if (rc) return rc;

@@ -77,7 +77,6 @@ template <bool IS3D>
 struct Shape {
   static constexpr int TY = IS3D ? 8 : 64, TZ = IS3D ? 8 : 1;
   static constexpr int GX = IS3D ? 1 : 2, GY = 2, GZ = IS3D ? 2 : 1;  // tiles per group
-  static constexpr int RX = GX * kTX, RY = GY * TY, RZ = GZ * TZ;     // group box
 };
 
 __device__ __forceinline__ unsigned long long pack(int x, int y, int z, uint32_t D) {
@@ -327,19 +326,6 @@ __device__ __forceinline__ void uncovered_range(uint32_t u, int& lo, int& hi) {
   hi = u ? 31 - __clz(u) : -(1 << 14);
 }
 
-// position of the n-th (0-based) set bit of m (requires popc(m) > n)
-__device__ __forceinline__ int nth_bit(uint32_t m, int n) {
-  int pos = 0, c = __popc(m & 0xFFFFu);
-  if (n >= c) { n -= c; m >>= 16; pos += 16; }
-  c = __popc(m & 0xFFu);
-  if (n >= c) { n -= c; m >>= 8; pos += 8; }
-  c = __popc(m & 0xFu);
-  if (n >= c) { n -= c; m >>= 4; pos += 4; }
-  c = __popc(m & 0x3u);
-  if (n >= c) { n -= c; m >>= 2; pos += 2; }
-  return pos + (n >= (int)(m & 1u) ? 1 : 0);
-}
-
 // 64-bit mask of the tile rows (row = lz*TY + ly) inside [ya,yb] x [za,zb]
 template <bool IS3D>
 __device__ __forceinline__ unsigned long long row_box(int ya, int yb, int za, int zb) {
@@ -384,7 +370,6 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
   const int64_t gzi = t % ngz;
   const int64_t b = t / ngz;
   const int64_t tx0 = gxi * P::GX, ty0 = gyi * P::GY, tz0 = g.tz_lo + gzi * P::GZ;
-  const int64_t rox = tx0 * kTX, roy = ty0 * TY, roz = tz0 * TZ;  // group origin
   const int wx = warp % P::GX, wy = (warp / P::GX) % P::GY, wz = warp / (P::GX * P::GY);
   const int64_t mtx = tx0 + wx, mty = ty0 + wy, mtz = tz0 + wz;
   const bool have_tile = mtx < g.ntx && mty < g.nty && mtz < g.tz_hi;
@@ -684,7 +669,7 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
   uncovered_range(f0, ul0, uh0);
   uncovered_range(f1, ul1, uh1);
   const int ly0 = IS3D ? (lane & 7) : lane, lz0 = IS3D ? (lane >> 3) : 0;
-  const int ly1 = IS3D ? ly0 : lane + 32, lz1 = IS3D ? lz0 + 4 : 0;
+  const int ly1 = IS3D ? ly0 : lane + 32;  // row lane + 32 lies 4 layers above row lane in 3D
   // rows of my tile that still hold uncovered foreground, per 8-column chunk of x
   unsigned long long Uc[4];
 #pragma unroll
