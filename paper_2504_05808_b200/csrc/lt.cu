@@ -245,11 +245,12 @@ __global__ void __launch_bounds__(256) k_epilogue(const int32_t* __restrict__ la
   const uint16_t* ltp16 = reinterpret_cast<const uint16_t*>(ltp);
   const int X = (int)g.X;
   uint32_t bad = 0;
-  for (int x0 = 0; x0 < X; x0 += 128) {
-    int32_t L[4];
-    uint32_t d[4], c[4];
+  constexpr int kEpiChunks = 8;  // 32-element chunks in flight per warp
+  for (int x0 = 0; x0 < X; x0 += 32 * kEpiChunks) {
+    int32_t L[kEpiChunks];
+    uint32_t d[kEpiChunks], c[kEpiChunks];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kEpiChunks; ++k) {
       const int x = x0 + 32 * k + lane;
       const bool in = x < X;
       L[k] = in ? __ldg(lab + base + x) : 0;
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(256) k_epilogue(const int32_t* __restrict__ la
       c[k] = (in && L[k] != 0) ? (wide ? __ldg(ltp + base + x) : (uint32_t)__ldg(ltp16 + base + x)) : 0u;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kEpiChunks; ++k) {
       if (x0 + 32 * k >= X) break;  // warp-uniform
       bad |= row_epilogue_v<FAST>(c[k], L[k], d[k], lane, base + x0 + 32 * k + lane, b, acc, do_reduce, scale, lt2_out,
                             lt_out, fxlut);
