@@ -1,3 +1,6 @@
+"""Host->device copy bandwidth from pinned memory (4 GiB of int32, one or two streams, whole or in
+16 chunks): the floor of the host-buffer (e2e) path, which must move the label volume over PCIe.
+usage: python tools/h2d_probe.py"""
 import torch, time
 n = 1 << 30
 h = torch.empty(n, dtype=torch.int32).pin_memory()
