@@ -59,7 +59,7 @@ int make_geom(const int64_t* dims, int ndim, int64_t batch, Geom& g) {
 inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t hdr, A, B, meta, fgm, oct, fbl, gcount, goff, pool, fxl, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd, total;
+  size_t hdr, A, B, meta, fgm, oct, fbl, gcount, goff, pool, fxl, sat, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd, total;
 };
 
 Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
@@ -82,6 +82,7 @@ Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
   L.goff = take((size_t)dilate_groups(g) * 4);
   L.pool = take((size_t)dilate_pool_entries(g) * 8);
   L.fxl = take(kFxLutBytes);
+  L.sat = take((size_t)col_blocks(g) * 4);
   L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
   L.vol = take(M * 8);
   L.nsh = take(M * 8);
@@ -162,6 +163,7 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
   uint32_t* B = (uint32_t*)(w + L.B);
   TileMeta* meta = (TileMeta*)(w + L.meta);
   uint2* cent = (uint2*)(w + L.cent);
+  uint32_t* sat = (uint32_t*)(w + L.sat);
   const bool border = (flags & kFlagBorder) != 0;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -194,13 +196,13 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
   uint32_t* D;
   if (g.ndim == 2) {
     D = stage == kEdtOnly ? d2_out : B;
-    launch_edt_col(A, D, g, 1, true, border, hdr, st);
+    launch_edt_col(A, D, g, 1, true, border, hdr, sat, st);
     tm.mark(1);
   } else {
-    launch_edt_col(A, B, g, 1, false, border, hdr, st);
+    launch_edt_col(A, B, g, 1, false, border, hdr, sat, st);
     tm.mark(1);
     D = stage == kEdtOnly ? d2_out : A;
-    launch_edt_col(B, D, g, 2, true, border, hdr, st);
+    launch_edt_col(B, D, g, 2, true, border, hdr, sat, st);
     tm.mark(2);
   }
   if (stage != kEdtOnly) {
@@ -269,7 +271,7 @@ int finish_call(WsHeader* hdr, uint32_t flags, cudaStream_t st) {
 }
 
 struct SlabLayout {
-  size_t hdr, P, meta, fgm, oct, fbl, gcount, goff, pool, fxl, cent, total;
+  size_t hdr, P, meta, fgm, oct, fbl, gcount, goff, pool, fxl, sat, cent, total;
 };
 SlabLayout make_slab_layout(const Geom& g) {
   SlabLayout L{};
@@ -289,6 +291,7 @@ SlabLayout make_slab_layout(const Geom& g) {
   L.goff = take((size_t)dilate_groups(g) * 4);
   L.pool = take((size_t)dilate_pool_entries(g) * 8);
   L.fxl = take(kFxLutBytes);
+  L.sat = take((size_t)col_blocks(g) * 4);
   L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
   L.total = off;
   return L;
@@ -347,6 +350,7 @@ int run_host_pipelined(const int32_t* labels_host, int32_t* dlab, const Geom& g,
   unsigned long long* pool = (unsigned long long*)(w + L.pool);
   uint32_t* gcount = (uint32_t*)(w + L.gcount);
   uint32_t* goff = (uint32_t*)(w + L.goff);
+  uint32_t* sat = (uint32_t*)(w + L.sat);
   const bool border = (flags & kFlagBorder) != 0;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -390,11 +394,11 @@ int run_host_pipelined(const int32_t* labels_host, int32_t* dlab, const Geom& g,
       make_geom(cd, 3, 1, gc);
       launch_edt_x(dlab + z0 * YX, z0 > 0 ? dlab + (z0 - 1) * YX : nullptr, A + z0 * YX, gc, max_label, border, hdr,
                    st);
-      launch_edt_col(A + z0 * YX, B + z0 * YX, gc, 1, false, border, hdr, st);
+      launch_edt_col(A + z0 * YX, B + z0 * YX, gc, 1, false, border, hdr, sat, st);
     }
     if (step >= 1 && step - 1 < nc) {  // K3 on chunk step-1: D into A
       zr(step - 1, z0, z1);
-      launch_edt_col(B, A + z0 * YX, g, 2, true, border, hdr, st, z0, z1);
+      launch_edt_col(B, A + z0 * YX, g, 2, true, border, hdr, sat, st, z0, z1);
     }
     if (step >= 2 && step - 2 < nc) {  // K4 on chunk step-2
       zr(step - 2, z0, z1);
@@ -631,7 +635,7 @@ int fastrs_slab_edt_xy(const int32_t* labels, const int32_t* labels_below, const
   uint32_t* tmp = (uint32_t*)((char*)ws + L.P);
   const bool border = (flags & kFlagBorder) != 0;
   launch_edt_x(labels, labels_below, tmp, g, max_label > 0 ? max_label : INT32_MAX, border, hdr, st);
-  launch_edt_col(tmp, packed_out, g, 1, false, border, hdr, st);
+  launch_edt_col(tmp, packed_out, g, 1, false, border, hdr, (uint32_t*)((char*)ws + L.sat), st);
   rc = header_word_out(hdr, &hdr->dxymax, dxy_max, st);
   if (rc) return rc;
   return finish_call(hdr, flags, st);
@@ -649,7 +653,8 @@ int fastrs_slab_edt_z(const uint32_t* packed_ext, const int64_t* dims_ext, int64
   if (!packed_ext || !d_out) return fail(FASTRS_EINVAL, "NULL pointer");
   if (own_lo < 0 || own_hi > g.Z || own_lo >= own_hi || z_ext0 < 0 || z_ext0 + g.Z > Z)
     return fail(FASTRS_EINVAL, "slab range outside the extended slab / the grid");
-  launch_edt_col(packed_ext, d_out, g, 2, true, (flags & kFlagBorder) != 0, hdr, st, own_lo, own_hi, z_ext0, Z);
+  launch_edt_col(packed_ext, d_out, g, 2, true, (flags & kFlagBorder) != 0, hdr, (uint32_t*)((char*)ws + L.sat), st, own_lo,
+                 own_hi, z_ext0, Z);
   rc = header_word_out(hdr, &hdr->dmax, dmax_out, st);
   if (rc) return rc;
   return finish_call(hdr, flags, st);

@@ -62,6 +62,7 @@ struct WsHeader {
   uint32_t scale_set;    // host pipeline: s + 1 of the per-chunk epilogues (0xFFFFFFFF: they differed)
   uint32_t epi_skipped;  // host pipeline: a per-chunk epilogue saw fallback tiles and did nothing
   uint32_t paint_next;   // K5b work counter (reset before each launch)
+  uint32_t sat_n;        // K2/K3: CTAs listed for the exact 32-bit column pass (reset per launch)
 };
 static_assert(sizeof(WsHeader) <= 256, "header");
 
@@ -143,9 +144,12 @@ void launch_edt_x(const int32_t* labels, const int32_t* labels_below, uint32_t* 
 // Column pass along axis 1 (y) or 2 (z) of g.  Positions [p_lo, p_hi) of the axis are written,
 // to out + (p - p_lo) * stride; gofs / Lg: global position of local 0 and the global axis length
 // (the border convention applies at global 0 and Lg).  Default: p_lo = 0, p_hi = L, gofs = 0.
+// satlist: workspace list of col_blocks(g) u32 for the CTAs the 16-bit kernel hands to the exact
+// 32-bit kernel (NULL: the 32-bit kernel everywhere).
 void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, bool final_pass,
-                    bool border, WsHeader* hdr, cudaStream_t st, int64_t p_lo = 0, int64_t p_hi = -1,
-                    int64_t gofs = 0, int64_t Lg = -1);
+                    bool border, WsHeader* hdr, uint32_t* satlist, cudaStream_t st, int64_t p_lo = 0,
+                    int64_t p_hi = -1, int64_t gofs = 0, int64_t Lg = -1);
+int64_t col_blocks(const Geom& g);  // column-pass CTAs of the larger of the y / z passes
 cudaError_t ensure_mtables(int device);  // builds the per-device lattice tables (sync, once)
 // K4; also writes per tile the foreground row masks (fgm: kRows u32) and the number of kept
 // entries with D bucket >= 8o for o = 0..15 (oct: 16 u16) used by K5's gather

@@ -12,12 +12,13 @@
 //              g = (distance to the nearest run end's neighbour)^2.  Fused: label
 //              validation (a1) and the y/z run-start flags packed into bits 31/30 (S2), so
 //              later passes never re-read labels.
-//   K2/K3    : column passes along y / z.  A CTA stages a [256 + 2*32][32] column tile of
-//              packed words in shared memory (coalesced 128-byte rows) and each thread runs
-//              the exact windowed scan  best = min(best, g(p +- dq) + dq^2)  until dq^2 >=
-//              best or a run end (a site at distance dq) is met; reads outside the staged
-//              window fall back to global (L2).  The final pass emits D, Dmax, n_fg and
-//              flags elements with no site (ENOSITE).
+//   K2/K3    : column passes along y / z.  A CTA stages a [256 + 2*48][32] column tile in
+//              shared memory (coalesced 128-byte rows) and each thread runs the exact
+//              windowed scan  best = min(best, g(p +- dq) + dq^2)  until dq^2 >= best; the
+//              default kernel packs both scan directions into u16 halves (one
+//              VIADDMNMX.U16x2 per row pair, run ends folded into the staged values) and
+//              hands CTAs with values >= 2^14-1 to the exact 32-bit kernel.  The final pass
+//              emits D, Dmax, n_fg and flags elements with no site (ENOSITE).
 #include "common.cuh"
 
 namespace fastrs {
@@ -103,13 +104,13 @@ constexpr int kColS = 256;  // positions per CTA
 constexpr int kColH = 48;   // staged halo on each side
 constexpr int kColRows = kColS + 2 * kColH;
 constexpr int kColWarps = 8;
-constexpr int kScanU = 4;  // rows per iteration of the hoisted scan loops (C4 y/z ms: 1: 7.33/6.19, 2: 6.45/5.55, 4: 6.20/5.50, 6: 6.27/5.61, 8: 6.34/5.80)
+constexpr int kScan16U = 4;  // row pairs per iteration of the 16-bit two-sided scan loop
 
 // Slow path of the column scan for an element whose window leaves the staged rows: the same
-// exact scan, reading beyond the window from global memory (L2).
+// exact scan in 32-bit arithmetic, every read from global memory (L2).
 __device__ __noinline__ uint32_t scan_global(const uint32_t* __restrict__ in, int64_t base, int64_t astride, int64_t p,
-                                             int64_t L, int64_t lo, int64_t hi, const uint32_t* tile, int lane,
-                                             uint32_t v, uint32_t chbit, int border, int64_t gofs, int64_t Lg) {
+                                             int64_t L, uint32_t v, uint32_t chbit, int border, int64_t gofs,
+                                             int64_t Lg) {
   uint32_t best = v & kMask;
   {
     uint32_t dq = 1, dq2 = 1;
@@ -119,7 +120,7 @@ __device__ __noinline__ uint32_t scan_global(const uint32_t* __restrict__ in, in
         if (border && gofs + q >= Lg) best = min(best, dq2);
         break;
       }
-      const uint32_t w = q < hi ? tile[(q - lo) * 32 + lane] : __ldg(in + base + q * astride);
+      const uint32_t w = __ldg(in + base + q * astride);
       if (w & chbit) {
         best = min(best, dq2);
         break;
@@ -138,7 +139,7 @@ __device__ __noinline__ uint32_t scan_global(const uint32_t* __restrict__ in, in
         if (gofs + q >= 0 || border) best = min(best, dq2);
         break;
       }
-      const uint32_t w = q >= lo ? tile[(q - lo) * 32 + lane] : __ldg(in + base + q * astride);
+      const uint32_t w = __ldg(in + base + q * astride);
       best = min(best, (w & kMask) + dq2);
       chk = w & chbit;
       dq2 += 2 * dq + 1;
@@ -149,22 +150,37 @@ __device__ __noinline__ uint32_t scan_global(const uint32_t* __restrict__ in, in
   return best;
 }
 
+struct ColArgs {
+  const uint32_t* in;
+  uint32_t* out;
+  int64_t L, astride;
+  int X, nxb, nseg;
+  int64_t n_inner, inner_mult, outer_mult;
+  uint32_t chbit;
+  int border;
+  int64_t p_lo, p_hi, gofs, Lg;
+};
+
+// ---- exact 32-bit column pass (one CTA = 256 positions x 32 columns) --------------------
+// The CTA stages a [256 + 2*48] x 32 column tile of packed words and each thread runs the
+// exact windowed scan  best = min(best, g(p +- dq) + dq^2)  until dq^2 >= best or a run end
+// (a site at distance dq); reads outside the staged window go to global (L2).  Runs for the
+// CTAs listed by the 16-bit kernel below (saturated values), or for every CTA when listed
+// is NULL.
 template <bool FINAL>
-__global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
-                                                 int64_t L, int64_t astride, int X, int nxb, int nseg,
-                                                 int64_t n_inner, int64_t inner_mult, int64_t outer_mult,
-                                                 uint32_t chbit, int border, int64_t p_lo, int64_t p_hi,
-                                                 int64_t gofs, int64_t Lg, WsHeader* __restrict__ hdr) {
-  __shared__ uint32_t tile[kColRows * 32];
-  int64_t bid = blockIdx.x;
-  const int xb = (int)(bid % nxb);
-  bid /= nxb;
-  const int seg = (int)(bid % nseg);
-  const int64_t outer = bid / nseg;
+__device__ __forceinline__ void col32_body(const ColArgs& a, int64_t bid, uint32_t* tile, WsHeader* __restrict__ hdr) {
+  const uint32_t* __restrict__ in = a.in;
+  const int64_t L = a.L, astride = a.astride;
+  const uint32_t chbit = a.chbit;
+  const int border = a.border;
+  const int xb = (int)(bid % a.nxb);
+  bid /= a.nxb;
+  const int seg = (int)(bid % a.nseg);
+  const int64_t outer = bid / a.nseg;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t base = (outer / n_inner) * outer_mult + (outer % n_inner) * inner_mult + (int64_t)xb * 32 + lane;
-  const bool xin = xb * 32 + lane < X;
-  const int64_t s0 = p_lo + (int64_t)seg * kColS;
+  const int64_t base = (outer / a.n_inner) * a.outer_mult + (outer % a.n_inner) * a.inner_mult + (int64_t)xb * 32 + lane;
+  const bool xin = xb * 32 + lane < a.X;
+  const int64_t s0 = a.p_lo + (int64_t)seg * kColS;
   const int64_t lo = s0 - kColH > 0 ? s0 - kColH : 0;
   const int64_t hi = s0 + kColS + kColH < L ? s0 + kColS + kColH : L;
   for (int64_t r = lo + warp; r < hi; r += kColWarps)
@@ -172,116 +188,57 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
   __syncthreads();
 
   uint32_t dmax = 0, nfg = 0, nosite = 0;
-  const int64_t pend = s0 + kColS < p_hi ? s0 + kColS : p_hi;
+  const int64_t pend = s0 + kColS < a.p_hi ? s0 + kColS : a.p_hi;
   for (int64_t p = s0 + warp; p < pend; p += kColWarps) {
     const uint32_t v = tile[(p - lo) * 32 + lane];
     const uint32_t g = v & kMask;
     uint32_t res = FINAL ? 0u : v;
     if (xin && g != 0) {
       uint32_t best = g;
-      // Fast path: pure shared-memory scan in 32-bit indices.  up side: rows p+1, p+2, ... until a
-      // run end (the element there is a site) or dq^2 >= best; leaving the staged rows before
-      // that hands the element to the slow path below.
       const int i = (int)(p - lo), nt = (int)(hi - lo);
       bool slow = false;
-      // dq^2 < best <= g bounds the scan: when isqrt(g-1) rows exist on a side, that side's loop
-      // needs no window-end check (the common case)
-      const int reach = (int)sqrtf((float)(g - 1)) + 1;  // >= isqrt(g - 1)
-      {
+      {  // up side: rows p+1, p+2, ... until a run end (a site) or dq^2 >= best
         uint32_t dq2 = 1, inc = 3;
         const uint32_t* w_ptr = tile + (i + 1) * 32 + lane;
-        if (reach + kScanU - 1 <= nt - 1 - i) {
-          // kScanU rows per iteration (the staged rows suffice): a row's term is an exact
-          // candidate even when an earlier one made dq^2 >= best
-          while (dq2 < best) {
-            uint32_t w[kScanU];
-#pragma unroll
-            for (int u = 0; u < kScanU; ++u) w[u] = w_ptr[32 * u];
-            bool stop = false;
-#pragma unroll
-            for (int u = 0; u < kScanU; ++u) {
-              if (w[u] & chbit) {
-                best = min(best, dq2);
-                stop = true;
-                break;
-              }
-              best = min(best, (w[u] & kMask) + dq2);
-              dq2 += inc;
-              inc += 2;
-            }
-            if (stop) break;
-            w_ptr += 32 * kScanU;
+        const uint32_t* w_end = tile + nt * 32 + lane;
+        while (dq2 < best) {
+          if (w_ptr >= w_end) {
+            if (hi < L) slow = true;  // more rows exist beyond the staged window
+            else if (border && a.gofs + L >= a.Lg) best = min(best, dq2);  // the grid end
+            break;
           }
-        } else {
-          const uint32_t* w_end = tile + nt * 32 + lane;
-          while (dq2 < best) {
-            if (w_ptr >= w_end) {
-              if (hi < L) slow = true;  // more rows exist beyond the staged window
-              else if (border && gofs + L >= Lg) best = min(best, dq2);  // the grid end
-              break;
-            }
-            const uint32_t w = *w_ptr;
-            if (w & chbit) {
-              best = min(best, dq2);
-              break;
-            }
-            best = min(best, (w & kMask) + dq2);
-            dq2 += inc;
-            inc += 2;
-            w_ptr += 32;
+          const uint32_t w = *w_ptr;
+          if (w & chbit) {
+            best = min(best, dq2);
+            break;
           }
+          best = min(best, (w & kMask) + dq2);
+          dq2 += inc;
+          inc += 2;
+          w_ptr += 32;
         }
       }
-      // down side: rows p-1, p-2, ...; element p-dq lies outside the run iff p-dq+1 starts it
-      {
+      {  // down side: element p-dq lies outside the run iff p-dq+1 starts it
         uint32_t dq2 = 1, inc = 3, chk = v & chbit;
-        const uint32_t* w_ptr = tile + (i - 1) * 32 + lane;
-        if (reach + kScanU - 1 <= i) {
-          while (dq2 < best) {
-            if (chk) {  // the element at p-dq is inside the staged window: a real site
-              best = min(best, dq2);
-              break;
-            }
-            uint32_t w[kScanU];
-#pragma unroll
-            for (int u = 0; u < kScanU; ++u) w[u] = w_ptr[-32 * u];
-            bool stop = false;
-#pragma unroll
-            for (int u = 0; u < kScanU; ++u) {
-              best = min(best, (w[u] & kMask) + dq2);
-              dq2 += inc;
-              inc += 2;
-              chk = w[u] & chbit;
-              if (u + 1 < kScanU && chk) {  // p-dq (now) lies below the run start: a site
-                best = min(best, dq2);
-                stop = true;
-                break;
-              }
-            }
-            if (stop) break;
-            w_ptr -= 32 * kScanU;
+        int r = i - 1;
+        while (dq2 < best) {
+          if (chk) {
+            if (a.gofs + lo + r >= 0 || border) best = min(best, dq2);
+            break;
           }
-        } else {
-          int r = i - 1;
-          while (dq2 < best) {
-            if (chk) {
-              if (gofs + lo + r >= 0 || border) best = min(best, dq2);
-              break;
-            }
-            if (r < 0) {  // lo > 0 here (element 0 of the axis always starts a run)
-              slow = true;
-              break;
-            }
-            const uint32_t w = tile[r * 32 + lane];
-            best = min(best, (w & kMask) + dq2);
-            chk = w & chbit;
-            dq2 += inc;
-            inc += 2;
-            --r;
+          if (r < 0) {  // lo > 0 here (element 0 of the axis always starts a run)
+            slow = true;
+            break;
           }
+          const uint32_t w = tile[r * 32 + lane];
+          best = min(best, (w & kMask) + dq2);
+          chk = w & chbit;
+          dq2 += inc;
+          inc += 2;
+          --r;
         }
       }
-      if (slow) best = scan_global(in, base, astride, p, L, lo, hi, tile, lane, v, chbit, border, gofs, Lg);
+      if (slow) best = scan_global(in, base, astride, p, L, v, chbit, border, a.gofs, a.Lg);
       dmax = max(dmax, best);
       if (FINAL) {
         res = best;
@@ -291,7 +248,7 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
         res = best | (v & (kBitY | kBitZ));
       }
     }
-    if (xin) out[base + (p - p_lo) * astride] = res;
+    if (xin) a.out[base + (p - a.p_lo) * astride] = res;
   }
   if (!FINAL) {  // the max partial distance bounds the next pass's window (slab z halo)
     dmax = __reduce_max_sync(kFull, dmax);
@@ -304,6 +261,174 @@ __global__ void __launch_bounds__(256) k_edt_col(const uint32_t* __restrict__ in
       if (dmax) atomicMax(&hdr->dmax, dmax);
       if (nfg) atomicAdd(&hdr->n_fg, (unsigned long long)nfg);
       if (nosite) atomicOr(&hdr->status, kStNoSite);
+    }
+  }
+}
+
+template <bool FINAL>
+__global__ void __launch_bounds__(256) k_edt_col(ColArgs a, const uint32_t* __restrict__ listed,
+                                                 WsHeader* __restrict__ hdr) {
+  __shared__ uint32_t tile[kColRows * 32];
+  if (!listed) {
+    col32_body<FINAL>(a, blockIdx.x, tile, hdr);
+    return;
+  }
+  const uint32_t n = *(volatile uint32_t*)&hdr->sat_n;
+  for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
+    col32_body<FINAL>(a, listed[k], tile, hdr);
+    __syncthreads();  // the tile is restaged for the next listed CTA
+  }
+}
+
+// ---- 16-bit two-sided column pass (the default) -------------------------------------------
+// Same exact windowed scan, restated so that one SIMD instruction advances both sides:
+//  * a site met on the way is folded into the staged values: scanning up from p, element q is
+//    outside p's run exactly when q starts a run, so up(q) = 0 there (a site at distance dq);
+//    scanning down, q is outside when q+1 starts a run, so down(q) = 0 there.  Terms read past
+//    a site are >= dq^2 > the site's own term, so they never change the minimum and the scan
+//    needs no branch at run ends;
+//  * values are clamped to kCap16 = 2^14 - 1 and each element's (up, down) pair is packed as
+//    two u16 halves: one VIADDMNMX.U16x2 computes min(best, g(p+dq) + dq^2) and
+//    min(best, g(p-dq) + dq^2) at once (dq^2 < kCap16 while scanning, so no half overflows);
+//  * rows outside the axis are staged as virtual rows: 0 (a site) at the grid border with
+//    FASTRS_BORDER_BACKGROUND, else kCap16 (no contribution).
+// A result >= kCap16 (a clamped value or no site at all) cannot be trusted: the CTA lists
+// itself and the exact 32-bit kernel above recomputes it (`sat_n` / `listed`).  Below kCap16
+// the result is exact: the winning term involves an unclamped value (K2/K3).
+constexpr uint32_t kCap16 = 16383u;
+
+template <bool FINAL, int U>
+__global__ void __launch_bounds__(256) k_edt_col16(ColArgs a, uint32_t* __restrict__ satlist,
+                                                   WsHeader* __restrict__ hdr) {
+  __shared__ uint32_t tile[kColRows * 32];
+  const uint32_t* __restrict__ in = a.in;
+  const int64_t L = a.L, astride = a.astride;
+  const uint32_t chbit = a.chbit;
+  int64_t bid = blockIdx.x;
+  const int xb = (int)(bid % a.nxb);
+  bid /= a.nxb;
+  const int seg = (int)(bid % a.nseg);
+  const int64_t outer = bid / a.nseg;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t base = (outer / a.n_inner) * a.outer_mult + (outer % a.n_inner) * a.inner_mult + (int64_t)xb * 32 + lane;
+  const bool xin = xb * 32 + lane < a.X;
+  const int64_t s0 = a.p_lo + (int64_t)seg * kColS;
+  const int64_t lo = s0 - kColH;  // staged rows [lo, lo + kColRows), virtual outside [0, L)
+  auto word = [&](int64_t q) -> uint32_t { return (xin && q >= 0 && q < L) ? __ldg(in + base + q * astride) : 0u; };
+  // virtual rows: above the axis only up-scans read them, below it only down-scans
+  const uint32_t vup = (a.border && a.gofs + L >= a.Lg) ? 0u : kCap16;
+  uint32_t vdn = kCap16;
+  if (lo < 0) vdn = a.gofs == 0 ? (a.border ? 0u : kCap16) : ((word(0) & chbit) ? 0u : kCap16);
+  {  // staging: warp w transforms the contiguous rows [lo + 44w, lo + 44w + 44), top down
+    constexpr int kPer = kColRows / kColWarps;
+    const int64_t r0 = lo + (int64_t)warp * kPer;
+    uint32_t* trow = tile + (r0 - lo + kPer - 1) * 32 + lane;
+    if (xin && r0 >= 0 && r0 + kPer < L) {  // interior block (the common case): no bounds tests
+      const uint32_t* src = in + base + (r0 + kPer) * astride;
+      uint32_t wn = __ldg(src);
+#pragma unroll 11
+      for (int k = kPer - 1; k >= 0; --k) {
+        src -= astride;
+        const uint32_t wq = __ldg(src);
+        const uint32_t gq = min(wq & kMask, kCap16);
+        *trow = ((wq & chbit) ? 0u : gq) | (((wn & chbit) ? 0u : gq) << 16);
+        trow -= 32;
+        wn = wq;
+      }
+    } else {
+      uint32_t wn = word(r0 + kPer);
+      for (int k = kPer - 1; k >= 0; --k) {
+        const int64_t q = r0 + k;
+        const uint32_t wq = word(q);
+        uint32_t pr;
+        if (q < 0) pr = vdn | (vdn << 16);
+        else if (q >= L) pr = vup | (vup << 16);
+        else {
+          const uint32_t gq = min(wq & kMask, kCap16);
+          pr = ((wq & chbit) ? 0u : gq) | (((wn & chbit) ? 0u : gq) << 16);
+        }
+        *trow = pr;
+        trow -= 32;
+        wn = wq;
+      }
+    }
+  }
+  __syncthreads();
+
+  uint32_t dmax = 0, nfg = 0, sat = 0;
+  const int64_t pend = s0 + kColS < a.p_hi ? s0 + kColS : a.p_hi;
+  // the raw word of p (its value and run flags) is loaded one iteration ahead; pointers step
+  // by 8 rows (no 64-bit index arithmetic per element)
+  const int np = (int)(pend - s0);
+  const int64_t step = (int64_t)kColWarps * astride;
+  const uint32_t* src = in + base + (s0 + warp) * astride;
+  uint32_t* dst = a.out + base + (s0 + warp - a.p_lo) * astride;
+  const uint32_t* trow = tile + (kColH + warp) * 32 + lane;  // row p of the tile
+  uint32_t v_next = (xin && warp < np) ? __ldg(src) : 0u;
+  for (int j = warp; j < np; j += kColWarps) {
+    const uint32_t v = v_next;
+    src += step;
+    if (xin && j + kColWarps < np) v_next = __ldg(src);
+    const uint32_t g = v & kMask;
+    uint32_t res = FINAL ? 0u : v;
+    if (g != 0) {  // (lanes beyond X read 0)
+      const uint32_t gc = min(g, kCap16);
+      const int i = kColH + j;
+      // dq^2 < best <= gc bounds the scan: isqrt(gc - 1) + U - 1 rows on each side suffice
+      float r;
+      asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)gc));
+      const int reach = (int)r + 1;
+      uint32_t best;
+      if (reach + U - 1 <= min(i, kColRows - 1 - i)) {
+        // dq2p = (dq^2, dq^2) and bmin2 = (m, m), m = min of the two halves of best2: the u32
+        // compare dq2p < bmin2 is dq^2 < m
+        uint32_t best2 = gc * 0x00010001u, bmin2 = best2;
+        uint32_t dq2p = 0x00010001u, incp = 0x00030003u;
+        const uint32_t* up = trow + 32;
+        const uint32_t* dn = trow - 32;
+        while (dq2p < bmin2) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            // low half: up(p + dq), high half: down(p - dq)
+            const uint32_t pr = __byte_perm(up[32 * u], dn[-32 * u], 0x7610);
+            best2 = __viaddmin_u16x2(pr, dq2p, best2);
+            dq2p += incp;
+            incp += 0x00020002u;
+          }
+          up += 32 * U;
+          dn -= 32 * U;
+          bmin2 = __vminu2(best2, __byte_perm(best2, 0, 0x1032));
+        }
+        best = bmin2 & 0xFFFFu;
+      } else {
+        best = scan_global(in, base, astride, s0 + j, L, v, chbit, a.border, a.gofs, a.Lg);  // exact, 32-bit
+      }
+      sat |= best >= kCap16;  // clamped, or no site at all (ENOSITE comes from the 32-bit kernel)
+      dmax = max(dmax, best);
+      if (FINAL) {
+        res = best;
+        nfg += 1;
+      } else {
+        res = best | (v & (kBitY | kBitZ));
+      }
+    }
+    if (xin) *dst = res;
+    dst += step;
+    trow += 32 * kColWarps;
+  }
+  // a CTA that saw a saturated value is recomputed by the 32-bit kernel (its statistics too)
+  if (__syncthreads_or(sat)) {
+    if (threadIdx.x == 0) satlist[atomicAdd(&hdr->sat_n, 1u)] = blockIdx.x;
+    return;
+  }
+  dmax = __reduce_max_sync(kFull, dmax);
+  if (!FINAL) {
+    if (lane == 0 && dmax) atomicMax(&hdr->dxymax, dmax);
+  } else {
+    nfg = __reduce_add_sync(kFull, nfg);
+    if (lane == 0) {
+      if (dmax) atomicMax(&hdr->dmax, dmax);
+      if (nfg) atomicAdd(&hdr->n_fg, (unsigned long long)nfg);
     }
   }
 }
@@ -322,40 +447,66 @@ void launch_edt_x(const int32_t* labels, const int32_t* labels_below, uint32_t* 
                                                          border ? 1 : 0, g.ndim == 3 ? 1 : 0, hdr);
 }
 
-// axis 1 = y, axis 2 = z.
+int64_t col_blocks(const Geom& g) {
+  const int64_t nxb = (g.X + 31) / 32;
+  const int64_t by = nxb * ((g.Y + kColS - 1) / kColS) * g.B * g.Z;
+  const int64_t bz = g.ndim == 3 ? nxb * ((g.Z + kColS - 1) / kColS) * g.B * g.Y : 0;
+  return by > bz ? by : bz;
+}
+
+// axis 1 = y, axis 2 = z.  16-bit kernel, then the exact 32-bit kernel over the CTAs it listed
+// (satlist NULL: the 32-bit kernel everywhere).
 void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, bool final_pass, bool border,
-                    WsHeader* hdr, cudaStream_t st, int64_t p_lo, int64_t p_hi, int64_t gofs, int64_t Lg) {
-  int64_t L, astride, n_outer, n_inner, inner_mult, outer_mult;
-  uint32_t chbit;
+                    WsHeader* hdr, uint32_t* satlist, cudaStream_t st, int64_t p_lo, int64_t p_hi, int64_t gofs,
+                    int64_t Lg) {
+  ColArgs a{};
+  a.in = in;
+  a.out = out;
+  a.border = border ? 1 : 0;
   if (axis == 1) {
-    L = g.Y;
-    astride = g.X;
-    n_outer = g.B * g.Z;
-    n_inner = 1;
-    inner_mult = 0;
-    outer_mult = g.Y * g.X;
-    chbit = kBitY;
+    a.L = g.Y;
+    a.astride = g.X;
+    a.n_inner = 1;
+    a.inner_mult = 0;
+    a.outer_mult = g.Y * g.X;
+    a.chbit = kBitY;
   } else {
-    L = g.Z;
-    astride = g.Y * g.X;
-    n_outer = g.B * g.Y;
-    n_inner = g.Y;
-    inner_mult = g.X;
-    outer_mult = g.Z * g.Y * g.X;
-    chbit = kBitZ;
+    a.L = g.Z;
+    a.astride = g.Y * g.X;
+    a.n_inner = g.Y;
+    a.inner_mult = g.X;
+    a.outer_mult = g.Z * g.Y * g.X;
+    a.chbit = kBitZ;
   }
-  if (p_hi < 0) p_hi = L;
-  if (Lg < 0) Lg = L;
-  const int nxb = (int)((g.X + 31) / 32);
-  const int nseg = (int)((p_hi - p_lo + kColS - 1) / kColS);
-  if (nseg <= 0) return;
-  const int64_t blocks = (int64_t)nxb * nseg * n_outer;
-  if (final_pass)
-    k_edt_col<true><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(in, out, L, astride, (int)g.X, nxb, nseg, n_inner,
-                                                                  inner_mult, outer_mult, chbit, border ? 1 : 0, p_lo, p_hi, gofs, Lg, hdr);
-  else
-    k_edt_col<false><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(in, out, L, astride, (int)g.X, nxb, nseg, n_inner,
-                                                                   inner_mult, outer_mult, chbit, border ? 1 : 0, p_lo, p_hi, gofs, Lg, hdr);
+  const int64_t n_outer = axis == 1 ? g.B * g.Z : g.B * g.Y;
+  if (p_hi < 0) p_hi = a.L;
+  if (Lg < 0) Lg = a.L;
+  a.p_lo = p_lo;
+  a.p_hi = p_hi;
+  a.gofs = gofs;
+  a.Lg = Lg;
+  a.X = (int)g.X;
+  a.nxb = (int)((g.X + 31) / 32);
+  a.nseg = (int)((p_hi - p_lo + kColS - 1) / kColS);
+  if (a.nseg <= 0) return;
+  const int64_t blocks = (int64_t)a.nxb * a.nseg * n_outer;
+  if (!satlist) {
+    if (final_pass) k_edt_col<true><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, nullptr, hdr);
+    else k_edt_col<false><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, nullptr, hdr);
+    return;
+  }
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaMemsetAsync(&hdr->sat_n, 0, sizeof(uint32_t), st);
+  const unsigned fix_grid = (unsigned)(nsm * 2);
+  if (final_pass) {
+    k_edt_col16<true, kScan16U><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, satlist, hdr);
+    k_edt_col<true><<<fix_grid, kColWarps * 32, 0, st>>>(a, satlist, hdr);
+  } else {
+    k_edt_col16<false, kScan16U><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, satlist, hdr);
+    k_edt_col<false><<<fix_grid, kColWarps * 32, 0, st>>>(a, satlist, hdr);
+  }
 }
 
 }  // namespace fastrs
