@@ -59,7 +59,7 @@ int make_geom(const int64_t* dims, int ndim, int64_t batch, Geom& g) {
 inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t hdr, A, B, meta, fgm, oct, fbl, gcount, goff, pool, fxl, sat, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd, total;
+  size_t hdr, A, B, meta, fgm, shm, oct, fbl, gcount, goff, pool, sat, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd, total;
 };
 
 Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
@@ -76,18 +76,18 @@ Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
   L.B = take((size_t)g.N * 4);
   L.meta = take((size_t)g.ntiles * sizeof(TileMeta));
   L.fgm = take((size_t)g.ntiles * kRows * 4);
+  L.shm = take((size_t)g.ntiles * kRows * 4);
   L.oct = take((size_t)g.ntiles * 16 * 2);
   L.fbl = take((size_t)g.ntiles * 4);
   L.gcount = take((size_t)dilate_groups(g) * 4);
   L.goff = take((size_t)dilate_groups(g) * 4);
   L.pool = take((size_t)dilate_pool_entries(g) * 8);
-  L.fxl = take(kFxLutBytes);
   L.sat = take((size_t)col_blocks(g) * 4);
   L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
   L.vol = take(M * 8);
   L.nsh = take(M * 8);
-  L.sum = take(M * 8);
-  L.sumsh = take(M * 8);
+  L.sum = take(2 * M * 8);    // hi | lo words (common.cuh "Accum")
+  L.sumsh = take(2 * M * 8);
   L.mx = take(M * 4);
   if (flags & kFlagHostIO) {
     L.h_labels = take((size_t)g.N * 4);
@@ -207,24 +207,31 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
   }
   if (stage != kEdtOnly) {
     uint32_t* fgm = (uint32_t*)(w + L.fgm);
+    uint32_t* shm = (uint32_t*)(w + L.shm);
     uint16_t* oct = (uint16_t*)(w + L.oct);
-    launch_prune(D, g, meta, cent, fgm, oct, hdr, st);  // K4
+    launch_prune(D, g, meta, cent, fgm, shm, oct, hdr, st);  // K4
     tm.mark(3);
-    uint32_t* ltp = D == A ? B : A;  // the plane the EDT no longer needs holds LT^2
+    uint32_t* ltp = D == A ? B : A;  // the plane the EDT no longer needs holds LT^2 (fallback / LT outputs)
     uint32_t* fbl = (uint32_t*)(w + L.fbl);
-    launch_dilate_gather(fgm, meta, cent, oct, fbl, (unsigned long long*)(w + L.pool), (uint32_t*)(w + L.gcount),
-                         (uint32_t*)(w + L.goff), g, (flags & kFlagForceFallback) != 0 ? 1 : 0, hdr, st);  // K5a
+    unsigned long long* pool = (unsigned long long*)(w + L.pool);
+    uint32_t* gcount = (uint32_t*)(w + L.gcount);
+    uint32_t* goff = (uint32_t*)(w + L.goff);
+    launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, g, (flags & kFlagForceFallback) != 0 ? 1 : 0,
+                         hdr, st);  // K5a
     tm.mark(7);
-    launch_dilate(labels, D, meta, cent, fgm, oct, fbl, (unsigned long long*)(w + L.pool), (uint32_t*)(w + L.gcount),
-                  (uint32_t*)(w + L.goff), g, stage == kFull ? &acc : nullptr, lt2_out, lt_out,
-                  (flags & kFlagForceFallback) != 0, ltp, hdr, st);  // K5
+    // K5b: with the reductions fused (S&R) or writing the LT plane (LT outputs); K5' for the
+    // tiles K5a handed over (every tile when Dmax > 65535)
+    launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, g, ltp, labels, stage == kFull ? &acc : nullptr, hdr, st);
+    launch_dilate_fallback(meta, cent, fbl, g, ltp, hdr, st);
     tm.mark(4);
-    launch_epilogue(labels, D, g, stage == kFull ? &acc : nullptr, lt2_out, lt_out, ltp,
-                    (unsigned long long*)(w + L.fxl), hdr, st);  // K5 epilogue
-    tm.mark(6);
     if (stage == kFull) {
+      launch_epilogue_fallback(labels, D, meta, fbl, g, acc, ltp, hdr, st);  // K5e on the fallback tiles only
+      tm.mark(6);
       launch_metrics(acc, g, *outs, hdr, st);  // K6
       tm.mark(5);
+    } else {
+      launch_epilogue(labels, D, g, nullptr, lt2_out, lt_out, ltp, hdr, st);  // LT outputs
+      tm.mark(6);
     }
   }
   e = cudaGetLastError();
@@ -271,7 +278,7 @@ int finish_call(WsHeader* hdr, uint32_t flags, cudaStream_t st) {
 }
 
 struct SlabLayout {
-  size_t hdr, P, meta, fgm, oct, fbl, gcount, goff, pool, fxl, sat, cent, total;
+  size_t hdr, P, meta, fgm, shm, oct, fbl, gcount, goff, pool, sat, cent, total;
 };
 SlabLayout make_slab_layout(const Geom& g) {
   SlabLayout L{};
@@ -285,12 +292,12 @@ SlabLayout make_slab_layout(const Geom& g) {
   L.P = take((size_t)g.N * 4);
   L.meta = take((size_t)g.ntiles * sizeof(TileMeta));
   L.fgm = take((size_t)g.ntiles * kRows * 4);
+  L.shm = take((size_t)g.ntiles * kRows * 4);
   L.oct = take((size_t)g.ntiles * 16 * 2);
   L.fbl = take((size_t)g.ntiles * 4);
   L.gcount = take((size_t)dilate_groups(g) * 4);
   L.goff = take((size_t)dilate_groups(g) * 4);
   L.pool = take((size_t)dilate_pool_entries(g) * 8);
-  L.fxl = take(kFxLutBytes);
   L.sat = take((size_t)col_blocks(g) * 4);
   L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
   L.total = off;
@@ -345,6 +352,7 @@ int run_host_pipelined(const int32_t* labels_host, int32_t* dlab, const Geom& g,
   TileMeta* meta = (TileMeta*)(w + L.meta);
   uint2* cent = (uint2*)(w + L.cent);
   uint32_t* fgm = (uint32_t*)(w + L.fgm);
+  uint32_t* shm = (uint32_t*)(w + L.shm);
   uint16_t* oct = (uint16_t*)(w + L.oct);
   uint32_t* fbl = (uint32_t*)(w + L.fbl);
   unsigned long long* pool = (unsigned long long*)(w + L.pool);
@@ -402,44 +410,35 @@ int run_host_pipelined(const int32_t* labels_host, int32_t* dlab, const Geom& g,
     }
     if (step >= 2 && step - 2 < nc) {  // K4 on chunk step-2
       zr(step - 2, z0, z1);
-      launch_prune(A, g, meta, cent, fgm, oct, hdr, st, z0 / kTZ3, (z1 + kTZ3 - 1) / kTZ3);
+      launch_prune(A, g, meta, cent, fgm, shm, oct, hdr, st, z0 / kTZ3, (z1 + kTZ3 - 1) / kTZ3);
     }
-    if (step >= 3 && step - 3 < nc) {  // K5a + K5b on chunk step-3 (LT^2 into B: its y-pass words are consumed)
+    if (step >= 3 && step - 3 < nc) {  // K5a + K5b (reductions fused) on chunk step-3
       zr(step - 3, z0, z1);
       Geom gg = g;
       gg.tz_lo = z0 / kTZ3;
       gg.tz_hi = (z1 + kTZ3 - 1) / kTZ3;
       launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, gg, 0, hdr, st);
-      launch_dilate_paint(fgm, meta, pool, gcount, goff, gg, B, hdr, st);
-      // K5e on the chunk's finished layers, with the scale of the Dmax seen so far (checked
-      // against the final Dmax below; fallback tiles make it skip)
-      launch_epilogue(dlab, A, gg, &acc, nullptr, nullptr, B, (unsigned long long*)(w + L.fxl), hdr, st, true);
+      launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, gg, B, dlab, &acc, hdr, st);
     }
   }
+  // tiles handed to the atomic kernel (LT^2 into B, whose y-pass words are consumed) and their
+  // reductions; then the closed forms.  The fixed-point scale does not depend on Dmax, so the
+  // per-chunk sums are final.
   launch_dilate_fallback(meta, cent, fbl, g, B, hdr, st);
-  launch_metrics(acc, g, outs, hdr, st);  // speculative: redone below if the chunked epilogue was not exact
-  // halo check: the chunked z pass and dilation were exact iff both halos fit in one chunk
+  launch_epilogue_fallback(dlab, A, meta, fbl, g, acc, B, hdr, st);
+  launch_metrics(acc, g, outs, hdr, st);
+  // halo check: the chunked z pass and dilation were exact iff both halos fit in one chunk.
+  // Decided first: the status bits of an inexact pass are not trusted (the caller reruns).
   WsHeader h;
   e = cudaMemcpyAsync(&h, hdr, sizeof h, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   for (auto& x : ev) cudaEventDestroy(x);
   if (e != cudaSuccess) return cuda_fail(e, "pipelined pass");
-  if (h.status & (kStBadLabel | kStNoSite)) {  // report through the caller's status read
-    *exact = true;
-    return FASTRS_OK;
-  }
   uint64_t hz = 0;
   while (hz * hz < h.dxymax && hz <= (uint64_t)kChunkZ) ++hz;
   uint64_t rr = 0;
   while ((rr + 1) * (rr + 1) <= (h.dmax ? h.dmax - 1 : 0) && rr <= (uint64_t)kChunkZ) ++rr;
   if (hz > (uint64_t)kChunkZ || rr > (uint64_t)kChunkZ || h.dxymax >= kInf) return FASTRS_OK;  // not exact: rerun
-  // the per-chunk epilogues are exact when no tile went to the fallback kernel and every chunk
-  // used the scale of the final Dmax; otherwise redo the reductions over the whole volume
-  if (h.n_fb != 0 || h.epi_skipped != 0 || h.scale_set != (uint32_t)sum_scale_log2(g.nscale, h.dmax) + 1u) {
-    cudaMemsetAsync(w + L.vol, 0, (L.mx - L.vol) + align256((size_t)acc.M * 4), st);
-    launch_epilogue(dlab, A, g, &acc, nullptr, nullptr, B, (unsigned long long*)(w + L.fxl), hdr, st);
-    launch_metrics(acc, g, outs, hdr, st);
-  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   *exact = true;
@@ -583,7 +582,7 @@ int fastrs_read_diagnostics(const void* ws, fastrs_diagnostics* out, void* strea
   out->n_fg = h.n_fg;
   out->n_kept = h.n_kept;
   out->n_intervals = h.n_intervals;
-  out->sum_scale_log2 = h.scale_log2;
+  out->sum_scale_log2 = 32;
   out->n_fallback = h.n_fallback;
   out->n_rounds_extra = h.n_rounds_extra;
   out->n_regathers = h.n_regathers;
@@ -679,16 +678,19 @@ int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64
   g.nscale = Z * g.Y * g.X;
   const int64_t M = max_label;
   cudaError_t e = cudaSuccess;
-  for (void* a : {(void*)vol, (void*)n_shell, (void*)sum_lt, (void*)sum_shell_lt})
+  for (void* a : {(void*)vol, (void*)n_shell})
     if (e == cudaSuccess) e = cudaMemsetAsync(a, 0, (size_t)M * 8, st);
+  for (void* a : {(void*)sum_lt, (void*)sum_shell_lt})
+    if (e == cudaSuccess) e = cudaMemsetAsync(a, 0, (size_t)M * 16, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(max_lt2, 0, (size_t)M * 4, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
   k_set_dmax<<<1, 1, 0, st>>>(hdr, dmax_global);
   TileMeta* meta = (TileMeta*)((char*)ws + L.meta);
   uint2* cent = (uint2*)((char*)ws + L.cent);
   uint32_t* fgm = (uint32_t*)((char*)ws + L.fgm);
+  uint32_t* shm = (uint32_t*)((char*)ws + L.shm);
   uint16_t* oct = (uint16_t*)((char*)ws + L.oct);
-  launch_prune(d_ext, g, meta, cent, fgm, oct, hdr, st);
+  launch_prune(d_ext, g, meta, cent, fgm, shm, oct, hdr, st);
   Accum acc{};
   acc.vol = (unsigned long long*)vol;
   acc.nshell = (unsigned long long*)n_shell;
@@ -697,17 +699,19 @@ int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64
   acc.maxlt2 = max_lt2;
   acc.M = M;
   acc.max_label = max_label;
-  // the epilogue indexes labels in the extended layout: shift the own-slab pointer (only own
-  // elements are ever read)
+  // labels are indexed in the extended layout: shift the own-slab pointer (only own elements
+  // are ever read: the fused paint reads labels at covered cells of own tiles)
   const int32_t* lab_ext = labels - own_lo * g.Y * g.X;
   uint32_t* ltp = (uint32_t*)((char*)ws + L.P);
   uint32_t* fbl = (uint32_t*)((char*)ws + L.fbl);
-  launch_dilate_gather(fgm, meta, cent, oct, fbl, (unsigned long long*)((char*)ws + L.pool), (uint32_t*)((char*)ws + L.gcount),
-                       (uint32_t*)((char*)ws + L.goff), g, (flags & kFlagForceFallback) != 0 ? 1 : 0, hdr, st);
-  launch_dilate(lab_ext, d_ext, meta, cent, fgm, oct, fbl, (unsigned long long*)((char*)ws + L.pool),
-                (uint32_t*)((char*)ws + L.gcount), (uint32_t*)((char*)ws + L.goff), g, &acc, nullptr, nullptr, (flags & kFlagForceFallback) != 0, ltp,
-                hdr, st);
-  launch_epilogue(lab_ext, d_ext, g, &acc, nullptr, nullptr, ltp, (unsigned long long*)((char*)ws + L.fxl), hdr, st);
+  unsigned long long* pool = (unsigned long long*)((char*)ws + L.pool);
+  uint32_t* gcount = (uint32_t*)((char*)ws + L.gcount);
+  uint32_t* goff = (uint32_t*)((char*)ws + L.goff);
+  launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, g, (flags & kFlagForceFallback) != 0 ? 1 : 0, hdr,
+                       st);
+  launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, g, ltp, lab_ext, &acc, hdr, st);
+  launch_dilate_fallback(meta, cent, fbl, g, ltp, hdr, st);
+  launch_epilogue_fallback(lab_ext, d_ext, meta, fbl, g, acc, ltp, hdr, st);
   return finish_call(hdr, flags, st);
 }
 

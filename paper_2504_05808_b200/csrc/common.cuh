@@ -49,7 +49,7 @@ struct WsHeader {
   unsigned long long n_fg;
   unsigned long long n_kept;
   unsigned long long n_intervals;
-  int32_t scale_log2;
+  int32_t scale_log2;   // fixed-point scale of the LT sums (always 32)
   uint32_t n_fallback;  // tile groups handed to the atomic fallback dilation
   uint32_t dxymax;      // max partial D after the y pass (slab path: the z halo width)
   uint32_t n_fb;        // tiles listed for the atomic fallback dilation
@@ -59,8 +59,7 @@ struct WsHeader {
   uint32_t pad[1];
   unsigned long long sum_group_list;  // K5 candidates summed over groups
   unsigned long long pool_used;       // K5 candidate pool entries allocated
-  uint32_t scale_set;    // host pipeline: s + 1 of the per-chunk epilogues (0xFFFFFFFF: they differed)
-  uint32_t epi_skipped;  // host pipeline: a per-chunk epilogue saw fallback tiles and did nothing
+  uint32_t pad2[2];
   uint32_t paint_next;   // K5b work counter (reset before each launch)
   uint32_t sat_n;        // K2/K3: CTAs listed for the exact 32-bit column pass (reset per launch)
 };
@@ -74,16 +73,23 @@ struct TileMeta {
   uint32_t pad;
 };
 
-// per-label accumulators (SoA)
+// per-label accumulators (SoA).  The LT sums are exact fixed-point integers with the fixed
+// scale 2^32: every term is fx(c) = round(sqrt(c) * 2^32) (c = LT^2), and each sum is kept as
+// two u64 words, hi = sum of (term >> 32) pieces and lo = sum of (term & (2^32-1)) pieces, so
+// the value is hi * 2^32 + lo with no overflow for objects below 2^32 elements.  Integer adds
+// are order-independent: the result is bit-identical for any launch order, chunking or
+// z-slab split, and no scale depends on Dmax.
 struct Accum {
   unsigned long long* vol;
   unsigned long long* nshell;
-  unsigned long long* sum;       // fixed point, scale 2^scale_log2
-  unsigned long long* sumshell;  // fixed point
+  unsigned long long* sum;       // hi words (M), lo words at sum + M
+  unsigned long long* sumshell;  // hi words (M), lo words at sumshell + M
   uint32_t* maxlt2;
   int64_t M;                     // batch*max_label
   int32_t max_label;
 };
+constexpr double kFxScale = 4294967296.0;  // 2^32
+constexpr uint32_t kFxLut = 65536;         // entries of the per-device fixed-point sqrt table
 
 struct Outputs {
   double* sphericity;
@@ -102,16 +108,6 @@ __host__ __device__ inline int ceil_log2_u64(unsigned long long v) {
   int r = 0;
   while ((1ull << r) < v && r < 63) ++r;
   return r;
-}
-
-// Fixed-point scale of the LT sums: every term sqrt(LT^2)*2^s < 2^15 * 2^s and an object
-// has at most Nb elements, so choosing s with Nb * (isqrt(Dmax)+1) * 2^s <= 2^62 makes the
-// u64 sums overflow-free and exact (integer adds are order-independent).  s in [0, 32].
-__host__ __device__ inline int sum_scale_log2(int64_t Nb, uint32_t dmax) {
-  unsigned long long r = 1;
-  while ((r + 1) * (r + 1) <= (unsigned long long)dmax) ++r;  // ~isqrt(dmax), small loop
-  int s = 62 - ceil_log2_u64((unsigned long long)Nb) - ceil_log2_u64(r + 1);
-  return s < 0 ? 0 : (s > 32 ? 32 : s);
 }
 
 // Monotone bucket of a squared radius D: 8 buckets per octave, 0..126 for D < 65536; every
@@ -151,19 +147,18 @@ void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, 
                     int64_t p_hi = -1, int64_t gofs = 0, int64_t Lg = -1);
 int64_t col_blocks(const Geom& g);  // column-pass CTAs of the larger of the y / z passes
 cudaError_t ensure_mtables(int device);  // builds the per-device lattice tables (sync, once)
-// K4; also writes per tile the foreground row masks (fgm: kRows u32) and the number of kept
-// entries with D bucket >= 8o for o = 0..15 (oct: 16 u16) used by K5's gather
-void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, uint32_t* fgm, uint16_t* oct,
-                  WsHeader* hdr, cudaStream_t st, int64_t tz_lo = 0, int64_t tz_hi = 0);
-void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta,
-                   const uint2* centres, const uint32_t* fgm, const uint16_t* oct, uint32_t* fbl,
-                   unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, const Accum* acc,
-                   uint32_t* lt2_out, float* lt_out, bool force_fallback, uint32_t* ltp, WsHeader* hdr,
-                   cudaStream_t st);
+const unsigned long long* device_fxlut(int device);  // fx(c) for c < kFxLut (after ensure_mtables)
+// K4; also writes per tile the foreground and shell (D == 1) row masks (fgm, shm: kRows u32 each)
+// and the number of kept entries with D bucket >= 8o for o = 0..15 (oct: 16 u16) used by K5's gather
+void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, uint32_t* fgm, uint32_t* shm,
+                  uint16_t* oct, WsHeader* hdr, cudaStream_t st, int64_t tz_lo = 0, int64_t tz_hi = 0);
 int64_t dilate_groups(const Geom& g);        // K5 tile groups (gcount / goff entries)
-void launch_dilate_paint(const uint32_t* fgm, const TileMeta* meta, const unsigned long long* pool,
-                         const uint32_t* gcount, const uint32_t* goff, const Geom& g, uint32_t* ltp, WsHeader* hdr,
-                         cudaStream_t st);
+// K5b.  acc == NULL: LT^2 of every painted tile -> the LT plane ltp (u16).  acc != NULL (fused):
+// no LT plane; every ball that covers cells adds (count, shell count, D) of those cells to the
+// per-label accumulators of the label of the cells it covers (labels read once per covering ball)
+void launch_dilate_paint(const uint32_t* fgm, const uint32_t* shm, const TileMeta* meta,
+                         const unsigned long long* pool, const uint32_t* gcount, const uint32_t* goff, const Geom& g,
+                         uint32_t* ltp, const int32_t* labels, const Accum* acc, WsHeader* hdr, cudaStream_t st);
 void launch_dilate_fallback(TileMeta* meta, const uint2* centres, const uint32_t* fbl, const Geom& g, uint32_t* ltp,
                             WsHeader* hdr, cudaStream_t st);
 // K5a: per tile group, gather the kept balls that reach it and write them sorted by D
@@ -172,10 +167,13 @@ void launch_dilate_gather(const uint32_t* fgm, TileMeta* meta, const uint2* cent
                           unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int force_fallback,
                           WsHeader* hdr, cudaStream_t st);
 int64_t dilate_pool_entries(const Geom& g);  // K5 candidate pool (sorted per-group lists), u64 entries
-// K5 epilogue: shell, per-label reductions and LT outputs from the LT plane ltp
+// K5 epilogue: shell, per-label reductions (acc nullable) and LT outputs from the LT plane ltp
 void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,
-                     float* lt_out, const uint32_t* ltp, unsigned long long* fxlut, WsHeader* hdr, cudaStream_t st, bool chunked = false);
-constexpr size_t kFxLutBytes = 65536 * 8;  // workspace for the epilogue's fixed-point sqrt table
+                     float* lt_out, const uint32_t* ltp, WsHeader* hdr, cudaStream_t st);
+// per-label reductions of the tiles the atomic fallback kernel painted (every tile when
+// Dmax > 65535, else the n_fb tiles listed in fbl); the fused paint covers all the others
+void launch_epilogue_fallback(const int32_t* labels, const uint32_t* D, const TileMeta* meta, const uint32_t* fbl,
+                              const Geom& g, const Accum& acc, const uint32_t* ltp, WsHeader* hdr, cudaStream_t st);
 cudaError_t launch_touch_edge(const int32_t* labels, const Geom& g, int32_t max_label, uint8_t* touch,
                               bool skip_zlo, bool skip_zhi, cudaStream_t st);
 cudaError_t launch_filter(double* sph, double* rnd, const int64_t* vol, const uint8_t* touch, int64_t n,

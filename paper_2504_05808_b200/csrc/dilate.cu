@@ -61,16 +61,18 @@ struct Smem {  // K5a (gather + sort)
 // K5b CTAs hold NW of a group's kWarps tiles (one warp each).  The warps share
 // nothing, so one warp per CTA lets every tile retire on its own: no warp slot idles while a
 // sibling tile of the same CTA is still painting.
-// K5b launch shape: warps per CTA and resident CTAs per SM (sets the register cap: 56 here, 36
-// resident warps).  C4 sweep (persistent): (2,16) 10.63 ms, (2,18) 10.58, (2,20) 10.71, (2,24)
-// 10.68, (1,32) 10.76, (4,10) 10.70.
-constexpr int kPaintNW = 2, kPaintMinB = 18;
-template <int NW>
+// K5b launch shape: warps per CTA and resident CTAs per SM (sets the register cap: 64 here, 32
+// resident warps; the fused reductions spill at 56).  C4 sweep (persistent, round 1, LT plane):
+// (2,16) 10.63 ms, (2,18) 10.58, (2,20) 10.71, (2,24) 10.68, (1,32) 10.76, (4,10) 10.70.
+constexpr int kPaintNW = 2, kPaintMinB = 16;
+template <int NW, bool FUSED>
 struct PaintSmem {  // K5b (one tile per warp)
-  uint16_t val[NW][kRows * 32];   // LT^2 per element of each warp's tile (D <= 65535 here)
+  uint16_t val[NW][FUSED ? 1 : kRows * 32];  // LT^2 per element of each warp's tile (D <= 65535 here)
   int4 sball[NW][32];             // survivors of a screened batch: centre (tile coords), D
   unsigned long long scand[NW][32];  // their candidate rows
   uint16_t ulist[NW][kPoint];     // point mode: the still-uncovered cells (row*32 + x)
+  uint32_t qa[NW][32];            // fused: covering events, (cell offset | count << 16)
+  uint32_t qb[NW][32];            //        and (D | shell count << 16)
 };
 
 template <bool IS3D>
@@ -616,16 +618,43 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
   }
 }
 
-template <bool IS3D, int NW>
+// Fused K5b reductions: the warp's queued covering events (lanes = events): the label of each
+// event's first cell (tile_labels: the tile origin in the label array), then the per-label
+// warp aggregation and the global atomics (dilate_common.cuh accumulate_records).  Out of line:
+// it runs once per 32 events and keeps the paint loop's registers free.
+template <bool IS3D>
+__device__ __noinline__ void flush_events(const uint32_t* qa, const uint32_t* qb, int n,
+                                          const int32_t* __restrict__ tile_labels, int64_t Y, int64_t X, int64_t b,
+                                          const Accum& acc, const unsigned long long* __restrict__ fxlut) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  int32_t L = 0;
+  uint32_t cnt = 0, scnt = 0, D = 0;
+  if (lane < n) {
+    const uint32_t ea = qa[lane], eb = qb[lane];
+    const int off = (int)(ea & 0xFFFFu), row = off >> 5;
+    const int ly = IS3D ? (row & 7) : row, lz = IS3D ? (row >> 3) : 0;
+    L = __ldg(tile_labels + ((int64_t)lz * Y + ly) * X + (off & 31));
+    cnt = ea >> 16;
+    D = eb & 0xFFFFu;
+    scnt = eb >> 16;
+  }
+  __syncwarp();  // the queue may be refilled after this
+  accumulate_records(L, cnt, scnt, D, lane, b, acc, fxlut);
+}
+
+template <bool IS3D, int NW, bool FUSED>
 __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* __restrict__ fgm,
-                                           const TileMeta* __restrict__ meta, const Geom& g,
-                                           const unsigned long long* __restrict__ pool,
+                                           const uint32_t* __restrict__ shm, const TileMeta* __restrict__ meta,
+                                           const Geom& g, const unsigned long long* __restrict__ pool,
                                            const uint32_t* __restrict__ gcount, const uint32_t* __restrict__ goff,
-                                           int point_at, uint32_t* __restrict__ ltp, WsHeader* __restrict__ hdr) {
+                                           int point_at, uint32_t* __restrict__ ltp, const int32_t* __restrict__ labels,
+                                           const Accum& acc, const unsigned long long* __restrict__ fxlut,
+                                           WsHeader* __restrict__ hdr) {
   using P = Shape<IS3D>;
   constexpr int TY = P::TY, TZ = P::TZ;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  PaintSmem<NW>& S = *reinterpret_cast<PaintSmem<NW>*>(smem_raw);
+  PaintSmem<NW, FUSED>& S = *reinterpret_cast<PaintSmem<NW, FUSED>*>(smem_raw);
   // bid numbers tiles: group bid / kWarps, tile bid % kWarps within it; wl = my warp's smem slot
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int warp = (int)(bid % kWarps);  // my tile within the group
@@ -657,13 +686,34 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
 
   // ---- per-warp init: values, foreground masks, coverage ----------------------------------
   uint16_t* val = S.val[wl];
-  {
+  if (!FUSED) {
     uint4* v4 = reinterpret_cast<uint4*>(val);
 #pragma unroll 4
     for (int i = lane; i < kRows * 32 / 8; i += 32) v4[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   // lane owns rows `lane` (0) and `lane + 32` (1): foreground and covered masks in registers
   const uint32_t f0 = active ? fgm[mtile * kRows + lane] : 0u, f1 = active ? fgm[mtile * kRows + lane + 32] : 0u;
+  // fused: shell masks of the same rows, and the queue of covering events.  An event is one
+  // ball covering `count` still-uncovered cells of one label (its own), `scount` of them shell
+  // cells, with LT^2 = D for each (exact descending order: the first cover is the max).  A
+  // full queue is flushed: lanes = events, the label of each event's first cell is read, and
+  // the events are summed per label in the warp before the global atomics.
+  const uint32_t s0 = FUSED ? shm[mtile * kRows + lane] : 0u, s1 = FUSED ? shm[mtile * kRows + lane + 32] : 0u;
+  int nev = 0;  // queued events (warp-uniform)
+  uint32_t* qa = S.qa[wl];
+  uint32_t* qb = S.qb[wl];
+  const int64_t tgx = rox + mox, tgy = roy + moy, tgz = roz + moz;  // my tile's origin in the item
+  auto ev_flush = [&]() {
+    flush_events<IS3D>(qa, qb, nev, labels + item + (tgz * g.Y + tgy) * g.X + tgx, g.Y, g.X, b, acc, fxlut);
+    nev = 0;
+  };
+  auto ev_push = [&](uint32_t off, uint32_t cnt, uint32_t D, uint32_t scnt) {  // warp-uniform call, lane 0 stores
+    if (lane == 0) {
+      qa[nev] = off | (cnt << 16);
+      qb[nev] = D | (scnt << 16);
+    }
+    if (++nev == 32) ev_flush();
+  };
   uint32_t c0 = 0, c1 = 0;
   int ul0, uh0, ul1, uh1;  // x range of the uncovered foreground of rows lane / lane + 32
   uncovered_range(f0, ul0, uh0);
@@ -716,8 +766,12 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
       if (bm) {
         const int wD = __shfl_sync(kFull, D, __ffs(bm) - 1);
         if (lane == 0) {
-          val[e] = (uint16_t)wD;
+          if (!FUSED) val[e] = (uint16_t)wD;
           ulist[q] = (uint16_t)(e | 0x8000u);
+        }
+        if (FUSED) {
+          const uint32_t srow = __shfl_sync(kFull, row >= 32 ? s1 : s0, row & 31);
+          ev_push(e, 1u, (uint32_t)wD, (srow >> x) & 1u);
         }
         hit = true;
       }
@@ -837,6 +891,8 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
         const int ns = __popc(act);
         for (int j = 0; j < ns; ++j) {
           const int4 bp = sball[j];
+          uint32_t ecnt = 0, escnt = 0;  // fused: cells of my rows this ball covers first
+          int efirst = -1;
           const uint2 jc2 = reinterpret_cast<const uint2*>(scand)[j];  // candidate rows 0-31 | 32-63
           const int jR2 = bp.w - 1;
           const uint16_t dv = (uint16_t)bp.w;
@@ -875,12 +931,26 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
               c0 |= m;
               uncovered_range(f0 & ~c0, ul0, uh0);
             }
-            uint16_t* vr = val + (32 * hf + lane) * 32;
-            do {
-              const int c = __ffs(m) - 1;
-              m &= m - 1;
-              vr[c] = dv;
-            } while (m);
+            if (FUSED) {
+              ecnt += __popc(m);
+              escnt += __popc(m & (hf ? s1 : s0));
+              if (efirst < 0) efirst = (32 * hf + lane) * 32 + __ffs(m) - 1;
+            } else {
+              uint16_t* vr = val + (32 * hf + lane) * 32;
+              do {
+                const int c = __ffs(m) - 1;
+                m &= m - 1;
+                vr[c] = dv;
+              } while (m);
+            }
+          }
+          if (FUSED) {
+            const uint32_t who = __ballot_sync(kFull, ecnt != 0);
+            if (who) {
+              const uint32_t tc = __reduce_add_sync(kFull, ecnt), ts = __reduce_add_sync(kFull, escnt);
+              const int off = __shfl_sync(kFull, efirst, __ffs(who) - 1);
+              ev_push((uint32_t)off, tc, (uint32_t)bp.w, ts);
+            }
           }
         }
         __syncwarp();
@@ -900,8 +970,16 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
   }
 
 
+  n_rows = __reduce_add_sync(kFull, n_rows);
+  if (lane == 0 && n_rows) atomicAdd(&hdr->n_intervals, (unsigned long long)n_rows);
+  if (FUSED) {
+    if (nev) ev_flush();
+    // every foreground cell lies in some kept ball that reaches the tile
+    if (nu != 0 && lane == 0) atomicOr(&hdr->status, kStInternal);
+    return;
+  }
   // ---- my tile's LT^2 -> the LT plane (coalesced rows); shell and reductions run in the
-  // streaming epilogue kernel (lt.cu), at full occupancy
+  // streaming epilogue kernel (lt.cu)
   // the LT plane holds u16 values whenever Dmax <= 65535 (always the case here)
   const int64_t gx = rox + mox + lane;
   const int64_t gy0 = roy + moy, gz0 = roz + moz;
@@ -919,21 +997,23 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
       if (gz0 + lz < g.Z && gy0 + ly < g.Y && gx < g.X) lt16[((int64_t)lz * g.Y + ly) * g.X] = val[row * 32 + lane];
     }
   }
-  n_rows = __reduce_add_sync(kFull, n_rows);
-  if (lane == 0 && n_rows) atomicAdd(&hdr->n_intervals, (unsigned long long)n_rows);
 }
 
 
-// Persistent K5b: resident one-warp CTAs take tiles from a global counter in launch order (the
-// four tiles of a group one after another), so no CTA slot idles between short tiles.
-template <bool IS3D, int NW, int MINB>
+// Persistent K5b: resident CTAs of NW independent warps take tiles from a global counter in
+// launch order (the four tiles of a group one after another), so no warp slot idles between
+// short tiles.
+template <bool IS3D, int NW, int MINB, bool FUSED>
 __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* __restrict__ fgm,
+                                                              const uint32_t* __restrict__ shm,
                                                               const TileMeta* __restrict__ meta, Geom g,
                                                               const unsigned long long* __restrict__ pool,
                                                               const uint32_t* __restrict__ gcount,
                                                               const uint32_t* __restrict__ goff, int point_at,
-                                                              uint32_t* __restrict__ ltp, WsHeader* __restrict__ hdr,
-                                                              uint32_t nbid) {
+                                                              uint32_t* __restrict__ ltp,
+                                                              const int32_t* __restrict__ labels, Accum acc,
+                                                              const unsigned long long* __restrict__ fxlut,
+                                                              WsHeader* __restrict__ hdr, uint32_t nbid) {
   if (hdr->dmax > kU16Max) return;  // k_dilate_atomic handles it
   const int lane = threadIdx.x & 31;
   for (;;) {
@@ -941,7 +1021,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* 
     if (lane == 0) bid = atomicAdd(&hdr->paint_next, 1u);
     bid = __shfl_sync(kFull, bid, 0);
     if (bid >= nbid) break;
-    paint_tile<IS3D, NW>(bid, fgm, meta, g, pool, gcount, goff, point_at, ltp, hdr);
+    paint_tile<IS3D, NW, FUSED>(bid, fgm, shm, meta, g, pool, gcount, goff, point_at, ltp, labels, acc, fxlut, hdr);
     __syncwarp();
   }
 }
@@ -984,10 +1064,10 @@ void launch_dilate_gather(const uint32_t* fgm, TileMeta* meta, const uint2* cent
 }
 
 namespace {
-template <bool IS3D, int NW, int MINB>
-void paint_go(int64_t ngroups, const uint32_t* fgm, const TileMeta* meta, const Geom& g,
+template <bool IS3D, int NW, int MINB, bool FUSED>
+void paint_go(int64_t ngroups, const uint32_t* fgm, const uint32_t* shm, const TileMeta* meta, const Geom& g,
               const unsigned long long* pool, const uint32_t* gcount, const uint32_t* goff, uint32_t* ltp,
-              WsHeader* hdr, cudaStream_t st) {
+              const int32_t* labels, const Accum& acc, WsHeader* hdr, cudaStream_t st) {
   const uint32_t nbid = (uint32_t)(ngroups * kWarps);
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -995,26 +1075,25 @@ void paint_go(int64_t ngroups, const uint32_t* fgm, const TileMeta* meta, const 
   const uint32_t cap = (uint32_t)nsm * MINB * NW;  // resident warps
   const uint32_t grid = ((nbid < cap ? nbid : cap) + NW - 1) / NW;
   cudaMemsetAsync(&hdr->paint_next, 0, sizeof(uint32_t), st);
-  k_dilate_paint<IS3D, NW, MINB><<<grid, NW * 32, sizeof(PaintSmem<NW>), st>>>(fgm, meta, g, pool, gcount, goff,
-                                                                             point_at_knob(), ltp, hdr, nbid);
-}
-template <bool IS3D>
-void paint_variant(int64_t ngroups, const uint32_t* fgm, const TileMeta* meta, const Geom& g,
-                   const unsigned long long* pool, const uint32_t* gcount, const uint32_t* goff, uint32_t* ltp,
-                   WsHeader* hdr, cudaStream_t st) {
-  paint_go<IS3D, kPaintNW, kPaintMinB>(ngroups, fgm, meta, g, pool, gcount, goff, ltp, hdr, st);
+  k_dilate_paint<IS3D, NW, MINB, FUSED><<<grid, NW * 32, sizeof(PaintSmem<NW, FUSED>), st>>>(
+      fgm, shm, meta, g, pool, gcount, goff, point_at_knob(), ltp, labels, acc, device_fxlut(dev), hdr, nbid);
 }
 }  // namespace
 
-void launch_dilate_paint(const uint32_t* fgm, const TileMeta* meta, const unsigned long long* pool,
-                         const uint32_t* gcount, const uint32_t* goff, const Geom& g, uint32_t* ltp, WsHeader* hdr,
-                         cudaStream_t st) {
+void launch_dilate_paint(const uint32_t* fgm, const uint32_t* shm, const TileMeta* meta,
+                         const unsigned long long* pool, const uint32_t* gcount, const uint32_t* goff, const Geom& g,
+                         uint32_t* ltp, const int32_t* labels, const Accum* acc, WsHeader* hdr, cudaStream_t st) {
   const int64_t ngroups = launched_groups(g);
   if (ngroups <= 0) return;
-  if (g.ndim == 3)
-    paint_variant<true>(ngroups, fgm, meta, g, pool, gcount, goff, ltp, hdr, st);
-  else
-    paint_variant<false>(ngroups, fgm, meta, g, pool, gcount, goff, ltp, hdr, st);
+  Accum a{};
+  if (acc) a = *acc;
+  if (g.ndim == 3) {
+    if (acc) paint_go<true, kPaintNW, kPaintMinB, true>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, hdr, st);
+    else paint_go<true, kPaintNW, kPaintMinB, false>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, hdr, st);
+  } else {
+    if (acc) paint_go<false, kPaintNW, kPaintMinB, true>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, hdr, st);
+    else paint_go<false, kPaintNW, kPaintMinB, false>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, hdr, st);
+  }
 }
 
 cudaError_t dilate_cover_setup() {

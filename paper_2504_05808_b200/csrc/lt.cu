@@ -201,46 +201,20 @@ __global__ void __launch_bounds__(256) k_dilate_atomic(const TileMeta* __restric
 
 
 // ---------------------------------------------------------------------------------------
-// K5 epilogue (streaming, full occupancy): per element LT^2 from the LT plane, shell (D == 1),
-// LT outputs and the per-label reductions (a7); one warp per x-row of the produced z range,
-// 4 chunks of 32 elements in flight.
+// K5 epilogue (streaming): per element LT^2 from the LT plane, shell (D == 1), LT outputs and
+// optionally the per-label reductions (a7); one warp per x-row, 8 chunks of 32 elements in
+// flight.  The S&R path does not use it: its reductions are fused into the paint.
 // ---------------------------------------------------------------------------------------
-// fxlut[c] = round(sqrt(c) * 2^s) for c < kFxLut: the fixed-point LT terms of the sums
-// (and the scale exponent s in the header, for the epilogue's terms beyond the table)
-// track (host pipeline): record s + 1 in scale_set, or 0xFFFFFFFF once two chunks' scales differ
-__global__ void k_fxlut(unsigned long long* __restrict__ fxlut, int64_t nscale, WsHeader* __restrict__ hdr, int track) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= kFxLut) return;
-  const int s = sum_scale_log2(nscale, hdr->dmax);
-  fxlut[c] = (unsigned long long)__double2ull_rn(sqrt((double)c) * ldexp(1.0, s));
-  if (c == 0) {
-    hdr->scale_log2 = s;
-    if (track) {
-      const uint32_t prev = hdr->scale_set;
-      hdr->scale_set = (prev == 0u || prev == (uint32_t)s + 1u) ? (uint32_t)s + 1u : 0xFFFFFFFFu;
-    }
-  }
-}
-
-template <bool FAST>
 __global__ void __launch_bounds__(256) k_epilogue(const int32_t* __restrict__ lab, const uint32_t* __restrict__ Dg,
                                                   const uint32_t* __restrict__ ltp, Geom g, int64_t z_lo, int64_t nz,
                                                   Accum acc, int do_reduce, uint32_t* __restrict__ lt2_out,
                                                   float* __restrict__ lt_out, const unsigned long long* __restrict__ fxlut,
-                                                  WsHeader* __restrict__ hdr, int guard) {
-  // guard (host pipeline, per chunk): tiles left to the fallback kernel have no LT yet; the
-  // call then redoes the whole epilogue at the end
-  if (guard && hdr->n_fb != 0) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) hdr->epi_skipped = 1u;
-    return;
-  }
+                                                  WsHeader* __restrict__ hdr) {
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= g.B * nz * g.Y) return;
   const int64_t y = row % g.Y, zb = row / g.Y, z = z_lo + zb % nz, b = zb / nz;
   const int64_t base = ((b * g.Z + z) * g.Y + y) * g.X;
-  // the sums' fixed-point scale: k_fxlut ran before this kernel whenever do_reduce is set
-  const double scale = do_reduce ? ldexp(1.0, hdr->scale_log2) : 1.0;
   const bool wide = hdr->dmax > kU16Max;  // LT plane element type: u32 if wide, else u16
   const uint16_t* ltp16 = reinterpret_cast<const uint16_t*>(ltp);
   const int X = (int)g.X;
@@ -260,13 +234,50 @@ __global__ void __launch_bounds__(256) k_epilogue(const int32_t* __restrict__ la
 #pragma unroll
     for (int k = 0; k < kEpiChunks; ++k) {
       if (x0 + 32 * k >= X) break;  // warp-uniform
-      bad |= row_epilogue_v<FAST>(c[k], L[k], d[k], lane, base + x0 + 32 * k + lane, b, acc, do_reduce, scale, lt2_out,
-                            lt_out, fxlut);
+      bad |= row_epilogue_v(c[k], L[k], d[k], lane, base + x0 + 32 * k + lane, b, acc, do_reduce, lt2_out, lt_out,
+                            fxlut);
     }
   }
   if (__any_sync(kFull, bad) && lane == 0) atomicOr(&hdr->status, kStInternal);
 }
 
+// Per-label reductions of the tiles painted by the atomic fallback kernel (grid-stride over
+// the same work list as k_dilate_atomic): one CTA per tile, one warp per row, lane = x.
+template <bool IS3D>
+__global__ void __launch_bounds__(256) k_epilogue_fallback(const int32_t* __restrict__ lab, const uint32_t* __restrict__ Dg,
+                                                           const uint32_t* __restrict__ ltp,
+                                                           const TileMeta* __restrict__ meta,
+                                                           const uint32_t* __restrict__ fbl, Geom g, Accum acc,
+                                                           const unsigned long long* __restrict__ fxlut,
+                                                           WsHeader* __restrict__ hdr) {
+  constexpr int TY = IS3D ? 8 : 64, TZ = IS3D ? 8 : 1;
+  const bool wide = hdr->dmax > kU16Max;
+  const int64_t nitems = wide ? g.ntiles : (int64_t)hdr->n_fb;
+  const uint16_t* ltp16 = reinterpret_cast<const uint16_t*>(ltp);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t bad = 0;
+  for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int64_t tile = wide ? it : (int64_t)fbl[it];
+    int64_t t = tile;
+    const int64_t tx = t % g.ntx;
+    t /= g.ntx;
+    const int64_t ty = t % g.nty;
+    t /= g.nty;
+    const int64_t tz = t % g.ntz;
+    const int64_t b = t / g.ntz;
+    if (tz < g.tz_lo || tz >= g.tz_hi || meta[tile].nfg == 0) continue;  // (block-uniform)
+    for (int row = warp; row < kRows; row += 8) {
+      const int64_t gz = tz * TZ + row / TY, gy = ty * TY + row % TY, gx = tx * kTX + lane;
+      const bool in = gz < g.Z && gy < g.Y && gx < g.X;
+      const int64_t gi = ((b * g.Z + gz) * g.Y + gy) * g.X + gx;
+      const int32_t L = in ? __ldg(lab + gi) : 0;
+      const uint32_t d = in ? __ldg(Dg + gi) : 0u;
+      const uint32_t c = (in && L != 0) ? (wide ? __ldg(ltp + gi) : (uint32_t)__ldg(ltp16 + gi)) : 0u;
+      bad |= row_epilogue_v(c, L, d, lane, gi, b, acc, 1, nullptr, nullptr, fxlut);
+    }
+  }
+  if (__any_sync(kFull, bad) && lane == 0) atomicOr(&hdr->status, kStInternal);
+}
 
 }  // namespace
 
@@ -291,41 +302,30 @@ void launch_dilate_fallback(TileMeta* meta, const uint2* centres, const uint32_t
     k_dilate_atomic<false><<<grid, 256, smem, st>>>(meta, centres, g, fbl, ltp, hdr);
 }
 
-void launch_dilate(const int32_t* labels, const uint32_t* D, TileMeta* meta, const uint2* centres,
-                   const uint32_t* fgm, const uint16_t* oct, uint32_t* fbl, unsigned long long* pool,
-                   uint32_t* gcount, uint32_t* goff, const Geom& g, const Accum* acc, uint32_t* lt2_out, float* lt_out,
-                   bool force_fallback, uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
-  (void)labels;
-  (void)D;
-  (void)acc;
-  (void)lt2_out;
-  (void)lt_out;
-  (void)oct;
-  (void)force_fallback;
-  // K5b paints the groups K5a sorted; the atomic kernel takes the tiles K5a listed (or every
-  // tile when Dmax > 65535).  Both write LT^2 to ltp.
-  launch_dilate_paint(fgm, meta, pool, gcount, goff, g, ltp, hdr, st);
-  launch_dilate_fallback(meta, centres, fbl, g, ltp, hdr, st);
-}
-
 void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,
-                     float* lt_out, const uint32_t* ltp, unsigned long long* fxlut, WsHeader* hdr, cudaStream_t st, bool chunked) {
+                     float* lt_out, const uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
   Accum a{};
   if (acc) a = *acc;
-  // epilogue over the produced layers
+  int dev = 0;
+  cudaGetDevice(&dev);
   const int TZ = g.ndim == 3 ? kTZ3 : 1;
   const int64_t z_lo = g.tz_lo * TZ, z_hi = g.tz_hi * TZ < g.Z ? g.tz_hi * TZ : g.Z;
   const int64_t rows = g.B * (z_hi - z_lo) * g.Y;
-  if (acc) k_fxlut<<<kFxLut / 256, 256, 0, st>>>(fxlut, g.nscale, hdr, chunked ? 1 : 0);
-  if (rows > 0) {
-    if (acc && !lt2_out && !lt_out)
-      k_epilogue<true><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(labels, D, ltp, g, z_lo, z_hi - z_lo, a, 1, nullptr,
-                                                                  nullptr, fxlut, hdr, chunked ? 1 : 0);
-    else
-      k_epilogue<false><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(labels, D, ltp, g, z_lo, z_hi - z_lo, a, acc ? 1 : 0,
-                                                                   lt2_out, lt_out, acc ? fxlut : nullptr, hdr,
-                                                                   chunked ? 1 : 0);
-  }
+  if (rows > 0)
+    k_epilogue<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(labels, D, ltp, g, z_lo, z_hi - z_lo, a, acc ? 1 : 0, lt2_out,
+                                                          lt_out, device_fxlut(dev), hdr);
+}
+
+void launch_epilogue_fallback(const int32_t* labels, const uint32_t* D, const TileMeta* meta, const uint32_t* fbl,
+                              const Geom& g, const Accum& acc, const uint32_t* ltp, WsHeader* hdr, cudaStream_t st) {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)(g.ntiles < (int64_t)nsm * 8 ? g.ntiles : (int64_t)nsm * 8);
+  if (g.ndim == 3)
+    k_epilogue_fallback<true><<<grid, 256, 0, st>>>(labels, D, ltp, meta, fbl, g, acc, device_fxlut(dev), hdr);
+  else
+    k_epilogue_fallback<false><<<grid, 256, 0, st>>>(labels, D, ltp, meta, fbl, g, acc, device_fxlut(dev), hdr);
 }
 
 }  // namespace fastrs

@@ -11,20 +11,23 @@
 namespace fastrs {
 namespace {
 
-__global__ void k_metrics(Accum acc, Outputs o, int ndim, int64_t Nb, WsHeader* __restrict__ hdr) {
+__global__ void k_metrics(Accum acc, Outputs o, int ndim, WsHeader* __restrict__ hdr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int s = sum_scale_log2(Nb, hdr->dmax);
-  if (i == 0) hdr->scale_log2 = s;
+  if (i == 0) hdr->scale_log2 = 32;
   if (i >= acc.M) return;
   const unsigned long long V = acc.vol[i];
   const unsigned long long nsh = acc.nshell[i];
   const uint32_t m2 = acc.maxlt2[i];
   double sph = nan(""), rnd = nan(""), mean = nan(""), rmax = nan(""), smean = nan(""), cb = nan("");
   if (V > 0) {
-    const double scale = ldexp(1.0, s), inv = ldexp(1.0, -s);
-    mean = (double)acc.sum[i] * inv / (double)V;
+    // sums = hi * 2^32 + lo in units of 2^-32 (common.cuh "Accum")
+    const unsigned long long sh = acc.sum[i], sl = acc.sum[acc.M + i];
+    const unsigned long long ssh = acc.sumshell[i], ssl = acc.sumshell[acc.M + i];
+    const double inv = 1.0 / kFxScale;
+    mean = ((double)sh + (double)sl * inv) / (double)V;
     rmax = sqrt((double)m2);
-    smean = nsh ? (double)acc.sumshell[i] * inv / (double)nsh : nan("");
+    const double sshell = (double)ssh + (double)ssl * inv;  // sum of shell LT radii
+    smean = nsh ? sshell / (double)nsh : nan("");
     if (ndim == 3) {
       sph = sphericity_3d((double)V, mean);
       cb = c_axis_3d((double)V, mean);
@@ -34,13 +37,13 @@ __global__ void k_metrics(Accum acc, Outputs o, int ndim, int64_t Nb, WsHeader* 
     }
     // roundness r_bar / R_max evaluated in the fixed-point system the shell terms were
     // summed in: every shell term is <= fx(R_max) (monotone rounding), so the invariant
-    // r_bar <= R_max is checked exactly in integers, and R = 1 exactly when
-    // every shell element carries the maximum.
-    const unsigned long long fxmax = __double2ull_rn(rmax * scale);
-    const unsigned long long ss = acc.sumshell[i];
-    const unsigned long long hi = __umul64hi(nsh, fxmax), lo = nsh * fxmax;
-    if (nsh == 0 || (hi == 0 && ss > lo)) atomicOr(&hdr->status, kStShell);
-    rnd = ((double)ss / (double)nsh) / (double)fxmax;
+    // r_bar <= R_max is checked exactly in (128-bit) integers, and R = 1 exactly
+    // when every shell element carries the maximum.
+    const unsigned long long fxmax = __double2ull_rn(rmax * kFxScale);
+    const unsigned __int128 ss = ((unsigned __int128)ssh << 32) + (unsigned __int128)ssl;
+    const unsigned __int128 bound = (unsigned __int128)nsh * fxmax;
+    if (nsh == 0 || ss > bound) atomicOr(&hdr->status, kStShell);
+    rnd = (ss == bound) ? 1.0 : (sshell / (double)nsh) / rmax;
   }
   if (o.sphericity) o.sphericity[i] = sph;
   if (o.roundness) o.roundness[i] = rnd;
@@ -58,7 +61,7 @@ __global__ void k_metrics(Accum acc, Outputs o, int ndim, int64_t Nb, WsHeader* 
 
 void launch_metrics(const Accum& acc, const Geom& g, const Outputs& o, WsHeader* hdr, cudaStream_t st) {
   const int64_t blocks = (acc.M + 255) / 256;
-  k_metrics<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(acc, o, g.ndim, g.nscale, hdr);
+  k_metrics<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(acc, o, g.ndim, hdr);
 }
 
 }  // namespace fastrs

@@ -96,9 +96,16 @@ __global__ void k_mtable2(uint32_t* M) {
   M[t] = best;
 }
 
+// fixed-point sqrt table of the LT sums: fx(c) = round(sqrt(c) * 2^32), c < kFxLut
+__global__ void k_fxtable(unsigned long long* fx) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < kFxLut) fx[c] = (unsigned long long)__double2ull_rn(sqrt((double)c) * kFxScale);
+}
+
 struct DeviceTables {
   uint32_t* m3 = nullptr;
   uint32_t* m2 = nullptr;
+  unsigned long long* fx = nullptr;
 };
 std::mutex g_mu;
 DeviceTables g_tables[64];
@@ -128,9 +135,10 @@ struct PruneTile {
 
 
 template <bool IS3D, bool TMA>
-__global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, Geom g, TileMeta* __restrict__ meta,
+__global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D, Geom g, TileMeta* __restrict__ meta,
                                                uint2* __restrict__ cent, uint32_t* __restrict__ fgm,
-                                               uint16_t* __restrict__ oct, const uint32_t* __restrict__ M,
+                                               uint32_t* __restrict__ shm, uint16_t* __restrict__ oct,
+                                               const uint32_t* __restrict__ M,
                                                int64_t tile0, WsHeader* __restrict__ hdr,
                                                const __grid_constant__ CUtensorMap tmap) {
   using P = PruneTile<IS3D>;
@@ -236,6 +244,10 @@ __global__ void __launch_bounds__(256) k_prune(const uint32_t* __restrict__ D, G
     const uint32_t d = s[c];
     fgr[k] = d != 0 && gz < g.Z && gy < g.Y && gx < g.X;
     dr[k] = d;
+    // shell <=> D == 1 (a face neighbour or the flagged border is a site):
+    // the per-row shell mask for the fused reductions of K5
+    const uint32_t shb = __ballot_sync(kFullMask, fgr[k] && d == 1u);
+    if (lane == 0) shm[tile * kRows + row] = shb;
     const bool test = fgr[k] && d <= (uint32_t)dcap;
     m0r[k] = test ? __ldg(M + d) : 0xFFFFFFFFu;
     m1r[k] = test ? __ldg(M + (dcap + 1) + d) : 0xFFFFFFFFu;
@@ -434,15 +446,19 @@ cudaError_t ensure_mtables(int dev) {
   DeviceTables& dt = g_tables[dev];
   if (dt.m3) return cudaSuccess;
   uint32_t *m3 = nullptr, *m2 = nullptr;
+  unsigned long long* fx = nullptr;
   cudaError_t e = cudaMalloc(&m3, sizeof(uint32_t) * kClasses3 * (kDcap3 + 1));
   if (e == cudaSuccess) e = cudaMalloc(&m2, sizeof(uint32_t) * kClasses2 * (kDcap2 + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&fx, sizeof(unsigned long long) * kFxLut);
   if (e != cudaSuccess) {
     cudaFree(m3);
+    cudaFree(m2);
     return e;
   }
   const int64_t n3 = (int64_t)kClasses3 * (kDcap3 + 1), n2 = (int64_t)kClasses2 * (kDcap2 + 1);
   k_mtable3<<<(unsigned)((n3 + 127) / 128), 128>>>(m3);
   k_mtable2<<<(unsigned)((n2 + 127) / 128), 128>>>(m2);
+  k_fxtable<<<kFxLut / 256, 256>>>(fx);
   e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) e = dilate_cover_setup();
@@ -450,19 +466,25 @@ cudaError_t ensure_mtables(int dev) {
   if (e != cudaSuccess) {
     cudaFree(m3);
     cudaFree(m2);
+    cudaFree(fx);
     return e;
   }
   dt.m3 = m3;
   dt.m2 = m2;
+  dt.fx = fx;
   return cudaSuccess;
 }
+
+const unsigned long long* device_fxlut(int dev) { return (dev >= 0 && dev < 64) ? g_tables[dev].fx : nullptr; }
 
 void release_mtables() {
   std::lock_guard<std::mutex> lk(g_mu);
   for (auto& dt : g_tables) {
     if (dt.m3) cudaFree(dt.m3);
     if (dt.m2) cudaFree(dt.m2);
+    if (dt.fx) cudaFree(dt.fx);
     dt.m3 = dt.m2 = nullptr;
+    dt.fx = nullptr;
   }
 }
 
@@ -510,8 +532,8 @@ static bool prune_tensor_map(CUtensorMap* m, const uint32_t* D, const Geom& g) {
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, uint32_t* fgm, uint16_t* oct,
-                  WsHeader* hdr, cudaStream_t st, int64_t tz_lo, int64_t tz_hi) {
+void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, uint32_t* fgm, uint32_t* shm,
+                  uint16_t* oct, WsHeader* hdr, cudaStream_t st, int64_t tz_lo, int64_t tz_hi) {
   int dev = 0;
   cudaGetDevice(&dev);
   // tile layers [tz_lo, tz_hi) of item 0 (batch 1), or every tile
@@ -523,14 +545,14 @@ void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centr
   const bool tma = prune_tensor_map(&tmap, D, g);
   if (g.ndim == 3) {
     if (tma)
-      k_prune<true, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m3, tile0, hdr, tmap);
+      k_prune<true, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m3, tile0, hdr, tmap);
     else
-      k_prune<true, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m3, tile0, hdr, tmap);
+      k_prune<true, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m3, tile0, hdr, tmap);
   } else {
     if (tma)
-      k_prune<false, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m2, tile0, hdr, tmap);
+      k_prune<false, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m2, tile0, hdr, tmap);
     else
-      k_prune<false, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, oct, g_tables[dev].m2, tile0, hdr, tmap);
+      k_prune<false, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m2, tile0, hdr, tmap);
   }
 }
 

@@ -311,11 +311,13 @@ def slab_edt_z(packed_ext: torch.Tensor, own_lo: int, own_hi: int, z_ext0: int, 
 def slab_reduce(labels: torch.Tensor, d_ext: torch.Tensor, own_lo: int, own_hi: int, Z: int, dmax_global: int,
                 max_label: int, flags=BORDER_BACKGROUND, ws=None) -> dict:
     """Phase C: prune + dilation + shell + partial per-label sums of the own slab.  Returns
-    int64 tensors vol, n_shell, sum_lt, sum_shell_lt (u64 bit patterns) and int32 max_lt2."""
+    int64 tensors vol, n_shell (max_label), sum_lt, sum_shell_lt (2*max_label: the hi | lo words
+    of the 2^-32 fixed-point sums; u64 bit patterns) and int32 max_lt2."""
     labels = _labels_arg(labels)
     d_ext = d_ext.contiguous()
     dev = labels.device
-    part = {k: torch.empty(max_label, dtype=torch.int64, device=dev) for k in PARTIAL_KEYS[:4]}
+    part = {k: torch.empty(max_label * (2 if k.startswith("sum") else 1), dtype=torch.int64, device=dev)
+            for k in PARTIAL_KEYS[:4]}
     part["max_lt2"] = torch.empty(max_label, dtype=torch.int32, device=dev)
     ws = slab_workspace(d_ext.shape, dev) if ws is None else ws
     _check(load().fastrs_slab_reduce(labels.data_ptr(), d_ext.data_ptr(), _dims3(d_ext.shape), own_lo, own_hi, Z,

@@ -44,13 +44,12 @@ def _line_min(g, a, b, site_lo, site_hi):
     return res
 
 
-def sum_scale_log2(nb: int, dmax: int) -> int:
-    r = math.isqrt(dmax) if dmax > 0 else 0
-    if (r + 1) * (r + 1) <= dmax:
-        r += 1
-    clog = lambda v: 0 if v <= 1 else (v - 1).bit_length()  # noqa: E731
-    s = 62 - clog(nb) - clog(r + 1)
-    return max(0, min(32, s))
+FX_SCALE = 2.0 ** 32  # fixed-point scale of the LT sums (csrc/common.cuh "Accum")
+
+
+def split_sum(fx: np.ndarray) -> tuple[int, int]:
+    """(hi, lo) accumulator words of a sum of fixed-point terms: sum(t >> 32), sum(t & (2^32-1))."""
+    return int((fx >> np.uint64(32)).sum(dtype=np.uint64)), int((fx & np.uint64(0xFFFFFFFF)).sum(dtype=np.uint64))
 
 
 class NumpyPhases:
@@ -131,10 +130,10 @@ class NumpyPhases:
                     w = math.isqrt(rem)
                     sl = lt2[z - own_lo, y, max(0, cx - w):min(X, cx + w + 1)]
                     np.maximum(sl, D[cz, cy, cx], out=sl)
-        s = sum_scale_log2(Z * Y * X, dmax)
-        fx = np.rint(np.sqrt(lt2.astype(np.float64)) * 2.0 ** s).astype(np.uint64)
+        fx = np.rint(np.sqrt(lt2.astype(np.float64)) * FX_SCALE).astype(np.uint64)
         shell = D[own_lo:own_hi] == 1
-        part = {k: np.zeros(max_label, np.uint64) for k in ("vol", "n_shell", "sum_lt", "sum_shell_lt")}
+        part = {k: np.zeros(max_label, np.uint64) for k in ("vol", "n_shell")}
+        part.update({k: np.zeros(2 * max_label, np.uint64) for k in ("sum_lt", "sum_shell_lt")})
         part["max_lt2"] = np.zeros(max_label, np.int64)
         for k in range(1, max_label + 1):
             m = lab == k
@@ -142,19 +141,23 @@ class NumpyPhases:
                 continue
             part["vol"][k - 1] = m.sum()
             part["n_shell"][k - 1] = (m & shell).sum()
-            part["sum_lt"][k - 1] = fx[m].sum(dtype=np.uint64)
-            part["sum_shell_lt"][k - 1] = fx[m & shell].sum(dtype=np.uint64)
+            part["sum_lt"][k - 1], part["sum_lt"][max_label + k - 1] = split_sum(fx[m])
+            part["sum_shell_lt"][k - 1], part["sum_shell_lt"][max_label + k - 1] = split_sum(fx[m & shell])
             part["max_lt2"][k - 1] = lt2[m].max()
         out = {k: torch.from_numpy(v.view(np.int64).copy()) for k, v in part.items() if k != "max_lt2"}
         out["max_lt2"] = torch.from_numpy(part["max_lt2"].astype(np.int32))
         return out
 
     def metrics(self, part, nscale, dmax, stats):
-        s = sum_scale_log2(nscale, dmax)
         vol = part["vol"].numpy().view(np.uint64).astype(np.float64)
         nsh = part["n_shell"].numpy().view(np.uint64).astype(np.float64)
-        sm = part["sum_lt"].numpy().view(np.uint64).astype(np.float64) * 2.0 ** -s
-        ss = part["sum_shell_lt"].numpy().view(np.uint64).astype(np.float64) * 2.0 ** -s
+        M = vol.shape[0]
+
+        def total(k):
+            w = part[k].numpy().view(np.uint64).astype(np.float64)
+            return w[:M] + w[M:] / FX_SCALE
+
+        sm, ss = total("sum_lt"), total("sum_shell_lt")
         mx = np.sqrt(part["max_lt2"].numpy().astype(np.float64))
         with np.errstate(invalid="ignore", divide="ignore"):
             a = sm / vol

@@ -298,9 +298,9 @@ def test_host_entry_point_pipelined_matches_device_call(F):
     s, r = F.sphericity_roundness_host(lab, max_label=ml)
     np.testing.assert_array_equal(s, want["sphericity"].cpu().numpy())
     np.testing.assert_array_equal(r, want["roundness"].cpu().numpy())
-    # small grains in the first chunks and a large ball near the end: the per-chunk epilogues
-    # run with the fixed-point scale of a smaller Dmax than the final one, so the call redoes
-    # the reductions; still bit-identical
+    # small grains in the first chunks and a large ball near the end: Dmax grows from chunk to
+    # chunk.  The fused per-chunk reductions use the fixed 2^-32 scale (no dependence on Dmax,
+    # ADVICE r1), so they are final: bit-identical to the device call and equal to the oracle
     mixed = np.zeros((512, 96, 96), np.int32)
     k = 0
     for z in range(8, 300, 12):
@@ -312,6 +312,9 @@ def test_host_entry_point_pipelined_matches_device_call(F):
     s, r = F.sphericity_roundness_host(mixed, max_label=k + 1)
     np.testing.assert_array_equal(s, want["sphericity"].cpu().numpy())
     np.testing.assert_array_equal(r, want["roundness"].cpu().numpy())
+    ref = oracle.sphericity_roundness(mixed, max_label=k + 1)
+    np.testing.assert_allclose(s, ref["sphericity"], rtol=RTOL, atol=0)
+    np.testing.assert_allclose(r, ref["roundness"], rtol=RTOL, atol=0)
     big = np.zeros((520, 310, 310), np.int32)
     big[5:306, 5:306, 5:306] = synth.sphere(150, canvas=301)
     big[400:440, 100:120, 100:130] = 2
