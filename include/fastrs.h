@@ -102,6 +102,8 @@ typedef struct {
   uint32_t n_regathers;  /* K5: list overflows that needed a second gather pass         */
   uint32_t max_group_list; /* K5: longest per-group candidate list                      */
   uint64_t sum_group_list; /* K5: candidates summed over tile groups                    */
+  uint64_t n_painted;      /* K5: balls painted row-parallel after the screens (S&R call) */
+  uint64_t n_covering;     /* K5: painted balls that covered at least one cell (S&R call) */
 } fastrs_diagnostics;
 
 /* Bytes of device workspace needed by every entry point below for this geometry.

@@ -588,6 +588,8 @@ int fastrs_read_diagnostics(const void* ws, fastrs_diagnostics* out, void* strea
   out->n_regathers = h.n_regathers;
   out->max_group_list = h.max_group_list;
   out->sum_group_list = h.sum_group_list;
+  out->n_painted = h.n_painted;
+  out->n_covering = h.n_covering;
   return FASTRS_OK;
 }
 

@@ -62,6 +62,9 @@ struct WsHeader {
   uint32_t pad2[2];
   uint32_t paint_next;   // K5b work counter (reset before each launch)
   uint32_t sat_n;        // K2/K3: CTAs listed for the exact 32-bit column pass (reset per launch)
+  uint32_t pad3;
+  unsigned long long n_painted;   // K5b: balls painted (lanes over rows) after the screens
+  unsigned long long n_covering;  // K5b: painted balls that covered at least one cell
 };
 static_assert(sizeof(WsHeader) <= 256, "header");
 

@@ -75,6 +75,7 @@ struct PaintSmem {  // K5b (one tile per warp)
   uint32_t qb[NW][32];            //        and (D | shell count << 16)
 };
 
+
 template <bool IS3D>
 struct Shape {
   static constexpr int TY = IS3D ? 8 : 64, TZ = IS3D ? 8 : 1;
@@ -796,7 +797,7 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
     __syncwarp();
   };
 
-  uint32_t n_rows = 0;
+  uint32_t n_rows = 0, n_painted = 0, n_covering = 0;  // (the last two warp-uniform)
   bool dirty = false;  // my rows' coverage changed since the masks were last refreshed
   {
     // --- cover: my tile, balls in descending D.  Lanes first screen 32 balls at a time (reach
@@ -891,10 +892,11 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
         const int ns = __popc(act);
         for (int j = 0; j < ns; ++j) {
           const int4 bp = sball[j];
+          const int jR2 = bp.w - 1;
+          ++n_painted;
           uint32_t ecnt = 0, escnt = 0;  // fused: cells of my rows this ball covers first
           int efirst = -1;
           const uint2 jc2 = reinterpret_cast<const uint2*>(scand)[j];  // candidate rows 0-31 | 32-63
-          const int jR2 = bp.w - 1;
           const uint16_t dv = (uint16_t)bp.w;
           // 3D: rows lane and lane + 32 share ly, and lie 4 layers apart
           const int dy0 = ly0 - bp.y, dz0 = lz0 - bp.z;
@@ -947,6 +949,7 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
           if (FUSED) {
             const uint32_t who = __ballot_sync(kFull, ecnt != 0);
             if (who) {
+              ++n_covering;
               const uint32_t tc = __reduce_add_sync(kFull, ecnt), ts = __reduce_add_sync(kFull, escnt);
               const int off = __shfl_sync(kFull, efirst, __ffs(who) - 1);
               ev_push((uint32_t)off, tc, (uint32_t)bp.w, ts);
@@ -972,6 +975,8 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
 
   n_rows = __reduce_add_sync(kFull, n_rows);
   if (lane == 0 && n_rows) atomicAdd(&hdr->n_intervals, (unsigned long long)n_rows);
+  if (lane == 0 && n_painted) atomicAdd(&hdr->n_painted, (unsigned long long)n_painted);
+  if (lane == 0 && n_covering) atomicAdd(&hdr->n_covering, (unsigned long long)n_covering);
   if (FUSED) {
     if (nev) ev_flush();
     // every foreground cell lies in some kept ball that reaches the tile

@@ -47,7 +47,8 @@ class _Diag(ctypes.Structure):
                 ("n_kept", ctypes.c_uint64), ("n_intervals", ctypes.c_uint64),
                 ("sum_scale_log2", ctypes.c_int32), ("n_fallback", ctypes.c_uint32),
                 ("n_rounds_extra", ctypes.c_uint32), ("n_regathers", ctypes.c_uint32),
-                ("max_group_list", ctypes.c_uint32), ("sum_group_list", ctypes.c_uint64)]
+                ("max_group_list", ctypes.c_uint32), ("sum_group_list", ctypes.c_uint64),
+                ("n_painted", ctypes.c_uint64), ("n_covering", ctypes.c_uint64)]
 
 
 def load(build_if_missing: bool = True) -> ctypes.CDLL:
