@@ -7,11 +7,20 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "fastrs.h"
 
 namespace fastrs {
 namespace {
+
+// NVTX range per stage of a call (host-side launch ranges; visible to Nsight tools, no cost
+// without an attached tool)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 thread_local std::string t_err = "";
 
@@ -191,17 +200,27 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
   if (lt_out) cudaMemsetAsync(lt_out, 0, (size_t)g.N * 4, st);
 
   // K1..K3: EDT
-  launch_edt_x(labels, nullptr, A, g, stage == kFull ? max_label : INT32_MAX, border, hdr, st);
+  Nvtx call_range(stage == kFull ? "fastrs_sphericity_roundness" : stage == kLtOnly ? "fastrs_local_thickness"
+                                                                                   : "fastrs_edt_sq");
+  {
+    Nvtx r("K1 edt_x");
+    launch_edt_x(labels, nullptr, A, g, stage == kFull ? max_label : INT32_MAX, border, hdr, st);
+  }
   tm.mark(0);
   uint32_t* D;
   if (g.ndim == 2) {
     D = stage == kEdtOnly ? d2_out : B;
+    Nvtx r("K2 edt_y (final)");
     launch_edt_col(A, D, g, 1, true, border, hdr, sat, st);
     tm.mark(1);
   } else {
-    launch_edt_col(A, B, g, 1, false, border, hdr, sat, st);
+    {
+      Nvtx r("K2 edt_y");
+      launch_edt_col(A, B, g, 1, false, border, hdr, sat, st);
+    }
     tm.mark(1);
     D = stage == kEdtOnly ? d2_out : A;
+    Nvtx r("K3 edt_z");
     launch_edt_col(B, D, g, 2, true, border, hdr, sat, st);
     tm.mark(2);
   }
@@ -209,28 +228,42 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
     uint32_t* fgm = (uint32_t*)(w + L.fgm);
     uint32_t* shm = (uint32_t*)(w + L.shm);
     uint16_t* oct = (uint16_t*)(w + L.oct);
-    launch_prune(D, g, meta, cent, fgm, shm, oct, hdr, st);  // K4
+    {
+      Nvtx r("K4 prune");
+      launch_prune(D, g, meta, cent, fgm, shm, oct, hdr, st);
+    }
     tm.mark(3);
     uint32_t* ltp = D == A ? B : A;  // the plane the EDT no longer needs holds LT^2 (fallback / LT outputs)
     uint32_t* fbl = (uint32_t*)(w + L.fbl);
     unsigned long long* pool = (unsigned long long*)(w + L.pool);
     uint32_t* gcount = (uint32_t*)(w + L.gcount);
     uint32_t* goff = (uint32_t*)(w + L.goff);
-    launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, g, (flags & kFlagForceFallback) != 0 ? 1 : 0,
-                         hdr, st);  // K5a
+    {
+      Nvtx r("K5a gather");
+      launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, g, (flags & kFlagForceFallback) != 0 ? 1 : 0,
+                           hdr, st);
+    }
     tm.mark(7);
     // K5b: with the reductions fused (S&R) or writing the LT plane (LT outputs); K5' for the
     // tiles K5a handed over (every tile when Dmax > 65535)
-    launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, g, ltp, labels, stage == kFull ? &acc : nullptr, hdr, st);
-    launch_dilate_fallback(meta, cent, fbl, g, ltp, hdr, st);
+    {
+      Nvtx r("K5b paint + K5' fallback");
+      launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, g, ltp, labels, stage == kFull ? &acc : nullptr, hdr, st);
+      launch_dilate_fallback(meta, cent, fbl, g, ltp, hdr, st);
+    }
     tm.mark(4);
     if (stage == kFull) {
-      launch_epilogue_fallback(labels, D, meta, fbl, g, acc, ltp, hdr, st);  // K5e on the fallback tiles only
+      {
+        Nvtx r("K5e fallback-tile reductions");
+        launch_epilogue_fallback(labels, D, meta, fbl, g, acc, ltp, hdr, st);
+      }
       tm.mark(6);
-      launch_metrics(acc, g, *outs, hdr, st);  // K6
+      Nvtx r("K6 metrics");
+      launch_metrics(acc, g, *outs, hdr, st);
       tm.mark(5);
     } else {
-      launch_epilogue(labels, D, g, nullptr, lt2_out, lt_out, ltp, hdr, st);  // LT outputs
+      Nvtx r("K5e LT outputs");
+      launch_epilogue(labels, D, g, nullptr, lt2_out, lt_out, ltp, hdr, st);
       tm.mark(6);
     }
   }

@@ -206,18 +206,45 @@ def test_config_full(F, cfg):
 
 
 def test_config_c3_full(F):
+    """C3 in full (512^3, 2000 grains), element by element: D, LT^2 (default and fallback
+    dilation), the float LT radius, and every per-label output."""
     lab, info = synth.make_config(3)
-    full_check(F, lab, 1, max_label=info["max_label"], fields=False)
+    full_check(F, lab, 1, max_label=info["max_label"], fields=True)
 
 
 def test_config_c5_subset(F):
+    """Three C5 images (touching cells), element by element.  Their Dmax exceeds the 1536-bin
+    single-pass sort, so K5a builds every candidate list in exact D-bucket rounds."""
     lab, info = synth.make_config(5, batch=3)
-    full_check(F, lab, 1, ndim=2, max_label=info["max_label"], fields=False)
+    full_check(F, lab, 1, ndim=2, max_label=info["max_label"], fields=True)
+    d = F.diagnostics(F.last_workspace())
+    assert d["dmax"] > 1536, d
 
 
 @pytest.fixture(scope="module")
 def c4():
     return synth.make_config(4)
+
+
+def test_config_c4_label_subset_fields(F, c4):
+    """C4 at full size (1024^3) with 2000 grains kept (its 250 largest and 1750 drawn at random)
+    and the others zeroed (exact: C4 grains are separated by >= 1 voxel, so the kept grains' D
+    and LT^2 are unchanged), element by element against the oracle's full-grid fields.  The
+    large grains' candidate lists overflow the shared list, so K5a's regather path is
+    exercised."""
+    lab, info = c4
+    ml = info["max_label"]
+    counts = np.bincount(lab.reshape(-1), minlength=ml + 1)
+    order = np.argsort(counts[1:]) + 1
+    rng = np.random.default_rng(45)
+    keep = np.zeros(ml + 1, bool)
+    keep[order[-250:]] = True
+    keep[rng.choice(order[:-250], 1750, replace=False)] = True
+    sub = np.where(keep[lab], lab, 0).astype(np.int32)
+    full_check(F, sub, 1, max_label=ml, fields=True)
+    d = F.diagnostics(F.last_workspace())
+    assert d["n_regathers"] > 0, d
+    del sub
 
 
 def test_config_c4_sampled(F, c4):
