@@ -34,17 +34,21 @@ sys.path.insert(0, ROOT)
 METRIC = "Gvoxels/s end-to-end (EDT+LT+sphericity+roundness); % of HBM roofline"
 UNIT = "Gvoxels/s"
 
-# algorithmic HBM bytes per grid element of each stage (DESIGN.md §6 "Algorithmic bytes"), 3D path
-# K5b writes LT^2 as u16 (Dmax <= 65535) and K5e reads labels, D and that u16 plane
-STAGE_BYTES_PER_ELEM = {"edt_x": 8.0, "edt_y": 8.0, "edt_z": 8.0, "prune": 4.0, "gather": 0.0, "dilate": 2.0,
-                        "epilogue": 10.0, "metrics": 0.0}
-STAGE_BYTES_PER_KEPT = {"prune": 8.0, "gather": 8.0}  # centre entries written by K4 / read once by K5a
-STAGE_BYTES_PER_CAND = {"gather": 8.0, "dilate": 8.0}  # sorted per-group candidates: written by K5a, read by K5b
-# the kernel behind each stage (names in the ncu summaries under profiles/)
-STAGE_KERNEL = {"edt_x": "k_edt_x", "edt_y": "k_edt_col<0>", "edt_z": "k_edt_col<1>", "prune": "k_prune<1>",
-                "gather": "k_dilate_gather<1>", "dilate": "k_dilate_paint<1>", "epilogue": "k_epilogue",
-                "metrics": "k_metrics"}
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r01_ncu_summary_c4.json")
+# SURVEY.md §8(d) "Algorithmic bytes per element" (the roofline numerator): what
+# the method must move with a multi-pass exact separable EDT on a grid larger than on-chip
+# memory.  3D: K1 8, K2 8, K3 8, K4 4 (+8 per kept centre), K5 (dilate + shell + reduce) 5 =
+# labels 4 + the shell flag 1; 2D: no K3.  K6 (per-label closed forms) is negligible.
+ALG_BYTES_PER_ELEM = {"edt_x": 8.0, "edt_y": 8.0, "edt_z": 8.0, "prune": 4.0, "k5": 5.0, "metrics": 0.0}
+ALG_BYTES_PER_KEPT = {"prune": 8.0}
+# the library's per-stage CUDA events (fastrs_profile): K5 as §8(d) defines it is the candidate
+# gather K5a + the paint with fused reductions K5b (+ the atomic fallback K5' and its
+# reductions K5e, empty on the configs)
+K5_PARTS = ("gather", "dilate", "epilogue")
+# the kernels behind each stage (names in the ncu summaries under profiles/)
+STAGE_KERNELS = {"edt_x": ["k_edt_x"], "edt_y": ["k_edt_col16<0", "k_edt_col<0"], "edt_z": ["k_edt_col16<1", "k_edt_col<1"],
+                 "prune": ["k_prune<1"], "k5": ["k_dilate_gather<1", "k_dilate_paint<1", "k_dilate_atomic<1",
+                                               "k_epilogue_fallback<1"], "metrics": ["k_metrics"]}
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02_ncu_summary_c4.json")
 
 
 def parse():
@@ -56,7 +60,8 @@ def parse():
     p.add_argument("--config", type=int, default=4, help="BASELINE.json config C1..C5 (default C4)")
     p.add_argument("--batch", type=int, default=None, help="C5 images per rank")
     p.add_argument("--e2e-steps", type=int, default=3)
-    p.add_argument("--cpu-sample-labels", type=int, default=1000)
+    p.add_argument("--cpu-sample-slices", type=int, default=96,
+                   help="CPU oracle sample: z-slices of the volume (3D) or images of the batch (2D)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--mode", default="volumes", choices=["volumes", "slab"],
                    help="volumes: one independent volume per rank (weak scaling, default); slab: one volume "
@@ -89,23 +94,30 @@ def ncu_record(kernel: str):
     return k
 
 
-def ncu_traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu summary, or None."""
-    k = ncu_record(kernel)
-    return None if k is None else k["traffic_bytes_per_launch"]
+def ncu_traffic(kernels) -> float | None:
+    """DRAM bytes per launch summed over `kernels` (committed ncu summary), None if absent."""
+    tot, found = 0.0, False
+    for k in kernels:
+        rec = ncu_record(k)
+        if rec is not None:
+            tot += rec["traffic_bytes_per_launch"]
+            found = True
+    return tot if found else None
 
 
-def issue_roofline(per_launch: dict, sm_mhz: float, n_sm: int) -> dict:
+def issue_roofline(per_stage_ms: dict, sm_mhz: float, n_sm: int) -> dict:
     """Instruction-issue roofline per stage: warp instructions per launch (committed ncu summary)
     / the live per-launch time, against 4 schedulers x 1 warp instruction per clock per SM at the
-    SM clock sampled during the run.  The kernels of this path are issue-bound, not HBM-bound."""
+    SM clock sampled during the run.  The explanation of the HBM fractions: the kernels of this
+    path are bound by instruction issue on data-dependent work, not by HBM bandwidth."""
     peak = n_sm * 4 * sm_mhz * 1e6
     out = {}
-    for stage, ms in per_launch.items():
-        rec = ncu_record(STAGE_KERNEL.get(stage, ""))
-        if rec is None or ms <= 0 or not rec.get("warp_instructions"):
+    for stage, ms in per_stage_ms.items():
+        recs = [ncu_record(k) for k in STAGE_KERNELS.get(stage, [])]
+        wi = sum(r["warp_instructions"] or 0 for r in recs if r is not None)
+        if ms <= 0 or not wi:
             continue
-        ach = rec["warp_instructions"] / (ms * 1e-3)
+        ach = wi / (ms * 1e-3)
         out[stage] = {"achieved_winst_per_s": ach, "frac": round(ach / peak, 4)}
     return {"peak_winst_per_s": peak, "sm_mhz": sm_mhz, "sms": n_sm, "source": os.path.relpath(NCU_SUMMARY, ROOT),
             "stages": out}
@@ -171,32 +183,32 @@ def make_input(cfg: int, batch):
     return lab, info, ndim
 
 
-def cpu_baseline(lab, info, ndim, n_labels: int, seed: int = 12345) -> dict:
-    """Time the oracle, as it stands, on a seeded sample of labels of the same workload."""
+def oracle_sample(lab, ndim: int, slices: int):
+    """The bounded CPU sample of a workload: a contiguous block of the volume (3D: `slices`
+    z-slices from the middle; 2D batch: `slices` images) processed as its own grid."""
+    if ndim == 3:
+        z0 = max(0, (lab.shape[0] - slices) // 2)
+        return np.ascontiguousarray(lab[z0:z0 + slices]), f"z-slab [{z0}, {z0 + slices}) of the volume"
+    if lab.ndim == 3:
+        return np.ascontiguousarray(lab[:slices]), f"images [0, {min(slices, lab.shape[0])}) of the batch"
+    return lab, "the whole image"
+
+
+def cpu_baseline(lab, info, ndim, slices: int) -> dict:
+    """Time the oracle, as it stands, on the host cores on a bounded sample of the same workload
+    (oracle_sample), processed as its own grid; value = sample elements / oracle wall time."""
     import oracle
+    sub, where = oracle_sample(lab, ndim, slices)
     ml = info["max_label"]
-    B = lab.shape[0] if lab.ndim == ndim + 1 else 1
-    M = B * ml
-    counts = np.bincount(lab.reshape(-1), minlength=ml + 1) if B == 1 else None
-    rng = np.random.default_rng(seed)
-    k = min(n_labels, M)
-    mask = np.zeros(M, np.uint8)
-    mask[rng.choice(M, k, replace=False)] = 1
     cores = os.cpu_count() or 1
     t0 = time.perf_counter()
-    oracle.sphericity_roundness(lab, max_label=ml, ndim=ndim, label_mask=mask, nthreads=cores)
+    oracle.sphericity_roundness(sub, max_label=ml, ndim=ndim, nthreads=cores)
     dt = time.perf_counter() - t0
-    if counts is not None:
-        fg_all = int(counts[1:].sum())
-        fg_s = int(counts[1:][mask.astype(bool)].sum())
-    else:
-        fg_all, fg_s = int(np.count_nonzero(lab)), int(np.count_nonzero(lab)) * k / M
-    frac = fg_s / max(fg_all, 1)
-    value = lab.size * frac / dt / 1e9
-    return {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": (f"{k} of {M} labels (seed {seed}), all {lab.size} grid elements scanned for "
-                       f"bounding boxes; value = grid elements x sampled-foreground fraction "
-                       f"({frac:.4f}) / oracle wall time ({dt:.2f} s)"),
+    n_obj = int(np.count_nonzero(np.bincount(sub.reshape(-1), minlength=ml + 1)[1:])) if sub.ndim == ndim else None
+    return {"value": sub.size / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": (f"{where}: {sub.size} grid elements" + (f", {n_obj} objects" if n_obj is not None else "")
+                       + f", run as its own grid (border background); value = elements / oracle wall time "
+                       f"({dt:.2f} s on {cores} threads)"),
             "seconds": dt}
 
 
@@ -207,13 +219,14 @@ def run_reference(args):
     lab, info, ndim = make_input(args.config, args.batch)
     vals = []
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(lab, info, ndim, max(50, args.cpu_sample_labels // 4), seed=1000 + i)
+        cb = cpu_baseline(lab, info, ndim, args.cpu_sample_slices)
         if i >= args.warmup:
             vals.append(cb)
     v = statistics.mean(c["value"] for c in vals)
     sec = statistics.mean(c["seconds"] for c in vals)
     cb = dict(vals[-1])
     cb["value"] = v
+    cb.pop("seconds", None)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
@@ -303,32 +316,36 @@ def run_fastrs(args):
     e2e_value = total_elems / (float(e2e_ms.item()) * 1e-3) / 1e9
     np.testing.assert_array_equal(hs, out["sphericity"].cpu().numpy())
 
-    # ---- roofline of the dominant kernel ---------------------------------------------------
+    # ---- roofline (SURVEY.md §8(d) algorithmic bytes / live CUDA-event stage times) ----------
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    per_launch = {k: v / max(calls, 1) for k, v in stage_ms.items()}
-    dom = max(per_launch, key=lambda k: per_launch[k])
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback"
+    per = {k: v / max(calls, 1) for k, v in stage_ms.items()}  # ms per call and stage
+    stage_ms_alg = {"edt_x": per["edt_x"], "edt_y": per["edt_y"], "prune": per["prune"], "metrics": per["metrics"],
+                    "k5": sum(per[k] for k in K5_PARTS)}
+    if ndim == 3:
+        stage_ms_alg["edt_z"] = per["edt_z"]
     n = lab.size
 
-    def stage_bytes(k):
-        return (STAGE_BYTES_PER_ELEM[k] * n + STAGE_BYTES_PER_KEPT.get(k, 0.0) * diag["n_kept"]
-                + STAGE_BYTES_PER_CAND.get(k, 0.0) * diag["sum_group_list"])
+    def alg_bytes(k):
+        return ALG_BYTES_PER_ELEM[k] * n + ALG_BYTES_PER_KEPT.get(k, 0.0) * diag["n_kept"]
 
-    alg_bytes = stage_bytes(dom)
-    achieved = alg_bytes / (per_launch[dom] * 1e-3) / 1e9
-    stage_gbs = {}
-    for k, v in per_launch.items():
-        if v > 0:
-            b = stage_bytes(k)
-            stage_gbs[k] = {"ms": round(v, 4), "GB/s": round(b / (v * 1e-3) / 1e9, 1),
-                            "frac": round(b / (v * 1e-3) / 1e9 / hbm_peak, 4)}
-    model_bytes = sum(stage_bytes(k) for k in per_launch if per_launch[k] > 0)
-    pipe_gbs = model_bytes / (ms * 1e-3) / 1e9
+    stages = {}
+    for k, v in stage_ms_alg.items():
+        gbs = alg_bytes(k) / (v * 1e-3) / 1e9 if v > 0 else 0.0
+        stages[k] = {"ms": round(v, 4), "alg_bytes": alg_bytes(k), "GB/s": round(gbs, 1),
+                     "frac": round(gbs / hbm_peak, 4), "kernels": STAGE_KERNELS[k]}
+    dom = max((k for k in stage_ms_alg if k != "metrics"), key=lambda k: stage_ms_alg[k])
+    dom_bytes = alg_bytes(dom)
+    achieved = dom_bytes / (stage_ms_alg[dom] * 1e-3) / 1e9
+    lt_bytes = alg_bytes("prune") + alg_bytes("k5")
+    lt_ms = stage_ms_alg["prune"] + stage_ms_alg["k5"]
+    path_bytes = sum(alg_bytes(k) for k in stage_ms_alg)
+    path_gbs = path_bytes / (ms * 1e-3) / 1e9
 
     if rank != 0:
         if world > 1:
@@ -336,7 +353,7 @@ def run_fastrs(args):
         return
     cb = None
     if not args.no_cpu_baseline and world == 1:
-        cb = cpu_baseline(lab, info, ndim, args.cpu_sample_labels)
+        cb = cpu_baseline(lab, info, ndim, args.cpu_sample_slices)
         cb.pop("seconds", None)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -348,16 +365,22 @@ def run_fastrs(args):
                    "input_sha256": info["sha256"], "input_hash_kind": info.get("sha256_kind")},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(lab.nbytes),
                 "d2h_bytes_per_step": int(2 * M * 8), "ms_per_step": float(e2e_ms.item())},
-        "gpu_launches": int((10 if ndim == 3 else 9) * args.steps),  # K1 K2 (K3) K4 K5a K5b K5' fxlut K5e K6
-        "roofline": {"bound": "hbm", "kernel": STAGE_KERNEL[dom], "stage": dom, "achieved": achieved,
+        # K1 K2 (+fixup) K3 (+fixup) K4 K5a K5b K5' K5e K6 (3D); the 2D path has no K3
+        "gpu_launches": int((11 if ndim == 3 else 9) * args.steps),
+        "roofline": {"bound": "hbm", "stage": dom, "kernels": STAGE_KERNELS[dom], "achieved": achieved,
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                     "traffic": ncu_traffic(STAGE_KERNEL[dom]),
+                     "traffic": ncu_traffic(STAGE_KERNELS[dom]),
                      "traffic_source": os.path.relpath(NCU_SUMMARY, ROOT), "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": alg_bytes},
-        "stages": stage_gbs,
-        "issue_roofline": issue_roofline(per_launch, float(clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0),
+                     "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": stage_ms_alg[dom],
+                     "bytes_rule": "SURVEY.md §8(d): K1 8, K2 8, K3 8, K4 4 + 8/kept centre, K5 5 B per grid element"},
+        # the north-star number: local-thickness + reduction kernels (K4 + K5) against HBM
+        "lt_reduction": {"stages": ["prune", "k5"], "ms": lt_ms, "alg_bytes": lt_bytes,
+                         "GB/s": lt_bytes / (lt_ms * 1e-3) / 1e9,
+                         "frac": lt_bytes / (lt_ms * 1e-3) / 1e9 / hbm_peak},
+        "path": {"alg_bytes": path_bytes, "GB/s": path_gbs, "frac": path_gbs / hbm_peak},
+        "stages": stages,
+        "issue_roofline": issue_roofline(stage_ms_alg, float(clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0),
                                          torch.cuda.get_device_properties(dev).multi_processor_count),
-        "pipeline_model": {"bytes_per_step": model_bytes, "GB/s": pipe_gbs, "frac": pipe_gbs / hbm_peak},
         "diagnostics": {k: int(v) for k, v in diag.items()},
         "clocks": clk,
         "cpu_baseline": cb,
