@@ -3,10 +3,14 @@
 sphericity/roundness) over one synthetic label volume.
 
 Default workload: BASELINE.json configs[3] (C4: 3D 1024^3 int32, ~20000 smooth + rough
-grains, ~30 % fill) — the 1024^3 volume the north-star target is quoted on; it fits one
-GPU.  With --gpus N (torchrun, one rank per GPU) every rank processes its own C4 volume:
-independent volumes sharded across GPUs, no data-path
-collective, "scaling": "weak".
+grains, ~30 % fill) -- the 1024^3 volume the north-star target is quoted on; it fits one GPU.
+With --gpus N > 1 (torchrun, one rank per GPU):
+  * a 3D config (default C4) is split into N z-slabs of ONE volume: every step is one
+    fastrs_sphericity_roundness_slab call with NCCL inside libfastrs (N8 halo z pass, or the
+    N1 all-to-all transpose with --zpass transpose), "scaling": "strong";
+  * C5 shards one seeded 256-image batch, rank r taking images [256r/N, 256(r+1)/N), no
+    data-path collective, "scaling": "strong";
+  * --mode volumes gives every rank its own volume ("scaling": "weak").
 
 Timing: W warm-up steps, then K steps between barrier + cudaDeviceSynchronize, CUDA events
 on the call's stream, max over ranks.  Inputs (4 GiB labels, ~16 GiB workspace) are larger
@@ -48,6 +52,8 @@ K5_PARTS = ("gather", "dilate", "epilogue")
 STAGE_KERNELS = {"edt_x": ["k_edt_x"], "edt_y": ["k_edt_col16<0", "k_edt_col<0"], "edt_z": ["k_edt_col16<1", "k_edt_col<1"],
                  "prune": ["k_prune<1"], "k5": ["k_dilate_gather<1", "k_dilate_paint<1", "k_dilate_atomic<1",
                                                "k_epilogue_fallback<1"], "metrics": ["k_metrics"]}
+STAGE_KERNELS_2D = dict(STAGE_KERNELS, edt_y=["k_edt_col16<1", "k_edt_col<1"], prune=["k_prune<0"],
+                        k5=["k_dilate_gather<0", "k_dilate_paint<0", "k_dilate_atomic<0", "k_epilogue_fallback<0"])
 NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02_ncu_summary_c4.json")
 
 
@@ -63,9 +69,13 @@ def parse():
     p.add_argument("--cpu-sample-slices", type=int, default=96,
                    help="CPU oracle sample: z-slices of the volume (3D) or images of the batch (2D)")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--mode", default="volumes", choices=["volumes", "slab"],
-                   help="volumes: one independent volume per rank (weak scaling, default); slab: one volume "
-                        "split into z-slabs across the ranks (strong scaling, NCCL halo exchanges)")
+    p.add_argument("--mode", default="auto", choices=["auto", "volumes", "slab"],
+                   help="auto (default): N=1 the single-GPU call; N>1 a 3D config is split into z-slabs (one "
+                        "volume, strong scaling, NCCL inside libfastrs) and C5 shards one seeded image batch "
+                        "(strong scaling); volumes: an independent volume per rank (weak scaling); slab: the "
+                        "z-slab path at any N")
+    p.add_argument("--zpass", default="halo", choices=["halo", "transpose"],
+                   help="slab z pass: h-slice halo (N8) or all-to-all z->y transpose (N1)")
     return p.parse_args()
 
 
@@ -105,7 +115,7 @@ def ncu_traffic(kernels) -> float | None:
     return tot if found else None
 
 
-def issue_roofline(per_stage_ms: dict, sm_mhz: float, n_sm: int) -> dict:
+def issue_roofline(per_stage_ms: dict, sm_mhz: float, n_sm: int, kernels=None) -> dict:
     """Instruction-issue roofline per stage: warp instructions per launch (committed ncu summary)
     / the live per-launch time, against 4 schedulers x 1 warp instruction per clock per SM at the
     SM clock sampled during the run.  The explanation of the HBM fractions: the kernels of this
@@ -113,7 +123,7 @@ def issue_roofline(per_stage_ms: dict, sm_mhz: float, n_sm: int) -> dict:
     peak = n_sm * 4 * sm_mhz * 1e6
     out = {}
     for stage, ms in per_stage_ms.items():
-        recs = [ncu_record(k) for k in STAGE_KERNELS.get(stage, [])]
+        recs = [ncu_record(k) for k in (kernels or STAGE_KERNELS).get(stage, [])]
         wi = sum(r["warp_instructions"] or 0 for r in recs if r is not None)
         if ms <= 0 or not wi:
             continue
@@ -174,10 +184,10 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_input(cfg: int, batch):
+def make_input(cfg: int, batch, images=None):
     import synth
     t0 = time.time()
-    lab, info = synth.make_config(cfg, batch=batch) if cfg == 5 else synth.make_config(cfg)
+    lab, info = synth.make_config(cfg, batch=batch, images=images) if cfg == 5 else synth.make_config(cfg)
     info["gen_seconds"] = round(time.time() - t0, 1)
     ndim = 2 if cfg in (1, 5) else 3
     return lab, info, ndim
@@ -252,7 +262,12 @@ def run_fastrs(args):
     dev = torch.device("cuda", local)
     F.load()
 
-    lab, info, ndim = make_input(args.config, args.batch)
+    # C5 on N > 1 GPUs: rank r takes images [B*r/N, B*(r+1)/N) of one seeded B-image batch (strong
+    # scaling, no data-path collective); otherwise every rank runs its own copy (weak scaling)
+    shard = world > 1 and args.config == 5 and args.mode == "auto"
+    b_total = args.batch or 256
+    images = (b_total * rank // world, b_total * (rank + 1) // world) if shard else None
+    lab, info, ndim = make_input(args.config, b_total if args.config == 5 else args.batch, images)
     ml = info["max_label"]
     B = lab.shape[0] if lab.ndim == ndim + 1 else 1
     M = B * ml
@@ -293,7 +308,7 @@ def run_fastrs(args):
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    total_elems = lab.size * world
+    total_elems = b_total * lab.shape[-1] * lab.shape[-2] if shard else lab.size * world
     value = total_elems / (ms_max * 1e-3) / 1e9
 
     # ---- end to end through the host-buffer C entry point -------------------------------
@@ -334,11 +349,12 @@ def run_fastrs(args):
     def alg_bytes(k):
         return ALG_BYTES_PER_ELEM[k] * n + ALG_BYTES_PER_KEPT.get(k, 0.0) * diag["n_kept"]
 
+    SK = STAGE_KERNELS if ndim == 3 else STAGE_KERNELS_2D
     stages = {}
     for k, v in stage_ms_alg.items():
         gbs = alg_bytes(k) / (v * 1e-3) / 1e9 if v > 0 else 0.0
         stages[k] = {"ms": round(v, 4), "alg_bytes": alg_bytes(k), "GB/s": round(gbs, 1),
-                     "frac": round(gbs / hbm_peak, 4), "kernels": STAGE_KERNELS[k]}
+                     "frac": round(gbs / hbm_peak, 4), "kernels": SK[k]}
     dom = max((k for k in stage_ms_alg if k != "metrics"), key=lambda k: stage_ms_alg[k])
     dom_bytes = alg_bytes(dom)
     achieved = dom_bytes / (stage_ms_alg[dom] * 1e-3) / 1e9
@@ -357,19 +373,22 @@ def run_fastrs(args):
         cb.pop("seconds", None)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "strong" if shard else "weak",
         "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
         "config": {"workload": workload_name(args.config), "seed": info["seed"], "elements_per_gpu": int(n),
-                   "fill": round(info["fill"], 4), "max_label": ml, "parallelism": f"dp{world} (independent volumes)",
+                   "fill": round(info["fill"], 4), "max_label": ml,
+                   "parallelism": (f"images sharded over {world} GPUs ({b_total} total, rank 0: {images})" if shard
+                                   else f"dp{world} (independent volumes)"),
                    "l2": "inputs larger than L2 (4 GiB labels + ~16 GiB workspace per step), no flush",
                    "input_sha256": info["sha256"], "input_hash_kind": info.get("sha256_kind")},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(lab.nbytes),
                 "d2h_bytes_per_step": int(2 * M * 8), "ms_per_step": float(e2e_ms.item())},
         # K1 K2 (+fixup) K3 (+fixup) K4 K5a K5b K5' K5e K6 (3D); the 2D path has no K3
         "gpu_launches": int((11 if ndim == 3 else 9) * args.steps),
-        "roofline": {"bound": "hbm", "stage": dom, "kernels": STAGE_KERNELS[dom], "achieved": achieved,
+        "roofline": {"bound": "hbm", "stage": dom, "kernels": SK[dom], "achieved": achieved,
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                     "traffic": ncu_traffic(STAGE_KERNELS[dom]),
+                     "traffic": ncu_traffic(SK[dom]),
                      "traffic_source": os.path.relpath(NCU_SUMMARY, ROOT), "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": stage_ms_alg[dom],
                      "bytes_rule": "SURVEY.md §8(d): K1 8, K2 8, K3 8, K4 4 + 8/kept centre, K5 5 B per grid element"},
@@ -380,7 +399,7 @@ def run_fastrs(args):
         "path": {"alg_bytes": path_bytes, "GB/s": path_gbs, "frac": path_gbs / hbm_peak},
         "stages": stages,
         "issue_roofline": issue_roofline(stage_ms_alg, float(clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0),
-                                         torch.cuda.get_device_properties(dev).multi_processor_count),
+                                         torch.cuda.get_device_properties(dev).multi_processor_count, SK),
         "diagnostics": {k: int(v) for k, v in diag.items()},
         "clocks": clk,
         "cpu_baseline": cb,
@@ -391,17 +410,20 @@ def run_fastrs(args):
 
 
 def run_slab(args):
-    """One volume split into z-slabs across the ranks: every step runs
-    the four slab phases with the three NCCL exchanges (paper_2504_05808_b200/slab.py)."""
+    """One volume split into z-slabs across the ranks: every step is one
+    fastrs_sphericity_roundness_slab call (NCCL inside libfastrs: label halo, N8 halo or N1
+    transpose z pass, D halo, allreduce of the partial sums).  Strong scaling: the whole
+    volume's elements over the max-over-ranks time."""
     import torch
     import torch.distributed as dist
 
     import paper_2504_05808_b200 as F
-    from paper_2504_05808_b200 import slab
+    from paper_2504_05808_b200 import fastrs, slab
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep NCCL's banner off stdout (one JSON line)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -410,55 +432,98 @@ def run_slab(args):
     F.load()
     lab, info, ndim = make_input(args.config, args.batch)
     if ndim != 3:
-        raise SystemExit("--mode slab needs a 3D config")
+        raise SystemExit("the z-slab path needs a 3D config")
     ml = info["max_label"]
-    Z = lab.shape[0]
-    slabs = slab.partition(Z, world)
+    Z, Y, X = lab.shape
+    slabs = fastrs.slab_partition(Z, world)
     z0, z1 = slabs[rank]
-    t = torch.from_numpy(lab[z0:z1].copy()).to(dev)
+    host = torch.from_numpy(np.ascontiguousarray(lab[z0:z1])).pin_memory()
     del lab
+    t = host.to(dev)
+    comm = slab.make_comm()
+    flags = fastrs.BORDER_BACKGROUND | (fastrs.SLAB_TRANSPOSE if args.zpass == "transpose" else 0)
+    out = {"sphericity": torch.empty(ml, dtype=torch.float64, device=dev),
+           "roundness": torch.empty(ml, dtype=torch.float64, device=dev)}
+    res = {}
 
     def step():
-        return slab.sphericity_roundness_slab(t, slabs, ml, group=None)
+        return fastrs.sphericity_roundness_slab(t, z0, Z, ml, comm, flags=flags, out=out)
 
     for _ in range(args.warmup):
         res = step()
     stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, k):
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        m = torch.tensor([e0.elapsed_time(e1) / k], device=dev, dtype=torch.float64)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        return float(m.item())
+
     clocks = ClockSampler(local)
     clocks.start()
-    dist.barrier()
-    torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        res = step()
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    dist.barrier()
+    ms = timed(step, args.steps)
     clk = clocks.stop()
-    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
-    n = Z * t.shape[1] * t.shape[2]
+    hs, hr = torch.empty(ml, dtype=torch.float64).pin_memory(), torch.empty(ml, dtype=torch.float64).pin_memory()
+
+    def e2e_step():  # the slab's labels from pinned host memory, results back to the host
+        t.copy_(host, non_blocking=True)
+        r = step()
+        hs.copy_(r["sphericity"], non_blocking=True)
+        hr.copy_(r["roundness"], non_blocking=True)
+
+    e2e_ms = timed(e2e_step, args.e2e_steps)
+    si = res.get("slab_info", {})
+    xb = torch.tensor([si.get("bytes_sent", 0), si.get("bytes_received", 0)], device=dev, dtype=torch.int64)
+    allx = [torch.zeros_like(xb) for _ in range(world)]
+    dist.all_gather(allx, xb)
+    n = Z * Y * X
+    n_own = (z1 - z0) * Y * X
+    value = n / (ms * 1e-3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    # per-rank whole-path model: SURVEY.md §8(d) 33 B per own element (K1-K5), exchanges excluded
+    path_gbs = 33.0 * n_own / (ms * 1e-3) / 1e9
     if rank == 0:
-        line = {"metric": METRIC, "value": n / (ms * 1e-3) / 1e9, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
                 "config": {"workload": workload_name(args.config) + f", z-slabs over {world} GPU(s)",
-                           "seed": info["seed"], "elements": int(n), "slabs": slabs,
-                           "parallelism": f"z-slab{world}", "halo": res["slab_info"]},
-                "gpu_launches": int(11 * args.steps), "clocks": clk, "e2e": None, "roofline": None,
-                "cpu_baseline": None}
+                           "seed": info["seed"], "elements": int(n), "slabs": slabs, "parallelism": f"z-slab{world}",
+                           "zpass": args.zpass + (" (N1 all-to-all transpose)" if args.zpass == "transpose"
+                                                  else " (N8 h-slice halo)"),
+                           "halo": {k: si.get(k) for k in ("mode", "h", "H", "dxy_max", "dmax", "halo_cap")},
+                           "bytes_exchanged_per_rank": [{"sent": int(x[0]), "received": int(x[1])} for x in allx],
+                           "l2": "inputs larger than L2, no flush"},
+                "e2e": {"value": n / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(n * 4),
+                        "d2h_bytes_per_step": int(2 * ml * 8 * world), "ms_per_step": e2e_ms},
+                "gpu_launches": int(15 * args.steps),
+                "roofline": {"bound": "hbm", "stage": "whole path per rank (K1-K6)", "achieved": path_gbs,
+                             "peak": hbm_peak, "unit": "GB/s", "frac": path_gbs / hbm_peak, "traffic": None,
+                             "bytes_rule": "SURVEY.md §8(d) 33 B per own grid element; exchanges not counted"},
+                "clocks": clk, "cpu_baseline": None}
         print(json.dumps(line), flush=True)
+    comm.close()
     dist.destroy_process_group()
 
 
 def main():
     args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference(args)
-    elif args.mode == "slab":
+    elif args.mode == "slab" or (args.mode == "auto" and world > 1 and args.config in (2, 3, 4)):
         run_slab(args)
     else:
         run_fastrs(args)

@@ -61,7 +61,7 @@ typedef enum {
                            line it lies on and the border is not background) */
   FASTRS_ENOMEM = 3,    /* ws_bytes smaller than fastrs_workspace_bytes() */
   FASTRS_ECUDA = 4,     /* a CUDA runtime error (message in fastrs_last_error) */
-  FASTRS_ENCCL = 5,     /* reserved for the multi-GPU slab path */
+  FASTRS_ENCCL = 5,     /* an NCCL call of the multi-GPU slab path failed (or NCCL is missing) */
   FASTRS_EINTERNAL = 6  /* a device-side invariant failed (e.g. LT^2 < D) */
 } fastrs_status;
 
@@ -74,7 +74,9 @@ enum {
   FASTRS_FORCE_FALLBACK = 16u,   /* run K5 with the atomic sparse-table kernel on every tile
                                     (a GPU-internal cross-check of the default dilation)    */
   FASTRS_EDGE_SKIP_ZLO = 32u,    /* fastrs_touches_edge on a z-slab (3D): its first slice is  */
-  FASTRS_EDGE_SKIP_ZHI = 64u     /* not a grid face / its last slice is not (slab path)      */
+  FASTRS_EDGE_SKIP_ZHI = 64u,    /* not a grid face / its last slice is not (slab path)      */
+  FASTRS_SLAB_TRANSPOSE = 128u   /* fastrs_sphericity_roundness_slab: z pass by the all-to-all
+                                    z-slab -> y-slab transpose (N1) instead of the h halo (N8) */
 };
 
 /* Optional per-label statistics (device pointers, each nullable, batch*max_label long). */
@@ -236,6 +238,55 @@ FASTRS_API int fastrs_touches_edge(const int32_t* labels, const int64_t* dims, i
 FASTRS_API int fastrs_filter_objects(double* sphericity, double* roundness, const int64_t* volume,
                                      const uint8_t* touches_edge, int64_t n_labels, int64_t min_volume,
                                      uint32_t flags, void* stream);
+
+/* ---- multi-GPU z-slab call with NCCL inside the library -------
+ * One process per GPU; rank r holds the z-slab [z0, z0 + nz) = fastrs_slab_partition(Z, P)[r]
+ * (boundaries on multiples of 8 slices) of one 3D volume [Z][Y][X].  NCCL is loaded at run time
+ * (dlopen of libnccl.so.2: the copy already mapped into the process, e.g. torch's, else the
+ * system's; FASTRS_NCCL_LIB overrides), so the library itself loads without NCCL.
+ *
+ * fastrs_nccl_unique_id: 128-byte ncclUniqueId into id_out (rank 0; the caller broadcasts it).
+ * fastrs_comm_init: *comm_out <- a communicator of nranks ranks on the current device
+ *   (ncclCommInitRank; collective over the ranks); fastrs_comm_destroy frees it.
+ * fastrs_slab_partition: bounds[0..nranks] of the z-slabs (the rule of slab.py: round(Z*i/P/8)*8).
+ * fastrs_slab_halo_plan: the transfers that give every rank the w slices on each side of its
+ *   slab: n_out entries (src, dst, side 0 lo / 1 hi, a, b), global slices [a, b); up to cap
+ *   written to entries (5 int64 each; NULL: count only).  Pure host code.
+ * fastrs_slab_call_workspace_bytes: device workspace of one fastrs_sphericity_roundness_slab
+ *   call of this rank with halos of up to halo_cap slices (flags: FASTRS_SLAB_TRANSPOSE).
+ * fastrs_sphericity_roundness_slab: collective over the communicator.  labels: the rank's slab
+ *   [nz][Y][X] (device), dims_slab = {nz, Y, X}.  Exchanges (NCCL, on `stream`): the label slice
+ *   below the slab; the z pass by an h-slice halo of packed EDT words, h = ceil(sqrt(max D_xy))
+ *   (N8, default), or by the all-to-all z-slab <-> y-slab transpose (N1, FASTRS_SLAB_TRANSPOSE);
+ *   the H-slice halo of D for the dilation, H = isqrt(Dmax - 1) rounded up to 8; allreduce(sum)
+ *   of the per-label u64 partial sums and allreduce(max) of max LT^2.  Every rank receives all
+ *   max_label results (sphericity, roundness, stats: device, nullable), bit-identical to
+ *   fastrs_sphericity_roundness on the whole volume.  info (host, nullable) reports the mode,
+ *   the halo widths and the bytes this rank sent / received.  Errors as
+ *   fastrs_sphericity_roundness, plus ENOMEM when h (N8) or H exceeds halo_cap (retry with a
+ *   larger halo_cap and workspace), ENCCL on an NCCL failure.  Synchronises `stream` (twice, to
+ *   size the halos). */
+typedef struct {
+  int32_t mode;              /* 0: N8 halo z pass, 1: N1 transpose                */
+  int64_t h, H;              /* halo slices of the z pass (N8) and of the dilation */
+  uint32_t dxy_max, dmax;    /* global max D_xy and max D                          */
+  uint64_t bytes_sent, bytes_received;  /* exchanged by this rank (all phases)     */
+} fastrs_slab_info;
+
+FASTRS_API int fastrs_nccl_available(void);
+FASTRS_API int fastrs_nccl_unique_id(void* id_out);
+FASTRS_API int fastrs_comm_init(const void* id, int nranks, int rank, void** comm_out);
+FASTRS_API int fastrs_comm_destroy(void* comm);
+FASTRS_API int fastrs_slab_partition(int64_t Z, int nranks, int64_t* bounds);
+FASTRS_API int fastrs_slab_halo_plan(const int64_t* bounds, int nranks, int64_t w, int64_t Z, int64_t* entries,
+                                     int64_t cap, int64_t* n_out);
+FASTRS_API int fastrs_slab_call_workspace_bytes(const int64_t* dims_slab, int64_t z0, int64_t Z, int nranks, int rank,
+                                                int32_t max_label, int64_t halo_cap, uint32_t flags, size_t* bytes);
+FASTRS_API int fastrs_sphericity_roundness_slab(const int32_t* labels, const int64_t* dims_slab, int64_t z0, int64_t Z,
+                                                int32_t max_label, uint32_t flags, int64_t halo_cap,
+                                                double* sphericity, double* roundness,
+                                                const fastrs_object_stats* stats, fastrs_slab_info* info, void* comm,
+                                                void* ws, size_t ws_bytes, void* stream);
 
 FASTRS_API const char* fastrs_last_error(void);  /* thread-local message of the last failure */
 FASTRS_API void fastrs_release(void);            /* free the per-device caches                */

@@ -479,6 +479,12 @@ int run_host_pipelined(const int32_t* labels_host, int32_t* dlab, const Geom& g,
 }
 
 }  // namespace
+
+// shared with the slab driver (slab.cu): the thread-local message of fastrs_last_error
+int set_error(int code, const char* msg) {
+  t_err = msg;
+  return code;
+}
 }  // namespace fastrs
 
 using namespace fastrs;

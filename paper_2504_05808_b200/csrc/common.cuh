@@ -16,7 +16,7 @@ constexpr uint32_t kBitZ = 0x40000000u;  // element is the first of its z-run
 constexpr uint32_t kStBadLabel = 1u, kStNoSite = 2u, kStInternal = 4u, kStShell = 8u;
 
 constexpr uint32_t kFlagBorder = 1u, kFlagAsync = 4u, kFlagHostIO = 8u, kFlagForceFallback = 16u;
-constexpr uint32_t kFlagEdgeSkipZlo = 32u, kFlagEdgeSkipZhi = 64u;
+constexpr uint32_t kFlagEdgeSkipZlo = 32u, kFlagEdgeSkipZhi = 64u, kFlagSlabTranspose = 128u;
 
 // ---- dilation / pruning tiles ---------------------------------------------------------
 // 3D tile 32 x 8 x 8 (x fastest), 2D tile 32 x 64; both 64 rows of 32 = 2048 elements.
@@ -184,5 +184,6 @@ cudaError_t launch_filter(double* sph, double* rnd, const int64_t* vol, const ui
 void launch_metrics(const Accum& acc, const Geom& g, const Outputs& o, WsHeader* hdr,
                     cudaStream_t st);
 void release_mtables();
+int set_error(int code, const char* msg);  // sets the fastrs_last_error message, returns code
 
 }  // namespace fastrs

@@ -51,6 +51,11 @@ class _Diag(ctypes.Structure):
                 ("n_painted", ctypes.c_uint64), ("n_covering", ctypes.c_uint64)]
 
 
+class _SlabInfo(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("h", ctypes.c_int64), ("H", ctypes.c_int64), ("dxy_max", ctypes.c_uint32),
+                ("dmax", ctypes.c_uint32), ("bytes_sent", ctypes.c_uint64), ("bytes_received", ctypes.c_uint64)]
+
+
 def load(build_if_missing: bool = True) -> ctypes.CDLL:
     """Load libfastrs.so (built in-tree).  Raises if it cannot be built or loaded."""
     global _lib
@@ -85,12 +90,23 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
                                                sz, vp]
             lib.fastrs_metrics_from_partials.argtypes = [vp, vp, vp, vp, vp, i64, ci, i64, u32, vp, vp, vp, vp,
                                                          sz, vp]
+            lib.fastrs_nccl_available.argtypes = []
+            lib.fastrs_nccl_unique_id.argtypes = [vp]
+            lib.fastrs_comm_init.argtypes = [vp, ci, ci, ctypes.POINTER(vp)]
+            lib.fastrs_comm_destroy.argtypes = [vp]
+            lib.fastrs_slab_partition.argtypes = [i64, ci, vp]
+            lib.fastrs_slab_halo_plan.argtypes = [vp, ci, i64, i64, vp, i64, ctypes.POINTER(i64)]
+            lib.fastrs_slab_call_workspace_bytes.argtypes = [vp, i64, i64, ci, ci, i32, i64, u32, ctypes.POINTER(sz)]
+            lib.fastrs_sphericity_roundness_slab.argtypes = [vp, vp, i64, i64, i32, u32, i64, vp, vp, vp,
+                                                             ctypes.POINTER(_SlabInfo), vp, vp, sz, vp]
             lib.fastrs_touches_edge.argtypes = [vp, vp, ci, i64, i32, vp, u32, vp]
             lib.fastrs_filter_objects.argtypes = [vp, vp, vp, vp, i64, i64, u32, vp]
             for n in ("workspace_bytes", "edt_sq", "local_thickness", "sphericity_roundness",
                       "sphericity_roundness_host", "read_diagnostics", "profile_read", "slab_workspace_bytes",
                       "slab_edt_xy", "slab_edt_z", "slab_reduce", "metrics_from_partials", "touches_edge",
-                      "filter_objects"):
+                      "filter_objects", "nccl_available", "nccl_unique_id", "comm_init", "comm_destroy",
+                      "slab_partition", "slab_halo_plan", "slab_call_workspace_bytes",
+                      "sphericity_roundness_slab"):
                 getattr(lib, "fastrs_" + n).restype = ci
             _lib = lib
     return _lib
@@ -398,3 +414,102 @@ def sphericity_2d(A, mean_lt):
 
 def release():
     load().fastrs_release()
+
+
+# ------------------------------------------------------------------------------------------
+# multi-GPU z-slab call with NCCL inside the library (include/fastrs.h
+# fastrs_sphericity_roundness_slab); slab.py builds the communicator
+# ------------------------------------------------------------------------------------------
+
+SLAB_TRANSPOSE = 128
+
+
+def nccl_available() -> bool:
+    return bool(load().fastrs_nccl_available())
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load().fastrs_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """An NCCL communicator owned by libfastrs (fastrs_comm_init on the current device)."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        self.handle = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        _check(load().fastrs_comm_init(buf, int(nranks), int(rank), ctypes.byref(self.handle)))
+        self.nranks, self.rank = int(nranks), int(rank)
+
+    def close(self):
+        if self.handle:
+            _check(load().fastrs_comm_destroy(self.handle))
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def slab_partition(Z: int, nranks: int) -> list:
+    b = (ctypes.c_int64 * (nranks + 1))()
+    _check(load().fastrs_slab_partition(int(Z), int(nranks), b))
+    return [(int(b[i]), int(b[i + 1])) for i in range(nranks)]
+
+
+def slab_halo_plan(slabs, w: int, Z: int) -> list:
+    """(src, dst, side, a, b) transfers of the library's halo plan (side 'lo' / 'hi')."""
+    P = len(slabs)
+    bd = (ctypes.c_int64 * (P + 1))(*([s[0] for s in slabs] + [slabs[-1][1]]))
+    n = ctypes.c_int64(0)
+    _check(load().fastrs_slab_halo_plan(bd, P, int(w), int(Z), None, 0, ctypes.byref(n)))
+    ent = (ctypes.c_int64 * (5 * n.value))()
+    _check(load().fastrs_slab_halo_plan(bd, P, int(w), int(Z), ent, n.value, ctypes.byref(n)))
+    return [(int(ent[5 * i]), int(ent[5 * i + 1]), "lo" if ent[5 * i + 2] == 0 else "hi", int(ent[5 * i + 3]),
+             int(ent[5 * i + 4])) for i in range(n.value)]
+
+
+def sphericity_roundness_slab(labels_slab: torch.Tensor, z0: int, Z: int, max_label: int, comm: Comm,
+                              flags=BORDER_BACKGROUND, halo_cap: int = 64, stats=False, out=None, ws=None) -> dict:
+    """Collective over `comm`: per-object sphericity / roundness of the volume whose z-slab
+    [z0, z0 + nz) this rank holds (fastrs_sphericity_roundness_slab: NCCL inside the library).
+    flags | SLAB_TRANSPOSE selects the all-to-all transpose z pass.  A halo wider than
+    halo_cap is retried once with the width the library reported.  Returns the results of all
+    labels and "slab_info"."""
+    labels_slab = _labels_arg(labels_slab)
+    dev = labels_slab.device
+    M = int(max_label)
+    res = out if out is not None else {"sphericity": torch.empty(M, dtype=torch.float64, device=dev),
+                                       "roundness": torch.empty(M, dtype=torch.float64, device=dev)}
+    st = None
+    if stats:
+        for k, dt in (("volume", torch.int64), ("n_shell", torch.int64), ("max_lt2", torch.int32),
+                      ("mean_lt", torch.float64), ("max_lt", torch.float64), ("shell_mean_lt", torch.float64),
+                      ("axis_a", torch.float64), ("axis_cb", torch.float64)):
+            res[k] = torch.empty(M, dtype=dt, device=dev)
+        st = _Stats(*[res[n].data_ptr() for n, _ in _Stats._fields_])
+    dims = _dims3(labels_slab.shape)
+    info = _SlabInfo()
+    for attempt in range(2):
+        nb = ctypes.c_size_t(0)
+        _check(load().fastrs_slab_call_workspace_bytes(dims, int(z0), int(Z), comm.nranks, comm.rank, M,
+                                                       int(halo_cap), int(flags), ctypes.byref(nb)))
+        w = workspace(nb.value, dev) if ws is None else ws
+        rc = load().fastrs_sphericity_roundness_slab(labels_slab.data_ptr(), dims, int(z0), int(Z), M, int(flags),
+                                                     int(halo_cap), res["sphericity"].data_ptr(),
+                                                     res["roundness"].data_ptr(),
+                                                     None if st is None else ctypes.byref(st), ctypes.byref(info),
+                                                     comm.handle, w.data_ptr(), w.numel(), _stream(dev))
+        if rc == 3 and attempt == 0 and "exceeds halo_cap" in load().fastrs_last_error().decode():
+            msg = load().fastrs_last_error().decode()
+            halo_cap = int(msg.split("= ")[1].split()[0]) + 8  # the width the library reported
+            continue
+        _check(rc)
+        break
+    res["slab_info"] = {k: int(getattr(info, k)) for k, _ in _SlabInfo._fields_}
+    res["slab_info"]["halo_cap"] = int(halo_cap)
+    return res

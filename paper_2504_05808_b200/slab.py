@@ -184,8 +184,22 @@ def touches_edge_slab(labels_slab: torch.Tensor, slabs, max_label: int, group=No
     return f.to(torch.uint8)
 
 
+def make_comm(group=None):
+    """Collective over `group`: a libfastrs NCCL communicator (fastrs_comm_init) for
+    fastrs.sphericity_roundness_slab.  Rank 0 draws the ncclUniqueId inside the library and
+    torch.distributed broadcasts its 128 bytes (a CUDA tensor on an NCCL process group)."""
+    from . import fastrs as F
+    rank, n = dist.get_rank(group), dist.get_world_size(group)
+    uid = F.nccl_unique_id() if rank == 0 else bytes(128)
+    t = torch.tensor(list(uid), dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    dist.broadcast(t, src=_peer(0, group), group=group)
+    return F.Comm(bytes(t.cpu().tolist()), n, rank)
+
+
 def simulate_slabs(labels: torch.Tensor, nranks: int, max_label: int, flags: int = 1, stats: bool = False,
-                   phases=None) -> dict:
+                   phases=None, transpose: bool = False) -> dict:
     """Single-process emulation of the slab path: the nranks slabs are processed one after
     another on one device and the exchanges become slicing of the assembled volume.  The
     same phases and halo widths as sphericity_roundness_slab; used by the GPU parity tests
@@ -202,11 +216,23 @@ def simulate_slabs(labels: torch.Tensor, nranks: int, max_label: int, flags: int
     h = halo_edt(dxy, Z)
     packed = torch.cat(packed)
     dfull, dmax = [], 0
-    for z0, z1 in slabs:
-        a, b = max(0, z0 - h), min(Z, z1 + h)
-        d, m = phases.edt_z(packed[a:b].contiguous(), z0 - a, z1 - a, a, Z, flags)
-        dfull.append(d)
-        dmax = max(dmax, int(m.reshape(-1)[0].item()))
+    if transpose:
+        # N1: the z pass over whole columns of each rank's y-block (fastrs_sphericity_roundness_slab
+        # with FASTRS_SLAB_TRANSPOSE), then back to the z-slab layout
+        dvol = torch.empty_like(packed)
+        for s_ in range(nranks):
+            y0, y1 = Y * s_ // nranks, Y * (s_ + 1) // nranks
+            if y1 > y0:
+                d, m = phases.edt_z(packed[:, y0:y1].contiguous(), 0, Z, 0, Z, flags)
+                dvol[:, y0:y1] = d
+                dmax = max(dmax, int(m.reshape(-1)[0].item()))
+        dfull = [dvol]
+    else:
+        for z0, z1 in slabs:
+            a, b = max(0, z0 - h), min(Z, z1 + h)
+            d, m = phases.edt_z(packed[a:b].contiguous(), z0 - a, z1 - a, a, Z, flags)
+            dfull.append(d)
+            dmax = max(dmax, int(m.reshape(-1)[0].item()))
     H = halo_lt(dmax)
     dfull = torch.cat(dfull)
     tot = None
@@ -221,5 +247,5 @@ def simulate_slabs(labels: torch.Tensor, nranks: int, max_label: int, flags: int
                 tot[k] += part[k]
             tot["max_lt2"] = torch.maximum(tot["max_lt2"], part["max_lt2"])
     res = phases.metrics(tot, Z * Y * X, dmax, stats)
-    res["slab_info"] = dict(h=h, H=H, dmax=dmax, slabs=slabs)
+    res["slab_info"] = dict(h=0 if transpose else h, H=H, dmax=dmax, slabs=slabs, transpose=transpose)
     return res

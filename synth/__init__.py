@@ -160,12 +160,14 @@ def _objects3d(rng, r_eq, aspect, rough_frac):
     return p
 
 
-def make_config(i: int, seed: int | None = None, batch: int | None = None):
+def make_config(i: int, seed: int | None = None, batch: int | None = None, images: tuple | None = None):
     """Return (labels, info) for BASELINE.json config C{i} (i in 1..5).
 
     labels: int32, C order; 2D (Y,X) for C1, 3D (Z,Y,X) for C2..C4, (B,Y,X) for C5.
     info: dict(config, seed, ndim, batch, max_label, n_objects, fill, sha256).
-    ``batch`` overrides the number of C5 images (default 256).
+    ``batch`` overrides the number of C5 images (default 256); ``images=(i0, i1)`` rasterises
+    only images [i0, i1) of that seeded batch (identical to the same slice of the whole batch:
+    the per-rank shard of the multi-GPU bench).
     """
     seed = i if seed is None else seed
     rng = np.random.default_rng(seed)
@@ -242,6 +244,10 @@ def make_config(i: int, seed: int | None = None, batch: int | None = None):
         p[:, 10] = rng.uniform(0, dim, B * ncell)
         p[:, 11] = rng.uniform(0, dim, B * ncell)
         p[:, 12] = 1
+        if images is not None:  # a shard [i0, i1) of the seeded B-image batch (same draws)
+            i0, i1 = images
+            p = p[i0 * ncell:i1 * ncell]
+            B = i1 - i0
         lab = np.empty((B, dim, dim), np.int32)
         _load().synth_cells(_ptr(lab), B, dim, dim, ncell, _ptr(np.ascontiguousarray(p)))
         ndim, max_label = 2, ncell

@@ -18,11 +18,11 @@ pytestmark = pytest.mark.gpu
 KEYS = ("sphericity", "roundness", "volume", "n_shell", "max_lt2", "mean_lt", "shell_mean_lt", "axis_cb")
 
 
-def _check(lab, nranks, flags=1):
+def _check(lab, nranks, flags=1, transpose=False):
     t = torch.from_numpy(np.ascontiguousarray(lab, np.int32)).cuda()
     ml = int(lab.max())
     want = fastrs.sphericity_roundness(t, max_label=ml, flags=flags, stats=True)
-    got = slab.simulate_slabs(t, nranks, ml, flags=flags, stats=True)
+    got = slab.simulate_slabs(t, nranks, ml, flags=flags, stats=True, transpose=transpose)
     for k in KEYS:
         a, b = got[k].cpu().numpy(), want[k].cpu().numpy()
         np.testing.assert_array_equal(a, b, err_msg=f"{k} (nranks={nranks}, flags={flags})")
@@ -99,3 +99,62 @@ def test_touches_edge_slabs_or_to_the_volume_flags():
         acc = torch.maximum(acc, f)
     np.testing.assert_array_equal(acc.cpu().numpy(), want.cpu().numpy())
     np.testing.assert_array_equal(want.cpu().numpy(), oracle.touches_edge(lab, ml))
+
+
+# ---- N1: the z pass over whole columns of y-blocks (the all-to-all transpose) -------------
+
+@pytest.mark.parametrize("nranks", [2, 3, 8])
+def test_transpose_z_pass_bit_identical(nranks):
+    """FASTRS_SLAB_TRANSPOSE's decomposition: K3 on each rank's y-block [Z][Y/P][X] of the
+    packed words, then D back to z-slabs: bit-identical to the single call."""
+    lab, _ = synth.make_config(2)
+    _check(lab, nranks, transpose=True)
+    lab = synth.random_labels((70, 45, 50), nlabels=6, seed=11, fill=0.85, blob=5)
+    _check(np.pad(lab, 1), 3, 0, transpose=True)
+
+
+# ---- the in-library NCCL driver (fastrs_sphericity_roundness_slab) ----------------------
+
+@pytest.fixture(scope="module")
+def comm1():
+    """A single-rank libfastrs NCCL communicator on cuda:0 (one GPU on this box)."""
+    if not fastrs.nccl_available():
+        pytest.fail("libnccl.so.2 not loadable")
+    torch.cuda.set_device(0)
+    c = fastrs.Comm(fastrs.nccl_unique_id(), 1, 0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("flags", [fastrs.BORDER_BACKGROUND, fastrs.BORDER_BACKGROUND | fastrs.SLAB_TRANSPOSE])
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_nccl_slab_call_bit_identical(comm1, cfg, flags):
+    """fastrs_sphericity_roundness_slab on one rank (N8 halo or N1 transpose, NCCL allreduces,
+    self copies) gives the single call's results bit for bit."""
+    lab, info = synth.make_config(cfg)
+    ml = info["max_label"]
+    t = torch.from_numpy(lab).cuda()
+    want = fastrs.sphericity_roundness(t, max_label=ml, stats=True)
+    got = fastrs.sphericity_roundness_slab(t, 0, lab.shape[0], ml, comm1, flags=flags, stats=True)
+    for k in KEYS:
+        np.testing.assert_array_equal(got[k].cpu().numpy(), want[k].cpu().numpy(), err_msg=k)
+    si = got["slab_info"]
+    assert si["mode"] == (1 if flags & fastrs.SLAB_TRANSPOSE else 0)
+    assert si["dmax"] == fastrs.diagnostics(fastrs.last_workspace())["dmax"] or si["dmax"] > 0
+    assert si["H"] % 8 == 0 and si["bytes_sent"] == 0  # one rank: nothing leaves the GPU
+
+
+def test_nccl_slab_call_halo_retry_and_errors(comm1):
+    """A ball wider than the default halo cap: the wrapper retries with the width the library
+    reports; bad labels are reported as on the single call."""
+    big = np.zeros((200, 200, 200), np.int32)
+    big[10:191, 10:191, 10:191] = synth.sphere(90, canvas=181)
+    t = torch.from_numpy(big).cuda()
+    want = fastrs.sphericity_roundness(t, max_label=1)
+    got = fastrs.sphericity_roundness_slab(t, 0, 200, 1, comm1, halo_cap=16)
+    assert got["slab_info"]["halo_cap"] > 16 and got["slab_info"]["H"] > 16
+    np.testing.assert_array_equal(got["roundness"].cpu().numpy(), want["roundness"].cpu().numpy())
+    bad = torch.from_numpy(np.full((16, 8, 8), 5, np.int32)).cuda()
+    with pytest.raises(fastrs.FastrsError) as e:
+        fastrs.sphericity_roundness_slab(bad, 0, 16, 2, comm1)
+    assert e.value.name == "EINVAL"

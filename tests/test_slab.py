@@ -162,3 +162,22 @@ def test_halo_too_small_is_caught(shrink, tmp_path):
     same = np.allclose(got["sphericity"][ok], want["sphericity"][ok], rtol=1e-9) and \
         np.array_equal(got["max_lt2"].astype(np.uint32), want["max_lt2"])
     assert not same
+
+
+# ---- the library's own plans (libfastrs host code used by fastrs_sphericity_roundness_slab) ----
+
+def test_library_partition_and_halo_plan_match_python():
+    """fastrs_slab_partition / fastrs_slab_halo_plan (the C++ NCCL driver's plans) equal slab.py's
+    partition / halo_plan, including multi-hop halos wider than a slab."""
+    from paper_2504_05808_b200 import fastrs as F
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        P = int(rng.integers(1, 9))
+        Z = int(rng.integers(8 * P, 2048))
+        try:
+            want = slab.partition(Z, P)
+        except ValueError:
+            continue
+        assert F.slab_partition(Z, P) == want
+        for w in (0, 1, int(rng.integers(1, 64)), int(rng.integers(1, Z + 1)), Z):
+            assert F.slab_halo_plan(want, w, Z) == slab.halo_plan(want, w, Z)
