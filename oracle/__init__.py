@@ -20,6 +20,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.cpp")
+_SRCS = [_SRC, os.path.join(_HERE, "oracle_analysis.cpp")]
 _lock = threading.Lock()
 _lib = None
 
@@ -36,9 +37,9 @@ class OracleError(RuntimeError):
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so in-tree (plain g++ -O2; building the checker is not using it)."""
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_SO) or any(os.path.getmtime(_SO) < os.path.getmtime(s) for s in _SRCS):
         subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-pthread",
-                               _SRC, "-o", _SO + ".tmp"])
+                               *_SRCS, "-o", _SO + ".tmp"])
         os.replace(_SO + ".tmp", _SO)
     return _SO
 
@@ -57,6 +58,12 @@ def _load():
             lib.fastrs_oracle_fields.restype = ci
             lib.fastrs_oracle_sphericity_roundness.argtypes = [vp, vp, ci, i64, i32, u32] + [vp] * 10 + [ci]
             lib.fastrs_oracle_sphericity_roundness.restype = ci
+            lib.fastrs_oracle_label_components.argtypes = [vp, vp, ci, i64, ci, vp, vp]
+            lib.fastrs_oracle_label_components.restype = ci
+            lib.fastrs_oracle_sphericity_wl.argtypes = [vp, vp, ci, i64, i32, vp, vp, vp]
+            lib.fastrs_oracle_sphericity_wl.restype = ci
+            lib.fastrs_oracle_mc_measure.argtypes = [vp, vp, ci, i64, i32, vp, vp]
+            lib.fastrs_oracle_mc_measure.restype = ci
             for name in ("spheroid_area", "ramanujan_perimeter", "sphericity_3d", "sphericity_2d"):
                 f = getattr(lib, "fastrs_oracle_" + name)
                 f.argtypes = [cd, cd]
@@ -176,4 +183,52 @@ def filter_objects(res: dict, min_volume=None, edge=None) -> dict:
         v = np.array(res[k], dtype=np.float64)
         v[drop] = np.nan
         out[k] = v
+    return out
+
+
+def label_components(mask, connectivity=None, ndim=None, batch=None):
+    """Connected components of a binary mask (oracle_analysis.cpp): int32 labels 1..K per item in
+    row-major first-encounter order, and the per-item counts.  connectivity: 4 / 8 (2D, default
+    8), 6 / 18 / 26 (3D, default 26)."""
+    m = np.ascontiguousarray(np.asarray(mask) != 0, dtype=np.uint8)
+    ndim = m.ndim if ndim is None else ndim
+    batch = (1 if m.ndim == ndim else m.shape[0]) if batch is None else batch
+    dims = np.ascontiguousarray(m.shape[-ndim:], dtype=np.int64)
+    if connectivity is None:
+        connectivity = 8 if ndim == 2 else 26
+    out = np.zeros(m.shape, np.int32)
+    counts = np.zeros(batch, np.int64)
+    st = _load().fastrs_oracle_label_components(_p(m), _p(dims), ndim, batch, int(connectivity), _p(out),
+                                                _p(counts))
+    if st:
+        raise OracleError(st)
+    return out, counts
+
+
+def sphericity_wl(labels, max_label=None, batch=None):
+    """Eq. 3 width-to-length sphericity (2D): dict of swl, d1, d2 (batch*max_label)."""
+    labels, ndim, batch, dims = _geom(labels, 2, batch)
+    if max_label is None:
+        max_label = max(1, int(labels.max(initial=0)))
+    M = batch * max_label
+    out = dict(swl=np.empty(M), d1=np.empty(M), d2=np.empty(M))
+    st = _load().fastrs_oracle_sphericity_wl(_p(labels), _p(dims), 2, batch, int(max_label), _p(out["swl"]),
+                                             _p(out["d1"]), _p(out["d2"]))
+    if st:
+        raise OracleError(st)
+    return out
+
+
+def mc_measure(labels, max_label=None, ndim=None, batch=None):
+    """S_MC baseline: per-label marching-squares perimeter (2D) / marching-tetrahedra surface area
+    (3D) and the sphericity from it (Eq. 2 / Eq. 1): dict measure, sphericity_mc."""
+    labels, ndim, batch, dims = _geom(labels, ndim, batch)
+    if max_label is None:
+        max_label = max(1, int(labels.max(initial=0)))
+    M = batch * max_label
+    out = dict(measure=np.empty(M), sphericity_mc=np.empty(M))
+    st = _load().fastrs_oracle_mc_measure(_p(labels), _p(dims), ndim, batch, int(max_label), _p(out["measure"]),
+                                          _p(out["sphericity_mc"]))
+    if st:
+        raise OracleError(st)
     return out
