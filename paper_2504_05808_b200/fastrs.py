@@ -99,6 +99,12 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
             lib.fastrs_slab_call_workspace_bytes.argtypes = [vp, i64, i64, ci, ci, i32, i64, u32, ctypes.POINTER(sz)]
             lib.fastrs_sphericity_roundness_slab.argtypes = [vp, vp, i64, i64, i32, u32, i64, vp, vp, vp,
                                                              ctypes.POINTER(_SlabInfo), vp, vp, sz, vp]
+            lib.fastrs_ccl_workspace_bytes.argtypes = [vp, ci, i64, ctypes.POINTER(sz)]
+            lib.fastrs_label_components.argtypes = [vp, vp, ci, i64, ci, vp, vp, vp, sz, vp]
+            lib.fastrs_wl_workspace_bytes.argtypes = [i64, i32, ctypes.POINTER(sz)]
+            lib.fastrs_sphericity_wl.argtypes = [vp, vp, ci, i64, i32, vp, vp, vp, vp, sz, vp]
+            lib.fastrs_mc_workspace_bytes.argtypes = [i64, i32, ctypes.POINTER(sz)]
+            lib.fastrs_mc_measure.argtypes = [vp, vp, ci, i64, i32, vp, vp, vp, sz, vp]
             lib.fastrs_touches_edge.argtypes = [vp, vp, ci, i64, i32, vp, u32, vp]
             lib.fastrs_filter_objects.argtypes = [vp, vp, vp, vp, i64, i64, u32, vp]
             for n in ("workspace_bytes", "edt_sq", "local_thickness", "sphericity_roundness",
@@ -106,7 +112,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
                       "slab_edt_xy", "slab_edt_z", "slab_reduce", "metrics_from_partials", "touches_edge",
                       "filter_objects", "nccl_available", "nccl_unique_id", "comm_init", "comm_destroy",
                       "slab_partition", "slab_halo_plan", "slab_call_workspace_bytes",
-                      "sphericity_roundness_slab"):
+                      "sphericity_roundness_slab", "ccl_workspace_bytes", "label_components",
+                      "wl_workspace_bytes", "sphericity_wl", "mc_workspace_bytes", "mc_measure"):
                 getattr(lib, "fastrs_" + n).restype = ci
             _lib = lib
     return _lib
@@ -513,3 +520,55 @@ def sphericity_roundness_slab(labels_slab: torch.Tensor, z0: int, Z: int, max_la
     res["slab_info"] = {k: int(getattr(info, k)) for k, _ in _SlabInfo._fields_}
     res["slab_info"]["halo_cap"] = int(halo_cap)
     return res
+
+
+# ------------------------------------------------------------------------------------------
+# analysis protocol (include/fastrs.h "analysis protocol around the hot path")
+# ------------------------------------------------------------------------------------------
+
+def label_components(mask: torch.Tensor, connectivity=None, ndim=None):
+    """Connected components of a binary mask (fastrs_label_components): (int32 labels, int64
+    per-item counts).  connectivity 4 / 8 (2D, default 8), 6 / 18 / 26 (3D, default 26)."""
+    m = (mask != 0).to(torch.uint8).contiguous() if mask.dtype != torch.uint8 else mask.contiguous()
+    ndim, b, dims = _geometry(m.shape, ndim, None)
+    conn = connectivity or (8 if ndim == 2 else 26)
+    nb = ctypes.c_size_t(0)
+    _check(load().fastrs_ccl_workspace_bytes(dims, ndim, b, ctypes.byref(nb)))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device=m.device)
+    out = torch.empty(m.shape, dtype=torch.int32, device=m.device)
+    counts = torch.zeros(b, dtype=torch.int64, device=m.device)
+    _check(load().fastrs_label_components(m.data_ptr(), dims, ndim, b, int(conn), out.data_ptr(), counts.data_ptr(),
+                                          ws.data_ptr(), ws.numel(), _stream(m.device)))
+    return out, counts
+
+
+def sphericity_wl(labels: torch.Tensor, max_label: int) -> dict:
+    """Eq. 3 width/length sphericity of a 2D label image or a batch [B][Y][X] (fastrs_sphericity_wl):
+    dict swl, d1, d2 (float64, batch*max_label)."""
+    labels = _labels_arg(labels)
+    ndim, b, dims = _geometry(labels.shape, 2, None)
+    M = b * int(max_label)
+    out = {k: torch.empty(M, dtype=torch.float64, device=labels.device) for k in ("swl", "d1", "d2")}
+    nb = ctypes.c_size_t(0)
+    _check(load().fastrs_wl_workspace_bytes(b, int(max_label), ctypes.byref(nb)))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device=labels.device)
+    _check(load().fastrs_sphericity_wl(labels.data_ptr(), dims, 2, b, int(max_label), out["swl"].data_ptr(),
+                                       out["d1"].data_ptr(), out["d2"].data_ptr(), ws.data_ptr(), ws.numel(),
+                                       _stream(labels.device)))
+    return out
+
+
+def mc_measure(labels: torch.Tensor, max_label: int, ndim=None) -> dict:
+    """S_MC baseline (fastrs_mc_measure): dict measure (perimeter 2D / surface area 3D) and
+    sphericity_mc, float64, batch*max_label."""
+    labels = _labels_arg(labels)
+    ndim, b, dims = _geometry(labels.shape, ndim, None)
+    M = b * int(max_label)
+    out = {k: torch.empty(M, dtype=torch.float64, device=labels.device) for k in ("measure", "sphericity_mc")}
+    nb = ctypes.c_size_t(0)
+    _check(load().fastrs_mc_workspace_bytes(b, int(max_label), ctypes.byref(nb)))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device=labels.device)
+    _check(load().fastrs_mc_measure(labels.data_ptr(), dims, ndim, b, int(max_label), out["measure"].data_ptr(),
+                                    out["sphericity_mc"].data_ptr(), ws.data_ptr(), ws.numel(),
+                                    _stream(labels.device)))
+    return out

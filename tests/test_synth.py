@@ -43,3 +43,11 @@ def test_count_volume_matches_the_paper_experiment_shape():
     v = np.bincount(lab.ravel(), minlength=15504)[1:]
     assert v.min() >= 10 and 27 * 0.5 <= np.percentile(v, 1) and v.max() <= 2 * 130000
     assert 0.15 < info["fill"] < 0.30
+
+
+def test_c5_image_shards_equal_the_batch():
+    """bench.py's C5 shard of rank r (images [i0, i1) of the seeded batch) equals that slice of the
+    whole batch: the draws do not depend on the shard."""
+    a, _ = synth.make_config(5, batch=5)
+    b, _ = synth.make_config(5, batch=5, images=(1, 4))
+    np.testing.assert_array_equal(a[1:4], b)
