@@ -63,7 +63,8 @@ struct Smem {  // K5a (gather + sort)
 // sibling tile of the same CTA is still painting.
 // K5b launch shape: warps per CTA and resident CTAs per SM (sets the register cap: 64 here, 32
 // resident warps; the fused reductions spill at 56).  C4 sweep (persistent, round 1, LT plane):
-// (2,16) 10.63 ms, (2,18) 10.58, (2,20) 10.71, (2,24) 10.68, (1,32) 10.76, (4,10) 10.70.
+// (2,16) 10.63 ms, (2,18) 10.58, (2,20) 10.71, (2,24) 10.68, (1,32) 10.76, (4,10) 10.70; round 2
+// (fused, K5a + K5b): (2,16) 16.40 ms, (2,14) 16.48, (2,12) 16.88, (2,10) 17.87.
 constexpr int kPaintNW = 2, kPaintMinB = 16;
 template <int NW, bool FUSED>
 struct PaintSmem {  // K5b (one tile per warp)

@@ -19,6 +19,8 @@
 //              VIADDMNMX.U16x2 per row pair, run ends folded into the staged values) and
 //              hands CTAs with values >= 2^14-1 to the exact 32-bit kernel.  The final pass
 //              emits D, Dmax, n_fg and flags elements with no site (ENOSITE).
+#include <mutex>
+
 #include "common.cuh"
 
 namespace fastrs {
@@ -26,10 +28,13 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
-template <int U>
+// K1, one warp per x-row.  FULL: X % 32 == 0 (no bounds tests).  Ly / Lz point at the row above
+// in y / z, or at a row of -1 sentinels (no such neighbour: "first of its run" holds, as for a
+// different label), so the loops carry no pointer tests.
+template <int U, bool FULL>
 __global__ void __launch_bounds__(256) k_edt_x(const int32_t* __restrict__ lab,
-                                               const int32_t* __restrict__ below, uint32_t* __restrict__ out,
-                                               int64_t nrows, int X, int64_t Y, int64_t Z,
+                                               const int32_t* __restrict__ below, const int32_t* __restrict__ sent,
+                                               uint32_t* __restrict__ out, int64_t nrows, int X, int64_t Y, int64_t Z,
                                                int32_t max_label, int border, int is3d,
                                                WsHeader* __restrict__ hdr) {
   extern __shared__ uint16_t s_end[];
@@ -41,26 +46,29 @@ __global__ void __launch_bounds__(256) k_edt_x(const int32_t* __restrict__ lab,
   const int64_t y = row % Y;
   const int64_t z = (row / Y) % Z;
   const int32_t* L = lab + row * X;
-  const int32_t* Ly = y > 0 ? L - X : nullptr;
+  const int32_t* Ly = y > 0 ? L - X : sent;
   // z-1 neighbour: the previous slice, or (slab path) the caller's slice just below the slab
-  const int32_t* Lz = is3d ? (z > 0 ? L - X * Y : (below ? below + y * X : nullptr)) : nullptr;
+  const int32_t* Lz = is3d ? (z > 0 ? L - X * Y : (below ? below + y * X : sent)) : sent;
   uint32_t* O = out + row * X;
   const int nchunk = (X + 31) >> 5;
+  const uint32_t far = (uint32_t)kFull;  // "no site on this side" (unsigned distance)
 
-  // sweep 1 (right to left): end of the run containing x
+  // sweep 1 (right to left): end of the run containing x (pointers step by 32 elements)
   int carry_end = X - 1;
   int32_t right_next = 0;
+  const int32_t* pL = L + ((nchunk - 1) << 5) + lane;
 #pragma unroll U
-  for (int c = nchunk - 1; c >= 0; --c) {
+  for (int c = nchunk - 1; c >= 0; --c, pL -= 32) {
     const int x = (c << 5) + lane;
-    const int32_t v = x < X ? __ldg(L + x) : 0;
+    const bool in = FULL || x < X;
+    const int32_t v = in ? __ldg(pL) : 0;
     int32_t r = __shfl_down_sync(kFull, v, 1);
     if (lane == 31) r = right_next;
-    const bool is_end = x < X && (x == X - 1 || v != r);
+    const bool is_end = in && (x == X - 1 || v != r);
     const uint32_t m = __ballot_sync(kFull, is_end);
     const uint32_t ge = m & (kFull << lane);
     const int e = ge ? (c << 5) + __ffs(ge) - 1 : carry_end;
-    if (x < X) ends[x] = (uint16_t)e;
+    if (in) ends[x] = (uint16_t)e;
     if (m) carry_end = (c << 5) + __ffs(m) - 1;
     right_next = __shfl_sync(kFull, v, 0);
   }
@@ -69,32 +77,33 @@ __global__ void __launch_bounds__(256) k_edt_x(const int32_t* __restrict__ lab,
   int carry_start = 0;
   int32_t left_prev = 0;
   uint32_t bad = 0;
+  const int32_t *qL = L + lane, *qY = Ly + lane, *qZ = Lz + lane;
+  uint32_t* qO = O + lane;
 #pragma unroll U
-  for (int c = 0; c < nchunk; ++c) {
+  for (int c = 0; c < nchunk; ++c, qL += 32, qY += 32, qZ += 32, qO += 32) {
     const int x = (c << 5) + lane;
-    const int32_t v = x < X ? __ldg(L + x) : 0;
+    const bool in = FULL || x < X;
+    const int32_t v = in ? __ldg(qL) : 0;
+    const int32_t vy = in ? __ldg(qY) : 0, vz = in ? __ldg(qZ) : 0;
     int32_t l = __shfl_up_sync(kFull, v, 1);
     if (lane == 0) l = left_prev;
-    const bool is_start = x < X && (x == 0 || v != l);
+    const bool is_start = in && (x == 0 || v != l);
     const uint32_t m = __ballot_sync(kFull, is_start);
     const uint32_t le = m & (kFull >> (31 - lane));
     const int s = le ? (c << 5) + 31 - __clz(le) : carry_start;
     if (m) carry_start = (c << 5) + 31 - __clz(m);
     left_prev = __shfl_sync(kFull, v, 31);
-    if (x < X) {
+    if (in) {
       uint32_t g = 0;
       if (v != 0) {
-        if (v < 0 || v > max_label) bad = 1;
+        bad |= (uint32_t)v > (uint32_t)max_label;  // also v < 0
         const int e = ends[x];
-        const uint32_t dl = (s > 0 || border) ? (uint32_t)(x - s + 1) : kFull;
-        const uint32_t dr = (e < X - 1 || border) ? (uint32_t)(e + 1 - x) : kFull;
+        const uint32_t dl = (s > 0 || border) ? (uint32_t)(x - s + 1) : far;
+        const uint32_t dr = (e < X - 1 || border) ? (uint32_t)(e + 1 - x) : far;
         const uint32_t d = min(dl, dr);
-        g = d == kFull ? kInf : d * d;
+        g = d == far ? kInf : d * d;
       }
-      uint32_t bits = 0;
-      if (!Ly || __ldg(Ly + x) != v) bits |= kBitY;
-      if (!Lz || __ldg(Lz + x) != v) bits |= kBitZ;
-      O[x] = g | bits;
+      *qO = g | (vy != v ? kBitY : 0u) | (vz != v ? kBitZ : 0u);
     }
   }
   if (__any_sync(kFull, bad) && lane == 0) atomicOr(&hdr->status, kStBadLabel);
@@ -435,16 +444,33 @@ __global__ void __launch_bounds__(256) k_edt_col16(ColArgs a, uint32_t* __restri
 
 }  // namespace
 
+// a per-device row of -1 labels (16384 entries): the y / z neighbour row of the first row / slice
+std::mutex g_sent_mu;
+int32_t* g_sent[64];
+
 void launch_edt_x(const int32_t* labels, const int32_t* labels_below, uint32_t* out, const Geom& g,
                   int32_t max_label, bool border, WsHeader* hdr, cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(g_sent_mu);
+    if (!g_sent[dev] && cudaMalloc(&g_sent[dev], 16384 * sizeof(int32_t)) == cudaSuccess)
+      cudaMemset(g_sent[dev], 0xFF, 16384 * sizeof(int32_t));
+  }
   const int64_t nrows = g.B * g.Z * g.Y;
   int warps = (int)(49152 / (2 * g.X));
   warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
   const size_t smem = (size_t)warps * g.X * sizeof(uint16_t);
   const int64_t blocks = (nrows + warps - 1) / warps;
-  // sweep unroll 2: measured on C4 4.13 ms vs 4.46 (4), 4.35 (8), 4.26 (16)
-  k_edt_x<2><<<(unsigned)blocks, warps * 32, smem, st>>>(labels, labels_below, out, nrows, (int)g.X, g.Y, g.Z, max_label,
-                                                         border ? 1 : 0, g.ndim == 3 ? 1 : 0, hdr);
+  // sweep unroll 2: measured on C4 4.13 ms vs 4.46 (4), 4.35 (8), 4.26 (16) (round 1)
+  if (g.X % 32 == 0)
+    k_edt_x<2, true><<<(unsigned)blocks, warps * 32, smem, st>>>(labels, labels_below, g_sent[dev], out, nrows, (int)g.X,
+                                                                 g.Y, g.Z, max_label, border ? 1 : 0,
+                                                                 g.ndim == 3 ? 1 : 0, hdr);
+  else
+    k_edt_x<2, false><<<(unsigned)blocks, warps * 32, smem, st>>>(labels, labels_below, g_sent[dev], out, nrows,
+                                                                  (int)g.X, g.Y, g.Z, max_label, border ? 1 : 0,
+                                                                  g.ndim == 3 ? 1 : 0, hdr);
 }
 
 int64_t col_blocks(const Geom& g) {
