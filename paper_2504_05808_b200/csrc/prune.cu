@@ -149,16 +149,19 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
   __shared__ uint32_t red_cnt[8], red_max[8];
   __shared__ uint16_t surv[kTileVol];
   __shared__ uint32_t s_nsurv;
+  __shared__ unsigned long long s_rows;  // rows with kept centres (the compaction loops skip the others)
   __shared__ uint32_t bhist[128];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t tile = tile0 + blockIdx.x;
-  int64_t t = tile;
-  const int64_t tx = t % g.ntx;
-  t /= g.ntx;
-  const int64_t ty = t % g.nty;
-  t /= g.nty;
-  const int64_t tz = t % g.ntz;
-  const int64_t b = t / g.ntz;
+  // tile -> (tx, ty, tz, b) in 32-bit arithmetic (ntiles < 2^32, checked in make_geom)
+  uint32_t t = (uint32_t)tile;
+  const uint32_t ntx = (uint32_t)g.ntx, nty = (uint32_t)g.nty, ntz = (uint32_t)g.ntz;
+  const int64_t tx = t % ntx;
+  t /= ntx;
+  const int64_t ty = t % nty;
+  t /= nty;
+  const int64_t tz = t % ntz;
+  const int64_t b = t / ntz;
   const int64_t z0 = tz * P::TZ - P::HZ, y0 = ty * P::TY - P::H, x0 = tx * kTX - P::HX;
   const uint32_t* Db = D + b * g.Z * g.Y * g.X;
   // halo staging with cp.async (zero-fill outside the grid), one warp per (z, y) row of the
@@ -263,6 +266,9 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
     if (__any_sync(kFullMask, fg)) {
       const uint32_t m0 = m0r[k], m1 = m1r[k], m2 = m2r[k];
       if (IS3D) {
+        // per offset class, the max over its neighbours against one threshold (3-input max:
+        // VIMNMX3), instead of 26 separate compares
+        uint32_t mx[3] = {0u, 0u, 0u};
 #pragma unroll
         for (int dz = -1; dz <= 1; ++dz)
 #pragma unroll
@@ -271,9 +277,9 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
             for (int dx = -1; dx <= 1; ++dx) {
               const int cls = (dz != 0) + (dy != 0) + (dx != 0) - 1;
               if (cls < 0) continue;
-              const uint32_t m = cls == 0 ? m0 : (cls == 1 ? m1 : m2);
-              keep &= s[c + (dz * P::PY + dy) * P::PX + dx] <= m;
+              mx[cls] = max(mx[cls], s[c + (dz * P::PY + dy) * P::PX + dx]);
             }
+        keep &= mx[0] <= m0 && mx[1] <= m1 && mx[2] <= m2;
       } else {
 #pragma unroll
         for (int dy = -1; dy <= 1; ++dy)
@@ -308,10 +314,14 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
     pre[2 * lane] = ex;
     pre[2 * lane + 1] = ex + c0;
     if (lane == 31) s_nsurv = inc;
+    const uint32_t lo = __ballot_sync(kFullMask, keepmask[lane] != 0u), hi = __ballot_sync(kFullMask, keepmask[lane + 32] != 0u);
+    if (lane == 0) s_rows = (unsigned long long)lo | ((unsigned long long)hi << 32);
   }
   __syncthreads();
+  const unsigned long long my_rows = 0x0101010101010101ull << warp;  // rows warp, warp + 8, ...
 #pragma unroll 1
-  for (int row = warp; row < kRows; row += 8) {
+  for (unsigned long long rm = s_rows & my_rows; rm; rm &= rm - 1) {
+    const int row = __ffsll((long long)rm) - 1;
     const uint32_t km = keepmask[row];
     if ((km >> lane) & 1u) surv[pre[row] + __popc(km & ((1u << lane) - 1u))] = (uint16_t)(row * 32 + lane);
   }
@@ -320,7 +330,8 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
 #pragma unroll 1
   for (uint32_t i0 = warp * 32; i0 < nsurv; i0 += 256) {
     const uint32_t i = i0 + lane;
-    int v = 0, c = 0;
+    // (lanes without a survivor test the first core element: every offset stays inside the block)
+    int v = 0, c = (P::HZ * P::PY + P::H) * P::PX + P::HX;
     uint32_t d = 0;
     bool keep = false;
     if (i < nsurv) {
@@ -337,7 +348,9 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
 #pragma unroll
     for (int k = 0; k < P::NC - P::C1; ++k) {
       if (!__any_sync(kFullMask, test && keep)) break;
-      // all offsets of class C1+k; the class test folds at compile time after unrolling
+      // all offsets of class C1+k (the class test folds at compile time after unrolling): their
+      // max against the class threshold
+      uint32_t mxk = 0;
       if (IS3D) {
 #pragma unroll
         for (int dz = -3; dz <= 3; ++dz)
@@ -345,14 +358,15 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
           for (int dy = -3; dy <= 3; ++dy)
 #pragma unroll
             for (int dx = -3; dx <= 3; ++dx)
-              if (class3(dz, dy, dx) == P::C1 + k && test) keep &= s[c + (dz * P::PY + dy) * P::PX + dx] <= mv[k];
+              if (class3(dz, dy, dx) == P::C1 + k) mxk = max(mxk, s[c + (dz * P::PY + dy) * P::PX + dx]);
       } else {
 #pragma unroll
         for (int dy = -2; dy <= 2; ++dy)
 #pragma unroll
           for (int dx = -2; dx <= 2; ++dx)
-            if (class2(dy, dx) == P::C1 + k && test) keep &= s[c + dy * P::PX + dx] <= mv[k];
+            if (class2(dy, dx) == P::C1 + k) mxk = max(mxk, s[c + dy * P::PX + dx]);
       }
+      if (test) keep &= mxk <= mv[k];
     }
     if (i < nsurv && !keep) atomicAnd(&keepmask[v >> 5], ~(1u << (v & 31)));
     if (keep) maxd = max(maxd, d);
@@ -362,10 +376,14 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
   // dilation's gather stops scanning a home tile once its remaining balls cannot reach the
   // output tile.  All warps: bucket histogram -> warp-0 descending exclusive scan -> scatter.
   for (int k = tid; k < 128; k += 256) bhist[k] = 0;
+  if (warp == 0) {  // the rows still holding kept centres after stage 2
+    const uint32_t lo = __ballot_sync(kFullMask, keepmask[lane] != 0u), hi = __ballot_sync(kFullMask, keepmask[lane + 32] != 0u);
+    if (lane == 0) s_rows = (unsigned long long)lo | ((unsigned long long)hi << 32);
+  }
   __syncthreads();
-  for (int row = warp; row < kRows; row += 8) {
+  for (unsigned long long rm = s_rows & my_rows; rm; rm &= rm - 1) {
+    const int row = __ffsll((long long)rm) - 1;
     const uint32_t km = keepmask[row];
-    if (!km) continue;
     const int ly = row % P::TY, lz = row / P::TY;
     const bool kept = (km >> lane) & 1u;
     const int bk = kept ? dbucket(s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::HX)]) : -1;
@@ -401,9 +419,9 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
   __syncthreads();
   {
     uint2* out = cent + tile * kTileVol;
-    for (int row = warp; row < kRows; row += 8) {
+    for (unsigned long long rm = s_rows & my_rows; rm; rm &= rm - 1) {
+      const int row = __ffsll((long long)rm) - 1;
       const uint32_t km = keepmask[row];
-      if (!km) continue;
       const int ly = row % P::TY, lz = row / P::TY;
       const bool kept = (km >> lane) & 1u;
       const uint32_t d = kept ? s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::HX)] : 0u;
