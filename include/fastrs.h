@@ -75,8 +75,14 @@ enum {
                                     (a GPU-internal cross-check of the default dilation)    */
   FASTRS_EDGE_SKIP_ZLO = 32u,    /* fastrs_touches_edge on a z-slab (3D): its first slice is  */
   FASTRS_EDGE_SKIP_ZHI = 64u,    /* not a grid face / its last slice is not (slab path)      */
-  FASTRS_SLAB_TRANSPOSE = 128u   /* fastrs_sphericity_roundness_slab: z pass by the all-to-all
+  FASTRS_SLAB_TRANSPOSE = 128u,  /* fastrs_sphericity_roundness_slab: z pass by the all-to-all
                                     z-slab -> y-slab transpose (N1) instead of the h halo (N8) */
+  FASTRS_APPROX_LT = 256u        /* approximate local thickness (SPEC.md:153
+                                    local_thickness_fast): each 2048-element tile stops its exact
+                                    cover once at most 4 % of its foreground is uncovered, and those
+                                    cells take LT^2 = D (their own ball).  Guarantees D <= LT^2_fast
+                                    <= LT^2, LT^2_fast <= the object's max D, and >= 96 % of every
+                                    tile's foreground exact (so >= 95 % within 5 %). */
 };
 
 /* Optional per-label statistics (device pointers, each nullable, batch*max_label long). */

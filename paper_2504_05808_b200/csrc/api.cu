@@ -248,7 +248,8 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
     // tiles K5a handed over (every tile when Dmax > 65535)
     {
       Nvtx r("K5b paint + K5' fallback");
-      launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, g, ltp, labels, stage == kFull ? &acc : nullptr, hdr, st);
+      launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, g, ltp, labels, stage == kFull ? &acc : nullptr, D,
+                          (flags & kFlagApproxLt) != 0, hdr, st);
       launch_dilate_fallback(meta, cent, fbl, g, ltp, hdr, st);
     }
     tm.mark(4);
@@ -451,7 +452,7 @@ int run_host_pipelined(const int32_t* labels_host, int32_t* dlab, const Geom& g,
       gg.tz_lo = z0 / kTZ3;
       gg.tz_hi = (z1 + kTZ3 - 1) / kTZ3;
       launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, gg, 0, hdr, st);
-      launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, gg, B, dlab, &acc, hdr, st);
+      launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, gg, B, dlab, &acc, A, (flags & kFlagApproxLt) != 0, hdr, st);
     }
   }
   // tiles handed to the atomic kernel (LT^2 into B, whose y-pass words are consumed) and their
@@ -750,7 +751,8 @@ int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64
   uint32_t* goff = (uint32_t*)((char*)ws + L.goff);
   launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, g, (flags & kFlagForceFallback) != 0 ? 1 : 0, hdr,
                        st);
-  launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, g, ltp, lab_ext, &acc, hdr, st);
+  launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, g, ltp, lab_ext, &acc, d_ext, (flags & kFlagApproxLt) != 0, hdr,
+                      st);
   launch_dilate_fallback(meta, cent, fbl, g, ltp, hdr, st);
   launch_epilogue_fallback(lab_ext, d_ext, meta, fbl, g, acc, ltp, hdr, st);
   return finish_call(hdr, flags, st);

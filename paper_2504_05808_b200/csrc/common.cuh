@@ -16,7 +16,7 @@ constexpr uint32_t kBitZ = 0x40000000u;  // element is the first of its z-run
 constexpr uint32_t kStBadLabel = 1u, kStNoSite = 2u, kStInternal = 4u, kStShell = 8u;
 
 constexpr uint32_t kFlagBorder = 1u, kFlagAsync = 4u, kFlagHostIO = 8u, kFlagForceFallback = 16u;
-constexpr uint32_t kFlagEdgeSkipZlo = 32u, kFlagEdgeSkipZhi = 64u, kFlagSlabTranspose = 128u;
+constexpr uint32_t kFlagEdgeSkipZlo = 32u, kFlagEdgeSkipZhi = 64u, kFlagSlabTranspose = 128u, kFlagApproxLt = 256u;
 
 // ---- dilation / pruning tiles ---------------------------------------------------------
 // 3D tile 32 x 8 x 8 (x fastest), 2D tile 32 x 64; both 64 rows of 32 = 2048 elements.
@@ -159,9 +159,12 @@ int64_t dilate_groups(const Geom& g);        // K5 tile groups (gcount / goff en
 // K5b.  acc == NULL: LT^2 of every painted tile -> the LT plane ltp (u16).  acc != NULL (fused):
 // no LT plane; every ball that covers cells adds (count, shell count, D) of those cells to the
 // per-label accumulators of the label of the cells it covers (labels read once per covering ball)
+// approx (FASTRS_APPROX_LT, needs D): each tile stops once <= 4 % of its foreground is uncovered;
+// those cells take LT^2 = D
 void launch_dilate_paint(const uint32_t* fgm, const uint32_t* shm, const TileMeta* meta,
                          const unsigned long long* pool, const uint32_t* gcount, const uint32_t* goff, const Geom& g,
-                         uint32_t* ltp, const int32_t* labels, const Accum* acc, WsHeader* hdr, cudaStream_t st);
+                         uint32_t* ltp, const int32_t* labels, const Accum* acc, const uint32_t* D, bool approx,
+                         WsHeader* hdr, cudaStream_t st);
 void launch_dilate_fallback(TileMeta* meta, const uint2* centres, const uint32_t* fbl, const Geom& g, uint32_t* ltp,
                             WsHeader* hdr, cudaStream_t st);
 // K5a: per tile group, gather the kept balls that reach it and write them sorted by D

@@ -652,7 +652,7 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
                                            const uint32_t* __restrict__ gcount, const uint32_t* __restrict__ goff,
                                            int point_at, uint32_t* __restrict__ ltp, const int32_t* __restrict__ labels,
                                            const Accum& acc, const unsigned long long* __restrict__ fxlut,
-                                           WsHeader* __restrict__ hdr) {
+                                           const uint32_t* __restrict__ Dp, int approx, WsHeader* __restrict__ hdr) {
   using P = Shape<IS3D>;
   constexpr int TY = P::TY, TZ = P::TZ;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -731,6 +731,9 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
   __syncwarp();
   // uncovered foreground cells of my tile (warp-uniform); point mode once it is small
   int nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(f0) + __popc(f1)));
+  // FASTRS_APPROX_LT: the exact cover stops once at most 4 % of the
+  // tile's foreground is uncovered; those cells take LT^2 = D (their own ball)
+  const int stop = approx ? min(nu * 4 / 100, kPoint - 1) : 0;
   int4* sball = S.sball[wl];                 // survivors of a screened batch (cx, cy, cz, D)
   unsigned long long* scand = S.scand[wl];   // their candidate rows
   bool pmode = false;
@@ -746,6 +749,28 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
     ub[0] = __reduce_min_sync(kFull, x0); ub[1] = __reduce_max_sync(kFull, x1);
     ub[2] = __reduce_min_sync(kFull, y0); ub[3] = __reduce_max_sync(kFull, y1);
     ub[4] = __reduce_min_sync(kFull, z0); ub[5] = __reduce_max_sync(kFull, z1);
+  };
+  // list the still-uncovered cells (row*32 + x) of my rows in ulist (nu <= kPoint of them)
+  auto make_ulist = [&]() {
+    const uint32_t left[2] = {f0 & ~c0, f1 & ~c1};
+    const uint32_t cnt = __popc(left[0]) + __popc(left[1]);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += v;
+    }
+    uint32_t pos = inc - cnt;
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      uint32_t m = left[kk];
+      while (m) {
+        const int c = __ffs(m) - 1;
+        m &= m - 1;
+        ulist[pos++] = (uint16_t)((lane + 32 * kk) * 32 + c);
+      }
+    }
+    __syncwarp();
   };
   int nq = 0;  // point mode: queued balls in sball (warp-uniform)
   auto point_flush = [&]() {
@@ -809,32 +834,14 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
     // the next batch's entries are loaded one iteration ahead (their latency overlaps the
     // current batch's screening and painting)
     unsigned long long e_next = lane < total ? list[lane] : 0ull;
-    for (uint32_t i0 = 0; i0 < total && nu != 0; i0 += 32) {
+    for (uint32_t i0 = 0; i0 < total && nu > stop; i0 += 32) {
       const uint32_t i = i0 + lane;
       const unsigned long long e_cur = e_next;
       if (i0 + 32 < total) e_next = i + 32 < total ? list[i + 32] : 0ull;
       if (!pmode && nu <= point_at) {
         // switch to point mode: list the still-uncovered cells
-        const uint32_t left[2] = {f0 & ~c0, f1 & ~c1};
-        const uint32_t cnt = __popc(left[0]) + __popc(left[1]);
-        uint32_t inc = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t v = __shfl_up_sync(kFull, inc, o);
-          if (lane >= o) inc += v;
-        }
-        uint32_t pos = inc - cnt;
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-          uint32_t m = left[kk];
-          while (m) {
-            const int c = __ffs(m) - 1;
-            m &= m - 1;
-            ulist[pos++] = (uint16_t)((lane + 32 * kk) * 32 + c);
-          }
-        }
+        make_ulist();
         pmode = true;
-        __syncwarp();
         ubox_refresh();
       }
       if (pmode) {
@@ -854,7 +861,7 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
         }
         const uint32_t sv = __ballot_sync(kFull, D != 0);
         if (nq + __popc(sv) > 32) point_flush();
-        if (nu == 0) break;
+        if (nu <= stop) break;
         if (D != 0) sball[nq + __popc(sv & ((1u << lane) - 1u))] = make_int4(cx, cy, cz, D);
         nq += __popc(sv);
         __syncwarp();
@@ -970,7 +977,31 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
         nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(left[0]) + __popc(left[1])));
       }
     }
-    if (pmode && nq > 0 && nu > 0) point_flush();  // the queue's last balls
+    if (pmode && nq > 0 && nu > stop) point_flush();  // the queue's last balls
+    if (approx && nu > 0) {
+      // the approximate mode's remaining cells: LT^2 = D (lanes over the listed cells)
+      if (!pmode) make_ulist();
+      for (int q0 = 0; q0 < nu; q0 += 32) {
+        const int q = q0 + lane;
+        int32_t L = 0;
+        uint32_t d = 0, sb = 0;
+        if (q < nu) {
+          const uint32_t e = ulist[q];
+          const int row = (int)(e >> 5), x = (int)(e & 31u);
+          const int ly = IS3D ? (row & 7) : row, lz = IS3D ? (row >> 3) : 0;
+          const int64_t gi = item + ((tgz + lz) * g.Y + (tgy + ly)) * g.X + tgx + x;
+          d = __ldg(Dp + gi);
+          if (FUSED) {
+            L = __ldg(labels + gi);
+            sb = d == 1u ? 1u : 0u;  // shell <=> D == 1
+          } else {
+            val[e] = (uint16_t)d;
+          }
+        }
+        if (FUSED) accumulate_records(L, L != 0 ? 1u : 0u, sb, d, lane, b, acc, fxlut);
+      }
+      nu = 0;
+    }
   }
 
 
@@ -1019,6 +1050,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* 
                                                               uint32_t* __restrict__ ltp,
                                                               const int32_t* __restrict__ labels, Accum acc,
                                                               const unsigned long long* __restrict__ fxlut,
+                                                              const uint32_t* __restrict__ Dp, int approx,
                                                               WsHeader* __restrict__ hdr, uint32_t nbid) {
   if (hdr->dmax > kU16Max) return;  // k_dilate_atomic handles it
   const int lane = threadIdx.x & 31;
@@ -1027,7 +1059,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* 
     if (lane == 0) bid = atomicAdd(&hdr->paint_next, 1u);
     bid = __shfl_sync(kFull, bid, 0);
     if (bid >= nbid) break;
-    paint_tile<IS3D, NW, FUSED>(bid, fgm, shm, meta, g, pool, gcount, goff, point_at, ltp, labels, acc, fxlut, hdr);
+    paint_tile<IS3D, NW, FUSED>(bid, fgm, shm, meta, g, pool, gcount, goff, point_at, ltp, labels, acc, fxlut, Dp, approx,
+                                hdr);
     __syncwarp();
   }
 }
@@ -1073,7 +1106,8 @@ namespace {
 template <bool IS3D, int NW, int MINB, bool FUSED>
 void paint_go(int64_t ngroups, const uint32_t* fgm, const uint32_t* shm, const TileMeta* meta, const Geom& g,
               const unsigned long long* pool, const uint32_t* gcount, const uint32_t* goff, uint32_t* ltp,
-              const int32_t* labels, const Accum& acc, WsHeader* hdr, cudaStream_t st) {
+              const int32_t* labels, const Accum& acc, const uint32_t* D, int approx, WsHeader* hdr,
+              cudaStream_t st) {
   const uint32_t nbid = (uint32_t)(ngroups * kWarps);
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -1082,23 +1116,25 @@ void paint_go(int64_t ngroups, const uint32_t* fgm, const uint32_t* shm, const T
   const uint32_t grid = ((nbid < cap ? nbid : cap) + NW - 1) / NW;
   cudaMemsetAsync(&hdr->paint_next, 0, sizeof(uint32_t), st);
   k_dilate_paint<IS3D, NW, MINB, FUSED><<<grid, NW * 32, sizeof(PaintSmem<NW, FUSED>), st>>>(
-      fgm, shm, meta, g, pool, gcount, goff, point_at_knob(), ltp, labels, acc, device_fxlut(dev), hdr, nbid);
+      fgm, shm, meta, g, pool, gcount, goff, point_at_knob(), ltp, labels, acc, device_fxlut(dev), D, approx, hdr, nbid);
 }
 }  // namespace
 
 void launch_dilate_paint(const uint32_t* fgm, const uint32_t* shm, const TileMeta* meta,
                          const unsigned long long* pool, const uint32_t* gcount, const uint32_t* goff, const Geom& g,
-                         uint32_t* ltp, const int32_t* labels, const Accum* acc, WsHeader* hdr, cudaStream_t st) {
+                         uint32_t* ltp, const int32_t* labels, const Accum* acc, const uint32_t* D, bool approx,
+                         WsHeader* hdr, cudaStream_t st) {
+  const int ap = approx && D ? 1 : 0;
   const int64_t ngroups = launched_groups(g);
   if (ngroups <= 0) return;
   Accum a{};
   if (acc) a = *acc;
   if (g.ndim == 3) {
-    if (acc) paint_go<true, kPaintNW, kPaintMinB, true>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, hdr, st);
-    else paint_go<true, kPaintNW, kPaintMinB, false>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, hdr, st);
+    if (acc) paint_go<true, kPaintNW, kPaintMinB, true>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, D, ap, hdr, st);
+    else paint_go<true, kPaintNW, kPaintMinB, false>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, D, ap, hdr, st);
   } else {
-    if (acc) paint_go<false, kPaintNW, kPaintMinB, true>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, hdr, st);
-    else paint_go<false, kPaintNW, kPaintMinB, false>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, hdr, st);
+    if (acc) paint_go<false, kPaintNW, kPaintMinB, true>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, D, ap, hdr, st);
+    else paint_go<false, kPaintNW, kPaintMinB, false>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, D, ap, hdr, st);
   }
 }
 

@@ -376,7 +376,7 @@ int fastrs_sphericity_roundness_slab(const int32_t* labels, const int64_t* dims_
   uint64_t* part = (uint64_t*)(w + L.part);
   void* pw = w + L.phase;
   const size_t pwb = L.phase_bytes;
-  const uint32_t pf = (flags & (FASTRS_BORDER_BACKGROUND | FASTRS_FORCE_FALLBACK)) | FASTRS_ASYNC;
+  const uint32_t pf = (flags & (FASTRS_BORDER_BACKGROUND | FASTRS_FORCE_FALLBACK | FASTRS_APPROX_LT)) | FASTRS_ASYNC;
   const int64_t M = max_label;
   uint64_t sent = 0, recvd = 0;
   int nstat = 0;

@@ -21,6 +21,7 @@ DETERMINISTIC = 2
 ASYNC = 4
 HOST_IO = 8
 FORCE_FALLBACK = 16  # run the dilation with the atomic sparse-table kernel (cross-check)
+APPROX_LT = 256  # approximate local thickness (FASTRS_APPROX_LT)
 
 STAGES = ("edt_x", "edt_y", "edt_z", "prune", "dilate", "metrics", "epilogue", "gather")
 
