@@ -77,6 +77,8 @@ enum {
   FASTRS_EDGE_SKIP_ZHI = 64u,    /* not a grid face / its last slice is not (slab path)      */
   FASTRS_SLAB_TRANSPOSE = 128u,  /* fastrs_sphericity_roundness_slab: z pass by the all-to-all
                                     z-slab -> y-slab transpose (N1) instead of the h halo (N8) */
+  FASTRS_SLAB_DENSE_HALO = 512u, /* fastrs_sphericity_roundness_slab: exchange H dense slices of D
+                                    for the dilation instead of the kept-centre halo (N4)        */
   FASTRS_APPROX_LT = 256u        /* approximate local thickness (SPEC.md:153
                                     local_thickness_fast): each 2048-element tile stops its exact
                                     cover once at most 4 % of its foreground is uncovered, and those
@@ -217,6 +219,31 @@ FASTRS_API int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, 
                                   uint64_t* sum_lt, uint64_t* sum_shell_lt, uint32_t* max_lt2, void* ws,
                                   size_t ws_bytes, void* stream);
 
+/* C, split for the kept-centre halo (N4: instead of the H slices of D, neighbours exchange the
+ * K4 outputs of the tile layers within H slices of each other's slab):
+ *   fastrs_slab_prune   K4 on the own tile layers only (d_ext must hold D of the own slab and the
+ *                       3 slices on each side that K4's |s|^2 <= 12 stencil reads; the other
+ *                       layers' tile data are cleared)
+ *   fastrs_slab_pack_tiles / fastrs_slab_unpack_tiles   the K4 outputs of tile layers
+ *                       [tz_a, tz_b) of the extended slab as 12 u32 per tile (count, max D, nfg,
+ *                       0, 16 u16 octave counts) plus the tiles' kept centres (uint2 each, tile
+ *                       order; *n_entries <- their number, a device u64); unpack writes them into
+ *                       the same layers of the receiver's workspace (its own layer indices)
+ *   fastrs_slab_dilate  K5 on the own tiles from the tile data in the workspace
+ * Together they give the same integer partials as fastrs_slab_reduce (K4's outputs for a tile
+ * depend only on D within 3 slices of it).  All enqueue on `stream`; prune and dilate synchronise
+ * once unless FASTRS_ASYNC. */
+FASTRS_API int fastrs_slab_prune(const uint32_t* d_ext, const int64_t* dims_ext, int64_t own_lo, int64_t own_hi,
+                                 uint32_t flags, void* ws, size_t ws_bytes, void* stream);
+FASTRS_API int fastrs_slab_pack_tiles(void* ws, const int64_t* dims_ext, int64_t tz_a, int64_t tz_b, uint32_t* rec_out,
+                                      void* ent_out, uint64_t* n_entries, void* stream);
+FASTRS_API int fastrs_slab_unpack_tiles(void* ws, const int64_t* dims_ext, int64_t tz_a, int64_t tz_b,
+                                        const uint32_t* rec_in, const void* ent_in, void* stream);
+FASTRS_API int fastrs_slab_dilate(const int32_t* labels, const uint32_t* d_ext, const int64_t* dims_ext, int64_t own_lo,
+                                  int64_t own_hi, int64_t Z, uint32_t dmax_global, int32_t max_label, uint32_t flags,
+                                  uint64_t* vol, uint64_t* n_shell, uint64_t* sum_lt, uint64_t* sum_shell_lt,
+                                  uint32_t* max_lt2, void* ws, size_t ws_bytes, void* stream);
+
 /* D: closed forms from (reduced) partials: n_labels entries, nscale = elements per item used
  * for the fixed-point scale, dmax_global as in C.  Outputs as fastrs_sphericity_roundness. */
 FASTRS_API int fastrs_metrics_from_partials(const uint64_t* vol, const uint64_t* n_shell, const uint64_t* sum_lt,
@@ -264,7 +291,9 @@ FASTRS_API int fastrs_filter_objects(double* sphericity, double* roundness, cons
  *   [nz][Y][X] (device), dims_slab = {nz, Y, X}.  Exchanges (NCCL, on `stream`): the label slice
  *   below the slab; the z pass by an h-slice halo of packed EDT words, h = ceil(sqrt(max D_xy))
  *   (N8, default), or by the all-to-all z-slab <-> y-slab transpose (N1, FASTRS_SLAB_TRANSPOSE);
- *   the H-slice halo of D for the dilation, H = isqrt(Dmax - 1) rounded up to 8; allreduce(sum)
+ *   the dilation halo, H = isqrt(Dmax - 1) rounded up to 8: by default the K4 outputs (tile records +
+ *   kept centres) of the tile layers within H slices of each neighbour's slab, after a 3-slice D
+ *   halo for K4's stencil (N4); with FASTRS_SLAB_DENSE_HALO the H slices of D; allreduce(sum)
  *   of the per-label u64 partial sums and allreduce(max) of max LT^2.  Every rank receives all
  *   max_label results (sphericity, roundness, stats: device, nullable), bit-identical to
  *   fastrs_sphericity_roundness on the whole volume.  info (host, nullable) reports the mode,

@@ -312,7 +312,7 @@ int finish_call(WsHeader* hdr, uint32_t flags, cudaStream_t st) {
 }
 
 struct SlabLayout {
-  size_t hdr, P, meta, fgm, shm, oct, fbl, gcount, goff, pool, sat, cent, total;
+  size_t hdr, P, meta, fgm, shm, oct, fbl, gcount, goff, pool, sat, poff, cent, total;
 };
 SlabLayout make_slab_layout(const Geom& g) {
   SlabLayout L{};
@@ -333,9 +333,65 @@ SlabLayout make_slab_layout(const Geom& g) {
   L.goff = take((size_t)dilate_groups(g) * 4);
   L.pool = take((size_t)dilate_pool_entries(g) * 8);
   L.sat = take((size_t)col_blocks(g) * 4);
+  L.poff = take((size_t)g.ntiles * 4 + 16);
   L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
   L.total = off;
   return L;
+}
+
+// ---- kept-centre halo (N4): pack / unpack the K4 outputs of whole tile layers ----------------
+// record per tile: TileMeta (4 u32) + the 16 octave counts (8 u32) = 12 u32; entries: the tile's
+// kept centres (uint2), tiles in index order
+constexpr int kRecWords = 12;
+
+// exclusive prefix of the tiles' centre counts (one CTA; counts from meta or from records)
+__global__ void k_tile_prefix(const TileMeta* __restrict__ meta, const uint32_t* __restrict__ rec, int64_t t0,
+                              int64_t n, uint32_t* __restrict__ off, unsigned long long* __restrict__ total) {
+  const int64_t per = (n + blockDim.x - 1) / blockDim.x, lo = threadIdx.x * per, hi = lo + per < n ? lo + per : n;
+  unsigned long long loc = 0;
+  for (int64_t i = lo; i < hi; ++i) loc += rec ? rec[i * kRecWords] : meta[t0 + i].count;
+  __shared__ unsigned long long part[1024];
+  part[threadIdx.x] = loc;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    const unsigned long long v = (int)threadIdx.x >= o ? part[threadIdx.x - o] : 0ull;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  unsigned long long run = part[threadIdx.x] - loc;
+  for (int64_t i = lo; i < hi; ++i) {
+    off[i] = (uint32_t)run;
+    run += rec ? rec[i * kRecWords] : meta[t0 + i].count;
+  }
+  if (threadIdx.x == blockDim.x - 1 && total) *total = part[threadIdx.x];
+}
+
+__global__ void k_tile_pack(const TileMeta* __restrict__ meta, const uint16_t* __restrict__ oct,
+                            const uint2* __restrict__ cent, int64_t t0, const uint32_t* __restrict__ off,
+                            uint32_t* __restrict__ rec, uint2* __restrict__ ent) {
+  const int64_t i = blockIdx.x, t = t0 + i;
+  const TileMeta m = meta[t];
+  if (threadIdx.x < 4) rec[i * kRecWords + threadIdx.x] = threadIdx.x == 0 ? m.count : threadIdx.x == 1 ? m.maxD
+                                                                              : threadIdx.x == 2 ? m.nfg : 0u;
+  if (threadIdx.x < 8)
+    rec[i * kRecWords + 4 + threadIdx.x] = (uint32_t)oct[t * 16 + 2 * threadIdx.x] |
+                                           ((uint32_t)oct[t * 16 + 2 * threadIdx.x + 1] << 16);
+  for (uint32_t k = threadIdx.x; k < m.count; k += blockDim.x) ent[off[i] + k] = cent[t * kTileVol + k];
+}
+
+__global__ void k_tile_unpack(TileMeta* __restrict__ meta, uint16_t* __restrict__ oct, uint2* __restrict__ cent,
+                              int64_t t0, const uint32_t* __restrict__ off, const uint32_t* __restrict__ rec,
+                              const uint2* __restrict__ ent) {
+  const int64_t i = blockIdx.x, t = t0 + i;
+  const uint32_t cnt = rec[i * kRecWords];
+  if (threadIdx.x == 0) meta[t] = TileMeta{cnt, rec[i * kRecWords + 1], rec[i * kRecWords + 2], 0u};
+  if (threadIdx.x < 8) {
+    const uint32_t w = rec[i * kRecWords + 4 + threadIdx.x];
+    oct[t * 16 + 2 * threadIdx.x] = (uint16_t)(w & 0xFFFFu);
+    oct[t * 16 + 2 * threadIdx.x + 1] = (uint16_t)(w >> 16);
+  }
+  for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) cent[t * kTileVol + k] = ent[off[i] + k];
 }
 
 int slab_prologue(const int64_t* dims, Geom& g, SlabLayout& L, void* ws, size_t ws_bytes, WsHeader*& hdr,
@@ -701,20 +757,16 @@ int fastrs_slab_edt_z(const uint32_t* packed_ext, const int64_t* dims_ext, int64
   return finish_call(hdr, flags, st);
 }
 
-int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64_t* dims_ext, int64_t own_lo,
-                       int64_t own_hi, int64_t Z, uint32_t dmax_global, int32_t max_label, uint32_t flags,
-                       uint64_t* vol, uint64_t* n_shell, uint64_t* sum_lt, uint64_t* sum_shell_lt, uint32_t* max_lt2,
-                       void* ws, size_t ws_bytes, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
-  Geom g;
-  SlabLayout L{};
-  WsHeader* hdr = nullptr;
-  int rc = slab_prologue(dims_ext, g, L, ws, ws_bytes, hdr, st);
-  if (rc) return rc;
-  if (!labels || !d_ext || !vol || !n_shell || !sum_lt || !sum_shell_lt || !max_lt2 || max_label < 1)
-    return fail(FASTRS_EINVAL, "NULL pointer or max_label < 1");
-  if (own_lo < 0 || own_hi > g.Z || own_lo >= own_hi || (own_lo % kTZ3) != 0 || ((own_hi % kTZ3) != 0 && own_hi != g.Z))
-    return fail(FASTRS_EINVAL, "own slab range must be tile aligned (multiples of 8 slices) inside the extended slab");
+}  // extern "C"
+
+namespace fastrs {
+namespace {
+// K5 (gather, paint with fused reductions, fallback) of the own tiles of an extended slab whose
+// K4 outputs are in the workspace (own layers from K4, halo layers from K4 or unpacked)
+int slab_dilate_impl(const int32_t* labels, const uint32_t* d_ext, Geom g, const SlabLayout& L, WsHeader* hdr,
+                     int64_t own_lo, int64_t own_hi, int64_t Z, uint32_t dmax_global, int32_t max_label,
+                     uint32_t flags, uint64_t* vol, uint64_t* n_shell, uint64_t* sum_lt, uint64_t* sum_shell_lt,
+                     uint32_t* max_lt2, void* ws, cudaStream_t st) {
   g.tz_lo = own_lo / kTZ3;
   g.tz_hi = (own_hi + kTZ3 - 1) / kTZ3;
   g.nscale = Z * g.Y * g.X;
@@ -732,7 +784,6 @@ int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64
   uint32_t* fgm = (uint32_t*)((char*)ws + L.fgm);
   uint32_t* shm = (uint32_t*)((char*)ws + L.shm);
   uint16_t* oct = (uint16_t*)((char*)ws + L.oct);
-  launch_prune(d_ext, g, meta, cent, fgm, shm, oct, hdr, st);
   Accum acc{};
   acc.vol = (unsigned long long*)vol;
   acc.nshell = (unsigned long long*)n_shell;
@@ -755,6 +806,118 @@ int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64
                       st);
   launch_dilate_fallback(meta, cent, fbl, g, ltp, hdr, st);
   launch_epilogue_fallback(lab_ext, d_ext, meta, fbl, g, acc, ltp, hdr, st);
+  return FASTRS_OK;
+}
+
+int check_own(const Geom& g, int64_t own_lo, int64_t own_hi) {
+  if (own_lo < 0 || own_hi > g.Z || own_lo >= own_hi || (own_lo % kTZ3) != 0 || ((own_hi % kTZ3) != 0 && own_hi != g.Z))
+    return fail(FASTRS_EINVAL, "own slab range must be tile aligned (multiples of 8 slices) inside the extended slab");
+  return FASTRS_OK;
+}
+}  // namespace
+}  // namespace fastrs
+
+extern "C" {
+
+int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, const int64_t* dims_ext, int64_t own_lo,
+                       int64_t own_hi, int64_t Z, uint32_t dmax_global, int32_t max_label, uint32_t flags,
+                       uint64_t* vol, uint64_t* n_shell, uint64_t* sum_lt, uint64_t* sum_shell_lt, uint32_t* max_lt2,
+                       void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  Geom g;
+  SlabLayout L{};
+  WsHeader* hdr = nullptr;
+  int rc = slab_prologue(dims_ext, g, L, ws, ws_bytes, hdr, st);
+  if (rc) return rc;
+  if (!labels || !d_ext || !vol || !n_shell || !sum_lt || !sum_shell_lt || !max_lt2 || max_label < 1)
+    return fail(FASTRS_EINVAL, "NULL pointer or max_label < 1");
+  if ((rc = check_own(g, own_lo, own_hi))) return rc;
+  // K4 on every tile of the extended slab (the halo tiles from the D halo), then K5 on the own tiles
+  launch_prune(d_ext, g, (TileMeta*)((char*)ws + L.meta), (uint2*)((char*)ws + L.cent), (uint32_t*)((char*)ws + L.fgm),
+               (uint32_t*)((char*)ws + L.shm), (uint16_t*)((char*)ws + L.oct), hdr, st);
+  rc = slab_dilate_impl(labels, d_ext, g, L, hdr, own_lo, own_hi, Z, dmax_global, max_label, flags, vol, n_shell,
+                        sum_lt, sum_shell_lt, max_lt2, ws, st);
+  if (rc) return rc;
+  return finish_call(hdr, flags, st);
+}
+
+int fastrs_slab_prune(const uint32_t* d_ext, const int64_t* dims_ext, int64_t own_lo, int64_t own_hi, uint32_t flags,
+                      void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  Geom g;
+  SlabLayout L{};
+  WsHeader* hdr = nullptr;
+  int rc = slab_prologue(dims_ext, g, L, ws, ws_bytes, hdr, st);
+  if (rc) return rc;
+  if (!d_ext) return fail(FASTRS_EINVAL, "NULL pointer");
+  if ((rc = check_own(g, own_lo, own_hi))) return rc;
+  TileMeta* meta = (TileMeta*)((char*)ws + L.meta);
+  // halo layers read as empty until fastrs_slab_unpack_tiles fills them
+  cudaError_t e = cudaMemsetAsync(meta, 0, (size_t)g.ntiles * sizeof(TileMeta), st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  launch_prune(d_ext, g, meta, (uint2*)((char*)ws + L.cent), (uint32_t*)((char*)ws + L.fgm),
+               (uint32_t*)((char*)ws + L.shm), (uint16_t*)((char*)ws + L.oct), hdr, st, own_lo / kTZ3,
+               (own_hi + kTZ3 - 1) / kTZ3);
+  return finish_call(hdr, flags, st);
+}
+
+int fastrs_slab_pack_tiles(void* ws, const int64_t* dims_ext, int64_t tz_a, int64_t tz_b, uint32_t* rec_out,
+                           void* ent_out, uint64_t* n_entries, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  Geom g;
+  int rc = make_geom(dims_ext, 3, 1, g);
+  if (rc) return rc;
+  if (!ws || !rec_out || !ent_out || !n_entries || tz_a < 0 || tz_b > g.ntz || tz_a >= tz_b)
+    return fail(FASTRS_EINVAL, "bad pack arguments");
+  const SlabLayout L = make_slab_layout(g);
+  const int64_t t0 = tz_a * g.nty * g.ntx, n = (tz_b - tz_a) * g.nty * g.ntx;
+  uint32_t* off = (uint32_t*)((char*)ws + L.poff);
+  k_tile_prefix<<<1, 1024, 0, st>>>((const TileMeta*)((char*)ws + L.meta), nullptr, t0, n, off,
+                                    (unsigned long long*)n_entries);
+  k_tile_pack<<<(unsigned)n, 128, 0, st>>>((const TileMeta*)((char*)ws + L.meta), (const uint16_t*)((char*)ws + L.oct),
+                                           (const uint2*)((char*)ws + L.cent), t0, off, rec_out, (uint2*)ent_out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? FASTRS_OK : cuda_fail(e, "pack tiles");
+}
+
+int fastrs_slab_unpack_tiles(void* ws, const int64_t* dims_ext, int64_t tz_a, int64_t tz_b, const uint32_t* rec_in,
+                             const void* ent_in, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  Geom g;
+  int rc = make_geom(dims_ext, 3, 1, g);
+  if (rc) return rc;
+  if (!ws || !rec_in || !ent_in || tz_a < 0 || tz_b > g.ntz || tz_a >= tz_b)
+    return fail(FASTRS_EINVAL, "bad unpack arguments");
+  const SlabLayout L = make_slab_layout(g);
+  const int64_t t0 = tz_a * g.nty * g.ntx, n = (tz_b - tz_a) * g.nty * g.ntx;
+  uint32_t* off = (uint32_t*)((char*)ws + L.poff);
+  k_tile_prefix<<<1, 1024, 0, st>>>(nullptr, rec_in, t0, n, off, nullptr);
+  k_tile_unpack<<<(unsigned)n, 128, 0, st>>>((TileMeta*)((char*)ws + L.meta), (uint16_t*)((char*)ws + L.oct),
+                                             (uint2*)((char*)ws + L.cent), t0, off, rec_in, (const uint2*)ent_in);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? FASTRS_OK : cuda_fail(e, "unpack tiles");
+}
+
+int fastrs_slab_dilate(const int32_t* labels, const uint32_t* d_ext, const int64_t* dims_ext, int64_t own_lo,
+                       int64_t own_hi, int64_t Z, uint32_t dmax_global, int32_t max_label, uint32_t flags,
+                       uint64_t* vol, uint64_t* n_shell, uint64_t* sum_lt, uint64_t* sum_shell_lt, uint32_t* max_lt2,
+                       void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  Geom g;
+  int rc = make_geom(dims_ext, 3, 1, g);
+  if (rc) return rc;
+  if (!ws || ((uintptr_t)ws & 255) != 0) return fail(FASTRS_EINVAL, "workspace NULL or not 256-byte aligned");
+  const SlabLayout L = make_slab_layout(g);
+  if (ws_bytes < L.total) return fail(FASTRS_ENOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+  if (!labels || !d_ext || !vol || !n_shell || !sum_lt || !sum_shell_lt || !max_lt2 || max_label < 1)
+    return fail(FASTRS_EINVAL, "NULL pointer or max_label < 1");
+  if ((rc = check_own(g, own_lo, own_hi))) return rc;
+  WsHeader* hdr = (WsHeader*)((char*)ws + L.hdr);
+  cudaError_t e = cudaMemsetAsync(hdr, 0, 256, st);  // (the tile data of fastrs_slab_prune stays)
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  rc = slab_dilate_impl(labels, d_ext, g, L, hdr, own_lo, own_hi, Z, dmax_global, max_label, flags, vol, n_shell,
+                        sum_lt, sum_shell_lt, max_lt2, ws, st);
+  if (rc) return rc;
   return finish_call(hdr, flags, st);
 }
 

@@ -195,6 +195,21 @@ int exchange(const Comm& cm, const std::vector<Xfer>& plan, const std::vector<in
   return FASTRS_OK;
 }
 
+// total kept centres announced by n tile records (12 u32 each, count first)
+__global__ void k_count_entries(const uint32_t* __restrict__ rec, int64_t n, uint64_t* __restrict__ out) {
+  uint32_t c = 0;  // (<= 2048 per tile: no u32 overflow per thread or warp for < 2^21 tiles)
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) c += rec[i * 12];
+  const unsigned long long s = __reduce_add_sync(0xFFFFFFFFu, c);
+  __shared__ unsigned long long w[8];
+  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += w[i];
+    *out = t;
+  }
+}
+
 __global__ void k_status_flags(const uint32_t* __restrict__ st, int n, uint32_t* __restrict__ flags) {
   uint32_t s = 0;
   for (int i = 0; i < n; ++i) s |= st[i];
@@ -207,7 +222,8 @@ __global__ void k_status_flags(const uint32_t* __restrict__ st, int n, uint32_t*
 inline size_t al256(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct CallLayout {
-  size_t stat, flags, dxy, dmax, below, ext, dext, t0, t1, part, phase, phase_bytes, total;
+  size_t stat, flags, dxy, dmax, below, ext, dext, t0, t1, part, srec, sent, rrec, rent, cnt, phase, phase_bytes, total;
+  int64_t send_tiles, recv_tiles;  // capacities of the kept-centre halo buffers (tiles)
 };
 
 int slab_phase_bytes(int64_t nz, int64_t Y, int64_t X, size_t* out) {
@@ -218,7 +234,7 @@ int slab_phase_bytes(int64_t nz, int64_t Y, int64_t X, size_t* out) {
 // workspace of one slab call: the exchange buffers, the partial sums and one phase workspace
 // sized for the largest geometry a phase runs on
 int call_layout(const std::vector<int64_t>& bd, int rank, int64_t Y, int64_t X, int32_t max_label, int64_t cap,
-                bool transpose, CallLayout& L) {
+                bool transpose, bool dense, CallLayout& L) {
   const int P = (int)bd.size() - 1;
   const int64_t nz = bd[rank + 1] - bd[rank], Z = bd[P];
   const int64_t YX = Y * X, M = max_label;
@@ -240,6 +256,15 @@ int call_layout(const std::vector<int64_t>& bd, int rank, int64_t Y, int64_t X, 
   L.t0 = take(tsz);  // N1: send buffer, then D of the y-slab
   L.t1 = take(tsz);  // N1: receive buffers
   L.part = take((size_t)M * 8 * 6 + (size_t)M * 4);
+  // kept-centre halo (N4): K4 records (12 u32 per tile) and kept centres (<= 2048 per tile)
+  const int64_t tpl = ((Y + kTZ3 - 1) / kTZ3) * ((X + 31) / 32), capl = (cap + kTZ3 - 1) / kTZ3;
+  L.recv_tiles = dense ? 0 : 2 * capl * tpl;
+  L.send_tiles = dense ? 0 : (2 * capl + (nz + kTZ3 - 1) / kTZ3) * tpl;
+  L.srec = take((size_t)L.send_tiles * 12 * 4);
+  L.sent = take((size_t)L.send_tiles * kTileVol * 8);
+  L.rrec = take((size_t)L.recv_tiles * 12 * 4);
+  L.rent = take((size_t)L.recv_tiles * kTileVol * 8);
+  L.cnt = take((size_t)8 * P * 8);
   size_t pb = 0, v = 0;
   int rc = slab_phase_bytes(nz + 2 * cap > Z ? Z : nz + 2 * cap, Y, X, &pb);
   if (rc) return rc;
@@ -338,7 +363,7 @@ int fastrs_slab_call_workspace_bytes(const int64_t* dims_slab, int64_t z0, int64
     return err(FASTRS_EINVAL, "the slab [z0, z0 + nz) is not fastrs_slab_partition(Z, nranks)[rank]");
   CallLayout L;
   const int rc = call_layout(bd, rank, dims_slab[1], dims_slab[2], max_label, halo_cap,
-                             (flags & FASTRS_SLAB_TRANSPOSE) != 0, L);
+                             (flags & FASTRS_SLAB_TRANSPOSE) != 0, (flags & FASTRS_SLAB_DENSE_HALO) != 0, L);
   if (rc) return rc;
   *bytes = L.total;
   return FASTRS_OK;
@@ -361,7 +386,8 @@ int fastrs_sphericity_roundness_slab(const int32_t* labels, const int64_t* dims_
   const int64_t nz = dims_slab[0], Y = dims_slab[1], X = dims_slab[2], YX = Y * X, z1 = z0 + nz;
   const bool transpose = (flags & FASTRS_SLAB_TRANSPOSE) != 0;
   CallLayout L;
-  int rc = call_layout(bd, rank, Y, X, max_label, halo_cap, transpose, L);
+  const bool dense = (flags & FASTRS_SLAB_DENSE_HALO) != 0;
+  int rc = call_layout(bd, rank, Y, X, max_label, halo_cap, transpose, dense, L);
   if (rc) return rc;
   if (ws_bytes < L.total) return err(FASTRS_ENOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   if (((uintptr_t)ws & 255) != 0) return err(FASTRS_EINVAL, "workspace must be 256-byte aligned");
@@ -487,9 +513,7 @@ int fastrs_sphericity_roundness_slab(const int32_t* labels, const int64_t* dims_
   if (H > halo_cap)
     return err(FASTRS_ENOMEM, "dilation halo H = %lld slices exceeds halo_cap = %lld", (long long)H,
                (long long)halo_cap);
-  // C: H slices of D per side, K4 on the extended slab, K5 on the own tiles
-  rc = exchange(cm, halo_plan(bd, H, Z), bd, d_own, dext, halo_cap, YX, ncclUint32, st, &sent, &recvd);
-  if (rc) return rc;
+  // C: the dilation halo.  The extended slab covers the global slices [z0 - Hlo, z1 + Hhi).
   const int64_t Hlo = z0 - H > 0 ? H : z0, Hhi = z1 + H < Z ? H : Z - z1;
   const int64_t dc[3] = {Hlo + nz + Hhi, Y, X};
   uint64_t* vol = part;
@@ -497,10 +521,101 @@ int fastrs_sphericity_roundness_slab(const int32_t* labels, const int64_t* dims_
   uint64_t* sum = part + 2 * M;
   uint64_t* sums = part + 4 * M;
   uint32_t* mx = (uint32_t*)(part + 6 * M);
-  rc = fastrs_slab_reduce(labels, dext + (halo_cap - Hlo) * YX, dc, Hlo, Hlo + nz, Z, h_dmax, max_label, pf, vol, nsh,
-                          sum, sums, mx, pw, pwb, stream);
-  if (rc) return rc;
-  CUDA_TRY(keep_status(), "status copy");
+  uint32_t* dwin = dext + (halo_cap - Hlo) * YX;
+  if (dense) {
+    // dense (FASTRS_SLAB_DENSE_HALO): H slices of D per side, K4 on the whole extended slab
+    rc = exchange(cm, halo_plan(bd, H, Z), bd, d_own, dext, halo_cap, YX, ncclUint32, st, &sent, &recvd);
+    if (rc) return rc;
+    rc = fastrs_slab_reduce(labels, dwin, dc, Hlo, Hlo + nz, Z, h_dmax, max_label, pf, vol, nsh, sum, sums, mx, pw, pwb,
+                            stream);
+    if (rc) return rc;
+    CUDA_TRY(keep_status(), "status copy");
+  } else {
+    // kept-centre halo (N4, default): 3 slices of D per side (K4's stencil), K4 on the own tile
+    // layers, then the K4 outputs (records + kept centres) of the tile layers within H slices of
+    // each neighbour's slab instead of its D; K5 on the own tiles
+    rc = exchange(cm, halo_plan(bd, 3, Z), bd, d_own, dext, halo_cap, YX, ncclUint32, st, &sent, &recvd);
+    if (rc) return rc;
+    rc = fastrs_slab_prune(dwin, dc, Hlo, Hlo + nz, pf, pw, pwb, stream);
+    if (rc) return rc;
+    CUDA_TRY(keep_status(), "status copy");
+    const std::vector<Xfer> plan = halo_plan(bd, H, Z);
+    const int64_t tpl = ((Y + kTZ3 - 1) / kTZ3) * ((X + 31) / 32);
+    auto win0 = [&](int r) {  // global slice of rank r's extended-slab slot 0
+      return bd[r] - (bd[r] - H > 0 ? H : bd[r]);
+    };
+    uint32_t* srec = (uint32_t*)(w + L.srec);
+    uint2* sent_e = (uint2*)(w + L.sent);
+    uint32_t* rrec = (uint32_t*)(w + L.rrec);
+    uint2* rent_e = (uint2*)(w + L.rent);
+    uint64_t* cnt = (uint64_t*)(w + L.cnt);  // [0, 4P): entries per send transfer, [4P, 8P): per receive
+    struct Part {
+      int peer;
+      int64_t la, lb, tile_off;  // own-window tile layers [la, lb), offset in the record / entry buffers
+    };
+    std::vector<Part> sends, recvs;
+    int64_t soff = 0, roff = 0;
+    for (const Xfer& x : plan) {
+      if (x.src == rank) {
+        const int64_t la = (x.a - win0(rank)) / kTZ3, lb = (x.b - win0(rank) + kTZ3 - 1) / kTZ3;
+        sends.push_back({x.dst, la, lb, soff});
+        soff += (lb - la) * tpl;
+      }
+      if (x.dst == rank) {
+        const int64_t la = (x.a - win0(rank)) / kTZ3, lb = (x.b - win0(rank) + kTZ3 - 1) / kTZ3;
+        recvs.push_back({x.src, la, lb, roff});
+        roff += (lb - la) * tpl;
+      }
+    }
+    if (soff > L.send_tiles || roff > L.recv_tiles || (int)(sends.size() + recvs.size()) > 4 * P)
+      return err(FASTRS_ENOMEM, "kept-centre halo buffers too small (halo H = %lld)", (long long)H);
+    for (size_t k = 0; k < sends.size(); ++k) {
+      rc = fastrs_slab_pack_tiles(pw, dc, sends[k].la, sends[k].lb, srec + sends[k].tile_off * 12,
+                                  sent_e + sends[k].tile_off * kTileVol, cnt + k, stream);
+      if (rc) return rc;
+    }
+    NCCL_TRY(n.GroupStart(), "ncclGroupStart");  // round 1: the fixed-size tile records
+    for (const Part& q : sends) {
+      const size_t c = (size_t)((q.lb - q.la) * tpl * 12);
+      NCCL_TRY(n.Send(srec + q.tile_off * 12, c, ncclUint32, q.peer, cm.c, st), "ncclSend");
+      sent += c * 4;
+    }
+    for (const Part& q : recvs) {
+      const size_t c = (size_t)((q.lb - q.la) * tpl * 12);
+      NCCL_TRY(n.Recv(rrec + q.tile_off * 12, c, ncclUint32, q.peer, cm.c, st), "ncclRecv");
+      recvd += c * 4;
+    }
+    NCCL_TRY(n.GroupEnd(), "ncclGroupEnd");
+    for (size_t k = 0; k < recvs.size(); ++k)  // entries announced by the received records
+      k_count_entries<<<1, 256, 0, st>>>(rrec + recvs[k].tile_off * 12, (recvs[k].lb - recvs[k].la) * tpl,
+                                         cnt + 4 * P + k);
+    std::vector<uint64_t> hc(8 * P, 0);
+    CUDA_TRY(cudaMemcpyAsync(hc.data(), cnt, 8 * P * sizeof(uint64_t), cudaMemcpyDeviceToHost, st), "D2H");
+    CUDA_TRY(cudaStreamSynchronize(st), "sync");
+    NCCL_TRY(n.GroupStart(), "ncclGroupStart");  // round 2: the kept centres (uint2 = 2 u32)
+    for (size_t k = 0; k < sends.size(); ++k)
+      if (hc[k]) {
+        NCCL_TRY(n.Send(sent_e + sends[k].tile_off * kTileVol, (size_t)hc[k] * 2, ncclUint32, sends[k].peer, cm.c, st),
+                 "ncclSend");
+        sent += hc[k] * 8;
+      }
+    for (size_t k = 0; k < recvs.size(); ++k)
+      if (hc[4 * P + k]) {
+        NCCL_TRY(n.Recv(rent_e + recvs[k].tile_off * kTileVol, (size_t)hc[4 * P + k] * 2, ncclUint32, recvs[k].peer,
+                        cm.c, st),
+                 "ncclRecv");
+        recvd += hc[4 * P + k] * 8;
+      }
+    NCCL_TRY(n.GroupEnd(), "ncclGroupEnd");
+    for (const Part& q : recvs) {
+      rc = fastrs_slab_unpack_tiles(pw, dc, q.la, q.lb, rrec + q.tile_off * 12, rent_e + q.tile_off * kTileVol, stream);
+      if (rc) return rc;
+    }
+    rc = fastrs_slab_dilate(labels, dwin, dc, Hlo, Hlo + nz, Z, h_dmax, max_label, pf, vol, nsh, sum, sums, mx, pw, pwb,
+                            stream);
+    if (rc) return rc;
+    CUDA_TRY(keep_status(), "status copy");
+  }
   NCCL_TRY(n.GroupStart(), "ncclGroupStart");
   NCCL_TRY(n.AllReduce(part, part, (size_t)(6 * M), ncclUint64, ncclSum, cm.c, st), "allreduce partial sums");
   NCCL_TRY(n.AllReduce(mx, mx, (size_t)M, ncclUint32, ncclMax, cm.c, st), "allreduce max LT^2");

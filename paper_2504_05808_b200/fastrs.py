@@ -91,6 +91,10 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
                                                sz, vp]
             lib.fastrs_metrics_from_partials.argtypes = [vp, vp, vp, vp, vp, i64, ci, i64, u32, vp, vp, vp, vp,
                                                          sz, vp]
+            lib.fastrs_slab_prune.argtypes = [vp, vp, i64, i64, u32, vp, sz, vp]
+            lib.fastrs_slab_pack_tiles.argtypes = [vp, vp, i64, i64, vp, vp, vp, vp]
+            lib.fastrs_slab_unpack_tiles.argtypes = [vp, vp, i64, i64, vp, vp, vp]
+            lib.fastrs_slab_dilate.argtypes = [vp, vp, vp, i64, i64, i64, u32, i32, u32, vp, vp, vp, vp, vp, vp, sz, vp]
             lib.fastrs_nccl_available.argtypes = []
             lib.fastrs_nccl_unique_id.argtypes = [vp]
             lib.fastrs_comm_init.argtypes = [vp, ci, ci, ctypes.POINTER(vp)]
@@ -112,7 +116,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
                       "sphericity_roundness_host", "read_diagnostics", "profile_read", "slab_workspace_bytes",
                       "slab_edt_xy", "slab_edt_z", "slab_reduce", "metrics_from_partials", "touches_edge",
                       "filter_objects", "nccl_available", "nccl_unique_id", "comm_init", "comm_destroy",
-                      "slab_partition", "slab_halo_plan", "slab_call_workspace_bytes",
+                      "slab_partition", "slab_halo_plan", "slab_call_workspace_bytes", "slab_prune",
+                      "slab_pack_tiles", "slab_unpack_tiles", "slab_dilate",
                       "sphericity_roundness_slab", "ccl_workspace_bytes", "label_components",
                       "wl_workspace_bytes", "sphericity_wl", "mc_workspace_bytes", "mc_measure"):
                 getattr(lib, "fastrs_" + n).restype = ci
@@ -302,6 +307,14 @@ def slab_workspace(dims_ext, device) -> torch.Tensor:
     return workspace(out.value, device)
 
 
+def workspace_for_slab(dims_ext, device) -> torch.Tensor:
+    """A fresh (uncached) slab-phase workspace: the kept-centre halo phases keep tile data in it
+    between calls, one per (virtual) rank."""
+    out = ctypes.c_size_t(0)
+    _check(load().fastrs_slab_workspace_bytes(_dims3(dims_ext), ctypes.byref(out)))
+    return torch.empty(out.value, dtype=torch.uint8, device=device)
+
+
 def _ptr_or_none(t):
     return None if t is None else t.data_ptr()
 
@@ -349,6 +362,52 @@ def slab_reduce(labels: torch.Tensor, d_ext: torch.Tensor, own_lo: int, own_hi: 
                                      int(dmax_global), int(max_label), flags,
                                      *[part[k].data_ptr() for k in PARTIAL_KEYS], ws.data_ptr(), ws.numel(),
                                      _stream(dev)))
+    return part
+
+
+def _new_partials(max_label: int, dev) -> dict:
+    part = {k: torch.empty(max_label * (2 if k.startswith("sum") else 1), dtype=torch.int64, device=dev)
+            for k in PARTIAL_KEYS[:4]}
+    part["max_lt2"] = torch.empty(max_label, dtype=torch.int32, device=dev)
+    return part
+
+
+def slab_prune(d_ext: torch.Tensor, own_lo: int, own_hi: int, ws: torch.Tensor, flags=BORDER_BACKGROUND):
+    """Phase C1 (kept-centre halo): K4 on the own tile layers of the extended slab into `ws`."""
+    d_ext = d_ext.contiguous()
+    _check(load().fastrs_slab_prune(d_ext.data_ptr(), _dims3(d_ext.shape), own_lo, own_hi, flags, ws.data_ptr(),
+                                    ws.numel(), _stream(d_ext.device)))
+
+
+def slab_pack_tiles(ws: torch.Tensor, dims_ext, tz_a: int, tz_b: int):
+    """K4 outputs of tile layers [tz_a, tz_b) of `ws`: (records int32 [tiles*12], centres int64 [n])."""
+    dev = ws.device
+    Y, X = int(dims_ext[1]), int(dims_ext[2])
+    tiles = (tz_b - tz_a) * ((Y + 7) // 8) * ((X + 31) // 32)
+    rec = torch.empty(tiles * 12, dtype=torch.int32, device=dev)
+    ent = torch.empty(tiles * 2048, dtype=torch.int64, device=dev)
+    n = torch.zeros(1, dtype=torch.int64, device=dev)
+    _check(load().fastrs_slab_pack_tiles(ws.data_ptr(), _dims3(dims_ext), tz_a, tz_b, rec.data_ptr(), ent.data_ptr(),
+                                         n.data_ptr(), _stream(dev)))
+    return rec, ent[:int(n.item())].clone()
+
+
+def slab_unpack_tiles(ws: torch.Tensor, dims_ext, tz_a: int, tz_b: int, rec: torch.Tensor, ent: torch.Tensor):
+    ent = ent if ent.numel() else torch.zeros(1, dtype=torch.int64, device=ws.device)
+    _check(load().fastrs_slab_unpack_tiles(ws.data_ptr(), _dims3(dims_ext), tz_a, tz_b, rec.data_ptr(),
+                                           ent.data_ptr(), _stream(ws.device)))
+
+
+def slab_dilate(labels: torch.Tensor, d_ext: torch.Tensor, own_lo: int, own_hi: int, Z: int, dmax_global: int,
+                max_label: int, ws: torch.Tensor, flags=BORDER_BACKGROUND) -> dict:
+    """Phase C2 (kept-centre halo): K5 on the own tiles from the tile data in `ws` -> partials."""
+    labels = _labels_arg(labels)
+    d_ext = d_ext.contiguous()
+    part = _new_partials(int(max_label), labels.device)
+    _check(load().fastrs_slab_dilate(labels.data_ptr(), d_ext.data_ptr(), _dims3(d_ext.shape), own_lo, own_hi, Z,
+                                     int(dmax_global), int(max_label), flags,
+                                     *[part[k].data_ptr() for k in PARTIAL_KEYS], ws.data_ptr(), ws.numel(),
+                                     _stream(labels.device)))
     return part
 
 
@@ -430,6 +489,7 @@ def release():
 # ------------------------------------------------------------------------------------------
 
 SLAB_TRANSPOSE = 128
+SLAB_DENSE_HALO = 512
 
 
 def nccl_available() -> bool:

@@ -199,7 +199,7 @@ def make_comm(group=None):
 
 
 def simulate_slabs(labels: torch.Tensor, nranks: int, max_label: int, flags: int = 1, stats: bool = False,
-                   phases=None, transpose: bool = False) -> dict:
+                   phases=None, transpose: bool = False, lt_halo: str = "dense") -> dict:
     """Single-process emulation of the slab path: the nranks slabs are processed one after
     another on one device and the exchanges become slicing of the assembled volume.  The
     same phases and halo widths as sphericity_roundness_slab; used by the GPU parity tests
@@ -236,10 +236,39 @@ def simulate_slabs(labels: torch.Tensor, nranks: int, max_label: int, flags: int
     H = halo_lt(dmax)
     dfull = torch.cat(dfull)
     tot = None
-    for z0, z1 in slabs:
-        a, b = max(0, z0 - H), min(Z, z1 + H)
-        part = phases.reduce(labels[z0:z1].contiguous(), dfull[a:b].contiguous(), z0 - a, z1 - a, Z, dmax, max_label,
-                             flags)
+    parts = []
+    if lt_halo == "centres":
+        # N4 (the in-library driver's default): each rank runs K4 on its own tile layers only
+        # (D known 3 slices beyond its slab; the rest of its window is poisoned, so a read there
+        # would show), then receives the K4 outputs of the layers within H slices from their owners
+        from . import fastrs as F
+        wins, wss = [], []
+        for z0, z1 in slabs:
+            a, b = max(0, z0 - H), min(Z, z1 + H)
+            d = torch.full((b - a, Y, X), 0x3FFFFFFF, dtype=torch.int32, device=labels.device)
+            lo, hi = max(a, z0 - 3), min(b, z1 + 3)
+            d[lo - a:hi - a] = dfull[lo:hi]
+            ws = F.workspace_for_slab((b - a, Y, X), labels.device)
+            F.slab_prune(d, z0 - a, z1 - a, ws, flags)
+            wins.append((a, b, d))
+            wss.append(ws)
+        recv_bytes = [0] * nranks
+        for src, dst, side, a, b in halo_plan(slabs, H, Z):
+            sa, da = wins[src][0], wins[dst][0]
+            rec, ent = F.slab_pack_tiles(wss[src], wins[src][2].shape, (a - sa) // 8, (b - sa + 7) // 8)
+            F.slab_unpack_tiles(wss[dst], wins[dst][2].shape, (a - da) // 8, (b - da + 7) // 8, rec, ent)
+            recv_bytes[dst] += rec.numel() * 4 + ent.numel() * 8
+        for src, dst, side, a, b in halo_plan(slabs, 3, Z):
+            recv_bytes[dst] += (b - a) * Y * X * 4  # the 3-slice D halo of K4
+        for r, (z0, z1) in enumerate(slabs):
+            a, _, d = wins[r]
+            parts.append(F.slab_dilate(labels[z0:z1].contiguous(), d, z0 - a, z1 - a, Z, dmax, max_label, wss[r], flags))
+    else:
+        for z0, z1 in slabs:
+            a, b = max(0, z0 - H), min(Z, z1 + H)
+            parts.append(phases.reduce(labels[z0:z1].contiguous(), dfull[a:b].contiguous(), z0 - a, z1 - a, Z, dmax,
+                                       max_label, flags))
+    for part in parts:
         if tot is None:
             tot = {k: v.clone() for k, v in part.items()}
         else:
@@ -247,5 +276,14 @@ def simulate_slabs(labels: torch.Tensor, nranks: int, max_label: int, flags: int
                 tot[k] += part[k]
             tot["max_lt2"] = torch.maximum(tot["max_lt2"], part["max_lt2"])
     res = phases.metrics(tot, Z * Y * X, dmax, stats)
-    res["slab_info"] = dict(h=0 if transpose else h, H=H, dmax=dmax, slabs=slabs, transpose=transpose)
+    res["slab_info"] = dict(h=0 if transpose else h, H=H, dmax=dmax, slabs=slabs, transpose=transpose, lt_halo=lt_halo)
+    # bytes each rank receives per exchange (what the NCCL driver moves for the same plan)
+    yx4 = Y * X * 4
+    zpass = [Z * (Y * (r + 1) // nranks - Y * r // nranks) * X * 4 - (z1 - z0) * (Y * (r + 1) // nranks - Y * r // nranks) * X * 4
+             for r, (z0, z1) in enumerate(slabs)] if transpose else \
+        [sum(b - a for s_, d_, _, a, b in halo_plan(slabs, h, Z) if d_ == r) * yx4 for r in range(nranks)]
+    lt = recv_bytes if lt_halo == "centres" else \
+        [sum(b - a for s_, d_, _, a, b in halo_plan(slabs, H, Z) if d_ == r) * yx4 for r in range(nranks)]
+    res["slab_info"]["recv_bytes_zpass"] = zpass
+    res["slab_info"]["recv_bytes_lt"] = lt
     return res

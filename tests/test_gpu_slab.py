@@ -18,11 +18,11 @@ pytestmark = pytest.mark.gpu
 KEYS = ("sphericity", "roundness", "volume", "n_shell", "max_lt2", "mean_lt", "shell_mean_lt", "axis_cb")
 
 
-def _check(lab, nranks, flags=1, transpose=False):
+def _check(lab, nranks, flags=1, transpose=False, lt_halo="dense"):
     t = torch.from_numpy(np.ascontiguousarray(lab, np.int32)).cuda()
     ml = int(lab.max())
     want = fastrs.sphericity_roundness(t, max_label=ml, flags=flags, stats=True)
-    got = slab.simulate_slabs(t, nranks, ml, flags=flags, stats=True, transpose=transpose)
+    got = slab.simulate_slabs(t, nranks, ml, flags=flags, stats=True, transpose=transpose, lt_halo=lt_halo)
     for k in KEYS:
         a, b = got[k].cpu().numpy(), want[k].cpu().numpy()
         np.testing.assert_array_equal(a, b, err_msg=f"{k} (nranks={nranks}, flags={flags})")
@@ -113,6 +113,29 @@ def test_transpose_z_pass_bit_identical(nranks):
     _check(np.pad(lab, 1), 3, 0, transpose=True)
 
 
+# ---- N4: the kept-centre halo (K4 outputs of the halo tile layers instead of D) -------------
+
+@pytest.mark.parametrize("nranks", [2, 3, 8])
+def test_kept_centre_halo_bit_identical(nranks):
+    """Each virtual rank runs K4 on its own tile layers (D beyond 3 slices of its slab poisoned)
+    and receives the packed K4 outputs of the layers within H slices; K5 from that: bit-identical
+    to the single call (fastrs_slab_prune / _pack_tiles / _unpack_tiles / _dilate)."""
+    lab, _ = synth.make_config(2)
+    _check(lab, nranks, lt_halo="centres")
+    lab = synth.random_labels((70, 45, 50), nlabels=6, seed=11, fill=0.85, blob=5)
+    _check(np.pad(lab, 1), 3, 0, lt_halo="centres")
+
+
+def test_kept_centre_halo_multi_hop_and_c3():
+    lab = np.zeros((96, 70, 70), np.int32)
+    lab[15:76, 4:65, 4:65] = synth.sphere(30, canvas=61)
+    lab[80:90, 10:60, 20:30] = 2
+    info = _check(lab, 6, lt_halo="centres")  # H = 32 > the 16-slice slabs: several sources per side
+    assert info["H"] > 16
+    lab, _ = synth.make_config(3)
+    _check(lab, 4, lt_halo="centres", transpose=True)
+
+
 # ---- the in-library NCCL driver (fastrs_sphericity_roundness_slab) ----------------------
 
 @pytest.fixture(scope="module")
@@ -126,7 +149,8 @@ def comm1():
     c.close()
 
 
-@pytest.mark.parametrize("flags", [fastrs.BORDER_BACKGROUND, fastrs.BORDER_BACKGROUND | fastrs.SLAB_TRANSPOSE])
+@pytest.mark.parametrize("flags", [fastrs.BORDER_BACKGROUND, fastrs.BORDER_BACKGROUND | fastrs.SLAB_TRANSPOSE,
+                                   fastrs.BORDER_BACKGROUND | fastrs.SLAB_DENSE_HALO])
 @pytest.mark.parametrize("cfg", [2, 3])
 def test_nccl_slab_call_bit_identical(comm1, cfg, flags):
     """fastrs_sphericity_roundness_slab on one rank (N8 halo or N1 transpose, NCCL allreduces,
