@@ -773,6 +773,14 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
     __syncwarp();
   };
   int nq = 0;  // point mode: queued balls in sball (warp-uniform)
+  // the uncovered-cell list in registers during point tests: entries lane and lane + 32 packed
+  // in u01 (16 bits each), entry lane + 64 in u2 (nu <= kPoint = 96): the flush loop fetches
+  // cell q by one shuffle instead of a shared load and its address arithmetic
+  uint32_t u01 = 0, u2 = 0;
+  auto ureload = [&]() {
+    u01 = (lane < nu ? (uint32_t)ulist[lane] : 0u) | ((lane + 32 < nu ? (uint32_t)ulist[lane + 32] : 0u) << 16);
+    u2 = lane + 64 < nu ? (uint32_t)ulist[lane + 64] : 0u;
+  };
   auto point_flush = [&]() {
     int cx = 0, cy = 0, cz = 0, D = 0;
     if (lane < nq) {
@@ -784,40 +792,43 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
     }
     nq = 0;
     bool hit = false;
-    for (int q = 0; q < nu; ++q) {
-      const uint32_t e = ulist[q];
-      const int x = (int)(e & 31u), row = (int)(e >> 5);
-      const int ly = IS3D ? (row & 7) : row, lz = IS3D ? (row >> 3) : 0;
-      const int dx = x - cx, dy = ly - cy, dz = lz - cz;
-      const uint32_t bm = __ballot_sync(kFull, dx * dx + dy * dy + dz * dz < D);
-      if (bm) {
-        const int wD = __shfl_sync(kFull, D, __ffs(bm) - 1);
-        if (lane == 0) {
-          if (!FUSED) val[e] = (uint16_t)wD;
-          ulist[q] = (uint16_t)(e | 0x8000u);
+    uint32_t cov = 0;  // bit k: my entry lane + 32k got covered
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int qn = min(32, nu - 32 * k);  // (warp-uniform)
+      const uint32_t src = k == 2 ? u2 : u01;
+      for (int qq = 0; qq < qn; ++qq) {
+        const uint32_t e = (__shfl_sync(kFull, src, qq) >> (k == 1 ? 16 : 0)) & 0xFFFFu;
+        const int x = (int)(e & 31u), row = (int)(e >> 5);
+        const int ly = IS3D ? (row & 7) : row, lz = IS3D ? (row >> 3) : 0;
+        const int dx = x - cx, dy = ly - cy, dz = lz - cz;
+        const uint32_t bm = __ballot_sync(kFull, dx * dx + dy * dy + dz * dz < D);
+        if (bm) {
+          const int wD = __shfl_sync(kFull, D, __ffs(bm) - 1);
+          if (lane == qq) cov |= 1u << k;
+          if (!FUSED && lane == 0) val[e] = (uint16_t)wD;
+          if (FUSED) {
+            const uint32_t srow = __shfl_sync(kFull, row >= 32 ? s1 : s0, row & 31);
+            ev_push(e, 1u, (uint32_t)wD, (srow >> x) & 1u);
+          }
+          hit = true;
         }
-        if (FUSED) {
-          const uint32_t srow = __shfl_sync(kFull, row >= 32 ? s1 : s0, row & 31);
-          ev_push(e, 1u, (uint32_t)wD, (srow >> x) & 1u);
-        }
-        hit = true;
       }
     }
-    if (hit) {  // drop the covered cells from the list
+    if (hit) {  // drop the covered cells from the list (the order of the list does not matter)
       __syncwarp();
       uint32_t newn = 0;
-      for (int q0 = 0; q0 < nu; q0 += 32) {
-        const int q = q0 + lane;
-        const uint32_t e = q < nu ? ulist[q] : 0x8000u;
-        const bool keep = !(e & 0x8000u);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const uint32_t e = (k == 2 ? u2 : (u01 >> (k == 1 ? 16 : 0))) & 0xFFFFu;
+        const bool keep = lane + 32 * k < nu && !((cov >> k) & 1u);
         const uint32_t km = __ballot_sync(kFull, keep);
-        __syncwarp();
         if (keep) ulist[newn + __popc(km & ((1u << lane) - 1u))] = (uint16_t)e;
         newn += __popc(km);
-        __syncwarp();
       }
       nu = (int)newn;
       __syncwarp();
+      ureload();
       ubox_refresh();
     }
     __syncwarp();
@@ -842,6 +853,7 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
         // switch to point mode: list the still-uncovered cells
         make_ulist();
         pmode = true;
+        ureload();
         ubox_refresh();
       }
       if (pmode) {
