@@ -88,6 +88,8 @@ Nccl& nccl() {
 struct Comm {
   ncclComm_t c = nullptr;
   int rank = 0, nranks = 1, device = 0;
+  cudaStream_t xs = nullptr;              // exchange stream (the z-halo overlaps the interior z pass)
+  cudaEvent_t ev_a = nullptr, ev_x = nullptr;
 };
 
 int err(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
@@ -248,7 +250,7 @@ int call_layout(const std::vector<int64_t>& bd, int rank, int64_t Y, int64_t X, 
   L.stat = take(16 * 4);
   L.flags = take(4 * 4);
   L.dxy = take(4);
-  L.dmax = take(4);
+  L.dmax = take(3 * 4);  // one max D per z-pass launch (interior / two boundary ranges)
   L.below = take((size_t)YX * 4);
   L.ext = take((size_t)(nz + 2 * cap) * YX * 4);   // packed words (N8 halo) / own packed slab
   L.dext = take((size_t)(nz + 2 * cap) * YX * 4);  // D with its H halo
@@ -314,6 +316,13 @@ int fastrs_comm_init(const void* id, int nranks, int rank, void** comm_out) {
     delete cm;
     return nccl_fail(r, "ncclCommInitRank");
   }
+  if (cudaStreamCreateWithFlags(&cm->xs, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&cm->ev_a, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&cm->ev_x, cudaEventDisableTiming) != cudaSuccess) {
+    n.CommDestroy(cm->c);
+    delete cm;
+    return err(FASTRS_ECUDA, "exchange stream / events");
+  }
   *comm_out = cm;
   return FASTRS_OK;
 }
@@ -323,6 +332,9 @@ int fastrs_comm_destroy(void* comm) {
   Comm* cm = (Comm*)comm;
   ncclResult_t r = ncclSuccess;
   if (cm->c) r = nccl().CommDestroy(cm->c);
+  if (cm->ev_a) cudaEventDestroy(cm->ev_a);
+  if (cm->ev_x) cudaEventDestroy(cm->ev_x);
+  if (cm->xs) cudaStreamDestroy(cm->xs);
   delete cm;
   return r == ncclSuccess ? FASTRS_OK : nccl_fail(r, "ncclCommDestroy");
 }
@@ -430,15 +442,36 @@ int fastrs_sphericity_roundness_slab(const int32_t* labels, const int64_t* dims_
                "FASTRS_SLAB_TRANSPOSE)", (long long)h, (long long)halo_cap);
   uint32_t* d_own = dext + halo_cap * YX;
   if (!use_t) {
-    // B (N8): h packed slices per side, K3 on the h-extended slab
-    rc = exchange(cm, halo_plan(bd, h, Z), bd, ext + halo_cap * YX, ext, halo_cap, YX, ncclUint32, st, &sent, &recvd);
-    if (rc) return rc;
+    // B (N8): h packed slices per side on the exchange stream while K3 runs on the interior slices
+    // (those >= h from both slab faces read no halo slice within their scan), then K3 on the two
+    // boundary ranges.  (Interior CTAs may stage halo rows that are still arriving: only rows
+    // within sqrt(D_xy) <= h of an element enter its minimum, and terms past that bound never
+    // lower it.)
     const int64_t hlo = z0 - h > 0 ? h : z0, hhi = z1 + h < Z ? h : Z - z1;
     const int64_t de[3] = {hlo + nz + hhi, Y, X};
-    rc = fastrs_slab_edt_z(ext + (halo_cap - hlo) * YX, de, hlo, hlo + nz, z0 - hlo, Z, pf, d_own, dmx, pw, pwb,
-                           stream);
+    const uint32_t* pe = ext + (halo_cap - hlo) * YX;
+    CUDA_TRY(cudaEventRecord(cm.ev_a, st), "event");
+    CUDA_TRY(cudaStreamWaitEvent(cm.xs, cm.ev_a, 0), "event wait");
+    rc = exchange(cm, halo_plan(bd, h, Z), bd, ext + halo_cap * YX, ext, halo_cap, YX, ncclUint32, cm.xs, &sent, &recvd);
     if (rc) return rc;
-    CUDA_TRY(keep_status(), "status copy");
+    CUDA_TRY(cudaEventRecord(cm.ev_x, cm.xs), "event");
+    const int64_t i0 = hlo + (z0 > 0 ? h : 0), i1 = hlo + nz - (z1 < Z ? h : 0);  // interior (own-local + hlo)
+    int nk = 0;
+    if (i1 > i0) {
+      rc = fastrs_slab_edt_z(pe, de, i0, i1, z0 - hlo, Z, pf, d_own + (i0 - hlo) * YX, dmx + nk++, pw, pwb, stream);
+      if (rc) return rc;
+      CUDA_TRY(keep_status(), "status copy");
+    }
+    CUDA_TRY(cudaStreamWaitEvent(st, cm.ev_x, 0), "event wait");
+    const int64_t rng[2][2] = {{hlo, i1 > i0 ? i0 : hlo + nz}, {i1 > i0 ? i1 : hlo + nz, hlo + nz}};
+    for (const auto& r : rng)
+      if (r[1] > r[0]) {
+        rc = fastrs_slab_edt_z(pe, de, r[0], r[1], z0 - hlo, Z, pf, d_own + (r[0] - hlo) * YX, dmx + nk++, pw, pwb,
+                               stream);
+        if (rc) return rc;
+        CUDA_TRY(keep_status(), "status copy");
+      }
+    for (; nk < 3; ++nk) CUDA_TRY(cudaMemsetAsync(dmx + nk, 0, 4, st), "memset");
   } else {
     // B (N1): z-slabs -> y-slabs, K3 over whole columns, back
     uint32_t* t0 = (uint32_t*)(w + L.t0);
@@ -479,6 +512,7 @@ int fastrs_sphericity_roundness_slab(const int32_t* labels, const int64_t* dims_
     } else {
       CUDA_TRY(cudaMemsetAsync(dmx, 0, 4, st), "memset");
     }
+    CUDA_TRY(cudaMemsetAsync(dmx + 1, 0, 8, st), "memset");
     NCCL_TRY(n.GroupStart(), "ncclGroupStart");
     for (int s = 0; s < P; ++s) {  // back: rank r gets [nz_r][ym][X] of D; from s a [nz][Y_s][X] block
       const int64_t ys = ylo(s + 1) - ylo(s);
@@ -505,10 +539,11 @@ int fastrs_sphericity_roundness_slab(const int32_t* labels, const int64_t* dims_
                                    cudaMemcpyDeviceToDevice, st), "unpack");
     }
   }
-  NCCL_TRY(n.AllReduce(dmx, dmx, 1, ncclUint32, ncclMax, cm.c, st), "allreduce max D");
-  uint32_t h_dmax = 0;
-  CUDA_TRY(cudaMemcpyAsync(&h_dmax, dmx, 4, cudaMemcpyDeviceToHost, st), "D2H");
+  NCCL_TRY(n.AllReduce(dmx, dmx, 3, ncclUint32, ncclMax, cm.c, st), "allreduce max D");
+  uint32_t hd[3] = {0, 0, 0};
+  CUDA_TRY(cudaMemcpyAsync(hd, dmx, 12, cudaMemcpyDeviceToHost, st), "D2H");
   CUDA_TRY(cudaStreamSynchronize(st), "sync");
+  const uint32_t h_dmax = hd[0] > hd[1] ? (hd[0] > hd[2] ? hd[0] : hd[2]) : (hd[1] > hd[2] ? hd[1] : hd[2]);
   const int64_t H = halo_lt(h_dmax);
   if (H > halo_cap)
     return err(FASTRS_ENOMEM, "dilation halo H = %lld slices exceeds halo_cap = %lld", (long long)H,

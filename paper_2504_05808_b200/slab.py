@@ -199,7 +199,7 @@ def make_comm(group=None):
 
 
 def simulate_slabs(labels: torch.Tensor, nranks: int, max_label: int, flags: int = 1, stats: bool = False,
-                   phases=None, transpose: bool = False, lt_halo: str = "dense") -> dict:
+                   phases=None, transpose: bool = False, lt_halo: str = "dense", split_zpass: bool = False) -> dict:
     """Single-process emulation of the slab path: the nranks slabs are processed one after
     another on one device and the exchanges become slicing of the assembled volume.  The
     same phases and halo widths as sphericity_roundness_slab; used by the GPU parity tests
@@ -230,6 +230,19 @@ def simulate_slabs(labels: torch.Tensor, nranks: int, max_label: int, flags: int
     else:
         for z0, z1 in slabs:
             a, b = max(0, z0 - h), min(Z, z1 + h)
+            if split_zpass:
+                # as the NCCL driver overlaps the halo exchange: the interior slices (>= h from a
+                # face with a neighbour) first, then the two boundary ranges, each its own call
+                i0, i1 = z0 + (h if z0 > 0 else 0), z1 - (h if z1 < Z else 0)
+                rngs = [(i0, i1), (z0, i0), (i1, z1)] if i1 > i0 else [(z0, z1)]
+                dd = torch.empty((z1 - z0,) + tuple(packed.shape[1:]), dtype=packed.dtype, device=packed.device)
+                for r0, r1 in rngs:
+                    if r1 > r0:
+                        d, m = phases.edt_z(packed[a:b].contiguous(), r0 - a, r1 - a, a, Z, flags)
+                        dd[r0 - z0:r1 - z0] = d
+                        dmax = max(dmax, int(m.reshape(-1)[0].item()))
+                dfull.append(dd)
+                continue
             d, m = phases.edt_z(packed[a:b].contiguous(), z0 - a, z1 - a, a, Z, flags)
             dfull.append(d)
             dmax = max(dmax, int(m.reshape(-1)[0].item()))

@@ -18,11 +18,12 @@ pytestmark = pytest.mark.gpu
 KEYS = ("sphericity", "roundness", "volume", "n_shell", "max_lt2", "mean_lt", "shell_mean_lt", "axis_cb")
 
 
-def _check(lab, nranks, flags=1, transpose=False, lt_halo="dense"):
+def _check(lab, nranks, flags=1, transpose=False, lt_halo="dense", split_zpass=False):
     t = torch.from_numpy(np.ascontiguousarray(lab, np.int32)).cuda()
     ml = int(lab.max())
     want = fastrs.sphericity_roundness(t, max_label=ml, flags=flags, stats=True)
-    got = slab.simulate_slabs(t, nranks, ml, flags=flags, stats=True, transpose=transpose, lt_halo=lt_halo)
+    got = slab.simulate_slabs(t, nranks, ml, flags=flags, stats=True, transpose=transpose, lt_halo=lt_halo,
+                              split_zpass=split_zpass)
     for k in KEYS:
         a, b = got[k].cpu().numpy(), want[k].cpu().numpy()
         np.testing.assert_array_equal(a, b, err_msg=f"{k} (nranks={nranks}, flags={flags})")
@@ -134,6 +135,16 @@ def test_kept_centre_halo_multi_hop_and_c3():
     assert info["H"] > 16
     lab, _ = synth.make_config(3)
     _check(lab, 4, lt_halo="centres", transpose=True)
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+def test_split_z_pass_bit_identical(nranks):
+    """The NCCL driver overlaps the z-halo exchange with the z pass of the interior slices and runs
+    the boundary ranges after it: the three sub-range calls give the one-call result."""
+    lab, _ = synth.make_config(2)
+    _check(lab, nranks, lt_halo="centres", split_zpass=True)
+    lab = synth.random_labels((70, 45, 50), nlabels=6, seed=11, fill=0.85, blob=5)
+    _check(np.pad(lab, 1), nranks, 0, split_zpass=True)
 
 
 # ---- the in-library NCCL driver (fastrs_sphericity_roundness_slab) ----------------------
