@@ -104,6 +104,7 @@ __global__ void k_fxtable(unsigned long long* fx) {
 
 struct DeviceTables {
   uint32_t* m3 = nullptr;
+  uint4* m3s1 = nullptr;
   uint32_t* m2 = nullptr;
   unsigned long long* fx = nullptr;
 };
@@ -134,24 +135,34 @@ struct PruneTile {
 };
 
 
+// Stage-2 stripes: warp w takes the survivor slots w*32 + 256*j + l (l < 32) of the CTA-wide
+// survivor list and compacts the ones it keeps in place into the same stripe (the k-th kept
+// entry lands at or before the slot it was read from, and no other warp touches the stripe), so
+// the bucket scatter needs no second pass over rows and no cross-warp prefix.
+// stage-2 class order (3D): (2,1,0), (2,1,1), (2,2,1), (3,1,1), (3,1,0), then the classes that
+// dropped no stage-1 survivor on C4: (2,0,0), (2,2,0), (3,0,0), (2,2,2)
+__host__ __device__ constexpr int stage2_order3(int q) {
+  return q == 0 ? 4 : q == 1 ? 5 : q == 2 ? 7 : q == 3 ? 10 : q == 4 ? 9 : q == 5 ? 3 : q == 6 ? 6 : q == 7 ? 8 : 11;
+}
+
+__device__ __forceinline__ int stripe_slot(int warp, int k) { return warp * 32 + ((k >> 5) << 8) + (k & 31); }
+
 template <bool IS3D, bool TMA>
 __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D, Geom g, TileMeta* __restrict__ meta,
                                                uint2* __restrict__ cent, uint32_t* __restrict__ fgm,
                                                uint32_t* __restrict__ shm, uint16_t* __restrict__ oct,
-                                               const uint32_t* __restrict__ M,
+                                               const uint32_t* __restrict__ M, const uint4* __restrict__ M1,
                                                int64_t tile0, WsHeader* __restrict__ hdr,
                                                const __grid_constant__ CUtensorMap tmap) {
   using P = PruneTile<IS3D>;
   __shared__ __align__(128) uint32_t s[P::PZ * P::PY * P::PX];
   __shared__ __align__(8) uint64_t s_bar;
-  __shared__ uint32_t keepmask[kRows];
-  __shared__ uint32_t pre[kRows];
   __shared__ uint32_t red_cnt[8], red_max[8];
   __shared__ uint16_t surv[kTileVol];
-  __shared__ uint32_t s_nsurv;
-  __shared__ unsigned long long s_rows;  // rows with kept centres (the compaction loops skip the others)
+  __shared__ uint32_t s_nsurv, s_nkept;
   __shared__ uint32_t bhist[128];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
   const int64_t tile = tile0 + blockIdx.x;
   // tile -> (tx, ty, tz, b) in 32-bit arithmetic (ntiles < 2^32, checked in make_geom)
   uint32_t t = (uint32_t)tile;
@@ -164,6 +175,8 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
   const int64_t b = t / ntz;
   const int64_t z0 = tz * P::TZ - P::HZ, y0 = ty * P::TY - P::H, x0 = tx * kTX - P::HX;
   const uint32_t* Db = D + b * g.Z * g.Y * g.X;
+  for (int k = tid; k < 128; k += 256) bhist[k] = 0;
+  if (tid == 0) s_nsurv = 0;
   // halo staging with cp.async (zero-fill outside the grid), one warp per (z, y) row of the
   // padded tile.  Rows are 40 words starting at a multiple of 4, so when X % 4 == 0 every
   // 16-byte chunk lies entirely inside or outside the grid: 10 chunk copies per row.
@@ -230,106 +243,95 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
   }
   __syncthreads();
 
+  // Both staging paths zero-fill outside the grid, so "foreground" is D != 0 (cells of the
+  // tile beyond the grid edge read 0), and neighbours outside the grid read 0 (never contain).
   constexpr int dcap = IS3D ? kDcap3 : kDcap2;
   uint32_t nfg = 0, maxd = 0;
-  const int64_t gx = tx * kTX + lane;
-  // stage 1 (26 / 8 neighbours), row-vectorised.  The containment thresholds of the warp's
-  // 8 rows are fetched first so the table loads overlap.
-  constexpr int kRowsPerWarp = kRows / 8;
-  uint32_t dr[kRowsPerWarp], m0r[kRowsPerWarp], m1r[kRowsPerWarp], m2r[kRowsPerWarp];
-  bool fgr[kRowsPerWarp];
-#pragma unroll
-  for (int k = 0; k < kRowsPerWarp; ++k) {
-    const int row = warp + 8 * k;
-    const int ly = row % P::TY, lz = row / P::TY;
-    const int64_t gz = tz * P::TZ + lz, gy = ty * P::TY + ly;
-    const int c = ((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::HX);
-    const uint32_t d = s[c];
-    fgr[k] = d != 0 && gz < g.Z && gy < g.Y && gx < g.X;
-    dr[k] = d;
+  // stage-1 survivors are appended to the CTA-wide list (one shared atomic per warp row; the
+  // list order does not matter: the output is sorted by D bucket, arbitrary inside a bucket)
+  auto emit_row = [&](int row, uint32_t d, bool keep) {
+    const bool fg = d != 0;
     // shell <=> D == 1 (a face neighbour or the flagged border is a site):
-    // the per-row shell mask for the fused reductions of K5
-    const uint32_t shb = __ballot_sync(kFullMask, fgr[k] && d == 1u);
-    if (lane == 0) shm[tile * kRows + row] = shb;
-    const bool test = fgr[k] && d <= (uint32_t)dcap;
-    m0r[k] = test ? __ldg(M + d) : 0xFFFFFFFFu;
-    m1r[k] = test ? __ldg(M + (dcap + 1) + d) : 0xFFFFFFFFu;
-    m2r[k] = (IS3D && test) ? __ldg(M + 2 * (dcap + 1) + d) : 0xFFFFFFFFu;
-  }
-#pragma unroll
-  for (int k = 0; k < kRowsPerWarp; ++k) {
-    const int row = warp + 8 * k;
-    const int ly = row % P::TY, lz = row / P::TY;
-    const int c = ((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::HX);
-    const bool fg = fgr[k];
-    bool keep = fg;
-    if (__any_sync(kFullMask, fg)) {
-      const uint32_t m0 = m0r[k], m1 = m1r[k], m2 = m2r[k];
-      if (IS3D) {
-        // per offset class, the max over its neighbours against one threshold (3-input max:
-        // VIMNMX3), instead of 26 separate compares
-        uint32_t mx[3] = {0u, 0u, 0u};
-#pragma unroll
-        for (int dz = -1; dz <= 1; ++dz)
-#pragma unroll
-          for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-            for (int dx = -1; dx <= 1; ++dx) {
-              const int cls = (dz != 0) + (dy != 0) + (dx != 0) - 1;
-              if (cls < 0) continue;
-              mx[cls] = max(mx[cls], s[c + (dz * P::PY + dy) * P::PX + dx]);
-            }
-        keep &= mx[0] <= m0 && mx[1] <= m1 && mx[2] <= m2;
-      } else {
-#pragma unroll
-        for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-          for (int dx = -1; dx <= 1; ++dx) {
-            const int cls = (dy != 0) + (dx != 0) - 1;
-            if (cls < 0) continue;
-            keep &= s[c + dy * P::PX + dx] <= (cls == 0 ? m0 : m1);
-          }
-      }
-    }
-    const uint32_t bal = __ballot_sync(kFullMask, keep);
+    // the per-row shell mask for the fused reductions of K5; the foreground mask for its coverage
+    const uint32_t shb = __ballot_sync(kFullMask, d == 1u);
     const uint32_t fgb = __ballot_sync(kFullMask, fg);
+    const uint32_t kb = __ballot_sync(kFullMask, keep);
+    uint32_t base = 0;
     if (lane == 0) {
-      keepmask[row] = bal;
-      fgm[tile * kRows + row] = fgb;  // foreground mask per row, for the dilation's coverage
+      shm[tile * kRows + row] = shb;
+      fgm[tile * kRows + row] = fgb;
+      if (kb) base = atomicAdd(&s_nsurv, (uint32_t)__popc(kb));
     }
+    base = __shfl_sync(kFullMask, base, 0);
+    if (keep) surv[base + __popc(kb & lt_mask)] = (uint16_t)(row * 32 + lane);
     nfg += fg;
-  }
-  __syncthreads();
-  // ---- stage 2: the remaining offsets (|s|^2 <= 12 / 8) on the compacted stage-1 survivors,
-  // lanes = survivors (warp-uniform offset loop, early exit per class)
-  if (warp == 0) {
-    const uint32_t c0 = __popc(keepmask[2 * lane]), c1 = __popc(keepmask[2 * lane + 1]);
-    uint32_t inc = c0 + c1;
+  };
+  if constexpr (IS3D) {
+    // ---- stage 1 (the 26-neighbourhood), warp = one y row of the tile, lane = x, a sliding
+    // window over z.  The per-class maxima are separable: per layer z', over the 3x3 (x, y)
+    // neighbourhood, a0 = centre, a1 = max of the 4 edge-adjacent, a2 = max of the 4 corners;
+    // then over z: class (1,0,0) = max(a1(z), a0(z-1), a0(z+1)), class (1,1,0) = max(a2(z),
+    // a1(z-1), a1(z+1)), class (1,1,1) = max(a2(z-1), a2(z+1)): 9 shared loads per layer, each
+    // layer serving three rows, instead of 26 per row.
+    constexpr int SZ = P::PY * P::PX;
+    const int cb = (P::HZ * P::PY + (warp + P::H)) * P::PX + (lane + P::HX);  // (x=lane, y=warp, z=0)
+    auto layer = [&](int lz, uint32_t& a0, uint32_t& a1, uint32_t& a2) {
+      const uint32_t* q = s + cb + lz * SZ;
+      a0 = q[0];
+      a1 = max(max(q[-1], q[1]), max(q[-P::PX], q[P::PX]));
+      a2 = max(max(q[-P::PX - 1], q[-P::PX + 1]), max(q[P::PX - 1], q[P::PX + 1]));
+    };
+    uint32_t p0, p1, p2, q0, q1, q2;
+    layer(-1, p0, p1, p2);
+    layer(0, q0, q1, q2);
+    uint4 mq = (q0 != 0u && q0 <= (uint32_t)dcap) ? __ldg(M1 + q0) : make_uint4(~0u, ~0u, ~0u, ~0u);
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t n = __shfl_up_sync(kFullMask, inc, o);
-      if (lane >= o) inc += n;
+    for (int lz = 0; lz < P::TZ; ++lz) {
+      uint32_t n0, n1, n2;
+      layer(lz + 1, n0, n1, n2);
+      // the next row's thresholds, one row ahead (their latency overlaps this row)
+      const uint4 mn = (lz + 1 < P::TZ && n0 != 0u && n0 <= (uint32_t)dcap) ? __ldg(M1 + n0)
+                                                                            : make_uint4(~0u, ~0u, ~0u, ~0u);
+      const uint32_t c0 = max(q1, max(p0, n0)), c1 = max(q2, max(p1, n1)), c2 = max(p2, n2);
+      const bool keep = q0 != 0u && c0 <= mq.x && c1 <= mq.y && c2 <= mq.z;
+      emit_row(warp + 8 * lz, q0, keep);
+      p0 = q0, p1 = q1, p2 = q2;
+      q0 = n0, q1 = n1, q2 = n2;
+      mq = mn;
     }
-    const uint32_t ex = inc - c0 - c1;
-    pre[2 * lane] = ex;
-    pre[2 * lane + 1] = ex + c0;
-    if (lane == 31) s_nsurv = inc;
-    const uint32_t lo = __ballot_sync(kFullMask, keepmask[lane] != 0u), hi = __ballot_sync(kFullMask, keepmask[lane + 32] != 0u);
-    if (lane == 0) s_rows = (unsigned long long)lo | ((unsigned long long)hi << 32);
+  } else {
+    // ---- stage 1 (2D: the 8-neighbourhood), row-vectorised; thresholds fetched first
+    constexpr int kRowsPerWarp = kRows / 8;
+    uint32_t dr[kRowsPerWarp], m0r[kRowsPerWarp], m1r[kRowsPerWarp];
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      const int row = warp + 8 * k;
+      const int c = (row + P::H) * P::PX + (lane + P::HX);
+      const uint32_t d = s[c];
+      dr[k] = d;
+      const bool test = d != 0u && d <= (uint32_t)dcap;
+      m0r[k] = test ? __ldg(M + d) : 0xFFFFFFFFu;
+      m1r[k] = test ? __ldg(M + (dcap + 1) + d) : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      const int row = warp + 8 * k;
+      const int c = (row + P::H) * P::PX + (lane + P::HX);
+      const uint32_t d = dr[k];
+      const uint32_t e1 = max(max(s[c - 1], s[c + 1]), max(s[c - P::PX], s[c + P::PX]));
+      const uint32_t e2 = max(max(s[c - P::PX - 1], s[c - P::PX + 1]), max(s[c + P::PX - 1], s[c + P::PX + 1]));
+      emit_row(row, d, d != 0u && e1 <= m0r[k] && e2 <= m1r[k]);
+    }
   }
   __syncthreads();
-  const unsigned long long my_rows = 0x0101010101010101ull << warp;  // rows warp, warp + 8, ...
+  // ---- stage 2: the remaining offsets (|s|^2 <= 12 / 8) on the stage-1 survivors, lanes =
+  // survivors (warp-uniform offset loop, early exit per class); the kept ones are counted in
+  // the D-bucket histogram and compacted in place in the warp's stripe
+  const int nsurv = (int)s_nsurv;
+  int nk = 0;  // kept by this warp (warp-uniform)
 #pragma unroll 1
-  for (unsigned long long rm = s_rows & my_rows; rm; rm &= rm - 1) {
-    const int row = __ffsll((long long)rm) - 1;
-    const uint32_t km = keepmask[row];
-    if ((km >> lane) & 1u) surv[pre[row] + __popc(km & ((1u << lane) - 1u))] = (uint16_t)(row * 32 + lane);
-  }
-  __syncthreads();
-  const uint32_t nsurv = s_nsurv;
-#pragma unroll 1
-  for (uint32_t i0 = warp * 32; i0 < nsurv; i0 += 256) {
-    const uint32_t i = i0 + lane;
+  for (int j0 = 0; warp * 32 + j0 < nsurv; j0 += 256) {
+    const int i = warp * 32 + j0 + lane;
     // (lanes without a survivor test the first core element: every offset stays inside the block)
     int v = 0, c = (P::HZ * P::PY + P::H) * P::PX + P::HX;
     uint32_t d = 0;
@@ -342,54 +344,62 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
       keep = true;
     }
     const bool test = keep && d <= (uint32_t)dcap;
-    uint32_t mv[P::NC - P::C1];
+    uint32_t mv[IS3D ? 12 : P::NC - P::C1];
+    if constexpr (IS3D) {
+      // the 9 stage-2 thresholds of D interleaved in three 16-byte words
 #pragma unroll
-    for (int k = 0; k < P::NC - P::C1; ++k) mv[k] = test ? __ldg(M + (P::C1 + k) * (dcap + 1) + d) : 0xFFFFFFFFu;
-#pragma unroll
-    for (int k = 0; k < P::NC - P::C1; ++k) {
-      if (!__any_sync(kFullMask, test && keep)) break;
-      // all offsets of class C1+k (the class test folds at compile time after unrolling): their
-      // max against the class threshold
-      uint32_t mxk = 0;
-      if (IS3D) {
-#pragma unroll
-        for (int dz = -3; dz <= 3; ++dz)
-#pragma unroll
-          for (int dy = -3; dy <= 3; ++dy)
-#pragma unroll
-            for (int dx = -3; dx <= 3; ++dx)
-              if (class3(dz, dy, dx) == P::C1 + k) mxk = max(mxk, s[c + (dz * P::PY + dy) * P::PX + dx]);
-      } else {
-#pragma unroll
-        for (int dy = -2; dy <= 2; ++dy)
-#pragma unroll
-          for (int dx = -2; dx <= 2; ++dx)
-            if (class2(dy, dx) == P::C1 + k) mxk = max(mxk, s[c + dy * P::PX + dx]);
+      for (int j = 0; j < 3; ++j) {
+        const uint4 m4 = test ? __ldg(M1 + (kDcap3 + 1) + 3 * d + j) : make_uint4(~0u, ~0u, ~0u, ~0u);
+        mv[4 * j] = m4.x, mv[4 * j + 1] = m4.y, mv[4 * j + 2] = m4.z, mv[4 * j + 3] = m4.w;
       }
-      if (test) keep &= mxk <= mv[k];
+    } else {
+#pragma unroll
+      for (int q = 0; q < P::NC - P::C1; ++q) mv[q] = test ? __ldg(M + (P::C1 + q) * (dcap + 1) + d) : 0xFFFFFFFFu;
     }
-    if (i < nsurv && !keep) atomicAnd(&keepmask[v >> 5], ~(1u << (v & 31)));
-    if (keep) maxd = max(maxd, d);
+#pragma unroll
+    for (int q = 0; q < P::NC - P::C1; ++q) {
+      if (!__any_sync(kFullMask, test && keep)) break;
+      // all offsets of class `cls` (the class test folds at compile time after unrolling): their
+      // max against the class threshold.  Only lanes still alive load (the stage is bound by
+      // shared-memory wavefronts), and the classes go in the order that drops most centres
+      // first (tools/prune_stats.py on C4; the kept set does not depend on the order).
+      const int cls = IS3D ? stage2_order3(q) : P::C1 + q;
+      if (test && keep) {
+        uint32_t mxk = 0;
+        if (IS3D) {
+#pragma unroll
+          for (int dz = -3; dz <= 3; ++dz)
+#pragma unroll
+            for (int dy = -3; dy <= 3; ++dy)
+#pragma unroll
+              for (int dx = -3; dx <= 3; ++dx)
+                if (class3(dz, dy, dx) == cls) mxk = max(mxk, s[c + (dz * P::PY + dy) * P::PX + dx]);
+        } else {
+#pragma unroll
+          for (int dy = -2; dy <= 2; ++dy)
+#pragma unroll
+            for (int dx = -2; dx <= 2; ++dx)
+              if (class2(dy, dx) == cls) mxk = max(mxk, s[c + dy * P::PX + dx]);
+        }
+        keep = mxk <= mv[cls - P::C1];
+      }
+    }
+    const uint32_t kb = __ballot_sync(kFullMask, keep);
+    __syncwarp();  // every lane has read its slot before the compaction overwrites slots <= it
+    if (keep) {
+      surv[stripe_slot(warp, nk + __popc(kb & lt_mask))] = (uint16_t)v;
+      atomicAdd(&bhist[dbucket(d)], 1u);
+      maxd = max(maxd, d);
+    }
+    nk += __popc(kb);
   }
-  __syncthreads();
   // ---- compaction sorted by D bucket (descending; order inside a bucket is arbitrary): the
   // dilation's gather stops scanning a home tile once its remaining balls cannot reach the
-  // output tile.  All warps: bucket histogram -> warp-0 descending exclusive scan -> scatter.
-  for (int k = tid; k < 128; k += 256) bhist[k] = 0;
-  if (warp == 0) {  // the rows still holding kept centres after stage 2
-    const uint32_t lo = __ballot_sync(kFullMask, keepmask[lane] != 0u), hi = __ballot_sync(kFullMask, keepmask[lane + 32] != 0u);
-    if (lane == 0) s_rows = (unsigned long long)lo | ((unsigned long long)hi << 32);
-  }
-  __syncthreads();
-  for (unsigned long long rm = s_rows & my_rows; rm; rm &= rm - 1) {
-    const int row = __ffsll((long long)rm) - 1;
-    const uint32_t km = keepmask[row];
-    const int ly = row % P::TY, lz = row / P::TY;
-    const bool kept = (km >> lane) & 1u;
-    const int bk = kept ? dbucket(s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::HX)]) : -1;
-    const uint32_t grp = __match_any_sync(kFullMask, bk);
-    if (kept && lane == __ffs(grp) - 1) atomicAdd(&bhist[bk], (uint32_t)__popc(grp));
-  }
+  // output tile.  Histogram (stage 2) -> warp-0 descending exclusive scan -> scatter.
+  auto centre_d = [&](int v) {
+    const int lx = v & 31, ly = (v >> 5) % P::TY, lz = v / (32 * P::TY);
+    return s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lx + P::HX)];
+  };
   __syncthreads();
   if (warp == 0) {
     uint32_t h[4], sum = 0;
@@ -414,24 +424,16 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
       bhist[127 - 4 * lane - q] = run;  // now: next free slot of each bucket
       run += h[q];
     }
-    if (lane == 31) s_nsurv = inc;  // total kept
+    if (lane == 31) s_nkept = inc;  // total kept
   }
   __syncthreads();
   {
     uint2* out = cent + tile * kTileVol;
-    for (unsigned long long rm = s_rows & my_rows; rm; rm &= rm - 1) {
-      const int row = __ffsll((long long)rm) - 1;
-      const uint32_t km = keepmask[row];
-      const int ly = row % P::TY, lz = row / P::TY;
-      const bool kept = (km >> lane) & 1u;
-      const uint32_t d = kept ? s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lane + P::HX)] : 0u;
-      const int bk = kept ? dbucket(d) : -1;
-      const uint32_t grp = __match_any_sync(kFullMask, bk);
-      const int leader = __ffs(grp) - 1;
-      uint32_t base = 0;
-      if (kept && lane == leader) base = atomicAdd(&bhist[bk], (uint32_t)__popc(grp));
-      base = __shfl_sync(kFullMask, base, leader);
-      if (kept) out[base + __popc(grp & ((1u << lane) - 1u))] = make_uint2((uint32_t)(row * 32 + lane), d);
+#pragma unroll 1
+    for (int k = lane; k < nk; k += 32) {
+      const int v = surv[warp * 32 + ((k >> 5) << 8) + lane];
+      const uint32_t d = centre_d(v);
+      out[atomicAdd(&bhist[dbucket(d)], 1u)] = make_uint2((uint32_t)v, d);
     }
   }
   nfg = __reduce_add_sync(kFullMask, nfg);
@@ -447,10 +449,22 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
       f += red_cnt[w];
       m = max(m, red_max[w]);
     }
-    const uint32_t cnt = s_nsurv;
+    const uint32_t cnt = s_nkept;
     meta[tile] = TileMeta{cnt, m, f, 0};
     if (cnt) atomicAdd(&hdr->n_kept, (unsigned long long)cnt);
   }
+}
+
+// The 3D thresholds interleaved per D for K4: [0, kDcap3] the stage-1 classes (1,0,0), (1,1,0),
+// (1,1,1) (one 16-byte load per row); then three 16-byte words per D with the stage-2 classes
+// 3..11 (and 3 unused words)
+__global__ void k_mtable3_il(const uint32_t* __restrict__ M, uint4* __restrict__ M1) {
+  const int D = blockIdx.x * blockDim.x + threadIdx.x;
+  if (D > kDcap3) return;
+  M1[D] = make_uint4(M[D], M[(kDcap3 + 1) + D], M[2 * (kDcap3 + 1) + D], 0u);
+  auto m = [&](int c) { return c < kClasses3 ? M[c * (kDcap3 + 1) + D] : 0xFFFFFFFFu; };
+  uint4* o = M1 + (kDcap3 + 1) + 3 * D;
+  for (int j = 0; j < 3; ++j) o[j] = make_uint4(m(3 + 4 * j), m(4 + 4 * j), m(5 + 4 * j), m(6 + 4 * j));
 }
 
 }  // namespace
@@ -464,17 +478,22 @@ cudaError_t ensure_mtables(int dev) {
   DeviceTables& dt = g_tables[dev];
   if (dt.m3) return cudaSuccess;
   uint32_t *m3 = nullptr, *m2 = nullptr;
+  uint4* m3s1 = nullptr;
   unsigned long long* fx = nullptr;
   cudaError_t e = cudaMalloc(&m3, sizeof(uint32_t) * kClasses3 * (kDcap3 + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&m3s1, sizeof(uint4) * 4 * (kDcap3 + 1));
   if (e == cudaSuccess) e = cudaMalloc(&m2, sizeof(uint32_t) * kClasses2 * (kDcap2 + 1));
   if (e == cudaSuccess) e = cudaMalloc(&fx, sizeof(unsigned long long) * kFxLut);
   if (e != cudaSuccess) {
     cudaFree(m3);
+    cudaFree(m3s1);
     cudaFree(m2);
+    cudaFree(fx);
     return e;
   }
   const int64_t n3 = (int64_t)kClasses3 * (kDcap3 + 1), n2 = (int64_t)kClasses2 * (kDcap2 + 1);
   k_mtable3<<<(unsigned)((n3 + 127) / 128), 128>>>(m3);
+  k_mtable3_il<<<(unsigned)((kDcap3 + 1 + 127) / 128), 128>>>(m3, m3s1);
   k_mtable2<<<(unsigned)((n2 + 127) / 128), 128>>>(m2);
   k_fxtable<<<kFxLut / 256, 256>>>(fx);
   e = cudaDeviceSynchronize();
@@ -483,11 +502,13 @@ cudaError_t ensure_mtables(int dev) {
   if (e == cudaSuccess) e = dilate_atomic_setup();
   if (e != cudaSuccess) {
     cudaFree(m3);
+    cudaFree(m3s1);
     cudaFree(m2);
     cudaFree(fx);
     return e;
   }
   dt.m3 = m3;
+  dt.m3s1 = m3s1;
   dt.m2 = m2;
   dt.fx = fx;
   return cudaSuccess;
@@ -499,9 +520,11 @@ void release_mtables() {
   std::lock_guard<std::mutex> lk(g_mu);
   for (auto& dt : g_tables) {
     if (dt.m3) cudaFree(dt.m3);
+    if (dt.m3s1) cudaFree(dt.m3s1);
     if (dt.m2) cudaFree(dt.m2);
     if (dt.fx) cudaFree(dt.fx);
     dt.m3 = dt.m2 = nullptr;
+    dt.m3s1 = nullptr;
     dt.fx = nullptr;
   }
 }
@@ -563,14 +586,14 @@ void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centr
   const bool tma = prune_tensor_map(&tmap, D, g);
   if (g.ndim == 3) {
     if (tma)
-      k_prune<true, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m3, tile0, hdr, tmap);
+      k_prune<true, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m3, g_tables[dev].m3s1, tile0, hdr, tmap);
     else
-      k_prune<true, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m3, tile0, hdr, tmap);
+      k_prune<true, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m3, g_tables[dev].m3s1, tile0, hdr, tmap);
   } else {
     if (tma)
-      k_prune<false, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m2, tile0, hdr, tmap);
+      k_prune<false, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m2, nullptr, tile0, hdr, tmap);
     else
-      k_prune<false, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m2, tile0, hdr, tmap);
+      k_prune<false, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m2, nullptr, tile0, hdr, tmap);
   }
 }
 
