@@ -72,6 +72,7 @@ struct PaintSmem {  // K5b (one tile per warp)
   int4 sball[NW][32];             // survivors of a screened batch: centre (tile coords), D
   unsigned long long scand[NW][32];  // their candidate rows
   uint16_t ulist[NW][kPoint];     // point mode: the still-uncovered cells (row*32 + x)
+  uint2 pcell[NW][kPoint];        // the same cells for the dot-product test: (2x, 2y, 2z) bytes, -|p|^2
   uint32_t qa[NW][32];            // fused: covering events, (cell offset | count << 16)
   uint32_t qb[NW][32];            //        and (D | shell count << 16)
 };
@@ -738,6 +739,7 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
   unsigned long long* scand = S.scand[wl];   // their candidate rows
   bool pmode = false;
   uint16_t* ulist = S.ulist[wl];
+  uint2* pcell = S.pcell[wl];
   int ub[6] = {0, kTX - 1, 0, TY - 1, 0, TZ - 1};  // bounding box of the uncovered cells (point mode)
   auto ubox_refresh = [&]() {
     int x0 = 1 << 20, x1 = -1, y0 = 1 << 20, y1 = -1, z0 = 1 << 20, z1 = -1;
@@ -764,23 +766,23 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
 #pragma unroll
     for (int kk = 0; kk < 2; ++kk) {
       uint32_t m = left[kk];
+      const int row = lane + 32 * kk;
+      const int ly = IS3D ? (row & 7) : row, lz = IS3D ? (row >> 3) : 0;
       while (m) {
         const int c = __ffs(m) - 1;
         m &= m - 1;
-        ulist[pos++] = (uint16_t)((lane + 32 * kk) * 32 + c);
+        pcell[pos] = make_uint2((uint32_t)(2 * c) | ((uint32_t)(2 * ly) << 8) | ((uint32_t)(2 * lz) << 16),
+                                (uint32_t)(-(c * c + ly * ly + lz * lz)));
+        ulist[pos++] = (uint16_t)(row * 32 + c);
       }
     }
     __syncwarp();
   };
   int nq = 0;  // point mode: queued balls in sball (warp-uniform)
-  // the uncovered-cell list in registers during point tests: entries lane and lane + 32 packed
-  // in u01 (16 bits each), entry lane + 64 in u2 (nu <= kPoint = 96): the flush loop fetches
-  // cell q by one shuffle instead of a shared load and its address arithmetic
-  uint32_t u01 = 0, u2 = 0;
-  auto ureload = [&]() {
-    u01 = (lane < nu ? (uint32_t)ulist[lane] : 0u) | ((lane + 32 < nu ? (uint32_t)ulist[lane + 32] : 0u) << 16);
-    u2 = lane + 64 < nu ? (uint32_t)ulist[lane + 64] : 0u;
-  };
+  // Point tests, lanes = queued balls, loop over the uncovered cells p (broadcast reads):
+  // |p - c|^2 < D  <=>  2p.c - |p|^2 > |c|^2 - D, one byte dot product (IDP4A) per cell and ball
+  // when every queued centre lies within [-128, 127] of the tile (radius <= ~96); otherwise
+  // the distance is formed directly.
   auto point_flush = [&]() {
     int cx = 0, cy = 0, cz = 0, D = 0;
     if (lane < nq) {
@@ -791,44 +793,69 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
       D = bp.w;
     }
     nq = 0;
+    const bool in8 = (unsigned)(cx + 128) < 256u && (unsigned)(cy + 128) < 256u && (unsigned)(cz + 128) < 256u;
+    const bool wide = !__all_sync(kFull, in8);
+    const int T = D != 0 ? cx * cx + cy * cy + cz * cz - D : 0x7FFFFFFF;
+    const int C8 = (cx & 0xFF) | ((cy & 0xFF) << 8) | ((cz & 0xFF) << 16);
     bool hit = false;
-    uint32_t cov = 0;  // bit k: my entry lane + 32k got covered
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int qn = min(32, nu - 32 * k);  // (warp-uniform)
-      const uint32_t src = k == 2 ? u2 : u01;
-      for (int qq = 0; qq < qn; ++qq) {
-        const uint32_t e = (__shfl_sync(kFull, src, qq) >> (k == 1 ? 16 : 0)) & 0xFFFFu;
-        const int x = (int)(e & 31u), row = (int)(e >> 5);
-        const int ly = IS3D ? (row & 7) : row, lz = IS3D ? (row >> 3) : 0;
-        const int dx = x - cx, dy = ly - cy, dz = lz - cz;
+    uint32_t cov = 0;  // bit k: list entry lane + 32k got covered
+    // 32-bit shared address of the cell list (one register across the loop instead of a
+    // rematerialised 64-bit generic pointer)
+    uint32_t pc_sh;
+    asm volatile("mov.u32 %0, %1;" : "=r"(pc_sh) : "r"((uint32_t)__cvta_generic_to_shared(pcell)));
+    auto on_hit = [&](int q, uint32_t bm) {
+      const uint32_t e = ulist[q];
+      const int wD = __shfl_sync(kFull, D, __ffs(bm) - 1);
+      if (lane == (q & 31)) cov |= 1u << (q >> 5);
+      if (!FUSED && lane == 0) val[e] = (uint16_t)wD;
+      if (FUSED) {
+        const int row = (int)(e >> 5);
+        const uint32_t srow = __shfl_sync(kFull, row >= 32 ? s1 : s0, row & 31);
+        ev_push(e, 1u, (uint32_t)wD, (srow >> (e & 31u)) & 1u);
+      }
+      hit = true;
+    };
+    if (!wide) {
+      for (int q = 0; q < nu; ++q) {
+        uint2 pq;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(pq.x), "=r"(pq.y) : "r"(pc_sh + 8u * (uint32_t)q));
+        const uint32_t bm = __ballot_sync(kFull, __dp4a((int)pq.x, C8, (int)pq.y) > T);
+        if (bm) on_hit(q, bm);
+      }
+    } else {
+      for (int q = 0; q < nu; ++q) {
+        const uint2 pq = pcell[q];
+        const int dx = (int)(pq.x & 0xFFu) / 2 - cx, dy = (int)((pq.x >> 8) & 0xFFu) / 2 - cy,
+                  dz = (int)((pq.x >> 16) & 0xFFu) / 2 - cz;
         const uint32_t bm = __ballot_sync(kFull, dx * dx + dy * dy + dz * dz < D);
-        if (bm) {
-          const int wD = __shfl_sync(kFull, D, __ffs(bm) - 1);
-          if (lane == qq) cov |= 1u << k;
-          if (!FUSED && lane == 0) val[e] = (uint16_t)wD;
-          if (FUSED) {
-            const uint32_t srow = __shfl_sync(kFull, row >= 32 ? s1 : s0, row & 31);
-            ev_push(e, 1u, (uint32_t)wD, (srow >> x) & 1u);
-          }
-          hit = true;
-        }
+        if (bm) on_hit(q, bm);
       }
     }
-    if (hit) {  // drop the covered cells from the list (the order of the list does not matter)
+    if (hit) {  // drop the covered cells from the lists (the order of the list does not matter)
+      uint32_t ek[3];
+      uint2 pk[3];
+      bool keep[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int idx = lane + 32 * k;
+        keep[k] = idx < nu && !((cov >> k) & 1u);
+        ek[k] = keep[k] ? ulist[idx] : 0u;
+        pk[k] = keep[k] ? pcell[idx] : make_uint2(0u, 0u);
+      }
       __syncwarp();
       uint32_t newn = 0;
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const uint32_t e = (k == 2 ? u2 : (u01 >> (k == 1 ? 16 : 0))) & 0xFFFFu;
-        const bool keep = lane + 32 * k < nu && !((cov >> k) & 1u);
-        const uint32_t km = __ballot_sync(kFull, keep);
-        if (keep) ulist[newn + __popc(km & ((1u << lane) - 1u))] = (uint16_t)e;
+        const uint32_t km = __ballot_sync(kFull, keep[k]);
+        if (keep[k]) {
+          const uint32_t at = newn + __popc(km & ((1u << lane) - 1u));
+          ulist[at] = (uint16_t)ek[k];
+          pcell[at] = pk[k];
+        }
         newn += __popc(km);
       }
       nu = (int)newn;
       __syncwarp();
-      ureload();
       ubox_refresh();
     }
     __syncwarp();
@@ -853,7 +880,6 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
         // switch to point mode: list the still-uncovered cells
         make_ulist();
         pmode = true;
-        ureload();
         ubox_refresh();
       }
       if (pmode) {
@@ -889,14 +915,19 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
         cz = (int)((e >> 48) & 0xFFFFu) - kOff - moz;
         const int R2 = D - 1;
         const int ddx = gap(0, kTX - 1, cx), ddy = gap(0, TY - 1, cy), ddz = gap(0, TZ - 1, cz);
-        if (ddx * ddx + ddy * ddy + ddz * ddz <= R2) {
-          const int rho = isqrt16(R2);
-          const int xa = max(cx - rho, 0), xb = min(cx + rho, kTX - 1);
+        const int gx2 = ddx * ddx, gy2 = ddy * ddy, gz2 = ddz * ddz;
+        if (gx2 + gy2 + gz2 <= R2) {
+          // the extent of ball ∩ tile along each axis: the half-chord at the tile's nearest
+          // point in the other two axes (a ball reaching the tile from outside in y/z meets it
+          // in a cap much narrower than its radius)
+          const int hx = isqrt16(R2 - gy2 - gz2), hy = isqrt16(R2 - gx2 - gz2);
+          const int hz = IS3D ? isqrt16(R2 - gx2 - gy2) : 0;
+          const int xa = max(cx - hx, 0), xb = min(cx + hx, kTX - 1);
           unsigned long long ux = 0;  // rows with uncovered foreground inside the ball's x-extent
 #pragma unroll
           for (int c = 0; c < 4; ++c)
             if (xa <= 8 * c + 7 && xb >= 8 * c) ux |= Uc[c];
-          cand = row_box<IS3D>(max(cy - rho, 0), min(cy + rho, TY - 1), max(cz - rho, 0), min(cz + rho, TZ - 1)) & ux;
+          cand = row_box<IS3D>(max(cy - hy, 0), min(cy + hy, TY - 1), max(cz - hz, 0), min(cz + hz, TZ - 1)) & ux;
         }
       }
       // survivors, compacted in lane order (= descending D) into the warp's buffer, then painted
