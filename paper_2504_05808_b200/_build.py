@@ -16,6 +16,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
+# tuning sweeps only (tools/): extra -D definitions, e.g. FASTRS_NVCC_DEFS="-DFASTRS_KPOINT=128"
+FLAGS += os.environ.get("FASTRS_NVCC_DEFS", "").split()
 
 
 def sources():

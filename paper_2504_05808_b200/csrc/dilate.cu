@@ -35,7 +35,15 @@ constexpr int kCap = 1536;   // candidate list capacity per round (3D single pas
 constexpr int kIdx = 2048;   // sort indices (rounds path) / gather scratch (record prefix sums and z offsets)
 constexpr int kBuckets = 128;
 constexpr int kHist = 1536;  // exact-D counting-sort bins per round
-constexpr int kPoint = 96;  // C4 sweep: 128 -> 11.98 ms, 96 -> 11.75, 64 -> 11.92, 32 -> 12.59, 0 -> 15.38
+#ifndef FASTRS_KPOINT
+#define FASTRS_KPOINT 64
+#endif
+// uncovered cells at which a warp switches to point tests (a multiple of 32).  Round-2 sweep
+// (C4, dot-product point tests, K5a + K5b, tools/sweep_define.sh): 32 -> 14.68 ms, 64 -> 14.51,
+// 96 -> 14.99, 128 -> 16.71, 192 -> 20.22, 256 -> 23.10
+constexpr int kPoint = FASTRS_KPOINT;
+static_assert(kPoint % 32 == 0 && kPoint <= 1024, "point-mode list: whole warps of entries");
+constexpr int kPointW = kPoint / 32;
 constexpr uint32_t kGroupFallback = 0xFFFFFFFFu;  // uncovered cells at which a warp switches to point tests
 constexpr int kOff = 16384;  // coordinate bias of packed candidates
 
@@ -832,11 +840,11 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
       }
     }
     if (hit) {  // drop the covered cells from the lists (the order of the list does not matter)
-      uint32_t ek[3];
-      uint2 pk[3];
-      bool keep[3];
+      uint32_t ek[kPointW];
+      uint2 pk[kPointW];
+      bool keep[kPointW];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
+      for (int k = 0; k < kPointW; ++k) {
         const int idx = lane + 32 * k;
         keep[k] = idx < nu && !((cov >> k) & 1u);
         ek[k] = keep[k] ? ulist[idx] : 0u;
@@ -845,7 +853,7 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
       __syncwarp();
       uint32_t newn = 0;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
+      for (int k = 0; k < kPointW; ++k) {
         const uint32_t km = __ballot_sync(kFull, keep[k]);
         if (keep[k]) {
           const uint32_t at = newn + __popc(km & ((1u << lane) - 1u));
