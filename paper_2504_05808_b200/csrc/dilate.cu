@@ -779,7 +779,9 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
       while (m) {
         const int c = __ffs(m) - 1;
         m &= m - 1;
-        pcell[pos] = make_uint2((uint32_t)(2 * c) | ((uint32_t)(2 * ly) << 8) | ((uint32_t)(2 * lz) << 16),
+        // byte 3 (multiplied by the centre's zero byte 3) carries the cell's shell bit
+        const uint32_t sb = ((kk ? s1 : s0) >> c) & 1u;
+        pcell[pos] = make_uint2((uint32_t)(2 * c) | ((uint32_t)(2 * ly) << 8) | ((uint32_t)(2 * lz) << 16) | (sb << 24),
                                 (uint32_t)(-(c * c + ly * ly + lz * lz)));
         ulist[pos++] = (uint16_t)(row * 32 + c);
       }
@@ -811,15 +813,19 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
     // rematerialised 64-bit generic pointer)
     uint32_t pc_sh;
     asm volatile("mov.u32 %0, %1;" : "=r"(pc_sh) : "r"((uint32_t)__cvta_generic_to_shared(pcell)));
-    auto on_hit = [&](int q, uint32_t bm) {
-      const uint32_t e = ulist[q];
-      const int wD = __shfl_sync(kFull, D, __ffs(bm) - 1);
+    // fused: the cells each ball (lane) covers first are counted on its lane and queued as one
+    // event per ball at the end of the flush (first cell, count, D, shell count)
+    uint32_t pcnt = 0, pscnt = 0, pfirst = 0;
+    auto on_hit = [&](int q, uint32_t bm, uint32_t px) {
+      const int w = __ffs(bm) - 1;
       if (lane == (q & 31)) cov |= 1u << (q >> 5);
-      if (!FUSED && lane == 0) val[e] = (uint16_t)wD;
-      if (FUSED) {
-        const int row = (int)(e >> 5);
-        const uint32_t srow = __shfl_sync(kFull, row >= 32 ? s1 : s0, row & 31);
-        ev_push(e, 1u, (uint32_t)wD, (srow >> (e & 31u)) & 1u);
+      if (!FUSED) {
+        const int wD = __shfl_sync(kFull, D, w);
+        if (lane == 0) val[ulist[q]] = (uint16_t)wD;
+      } else if (lane == w) {
+        if (pcnt == 0) pfirst = ulist[q];
+        ++pcnt;
+        pscnt += (px >> 24) & 1u;
       }
       hit = true;
     };
@@ -828,7 +834,7 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
         uint2 pq;
         asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(pq.x), "=r"(pq.y) : "r"(pc_sh + 8u * (uint32_t)q));
         const uint32_t bm = __ballot_sync(kFull, __dp4a((int)pq.x, C8, (int)pq.y) > T);
-        if (bm) on_hit(q, bm);
+        if (bm) on_hit(q, bm, pq.x);
       }
     } else {
       for (int q = 0; q < nu; ++q) {
@@ -836,8 +842,20 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
         const int dx = (int)(pq.x & 0xFFu) / 2 - cx, dy = (int)((pq.x >> 8) & 0xFFu) / 2 - cy,
                   dz = (int)((pq.x >> 16) & 0xFFu) / 2 - cz;
         const uint32_t bm = __ballot_sync(kFull, dx * dx + dy * dy + dz * dz < D);
-        if (bm) on_hit(q, bm);
+        if (bm) on_hit(q, bm, pq.x);
       }
+    }
+    if (FUSED && hit) {
+      const uint32_t who = __ballot_sync(kFull, pcnt != 0);
+      const int n = __popc(who);
+      if (nev + n > 32) ev_flush();
+      if (pcnt) {
+        const int at = nev + __popc(who & ((1u << lane) - 1u));
+        qa[at] = pfirst | (pcnt << 16);
+        qb[at] = (uint32_t)D | (pscnt << 16);
+      }
+      nev += n;
+      if (nev == 32) ev_flush();
     }
     if (hit) {  // drop the covered cells from the lists (the order of the list does not matter)
       uint32_t ek[kPointW];
