@@ -748,7 +748,26 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
   bool pmode = false;
   uint16_t* ulist = S.ulist[wl];
   uint2* pcell = S.pcell[wl];
-  int ub[6] = {0, kTX - 1, 0, TY - 1, 0, TZ - 1};  // bounding box of the uncovered cells (point mode)
+  int ub[6] = {0, kTX - 1, 0, TY - 1, 0, TZ - 1};  // bounding box of the uncovered cells
+  // the box from the coverage registers (row mode): x from the OR of the uncovered rows, y/z
+  // from the rows that still hold uncovered cells
+  auto ubox_rows = [&]() {
+    const uint32_t l0 = f0 & ~c0, l1 = f1 & ~c1;
+    const uint32_t orx = __reduce_or_sync(kFull, l0 | l1);
+    ub[0] = orx ? __ffs(orx) - 1 : 0;
+    ub[1] = orx ? 31 - __clz(orx) : -1;
+    constexpr int kBig = 1 << 20;
+    int ylo = kBig, yhi = -kBig, zlo = kBig, zhi = -kBig;
+    if (l0) ylo = yhi = ly0, zlo = zhi = lz0;
+    if (l1) {
+      const int y1 = IS3D ? ly0 : ly1, z1 = IS3D ? lz0 + 4 : 0;
+      ylo = min(ylo, y1), yhi = max(yhi, y1), zlo = min(zlo, z1), zhi = max(zhi, z1);
+    }
+    ub[2] = __reduce_min_sync(kFull, ylo);
+    ub[3] = __reduce_max_sync(kFull, yhi);
+    ub[4] = __reduce_min_sync(kFull, zlo);
+    ub[5] = __reduce_max_sync(kFull, zhi);
+  };
   auto ubox_refresh = [&]() {
     int x0 = 1 << 20, x1 = -1, y0 = 1 << 20, y1 = -1, z0 = 1 << 20, z1 = -1;
     for (int q = lane; q < nu; q += 32) {
@@ -760,6 +779,7 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
     ub[2] = __reduce_min_sync(kFull, y0); ub[3] = __reduce_max_sync(kFull, y1);
     ub[4] = __reduce_min_sync(kFull, z0); ub[5] = __reduce_max_sync(kFull, z1);
   };
+  ubox_rows();
   // list the still-uncovered cells (row*32 + x) of my rows in ulist (nu <= kPoint of them)
   auto make_ulist = [&]() {
     const uint32_t left[2] = {f0 & ~c0, f1 & ~c1};
@@ -940,20 +960,20 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
         cy = (int)((e >> 32) & 0xFFFFu) - kOff - moy;
         cz = (int)((e >> 48) & 0xFFFFu) - kOff - moz;
         const int R2 = D - 1;
-        const int ddx = gap(0, kTX - 1, cx), ddy = gap(0, TY - 1, cy), ddz = gap(0, TZ - 1, cz);
+        const int ddx = gap(ub[0], ub[1], cx), ddy = gap(ub[2], ub[3], cy), ddz = gap(ub[4], ub[5], cz);
         const int gx2 = ddx * ddx, gy2 = ddy * ddy, gz2 = ddz * ddz;
         if (gx2 + gy2 + gz2 <= R2) {
-          // the extent of ball ∩ tile along each axis: the half-chord at the tile's nearest
-          // point in the other two axes (a ball reaching the tile from outside in y/z meets it
-          // in a cap much narrower than its radius)
+          // the extent of ball ∩ B along each axis (B = the bounding box of the tile's uncovered
+          // cells): the half-chord at B's nearest point in the other two axes (a ball reaching
+          // B from outside meets it in a cap much narrower than its radius)
           const int hx = isqrt16(R2 - gy2 - gz2), hy = isqrt16(R2 - gx2 - gz2);
           const int hz = IS3D ? isqrt16(R2 - gx2 - gy2) : 0;
-          const int xa = max(cx - hx, 0), xb = min(cx + hx, kTX - 1);
+          const int xa = max(cx - hx, ub[0]), xb = min(cx + hx, ub[1]);
           unsigned long long ux = 0;  // rows with uncovered foreground inside the ball's x-extent
 #pragma unroll
           for (int c = 0; c < 4; ++c)
             if (xa <= 8 * c + 7 && xb >= 8 * c) ux |= Uc[c];
-          cand = row_box<IS3D>(max(cy - hy, 0), min(cy + hy, TY - 1), max(cz - hz, 0), min(cz + hz, TZ - 1)) & ux;
+          cand = row_box<IS3D>(max(cy - hy, ub[2]), min(cy + hy, ub[3]), max(cz - hz, ub[4]), min(cz + hz, ub[5])) & ux;
         }
       }
       // survivors, compacted in lane order (= descending D) into the warp's buffer, then painted
@@ -1044,6 +1064,7 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
           Uc[c] = (unsigned long long)__ballot_sync(kFull, (left[0] >> (8 * c)) & 0xFFu) |
                   ((unsigned long long)__ballot_sync(kFull, (left[1] >> (8 * c)) & 0xFFu) << 32);
         nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(left[0]) + __popc(left[1])));
+        ubox_rows();
       }
     }
     if (pmode && nq > 0 && nu > stop) point_flush();  // the queue's last balls
