@@ -190,6 +190,7 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
   // 2^32) is taken apart
   const uint32_t rx = 0xFFFFFFFFu / (uint32_t)nx + 1u, ry = 0xFFFFFFFFu / (uint32_t)ny + 1u;
   const int bb0 = S.bb[0], bb1 = S.bb[1], bb2 = S.bb[2], bb3 = S.bb[3], bb4 = S.bb[4], bb5 = S.bb[5];
+  const bool full_range = blo <= 0 && bhi >= kBucketTop;
   for (int nb0 = 0; nb0 < nneigh; nb0 += kRecCap) {
     __syncthreads();
     if (tid == 0) S.nrec = 0;
@@ -296,12 +297,18 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
       uint32_t pe32 = 0;
       if (e < wend) {
         const uint32_t o = rec[3 * lo + 2];
-        const int v = (int)en.x;
-        const int cx = (int)(o & 0xFFFFu) - kOff + (v & 31), cy = (int)(o >> 16) - kOff + ((v >> 5) % P::TY),
-                  cz = (int)recz[lo] + v / (32 * P::TY);
+        const uint32_t v = en.x;  // element index in the home tile (row * 32 + x)
+        const int cx = (int)(o & 0xFFFFu) - kOff + (int)(v & 31u),
+                  cy = (int)(o >> 16) - kOff + (int)((v >> 5) & (uint32_t)(P::TY - 1)),
+                  cz = (int)recz[lo] + (int)(v / (32u * P::TY));
         const int ddx = gap(bb0, bb1, cx), ddy = gap(bb2, bb3, cy), ddz = gap(bb4, bb5, cz);
-        bk = dbucket(en.y);
-        if (ddx * ddx + ddy * ddy + ddz * ddz <= (int)en.y - 1 && bk >= blo && bk <= bhi) {
+        // the bucket range test is void for a full-range pass (warp-uniform)
+        bool inr = true;
+        if (MODE == kListBucketHist || !full_range) {
+          bk = dbucket(en.y);
+          inr = bk >= blo && bk <= bhi;
+        }
+        if (ddx * ddx + ddy * ddy + ddz * ddz <= (int)en.y - 1 && inr) {
           take = true;
           pe = pack(cx, cy, cz, en.y);
           if (COMPACT) pe32 = pack32(cx, cy, cz, en.y);
