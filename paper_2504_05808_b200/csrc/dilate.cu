@@ -79,6 +79,7 @@ struct PaintSmem {  // K5b (one tile per warp)
   uint16_t val[NW][FUSED ? 1 : kRows * 32];  // LT^2 per element of each warp's tile (D <= 65535 here)
   int4 sball[NW][32];             // survivors of a screened batch: centre (tile coords), D
   unsigned long long scand[NW][32];  // their candidate rows
+  alignas(16) unsigned long long uc[NW][4];  // rows with uncovered foreground per 8-column chunk of x
   uint16_t ulist[NW][kPoint];     // point mode: the still-uncovered cells (row*32 + x)
   uint2 pcell[NW][kPoint];        // the same cells for the dot-product test: (2x, 2y, 2z) bytes, -|p|^2
   uint32_t qa[NW][32];            // fused: covering events, (cell offset | count << 16)
@@ -110,10 +111,11 @@ __device__ __forceinline__ unsigned long long unpack32(uint32_t e) {
 
 __device__ __forceinline__ int gap(int lo, int hi, int c) { return c < lo ? lo - c : (c > hi ? c - hi : 0); }
 
-// floor(sqrt(h)) for 0 <= h < 2^16 via the hardware approximation (error << 1/512)
+// floor(sqrt(h)) for 0 <= h < 2^16 via the hardware approximation (error << 1/512; integer
+// inputs are never denormal, so the flush-to-zero form needs no input scaling)
 __device__ __forceinline__ int isqrt16(int h) {
   float r;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"((float)h));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)h));
   return (int)(r + 1e-3f);
 }
 
@@ -739,11 +741,15 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
   const int ly0 = IS3D ? (lane & 7) : lane, lz0 = IS3D ? (lane >> 3) : 0;
   const int ly1 = IS3D ? ly0 : lane + 32;  // row lane + 32 lies 4 layers above row lane in 3D
   // rows of my tile that still hold uncovered foreground, per 8-column chunk of x
-  unsigned long long Uc[4];
+  // (in shared memory: four 64-bit masks read by two 16-byte loads per screened batch, instead
+  // of eight registers the paint loop would push to local memory)
+  unsigned long long* Uc = S.uc[wl];
 #pragma unroll
-  for (int c = 0; c < 4; ++c)
-    Uc[c] = (unsigned long long)__ballot_sync(kFull, (f0 >> (8 * c)) & 0xFFu) |
-            ((unsigned long long)__ballot_sync(kFull, (f1 >> (8 * c)) & 0xFFu) << 32);
+  for (int c = 0; c < 4; ++c) {
+    const unsigned long long m = (unsigned long long)__ballot_sync(kFull, (f0 >> (8 * c)) & 0xFFu) |
+                                 ((unsigned long long)__ballot_sync(kFull, (f1 >> (8 * c)) & 0xFFu) << 32);
+    if (lane == 0) Uc[c] = m;
+  }
   __syncwarp();
   // uncovered foreground cells of my tile (warp-uniform); point mode once it is small
   int nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(f0) + __popc(f1)));
@@ -977,9 +983,11 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
           const int hz = IS3D ? isqrt16(R2 - gx2 - gy2) : 0;
           const int xa = max(cx - hx, ub[0]), xb = min(cx + hx, ub[1]);
           unsigned long long ux = 0;  // rows with uncovered foreground inside the ball's x-extent
+          const ulonglong2 ua = reinterpret_cast<const ulonglong2*>(Uc)[0], ub2 = reinterpret_cast<const ulonglong2*>(Uc)[1];
+          const unsigned long long uc4[4] = {ua.x, ua.y, ub2.x, ub2.y};
 #pragma unroll
           for (int c = 0; c < 4; ++c)
-            if (xa <= 8 * c + 7 && xb >= 8 * c) ux |= Uc[c];
+            if (xa <= 8 * c + 7 && xb >= 8 * c) ux |= uc4[c];
           cand = row_box<IS3D>(max(cy - hy, ub[2]), min(cy + hy, ub[3]), max(cz - hz, ub[4]), min(cz + hz, ub[5])) & ux;
         }
       }
@@ -1067,11 +1075,14 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
         dirty = false;
         const uint32_t left[2] = {f0 & ~c0, f1 & ~c1};
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          Uc[c] = (unsigned long long)__ballot_sync(kFull, (left[0] >> (8 * c)) & 0xFFu) |
-                  ((unsigned long long)__ballot_sync(kFull, (left[1] >> (8 * c)) & 0xFFu) << 32);
+        for (int c = 0; c < 4; ++c) {
+          const unsigned long long m = (unsigned long long)__ballot_sync(kFull, (left[0] >> (8 * c)) & 0xFFu) |
+                                       ((unsigned long long)__ballot_sync(kFull, (left[1] >> (8 * c)) & 0xFFu) << 32);
+          if (lane == 0) Uc[c] = m;
+        }
         nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(left[0]) + __popc(left[1])));
         ubox_rows();
+        __syncwarp();
       }
     }
     if (pmode && nq > 0 && nu > stop) point_flush();  // the queue's last balls
