@@ -79,6 +79,8 @@ enum {
                                     z-slab -> y-slab transpose (N1) instead of the h halo (N8) */
   FASTRS_SLAB_DENSE_HALO = 512u, /* fastrs_sphericity_roundness_slab: exchange H dense slices of D
                                     for the dilation instead of the kept-centre halo (N4)        */
+  FASTRS_NO_LIST_STAGING = 1024u,/* test hook: a K5 candidate list that overflows the shared list is
+                                    regathered (a second pass) instead of staged in the pool      */
   FASTRS_APPROX_LT = 256u        /* approximate local thickness (SPEC.md:153
                                     local_thickness_fast): each 2048-element tile stops its exact
                                     cover once at most 4 % of its foreground is uncovered, and those
@@ -114,6 +116,8 @@ typedef struct {
   uint64_t sum_group_list; /* K5: candidates summed over tile groups                    */
   uint64_t n_painted;      /* K5: balls painted row-parallel after the screens (S&R call) */
   uint64_t n_covering;     /* K5: painted balls that covered at least one cell (S&R call) */
+  uint32_t n_staged;       /* K5: list overflows staged in the candidate pool (one pass)   */
+  uint32_t reserved;
 } fastrs_diagnostics;
 
 /* Bytes of device workspace needed by every entry point below for this geometry.

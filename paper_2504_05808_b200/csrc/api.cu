@@ -240,7 +240,7 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
     uint32_t* goff = (uint32_t*)(w + L.goff);
     {
       Nvtx r("K5a gather");
-      launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, g, (flags & kFlagForceFallback) != 0 ? 1 : 0,
+      launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, g, gather_mode_of(flags),
                            hdr, st);
     }
     tm.mark(7);
@@ -682,6 +682,7 @@ int fastrs_read_diagnostics(const void* ws, fastrs_diagnostics* out, void* strea
   out->n_fallback = h.n_fallback;
   out->n_rounds_extra = h.n_rounds_extra;
   out->n_regathers = h.n_regathers;
+  out->n_staged = h.n_staged;
   out->max_group_list = h.max_group_list;
   out->sum_group_list = h.sum_group_list;
   out->n_painted = h.n_painted;
@@ -800,7 +801,7 @@ int slab_dilate_impl(const int32_t* labels, const uint32_t* d_ext, Geom g, const
   unsigned long long* pool = (unsigned long long*)((char*)ws + L.pool);
   uint32_t* gcount = (uint32_t*)((char*)ws + L.gcount);
   uint32_t* goff = (uint32_t*)((char*)ws + L.goff);
-  launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, g, (flags & kFlagForceFallback) != 0 ? 1 : 0, hdr,
+  launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, g, gather_mode_of(flags), hdr,
                        st);
   launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, g, ltp, lab_ext, &acc, d_ext, (flags & kFlagApproxLt) != 0, hdr,
                       st);

@@ -16,6 +16,12 @@ constexpr uint32_t kBitZ = 0x40000000u;  // element is the first of its z-run
 constexpr uint32_t kStBadLabel = 1u, kStNoSite = 2u, kStInternal = 4u, kStShell = 8u;
 
 constexpr uint32_t kFlagBorder = 1u, kFlagAsync = 4u, kFlagHostIO = 8u, kFlagForceFallback = 16u;
+constexpr uint32_t kFlagNoListStaging = 1024u;  // test hook: K5a list overflow regathers instead of staging
+// launch_dilate_gather mode bits
+constexpr int kGatherForceFallback = 1, kGatherNoStaging = 2;
+__host__ inline int gather_mode_of(uint32_t flags) {
+  return ((flags & kFlagForceFallback) ? kGatherForceFallback : 0) | ((flags & kFlagNoListStaging) ? kGatherNoStaging : 0);
+}
 constexpr uint32_t kFlagEdgeSkipZlo = 32u, kFlagEdgeSkipZhi = 64u, kFlagSlabTranspose = 128u, kFlagApproxLt = 256u;
 
 // ---- dilation / pruning tiles ---------------------------------------------------------
@@ -56,15 +62,16 @@ struct WsHeader {
   uint32_t n_rounds_extra;  // K5 groups x rounds beyond the first
   uint32_t n_regathers;     // K5 list overflows that needed a second gather pass
   uint32_t max_group_list;  // K5 longest per-group candidate list
-  uint32_t pad[1];
+  uint32_t n_staged;        // K5 list overflows staged in the pool's top half (no second pass)
   unsigned long long sum_group_list;  // K5 candidates summed over groups
   unsigned long long pool_used;       // K5 candidate pool entries allocated
-  uint32_t pad2[2];
+  unsigned long long stage_used;      // K5a: list-overflow staging entries (reset per gather launch)
   uint32_t paint_next;   // K5b work counter (reset before each launch)
   uint32_t sat_n;        // K2/K3: CTAs listed for the exact 32-bit column pass (reset per launch)
   uint32_t pad3;
   unsigned long long n_painted;   // K5b: balls painted (lanes over rows) after the screens
   unsigned long long n_covering;  // K5b: painted balls that covered at least one cell
+  unsigned long long g_stats[3];  // K5a statistics (FASTRS_GATHER_STATS builds only): examined, D-cut, taken
 };
 static_assert(sizeof(WsHeader) <= 256, "header");
 
@@ -170,7 +177,7 @@ void launch_dilate_fallback(TileMeta* meta, const uint2* centres, const uint32_t
 // K5a: per tile group, gather the kept balls that reach it and write them sorted by D
 // (descending) to the candidate pool; groups that cannot be handled are listed in fbl
 void launch_dilate_gather(const uint32_t* fgm, TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
-                          unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int force_fallback,
+                          unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int gather_mode,
                           WsHeader* hdr, cudaStream_t st);
 int64_t dilate_pool_entries(const Geom& g);  // K5 candidate pool (sorted per-group lists), u64 entries
 // K5 epilogue: shell, per-label reductions (acc nullable) and LT outputs from the LT plane ltp

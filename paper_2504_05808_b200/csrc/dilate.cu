@@ -47,6 +47,8 @@ constexpr int kPointW = kPoint / 32;
 constexpr uint32_t kGroupFallback = 0xFFFFFFFFu;  // uncovered cells at which a warp switches to point tests
 constexpr int kOff = 16384;  // coordinate bias of packed candidates
 
+constexpr int kStgChunks = 8;  // record chunks a group may stage list overflow for
+
 struct Smem;
 static_assert(3 * 512 <= 1536 && 2 * (512 + 8) + 512 <= 2048, "gather scratch fits S.hist / S.idx");
 
@@ -64,6 +66,11 @@ struct Smem {  // K5a (gather + sort)
   uint32_t count, total, nrec;
   int round_lo, round_hi, round_top, next_hi, fallback, rounds;
   int bb[6];                         // bounding box of the group's foreground (group coordinates)
+  // single-pass list overflow staged in the pool's top half, one block per record chunk:
+  // list position pos >= stg_lo[k] of chunk k lives at stage[stg_off[k] + pos]
+  unsigned long long stg_off[kStgChunks];
+  uint32_t stg_lo[kStgChunks];
+  int nstg, stg_fail;
 };
 
 // K5b CTAs hold NW of a group's kWarps tiles (one warp each).  The warps share
@@ -174,11 +181,17 @@ enum { kListBucketHist = 0,  // append to S.list (up to kCap) and count its D bu
        kListExactHist = 2,   // append to S.list and count its exact D in S.dh (bin dtop - D)
        kScatter = 3 };       // store it at out[S.dh[dtop - D]++] (S.dh holds the sorted cursors)
 
+#ifdef FASTRS_GATHER_STATS
+__device__ unsigned long long g_stats_ptr[3];  // examined, D-cut by the record's own gap, taken
+#endif
+
 template <bool IS3D, int MODE, bool COMPACT = false>
 __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ meta, const uint2* __restrict__ cent,
                                        const uint16_t* __restrict__ oct, const Geom& g, int64_t b, int64_t tx0,
                                        int64_t ty0, int64_t tz0, int nrx, int nry, int nrz, int blo, int bhi,
-                                       uint32_t dtop = 0, unsigned long long* out = nullptr) {
+                                       uint32_t dtop = 0, unsigned long long* out = nullptr,
+                                       unsigned long long* stage = nullptr, unsigned long long* stage_used = nullptr,
+                                       unsigned long long stage_cap = 0) {
   using P = Shape<IS3D>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nx = P::GX + 2 * nrx, ny = P::GY + 2 * nry, nz = P::GZ + 2 * nrz;
@@ -258,6 +271,33 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
     }
     __syncthreads();
     const uint32_t total = pre[nrec];
+    // list overflow of this chunk (kListExactHist with a staging area): positions beyond the
+    // shared list go to a block of the staging area sized by the chunk's entry count
+    constexpr uint32_t kLCap = COMPACT ? 2 * kCap : kCap;
+    unsigned long long stg = 0;
+    bool stg_ok = false;
+    if (MODE == kListExactHist && stage) {
+      if (tid == 0) {
+        const uint32_t c0 = S.count, lo = max(c0, kLCap), hi = c0 + total;
+        if (hi > lo && !S.stg_fail) {
+          if (S.nstg >= kStgChunks) {
+            S.stg_fail = 1;
+          } else {
+            const unsigned long long b0 = atomicAdd(stage_used, (unsigned long long)(hi - lo));
+            if (b0 + (hi - lo) > stage_cap) {
+              S.stg_fail = 1;
+            } else {
+              S.stg_lo[S.nstg] = lo;
+              S.stg_off[S.nstg] = b0 - lo;
+              ++S.nstg;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      stg_ok = !S.stg_fail && S.nstg > 0;
+      if (stg_ok) stg = S.stg_off[S.nstg - 1];
+    }
     // every warp walks a contiguous quarter of the entries in batches of 32.  Records hold >= 1
     // entry, so at most 32 record starts fall in (e0, e0 + 32]: one load of the next 32 prefix
     // sums places every lane's entry in its record (no per-entry search)
@@ -310,6 +350,19 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
           bk = dbucket(en.y);
           inr = bk >= blo && bk <= bhi;
         }
+#ifdef FASTRS_GATHER_STATS
+        {
+          const int hox = (int)(o & 0xFFFFu) - kOff, hoy = (int)(o >> 16) - kOff, hoz = (int)recz[lo];
+          const int gx = max(0, max(hox - bb1, bb0 - (hox + kTX - 1)));
+          const int gy = max(0, max(hoy - bb3, bb2 - (hoy + P::TY - 1)));
+          const int gz = max(0, max(hoz - bb5, bb4 - (hoz + P::TZ - 1)));
+          const bool dcut = gx * gx + gy * gy + gz * gz > (int)en.y - 1;
+          const bool tk = ddx * ddx + ddy * ddy + ddz * ddz <= (int)en.y - 1 && inr;
+          atomicAdd(&g_stats_ptr[0], 1ull);
+          if (dcut) atomicAdd(&g_stats_ptr[1], 1ull);
+          if (tk) atomicAdd(&g_stats_ptr[2], 1ull);
+        }
+#endif
         if (ddx * ddx + ddy * ddy + ddz * ddz <= (int)en.y - 1 && inr) {
           take = true;
           pe = pack(cx, cy, cz, en.y);
@@ -335,6 +388,7 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
           } else {
             if (take && pos < kCap) S.list[pos] = pe;
           }
+          if (MODE == kListExactHist && take && pos >= kLCap && stg_ok) stage[stg + pos] = pe;
         }
       }
     }
@@ -366,7 +420,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
                                                                   const TileMeta* __restrict__ meta,
                                                                const uint2* __restrict__ cent,
                                                                const uint16_t* __restrict__ oct,
-                                                               uint32_t* __restrict__ fbl, Geom g, int force_fallback,
+                                                               uint32_t* __restrict__ fbl, Geom g, int gather_mode,
                                                                unsigned long long* __restrict__ pool,
                                                                unsigned long long pool_cap,
                                                                uint32_t* __restrict__ gcount,
@@ -403,7 +457,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
     if (tid == 0) gcount[group] = 0;
     return;
   }
-  if (force_fallback) {
+  if (gather_mode & kGatherForceFallback) {
     if (lane == 0 && have_tile) fbl[atomicAdd(&hdr->n_fb, 1u)] = (uint32_t)mtile;
     if (tid == 0) gcount[group] = kGroupFallback;
     return;
@@ -454,22 +508,40 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
     // positions; a list that overflowed the shared buffer is regathered straight to the pool
     const uint32_t dtop = dmax;
     for (int k = tid; k < (int)dtop; k += kWarps * 32) S.dh[k] = 0;
-    if (tid == 0) S.count = 0;
+    if (tid == 0) {
+      S.count = 0;
+      S.nstg = 0;
+      S.stg_fail = 0;
+    }
     __syncthreads();
-    gather<IS3D, kListExactHist, IS3D>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, 0, kBuckets - 1, dtop);
+    // the pool's top half stages list overflow (the slices are allocated below it); a chunk
+    // reserves room for all its examined entries, so the reservation is ~2x what is taken
+    const unsigned long long main_cap = pool_cap - pool_cap / 2;
+    unsigned long long* stage = (gather_mode & kGatherNoStaging) ? nullptr : pool + main_cap;
+    gather<IS3D, kListExactHist, IS3D>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, 0, kBuckets - 1, dtop,
+                                       nullptr, stage, &hdr->stage_used, pool_cap / 2);
     const uint32_t total = S.count;
     constexpr uint32_t kListCap = IS3D ? 2 * kCap : kCap;  // 3D keeps compact entries
     if (tid == 0) {
       const unsigned long long b0 = atomicAdd(&hdr->pool_used, (unsigned long long)total);
       S.base = b0;
-      if (b0 + total > pool_cap) S.fallback = 1;
+      if (b0 + total > main_cap) S.fallback = 1;
     }
     block_exclusive_scan(S.dh, (int)dtop, S.wsum);
     if (!S.fallback) {
       unsigned long long* out = pool + S.base;
-      if (total <= kListCap) {
+      if (total <= kListCap || (stage && !S.stg_fail)) {
+        const int nstg = S.nstg;
+        if (total > kListCap && tid == 0) atomicAdd(&hdr->n_staged, 1u);
         for (uint32_t i = tid; i < total; i += kWarps * 32) {
-          const unsigned long long pe = IS3D ? unpack32(S.list32[i]) : S.list[i];
+          unsigned long long pe;
+          if (i < kListCap) {
+            pe = IS3D ? unpack32(S.list32[i]) : S.list[i];
+          } else {  // staged: the last chunk block whose range starts at or below i
+            int k = nstg - 1;
+            while (k > 0 && S.stg_lo[k] > i) --k;
+            pe = stage[S.stg_off[k] + i];
+          }
           out[atomicAdd(&S.dh[dtop - (uint32_t)(pe & 0xFFFFu)], 1u)] = pe;
         }
       } else {
@@ -539,7 +611,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
       if (lane == 31 && S.rounds == 0) {  // first round: the histogram covers every candidate
         const unsigned long long b0 = atomicAdd(&hdr->pool_used, (unsigned long long)inc);
         S.base = b0;
-        if (b0 + inc > pool_cap) S.fallback = 1;
+        if (b0 + inc > pool_cap - pool_cap / 2) S.fallback = 1;  // the top half stages list overflow
       }
       __syncwarp();
       if (lane == 0) {
@@ -1195,19 +1267,29 @@ int64_t launched_groups(const Geom& g) {
 }  // namespace
 
 void launch_dilate_gather(const uint32_t* fgm, TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
-                          unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int force_fallback,
+                          unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int gather_mode,
                           WsHeader* hdr, cudaStream_t st) {
   const int64_t ngroups = launched_groups(g);
   if (ngroups <= 0) return;
   const unsigned long long pool_cap = (unsigned long long)dilate_pool_entries(g);
+#ifdef FASTRS_GATHER_STATS
+  {
+    static const unsigned long long zero3[3] = {0, 0, 0};
+    cudaMemcpyToSymbolAsync(g_stats_ptr, zero3, sizeof(zero3), 0, cudaMemcpyHostToDevice, st);
+  }
+#endif
+  cudaMemsetAsync(&hdr->stage_used, 0, sizeof(hdr->stage_used), st);
   if (g.ndim == 3)
     k_dilate_gather<true><<<(unsigned)ngroups, kWarps * 32, sizeof(Smem), st>>>(fgm, meta, centres, oct, fbl, g,
-                                                                                 force_fallback, pool, pool_cap, gcount,
+                                                                                 gather_mode, pool, pool_cap, gcount,
                                                                                  goff, hdr);
   else
     k_dilate_gather<false><<<(unsigned)ngroups, kWarps * 32, sizeof(Smem), st>>>(fgm, meta, centres, oct, fbl, g,
-                                                                                  force_fallback, pool, pool_cap, gcount,
+                                                                                  gather_mode, pool, pool_cap, gcount,
                                                                                   goff, hdr);
+#ifdef FASTRS_GATHER_STATS
+  cudaMemcpyFromSymbolAsync(hdr->g_stats, g_stats_ptr, 3 * sizeof(unsigned long long), 0, cudaMemcpyDeviceToDevice, st);
+#endif
 }
 
 namespace {

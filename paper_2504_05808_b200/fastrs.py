@@ -22,6 +22,7 @@ ASYNC = 4
 HOST_IO = 8
 FORCE_FALLBACK = 16  # run the dilation with the atomic sparse-table kernel (cross-check)
 APPROX_LT = 256  # approximate local thickness (FASTRS_APPROX_LT)
+NO_LIST_STAGING = 1024  # test hook: K5a list overflow takes the regather pass instead of staging
 
 STAGES = ("edt_x", "edt_y", "edt_z", "prune", "dilate", "metrics", "epilogue", "gather")
 
@@ -49,7 +50,8 @@ class _Diag(ctypes.Structure):
                 ("sum_scale_log2", ctypes.c_int32), ("n_fallback", ctypes.c_uint32),
                 ("n_rounds_extra", ctypes.c_uint32), ("n_regathers", ctypes.c_uint32),
                 ("max_group_list", ctypes.c_uint32), ("sum_group_list", ctypes.c_uint64),
-                ("n_painted", ctypes.c_uint64), ("n_covering", ctypes.c_uint64)]
+                ("n_painted", ctypes.c_uint64), ("n_covering", ctypes.c_uint64),
+                ("n_staged", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 class _SlabInfo(ctypes.Structure):

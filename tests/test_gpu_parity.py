@@ -230,7 +230,7 @@ def test_config_c4_label_subset_fields(F, c4):
     """C4 at full size (1024^3) with 2000 grains kept (its 250 largest and 1750 drawn at random)
     and the others zeroed (exact: C4 grains are separated by >= 1 voxel, so the kept grains' D
     and LT^2 are unchanged), element by element against the oracle's full-grid fields.  The
-    large grains' candidate lists overflow the shared list, so K5a's regather path is
+    large grains' candidate lists overflow the shared list, so K5a's list staging is
     exercised."""
     lab, info = c4
     ml = info["max_label"]
@@ -243,8 +243,25 @@ def test_config_c4_label_subset_fields(F, c4):
     sub = np.where(keep[lab], lab, 0).astype(np.int32)
     full_check(F, sub, 1, max_label=ml, fields=True)
     d = F.diagnostics(F.last_workspace())
-    assert d["n_regathers"] > 0, d
+    assert d["n_staged"] > 0 and d["n_regathers"] == 0, d
     del sub
+
+
+def test_config_c4_regather_path_identical(F, c4):
+    """C4 at full size with the list staging disabled (test hook FASTRS_NO_LIST_STAGING): the
+    overflowing candidate lists take K5a's second gather pass instead; every output is
+    bit-identical to the default (staged) call, which the oracle pins element by element above."""
+    lab, info = c4
+    ml = info["max_label"]
+    t = _dev(lab)
+    a = F.sphericity_roundness(t, max_label=ml, stats=True)
+    da = F.diagnostics(F.last_workspace(t.device))
+    b = F.sphericity_roundness(t, max_label=ml, stats=True, flags=F.BORDER_BACKGROUND | F.NO_LIST_STAGING)
+    db = F.diagnostics(F.last_workspace(t.device))
+    assert da["n_staged"] > 0 and da["n_regathers"] == 0, da
+    assert db["n_regathers"] > 0 and db["n_staged"] == 0, db
+    for k in a:
+        assert torch.equal(a[k], b[k]), k
 
 
 def test_config_c4_sampled(F, c4):
