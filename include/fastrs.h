@@ -89,6 +89,9 @@ enum {
                                     tile's foreground exact (so >= 95 % within 5 %). */
 };
 
+/* u32 words per tile record of fastrs_slab_pack_tiles / fastrs_slab_unpack_tiles. */
+#define FASTRS_TILE_RECORD_WORDS 20
+
 /* Optional per-label statistics (device pointers, each nullable, batch*max_label long). */
 typedef struct {
   int64_t* volume;        /* V (3D) or A (2D): element count           */
@@ -229,8 +232,9 @@ FASTRS_API int fastrs_slab_reduce(const int32_t* labels, const uint32_t* d_ext, 
  *                       3 slices on each side that K4's |s|^2 <= 12 stencil reads; the other
  *                       layers' tile data are cleared)
  *   fastrs_slab_pack_tiles / fastrs_slab_unpack_tiles   the K4 outputs of tile layers
- *                       [tz_a, tz_b) of the extended slab as 12 u32 per tile (count, max D, nfg,
- *                       0, 16 u16 octave counts) plus the tiles' kept centres (uint2 each, tile
+ *                       [tz_a, tz_b) of the extended slab as FASTRS_TILE_RECORD_WORDS (20) u32 per
+ *                       tile (count, max D, nfg, 0, 32 u16 counts of the entries with D bucket >= 4k)
+ *                       plus the tiles' kept centres (uint2 each, tile
  *                       order; *n_entries <- their number, a device u64); unpack writes them into
  *                       the same layers of the receiver's workspace (its own layer indices)
  *   fastrs_slab_dilate  K5 on the own tiles from the tile data in the workspace

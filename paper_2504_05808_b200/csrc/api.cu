@@ -86,7 +86,7 @@ Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
   L.meta = take((size_t)g.ntiles * sizeof(TileMeta));
   L.fgm = take((size_t)g.ntiles * kRows * 4);
   L.shm = take((size_t)g.ntiles * kRows * 4);
-  L.oct = take((size_t)g.ntiles * 16 * 2);
+  L.oct = take((size_t)g.ntiles * kOctPerTile * 2);
   L.fbl = take((size_t)g.ntiles * 4);
   L.gcount = take((size_t)dilate_groups(g) * 4);
   L.goff = take((size_t)dilate_groups(g) * 4);
@@ -327,7 +327,7 @@ SlabLayout make_slab_layout(const Geom& g) {
   L.meta = take((size_t)g.ntiles * sizeof(TileMeta));
   L.fgm = take((size_t)g.ntiles * kRows * 4);
   L.shm = take((size_t)g.ntiles * kRows * 4);
-  L.oct = take((size_t)g.ntiles * 16 * 2);
+  L.oct = take((size_t)g.ntiles * kOctPerTile * 2);
   L.fbl = take((size_t)g.ntiles * 4);
   L.gcount = take((size_t)dilate_groups(g) * 4);
   L.goff = take((size_t)dilate_groups(g) * 4);
@@ -342,7 +342,8 @@ SlabLayout make_slab_layout(const Geom& g) {
 // ---- kept-centre halo (N4): pack / unpack the K4 outputs of whole tile layers ----------------
 // record per tile: TileMeta (4 u32) + the 16 octave counts (8 u32) = 12 u32; entries: the tile's
 // kept centres (uint2), tiles in index order
-constexpr int kRecWords = 12;
+constexpr int kRecWords = FASTRS_TILE_RECORD_WORDS;
+static_assert(kRecWords == 4 + kOctPerTile / 2, "tile record: 4 meta words + the bucket counts");
 
 // exclusive prefix of the tiles' centre counts (one CTA; counts from meta or from records)
 __global__ void k_tile_prefix(const TileMeta* __restrict__ meta, const uint32_t* __restrict__ rec, int64_t t0,
@@ -374,9 +375,9 @@ __global__ void k_tile_pack(const TileMeta* __restrict__ meta, const uint16_t* _
   const TileMeta m = meta[t];
   if (threadIdx.x < 4) rec[i * kRecWords + threadIdx.x] = threadIdx.x == 0 ? m.count : threadIdx.x == 1 ? m.maxD
                                                                               : threadIdx.x == 2 ? m.nfg : 0u;
-  if (threadIdx.x < 8)
-    rec[i * kRecWords + 4 + threadIdx.x] = (uint32_t)oct[t * 16 + 2 * threadIdx.x] |
-                                           ((uint32_t)oct[t * 16 + 2 * threadIdx.x + 1] << 16);
+  if (threadIdx.x < kOctPerTile / 2)
+    rec[i * kRecWords + 4 + threadIdx.x] = (uint32_t)oct[t * kOctPerTile + 2 * threadIdx.x] |
+                                           ((uint32_t)oct[t * kOctPerTile + 2 * threadIdx.x + 1] << 16);
   for (uint32_t k = threadIdx.x; k < m.count; k += blockDim.x) ent[off[i] + k] = cent[t * kTileVol + k];
 }
 
@@ -386,10 +387,10 @@ __global__ void k_tile_unpack(TileMeta* __restrict__ meta, uint16_t* __restrict_
   const int64_t i = blockIdx.x, t = t0 + i;
   const uint32_t cnt = rec[i * kRecWords];
   if (threadIdx.x == 0) meta[t] = TileMeta{cnt, rec[i * kRecWords + 1], rec[i * kRecWords + 2], 0u};
-  if (threadIdx.x < 8) {
+  if (threadIdx.x < kOctPerTile / 2) {
     const uint32_t w = rec[i * kRecWords + 4 + threadIdx.x];
-    oct[t * 16 + 2 * threadIdx.x] = (uint16_t)(w & 0xFFFFu);
-    oct[t * 16 + 2 * threadIdx.x + 1] = (uint16_t)(w >> 16);
+    oct[t * kOctPerTile + 2 * threadIdx.x] = (uint16_t)(w & 0xFFFFu);
+    oct[t * kOctPerTile + 2 * threadIdx.x + 1] = (uint16_t)(w >> 16);
   }
   for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) cent[t * kTileVol + k] = ent[off[i] + k];
 }

@@ -28,6 +28,9 @@ constexpr uint32_t kFlagEdgeSkipZlo = 32u, kFlagEdgeSkipZhi = 64u, kFlagSlabTran
 // 3D tile 32 x 8 x 8 (x fastest), 2D tile 32 x 64; both 64 rows of 32 = 2048 elements.
 constexpr int kTX = 32;
 constexpr int kTileVol = 2048;
+// per tile: counts of the kept centres with D bucket >= 4k, k = 0..31 (K4 writes, K5a cuts each
+// home tile's bucket-sorted list with them)
+constexpr int kOctPerTile = 32;
 constexpr int kRows = 64;
 constexpr int kTZ3 = 8;                 // 3D tile extent along z (slab alignment unit)
 constexpr int kLevels = 6;              // sparse-table levels for 32-wide rows: 1..32

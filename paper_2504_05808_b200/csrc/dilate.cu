@@ -199,7 +199,7 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
   uint32_t* rec = S.hist;                                  // 3 words per record
   uint32_t* pre = reinterpret_cast<uint32_t*>(S.idx);      // kRecCap + 1 prefix sums
   int16_t* recz = reinterpret_cast<int16_t*>(S.idx) + 2 * (kRecCap + 8);  // home tile z offsets
-  const int o_start = (bhi + 1 + 7) >> 3;                  // entries with bucket > bhi come first
+  const int o_start = (bhi + 1 + 3) >> 2;                  // entries with bucket > bhi come first
   // n -> (ix, iy, iz) without integer divides: umulhi(n, floor((2^32-1)/d) + 1) = n / d
   // exactly whenever n * d < 2^32 (here n < 10^5, d < 100); d = 1 (the reciprocal would be
   // 2^32) is taken apart
@@ -229,9 +229,9 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
       if (g2 > (int)hm.maxD - 1 || dbucket(hm.maxD) < blo) continue;
       // lowest bucket whose largest D can still reach the gap: D - 1 >= g2 <=> D >= g2 + 1
       const int bmin = max(dbucket((uint32_t)g2 + 1u), blo);
-      const uint16_t* oc = oct + ht * 16;
-      const uint32_t end = oc[bmin >> 3];
-      const uint32_t start = o_start >= 16 ? 0u : oc[o_start];
+      const uint16_t* oc = oct + ht * kOctPerTile;
+      const uint32_t end = oc[bmin >> 2];
+      const uint32_t start = o_start >= kOctPerTile ? 0u : oc[o_start];
       if (end <= start) continue;
       const uint32_t slot = atomicAdd(&S.nrec, 1u);
       rec[3 * slot] = (uint32_t)ht;  // tile index (< 2^32, checked in make_geom)

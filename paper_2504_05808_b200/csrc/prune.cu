@@ -416,9 +416,10 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
     }
     uint32_t run = inc - sum;
     __syncwarp();
-    // entries with bucket >= 8o (o = 1..15) = the exclusive prefix at bucket 8o-1 (lane 32-2o, q 0)
-    if ((lane & 1) == 0 && lane >= 2) oct[tile * 16 + ((32 - lane) >> 1)] = (uint16_t)run;
-    if (lane == 31) oct[tile * 16] = (uint16_t)inc;
+    // entries with bucket >= 4k (k = 1..31) = the exclusive prefix at lane 32-k (its first
+    // bucket is 127-4(32-k) = 4k-1); k = 0: all
+    if (lane >= 1) oct[tile * kOctPerTile + (32 - lane)] = (uint16_t)run;
+    if (lane == 31) oct[tile * kOctPerTile] = (uint16_t)inc;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       bhist[127 - 4 * lane - q] = run;  // now: next free slot of each bucket

@@ -197,10 +197,10 @@ int exchange(const Comm& cm, const std::vector<Xfer>& plan, const std::vector<in
   return FASTRS_OK;
 }
 
-// total kept centres announced by n tile records (12 u32 each, count first)
+// total kept centres announced by n tile records (FASTRS_TILE_RECORD_WORDS u32 each, count first)
 __global__ void k_count_entries(const uint32_t* __restrict__ rec, int64_t n, uint64_t* __restrict__ out) {
   uint32_t c = 0;  // (<= 2048 per tile: no u32 overflow per thread or warp for < 2^21 tiles)
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) c += rec[i * 12];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) c += rec[i * FASTRS_TILE_RECORD_WORDS];
   const unsigned long long s = __reduce_add_sync(0xFFFFFFFFu, c);
   __shared__ unsigned long long w[8];
   if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = s;
@@ -258,13 +258,13 @@ int call_layout(const std::vector<int64_t>& bd, int rank, int64_t Y, int64_t X, 
   L.t0 = take(tsz);  // N1: send buffer, then D of the y-slab
   L.t1 = take(tsz);  // N1: receive buffers
   L.part = take((size_t)M * 8 * 6 + (size_t)M * 4);
-  // kept-centre halo (N4): K4 records (12 u32 per tile) and kept centres (<= 2048 per tile)
+  // kept-centre halo (N4): K4 records (FASTRS_TILE_RECORD_WORDS u32 per tile) and kept centres (<= 2048 per tile)
   const int64_t tpl = ((Y + kTZ3 - 1) / kTZ3) * ((X + 31) / 32), capl = (cap + kTZ3 - 1) / kTZ3;
   L.recv_tiles = dense ? 0 : 2 * capl * tpl;
   L.send_tiles = dense ? 0 : (2 * capl + (nz + kTZ3 - 1) / kTZ3) * tpl;
-  L.srec = take((size_t)L.send_tiles * 12 * 4);
+  L.srec = take((size_t)L.send_tiles * FASTRS_TILE_RECORD_WORDS * 4);
   L.sent = take((size_t)L.send_tiles * kTileVol * 8);
-  L.rrec = take((size_t)L.recv_tiles * 12 * 4);
+  L.rrec = take((size_t)L.recv_tiles * FASTRS_TILE_RECORD_WORDS * 4);
   L.rent = take((size_t)L.recv_tiles * kTileVol * 8);
   L.cnt = take((size_t)8 * P * 8);
   size_t pb = 0, v = 0;
@@ -605,24 +605,24 @@ int fastrs_sphericity_roundness_slab(const int32_t* labels, const int64_t* dims_
     if (soff > L.send_tiles || roff > L.recv_tiles || (int)(sends.size() + recvs.size()) > 4 * P)
       return err(FASTRS_ENOMEM, "kept-centre halo buffers too small (halo H = %lld)", (long long)H);
     for (size_t k = 0; k < sends.size(); ++k) {
-      rc = fastrs_slab_pack_tiles(pw, dc, sends[k].la, sends[k].lb, srec + sends[k].tile_off * 12,
+      rc = fastrs_slab_pack_tiles(pw, dc, sends[k].la, sends[k].lb, srec + sends[k].tile_off * FASTRS_TILE_RECORD_WORDS,
                                   sent_e + sends[k].tile_off * kTileVol, cnt + k, stream);
       if (rc) return rc;
     }
     NCCL_TRY(n.GroupStart(), "ncclGroupStart");  // round 1: the fixed-size tile records
     for (const Part& q : sends) {
-      const size_t c = (size_t)((q.lb - q.la) * tpl * 12);
-      NCCL_TRY(n.Send(srec + q.tile_off * 12, c, ncclUint32, q.peer, cm.c, st), "ncclSend");
+      const size_t c = (size_t)((q.lb - q.la) * tpl * FASTRS_TILE_RECORD_WORDS);
+      NCCL_TRY(n.Send(srec + q.tile_off * FASTRS_TILE_RECORD_WORDS, c, ncclUint32, q.peer, cm.c, st), "ncclSend");
       sent += c * 4;
     }
     for (const Part& q : recvs) {
-      const size_t c = (size_t)((q.lb - q.la) * tpl * 12);
-      NCCL_TRY(n.Recv(rrec + q.tile_off * 12, c, ncclUint32, q.peer, cm.c, st), "ncclRecv");
+      const size_t c = (size_t)((q.lb - q.la) * tpl * FASTRS_TILE_RECORD_WORDS);
+      NCCL_TRY(n.Recv(rrec + q.tile_off * FASTRS_TILE_RECORD_WORDS, c, ncclUint32, q.peer, cm.c, st), "ncclRecv");
       recvd += c * 4;
     }
     NCCL_TRY(n.GroupEnd(), "ncclGroupEnd");
     for (size_t k = 0; k < recvs.size(); ++k)  // entries announced by the received records
-      k_count_entries<<<1, 256, 0, st>>>(rrec + recvs[k].tile_off * 12, (recvs[k].lb - recvs[k].la) * tpl,
+      k_count_entries<<<1, 256, 0, st>>>(rrec + recvs[k].tile_off * FASTRS_TILE_RECORD_WORDS, (recvs[k].lb - recvs[k].la) * tpl,
                                          cnt + 4 * P + k);
     std::vector<uint64_t> hc(8 * P, 0);
     CUDA_TRY(cudaMemcpyAsync(hc.data(), cnt, 8 * P * sizeof(uint64_t), cudaMemcpyDeviceToHost, st), "D2H");
@@ -643,7 +643,7 @@ int fastrs_sphericity_roundness_slab(const int32_t* labels, const int64_t* dims_
       }
     NCCL_TRY(n.GroupEnd(), "ncclGroupEnd");
     for (const Part& q : recvs) {
-      rc = fastrs_slab_unpack_tiles(pw, dc, q.la, q.lb, rrec + q.tile_off * 12, rent_e + q.tile_off * kTileVol, stream);
+      rc = fastrs_slab_unpack_tiles(pw, dc, q.la, q.lb, rrec + q.tile_off * FASTRS_TILE_RECORD_WORDS, rent_e + q.tile_off * kTileVol, stream);
       if (rc) return rc;
     }
     rc = fastrs_slab_dilate(labels, dwin, dc, Hlo, Hlo + nz, Z, h_dmax, max_label, pf, vol, nsh, sum, sums, mx, pw, pwb,

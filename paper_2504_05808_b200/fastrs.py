@@ -23,6 +23,7 @@ HOST_IO = 8
 FORCE_FALLBACK = 16  # run the dilation with the atomic sparse-table kernel (cross-check)
 APPROX_LT = 256  # approximate local thickness (FASTRS_APPROX_LT)
 NO_LIST_STAGING = 1024  # test hook: K5a list overflow takes the regather pass instead of staging
+TILE_RECORD_WORDS = 20  # FASTRS_TILE_RECORD_WORDS: u32 per tile record of slab_pack_tiles
 
 STAGES = ("edt_x", "edt_y", "edt_z", "prune", "dilate", "metrics", "epilogue", "gather")
 
@@ -386,7 +387,7 @@ def slab_pack_tiles(ws: torch.Tensor, dims_ext, tz_a: int, tz_b: int):
     dev = ws.device
     Y, X = int(dims_ext[1]), int(dims_ext[2])
     tiles = (tz_b - tz_a) * ((Y + 7) // 8) * ((X + 31) // 32)
-    rec = torch.empty(tiles * 12, dtype=torch.int32, device=dev)
+    rec = torch.empty(tiles * TILE_RECORD_WORDS, dtype=torch.int32, device=dev)
     ent = torch.empty(tiles * 2048, dtype=torch.int64, device=dev)
     n = torch.zeros(1, dtype=torch.int64, device=dev)
     _check(load().fastrs_slab_pack_tiles(ws.data_ptr(), _dims3(dims_ext), tz_a, tz_b, rec.data_ptr(), ent.data_ptr(),
