@@ -19,6 +19,7 @@
 //              VIADDMNMX.U16x2 per row pair, run ends folded into the staged values) and
 //              hands CTAs with values >= 2^14-1 to the exact 32-bit kernel.  The final pass
 //              emits D, Dmax, n_fg and flags elements with no site (ENOSITE).
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -105,6 +106,173 @@ __global__ void __launch_bounds__(256) k_edt_x(const int32_t* __restrict__ lab,
       }
       *qO = g | (vy != v ? kBitY : 0u) | (vz != v ? kBitZ : 0u);
     }
+  }
+  if (__any_sync(kFull, bad) && lane == 0) atomicOr(&hdr->status, kStBadLabel);
+}
+
+// K1, segment form (X % 128 == 0, 16-byte aligned rows; the default): one warp per x-row, and
+// lane l owns the SEGMENT of 32 consecutive elements [32 s, 32 s + 32), s = 32 b + l, of each
+// 1024-element block b.  The warp-wide sweeps of k_edt_x above spend a shuffle, a ballot and a
+// bit scan on every 32 elements in each direction; here the per-element work is lane-local
+// straight-line code on two 32-bit masks:
+//   A. coalesced 16-byte label loads, transposed through shared memory (XOR-swizzled 16-byte
+//      granules, conflict-free both ways); each lane builds the boundary mask B (bit j: a site
+//      lies just left of element j, i.e. label(j) != label(j-1), or j = 0 with the border flag)
+//      and the foreground mask F of its segment;
+//   B. per segment, the nearest boundary before it (prefix max) and after it (suffix min; the
+//      virtual boundary X with the border flag), as warp scans over the segments;
+//   C. per element: s = last boundary <= x, e = first boundary > x, g = min(x - s + 1, e - x)^2
+//      (kInf when neither exists), by one forward and one backward pass over the mask with
+//      constant bit positions; the values go back through shared memory to coalesced 16-byte
+//      stores, where the y/z run-start flags are formed from coalesced loads of the rows below.
+// Same output word as k_edt_x, bit for bit.
+constexpr int kSegFar = 1 << 20;  // "no boundary on this side" (|distance| stays far above 32768)
+__device__ __forceinline__ int swz(int G) { return G ^ ((G >> 3) & 7); }  // 16-byte granule swizzle
+
+#ifndef FASTRS_K1_MINB
+#define FASTRS_K1_MINB 4
+#endif
+__global__ void __launch_bounds__(256, FASTRS_K1_MINB) k_edt_x_seg(const int32_t* __restrict__ lab,
+                                                   const int32_t* __restrict__ below, const int32_t* __restrict__ sent,
+                                                   uint32_t* __restrict__ out, int64_t nrows, int X, int64_t Y,
+                                                   int64_t Z, int32_t max_label, int border, int is3d,
+                                                   WsHeader* __restrict__ hdr) {
+  extern __shared__ __align__(16) uint32_t s_seg[];
+  const int warps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * warps + warp;
+  if (row >= nrows) return;
+  const int NS = X >> 5;  // segments of the row (a multiple of 4)
+  uint32_t* buf = s_seg + (size_t)warp * (1024 + 4 * NS);  // transpose buffer: 256 granules
+  int4* buf4 = reinterpret_cast<int4*>(buf);
+  uint32_t* sB = buf + 1024;
+  uint32_t* sF = sB + NS;
+  int* sP = reinterpret_cast<int*>(sF + NS);
+  int* sN = sP + NS;
+  const int64_t y = row % Y;
+  const int64_t z = (row / Y) % Z;
+  const int32_t* L = lab + row * X;
+  const int32_t* Ly = y > 0 ? L - X : sent;
+  const int32_t* Lz = is3d ? (z > 0 ? L - X * Y : (below ? below + y * X : sent)) : sent;
+  uint32_t* O = out + row * X;
+  const int nblk = (X + 1023) >> 10;
+  uint32_t bad = 0;
+
+  // ---- A: boundary and foreground masks per segment ----------------------------------------
+  int32_t carry = 0;  // the last label of the previous block
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int e0 = blk << 10;
+    const int ng = min(1024, X - e0) >> 2;  // granules in this block (a multiple of 32)
+    const int4* src = reinterpret_cast<const int4*>(L + e0);
+    for (int G = lane; G < ng; G += 32) buf4[swz(G)] = __ldg(src + G);
+    __syncwarp();
+    const int seg = (blk << 5) + lane;
+    int32_t pv = lane > 0 ? (int32_t)buf[swz(lane * 8 - 1) * 4 + 3] : carry;
+    if (seg < NS) {
+      uint32_t Bm = 0, Fm = 0;
+      if (lane == 0 && blk == 0) pv = buf4[swz(0)].x;  // element 0: a boundary only with the border flag
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int4 w = buf4[swz(lane * 8 + j)];
+        Bm |= (w.x != pv ? 1u : 0u) << (4 * j);
+        Bm |= (w.y != w.x ? 1u : 0u) << (4 * j + 1);
+        Bm |= (w.z != w.y ? 1u : 0u) << (4 * j + 2);
+        Bm |= (w.w != w.z ? 1u : 0u) << (4 * j + 3);
+        Fm |= (w.x != 0 ? 1u : 0u) << (4 * j);
+        Fm |= (w.y != 0 ? 1u : 0u) << (4 * j + 1);
+        Fm |= (w.z != 0 ? 1u : 0u) << (4 * j + 2);
+        Fm |= (w.w != 0 ? 1u : 0u) << (4 * j + 3);
+        bad |= ((uint32_t)w.x > (uint32_t)max_label) | ((uint32_t)w.y > (uint32_t)max_label) |
+               ((uint32_t)w.z > (uint32_t)max_label) | ((uint32_t)w.w > (uint32_t)max_label);  // also v < 0
+        pv = w.w;
+      }
+      if (seg == 0 && border) Bm |= 1u;
+      sB[seg] = Bm;
+      sF[seg] = Fm;
+    }
+    carry = __shfl_sync(kFull, pv, 31);
+    __syncwarp();
+  }
+
+  // ---- B: nearest boundary before / after each segment ---------------------------------------
+  {
+    int run = -kSegFar;  // prefix max of the boundaries of the segments before
+    for (int s0 = 0; s0 < NS; s0 += 32) {
+      const int s = s0 + lane;
+      const uint32_t Bm = s < NS ? sB[s] : 0u;
+      const int last = Bm ? 32 * s + 31 - __clz(Bm) : -kSegFar;
+      int inc = last;  // prefix max over lanes <= lane
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc = max(inc, v);
+      }
+      int exc = __shfl_up_sync(kFull, inc, 1);
+      if (lane == 0) exc = -kSegFar;
+      if (s < NS) sP[s] = max(run, exc);
+      run = max(run, __shfl_sync(kFull, inc, 31));
+    }
+    run = border ? X : kSegFar;  // suffix min of the boundaries of the segments after
+    for (int s0 = ((NS - 1) >> 5) << 5; s0 >= 0; s0 -= 32) {
+      const int s = s0 + lane;
+      const uint32_t Bm = s < NS ? sB[s] : 0u;
+      const int first = Bm ? 32 * s + __ffs(Bm) - 1 : kSegFar;
+      int inc = first;  // suffix min over lanes >= lane
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_down_sync(kFull, inc, o);
+        if (lane + o < 32) inc = min(inc, v);
+      }
+      int exc = __shfl_down_sync(kFull, inc, 1);
+      if (lane == 31) exc = kSegFar;
+      if (s < NS) sN[s] = min(run, exc);
+      run = min(run, __shfl_sync(kFull, inc, 0));
+    }
+  }
+  __syncwarp();
+
+  // ---- C: distances per segment, then coalesced stores with the y/z run-start flags ----------
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int e0 = blk << 10;
+    const int ng = min(1024, X - e0) >> 2;
+    const int seg = (blk << 5) + lane;
+    if (seg < NS) {
+      const uint32_t Bm = sB[seg], Fm = sF[seg];
+      const int base = 32 * seg;
+      uint32_t gv[32];
+      int s = sP[seg] - base;  // relative position of the last boundary so far
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if ((Bm >> j) & 1u) s = j;
+        gv[j] = (uint32_t)(j + 1 - s);  // x - s + 1
+      }
+      int e = sN[seg] - base;  // relative position of the next boundary
+#pragma unroll
+      for (int j = 31; j >= 0; --j) {
+        if (j < 31 && ((Bm >> (j + 1)) & 1u)) e = j + 1;
+        const uint32_t d = min(min(gv[j], (uint32_t)(e - j)), 32768u);
+        gv[j] = ((Fm >> j) & 1u) ? min(d * d, kInf) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        buf4[swz(lane * 8 + j)] = make_int4((int)gv[4 * j], (int)gv[4 * j + 1], (int)gv[4 * j + 2], (int)gv[4 * j + 3]);
+    }
+    __syncwarp();
+    const int4* sl = reinterpret_cast<const int4*>(L + e0);
+    const int4* sy = reinterpret_cast<const int4*>(Ly + e0);
+    const int4* sz = reinterpret_cast<const int4*>(Lz + e0);
+    uint4* dst = reinterpret_cast<uint4*>(O + e0);
+    for (int G = lane; G < ng; G += 32) {
+      const int4 gq = buf4[swz(G)];
+      const int4 v = __ldg(sl + G), vy = __ldg(sy + G), vz = __ldg(sz + G);
+      uint4 r;
+      r.x = (uint32_t)gq.x | (vy.x != v.x ? kBitY : 0u) | (vz.x != v.x ? kBitZ : 0u);
+      r.y = (uint32_t)gq.y | (vy.y != v.y ? kBitY : 0u) | (vz.y != v.y ? kBitZ : 0u);
+      r.z = (uint32_t)gq.z | (vy.z != v.z ? kBitY : 0u) | (vz.z != v.z ? kBitZ : 0u);
+      r.w = (uint32_t)gq.w | (vy.w != v.w ? kBitY : 0u) | (vz.w != v.w ? kBitZ : 0u);
+      dst[G] = r;
+    }
+    __syncwarp();
   }
   if (__any_sync(kFull, bad) && lane == 0) atomicOr(&hdr->status, kStBadLabel);
 }
@@ -462,6 +630,18 @@ void launch_edt_x(const int32_t* labels, const int32_t* labels_below, uint32_t* 
   warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
   const size_t smem = (size_t)warps * g.X * sizeof(uint16_t);
   const int64_t blocks = (nrows + warps - 1) / warps;
+  const bool aligned = ((uintptr_t)labels % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
+                       (!labels_below || (uintptr_t)labels_below % 16 == 0);
+  if (g.X % 128 == 0 && aligned && !getenv("FASTRS_K1_WARP")) {  // segment form (the default)
+    const size_t per_warp = (size_t)(1024 + 4 * (g.X / 32)) * sizeof(uint32_t);
+    int sw = (int)(49152 / per_warp);
+    sw = sw < 1 ? 1 : (sw > 8 ? 8 : sw);
+    const int64_t sblocks = (nrows + sw - 1) / sw;
+    k_edt_x_seg<<<(unsigned)sblocks, sw * 32, sw * per_warp, st>>>(labels, labels_below, g_sent[dev], out, nrows,
+                                                                   (int)g.X, g.Y, g.Z, max_label, border ? 1 : 0,
+                                                                   g.ndim == 3 ? 1 : 0, hdr);
+    return;
+  }
   // sweep unroll 2: measured on C4 4.13 ms vs 4.46 (4), 4.35 (8), 4.26 (16) (round 1)
   if (g.X % 32 == 0)
     k_edt_x<2, true><<<(unsigned)blocks, warps * 32, smem, st>>>(labels, labels_below, g_sent[dev], out, nrows, (int)g.X,

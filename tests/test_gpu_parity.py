@@ -96,6 +96,28 @@ def test_random_tiny(F, seed, border):
     full_check(F, lab, border)
 
 
+@pytest.mark.parametrize("border", [1, 0])
+@pytest.mark.parametrize("shape", [(5, 128), (3, 1152), (6, 2048), (4, 5, 256), (3, 4, 1024), (2, 3, 1152)])
+def test_k1_segment_form(F, shape, border):
+    """K1's segment form (X % 128 == 0: per-lane 32-element segments, 1024-element blocks, carries
+    between blocks; 1152 = one full block + a partial one) against the oracle's EDT and against
+    the warp-sweep form (FASTRS_K1_WARP) bit for bit, on runs short and long."""
+    for k, (nl, blob) in enumerate([(6, 1), (3, 9), (2, 40)]):
+        lab = synth.random_labels(shape, nlabels=nl, seed=sum(shape) + 7 * k + border, fill=0.7, blob=blob)
+        lab.flat[0] = 0  # a site in every case (no ENOSITE without the border flag)
+        if lab.max() == 0:
+            lab.flat[1] = 1
+        t = _dev(lab)
+        got = _u32(F.edt_sq(t, flags=border))
+        np.testing.assert_array_equal(got, oracle.edt_sq(lab, flags=border))
+        os.environ["FASTRS_K1_WARP"] = "1"
+        try:
+            warp_form = _u32(F.edt_sq(t, flags=border))
+        finally:
+            del os.environ["FASTRS_K1_WARP"]
+        np.testing.assert_array_equal(got, warp_form)
+
+
 @pytest.mark.parametrize("shape", [(1, 1), (1, 77), (77, 1), (2, 3, 1), (1, 1, 1), (9, 1, 40), (33, 65),
                                    (17, 9, 33), (8, 8, 32), (8, 64, 64), (3, 16384)])
 def test_ragged_and_degenerate_shapes(F, shape):
