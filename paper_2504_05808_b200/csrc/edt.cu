@@ -281,7 +281,14 @@ constexpr int kColS = 256;  // positions per CTA
 constexpr int kColH = 48;   // staged halo on each side
 constexpr int kColRows = kColS + 2 * kColH;
 constexpr int kColWarps = 8;
-constexpr int kScan16U = 4;  // row pairs per iteration of the 16-bit two-sided scan loop
+#ifndef FASTRS_SCAN_U
+#define FASTRS_SCAN_U 4
+#endif
+constexpr int kScan16U = FASTRS_SCAN_U;  // row pairs per iteration of the 16-bit two-sided scan loop
+#ifndef FASTRS_COL_PP
+#define FASTRS_COL_PP 2
+#endif
+constexpr int kColPP = FASTRS_COL_PP;  // positions per thread of the 16-bit column scan (1 or 2)
 
 // Slow path of the column scan for an element whose window leaves the staged rows: the same
 // exact scan in 32-bit arithmetic, every read from global memory (L2).
@@ -474,7 +481,13 @@ __global__ void __launch_bounds__(256) k_edt_col(ColArgs a, const uint32_t* __re
 // the result is exact: the winning term involves an unclamped value (K2/K3).
 constexpr uint32_t kCap16 = 16383u;
 
-template <bool FINAL, int U>
+// PP = 2 (the default): each thread scans two consecutive positions i, i+1 of its column at once.
+// The halves of the SIMD pairs are the two positions: up pair (up(i+dq), up(i+1+dq)) and down
+// pair (down(i-dq), down(i+1-dq)) are formed from two consecutive staged rows, of which one is
+// new per dq and side, so a row load serves both positions: per dq and two elements 2 shared
+// loads, 2 PRMT, 2 VIADDMNMX and the dq^2 step, against 2 loads, 1 PRMT, 1 VIADDMNMX and the step
+// per element for PP = 1.  A background position enters with best = 0 and never extends the scan.
+template <bool FINAL, int U, int PP>
 __global__ void __launch_bounds__(256) k_edt_col16(ColArgs a, uint32_t* __restrict__ satlist,
                                                    WsHeader* __restrict__ hdr) {
   __shared__ uint32_t tile[kColRows * 32];
@@ -540,58 +553,133 @@ __global__ void __launch_bounds__(256) k_edt_col16(ColArgs a, uint32_t* __restri
   const int64_t step = (int64_t)kColWarps * astride;
   const uint32_t* src = in + base + (s0 + warp) * astride;
   uint32_t* dst = a.out + base + (s0 + warp - a.p_lo) * astride;
-  const uint32_t* trow = tile + (kColH + warp) * 32 + lane;  // row p of the tile
-  uint32_t v_next = (xin && warp < np) ? __ldg(src) : 0u;
-  for (int j = warp; j < np; j += kColWarps) {
-    const uint32_t v = v_next;
-    src += step;
-    if (xin && j + kColWarps < np) v_next = __ldg(src);
-    const uint32_t g = v & kMask;
-    uint32_t res = FINAL ? 0u : v;
-    if (g != 0) {  // (lanes beyond X read 0)
-      const uint32_t gc = min(g, kCap16);
-      const int i = kColH + j;
-      // dq^2 < best <= gc bounds the scan: isqrt(gc - 1) + U - 1 rows on each side suffice
-      float r;
-      asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)gc));
-      const int reach = (int)r + 1;
-      uint32_t best;
-      if (reach + U - 1 <= min(i, kColRows - 1 - i)) {
-        // dq2p = (dq^2, dq^2) and bmin2 = (m, m), m = min of the two halves of best2: the u32
-        // compare dq2p < bmin2 is dq^2 < m
-        uint32_t best2 = gc * 0x00010001u, bmin2 = best2;
-        uint32_t dq2p = 0x00010001u, incp = 0x00030003u;
-        const uint32_t* up = trow + 32;
-        const uint32_t* dn = trow - 32;
-        while (dq2p < bmin2) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            // low half: up(p + dq), high half: down(p - dq)
-            const uint32_t pr = __byte_perm(up[32 * u], dn[-32 * u], 0x7610);
-            best2 = __viaddmin_u16x2(pr, dq2p, best2);
-            dq2p += incp;
-            incp += 0x00020002u;
-          }
-          up += 32 * U;
-          dn -= 32 * U;
-          bmin2 = __vminu2(best2, __byte_perm(best2, 0, 0x1032));
+  if constexpr (PP == 2) {
+    const int64_t step2 = (int64_t)(2 * kColWarps) * astride;
+    const uint32_t* src2 = in + base + (s0 + 2 * warp) * astride;
+    uint32_t* dst2 = a.out + base + (s0 + 2 * warp - a.p_lo) * astride;
+    auto finish = [&](uint32_t v, uint32_t best) -> uint32_t {
+      uint32_t res = FINAL ? 0u : v;
+      if ((v & kMask) != 0) {
+        sat |= best >= kCap16;
+        dmax = max(dmax, best);
+        if (FINAL) {
+          res = best;
+          nfg += 1;
+        } else {
+          res = best | (v & (kBitY | kBitZ));
         }
-        best = bmin2 & 0xFFFFu;
-      } else {
-        best = scan_global(in, base, astride, s0 + j, L, v, chbit, a.border, a.gofs, a.Lg);  // exact, 32-bit
       }
-      sat |= best >= kCap16;  // clamped, or no site at all (ENOSITE comes from the 32-bit kernel)
-      dmax = max(dmax, best);
-      if (FINAL) {
-        res = best;
-        nfg += 1;
-      } else {
-        res = best | (v & (kBitY | kBitZ));
+      return res;
+    };
+    for (int j = 2 * warp; j < np; j += 2 * kColWarps) {
+      const bool has1 = j + 1 < np;
+      const uint32_t v0 = xin ? __ldg(src2) : 0u;
+      const uint32_t v1 = (xin && has1) ? __ldg(src2 + astride) : 0u;
+      const uint32_t g0 = v0 & kMask, g1 = v1 & kMask;
+      uint32_t best0 = 0, best1 = 0;
+      if ((g0 | g1) != 0) {
+        const uint32_t gc0 = min(g0, kCap16), gc1 = min(g1, kCap16);
+        const int i = kColH + j;
+        float r;
+        asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)max(gc0, gc1)));
+        const int reach = (int)r + 1;
+        if (reach + U - 1 <= min(i, kColRows - 2 - i)) {
+          uint32_t bu = gc0 | (gc1 << 16), bd = bu;
+          const uint32_t gm = max(gc0, gc1);
+          uint32_t bmax2 = gm * 0x00010001u;
+          uint32_t dq2p = 0x00010001u, incp = 0x00030003u;
+          const uint32_t* t = tile + i * 32 + lane;  // row i
+          uint32_t uprev = t[32], dprev = t[0];    // rows i+1 and i
+          const uint32_t* up = t + 64;             // row i+2
+          const uint32_t* dn = t - 32;             // row i-1
+          while (dq2p < bmax2) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t wu = up[32 * u];   // row i+1+dq
+              const uint32_t wd = dn[-32 * u];  // row i-dq
+              // (up(i+dq), up(i+1+dq)) and (down(i-dq), down(i+1-dq))
+              bu = __viaddmin_u16x2(__byte_perm(uprev, wu, 0x5410), dq2p, bu);
+              bd = __viaddmin_u16x2(__byte_perm(wd, dprev, 0x7632), dq2p, bd);
+              dq2p += incp;
+              incp += 0x00020002u;
+              uprev = wu;
+              dprev = wd;
+            }
+            up += 32 * U;
+            dn -= 32 * U;
+            const uint32_t m2 = __vminu2(bu, bd);
+            bmax2 = __vmaxu2(m2, __byte_perm(m2, 0, 0x1032));
+          }
+          const uint32_t m2 = __vminu2(bu, bd);
+          best0 = m2 & 0xFFFFu;
+          best1 = m2 >> 16;
+        } else {  // exact, 32-bit
+          if (g0) best0 = scan_global(in, base, astride, s0 + j, L, v0, chbit, a.border, a.gofs, a.Lg);
+          if (g1) best1 = scan_global(in, base, astride, s0 + j + 1, L, v1, chbit, a.border, a.gofs, a.Lg);
+        }
       }
+      const uint32_t r0 = finish(v0, best0), r1 = finish(v1, best1);
+      if (xin) {
+        *dst2 = r0;
+        if (has1) dst2[astride] = r1;
+      }
+      src2 += step2;
+      dst2 += step2;
     }
-    if (xin) *dst = res;
-    dst += step;
-    trow += 32 * kColWarps;
+  } else {
+    const uint32_t* trow = tile + (kColH + warp) * 32 + lane;  // row p of the tile
+    uint32_t v_next = (xin && warp < np) ? __ldg(src) : 0u;
+    for (int j = warp; j < np; j += kColWarps) {
+      const uint32_t v = v_next;
+      src += step;
+      if (xin && j + kColWarps < np) v_next = __ldg(src);
+      const uint32_t g = v & kMask;
+      uint32_t res = FINAL ? 0u : v;
+      if (g != 0) {  // (lanes beyond X read 0)
+        const uint32_t gc = min(g, kCap16);
+        const int i = kColH + j;
+        // dq^2 < best <= gc bounds the scan: isqrt(gc - 1) + U - 1 rows on each side suffice
+        float r;
+        asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)gc));
+        const int reach = (int)r + 1;
+        uint32_t best;
+        if (reach + U - 1 <= min(i, kColRows - 1 - i)) {
+          // dq2p = (dq^2, dq^2) and bmin2 = (m, m), m = min of the two halves of best2: the u32
+          // compare dq2p < bmin2 is dq^2 < m
+          uint32_t best2 = gc * 0x00010001u, bmin2 = best2;
+          uint32_t dq2p = 0x00010001u, incp = 0x00030003u;
+          const uint32_t* up = trow + 32;
+          const uint32_t* dn = trow - 32;
+          while (dq2p < bmin2) {
+  #pragma unroll
+            for (int u = 0; u < U; ++u) {
+              // low half: up(p + dq), high half: down(p - dq)
+              const uint32_t pr = __byte_perm(up[32 * u], dn[-32 * u], 0x7610);
+              best2 = __viaddmin_u16x2(pr, dq2p, best2);
+              dq2p += incp;
+              incp += 0x00020002u;
+            }
+            up += 32 * U;
+            dn -= 32 * U;
+            bmin2 = __vminu2(best2, __byte_perm(best2, 0, 0x1032));
+          }
+          best = bmin2 & 0xFFFFu;
+        } else {
+          best = scan_global(in, base, astride, s0 + j, L, v, chbit, a.border, a.gofs, a.Lg);  // exact, 32-bit
+        }
+        sat |= best >= kCap16;  // clamped, or no site at all (ENOSITE comes from the 32-bit kernel)
+        dmax = max(dmax, best);
+        if (FINAL) {
+          res = best;
+          nfg += 1;
+        } else {
+          res = best | (v & (kBitY | kBitZ));
+        }
+      }
+      if (xin) *dst = res;
+      dst += step;
+      trow += 32 * kColWarps;
+    }
   }
   // a CTA that saw a saturated value is recomputed by the 32-bit kernel (its statistics too)
   if (__syncthreads_or(sat)) {
@@ -707,10 +795,10 @@ void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, 
   cudaMemsetAsync(&hdr->sat_n, 0, sizeof(uint32_t), st);
   const unsigned fix_grid = (unsigned)(nsm * 2);
   if (final_pass) {
-    k_edt_col16<true, kScan16U><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, satlist, hdr);
+    k_edt_col16<true, kScan16U, kColPP><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, satlist, hdr);
     k_edt_col<true><<<fix_grid, kColWarps * 32, 0, st>>>(a, satlist, hdr);
   } else {
-    k_edt_col16<false, kScan16U><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, satlist, hdr);
+    k_edt_col16<false, kScan16U, kColPP><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, satlist, hdr);
     k_edt_col<false><<<fix_grid, kColWarps * 32, 0, st>>>(a, satlist, hdr);
   }
 }
