@@ -79,8 +79,12 @@ struct Smem {  // K5a (gather + sort)
 // K5b launch shape: warps per CTA and resident CTAs per SM (sets the register cap: 64 here, 32
 // resident warps; the fused reductions spill at 56).  C4 sweep (persistent, round 1, LT plane):
 // (2,16) 10.63 ms, (2,18) 10.58, (2,20) 10.71, (2,24) 10.68, (1,32) 10.76, (4,10) 10.70; round 2
-// (fused, K5a + K5b): (2,16) 16.40 ms, (2,14) 16.48, (2,12) 16.88, (2,10) 17.87.
-constexpr int kPaintNW = 2, kPaintMinB = 16;
+// (fused, K5a + K5b): (2,16) 16.40 ms, (2,14) 16.48, (2,12) 16.88, (2,10) 17.87; round 2b (straight-line
+// per-ball rows, C4 K5a + K5b): (2,16) 11.80 ms, (2,14) 11.44, (2,12) 11.88.
+#ifndef FASTRS_PAINT_MINB
+#define FASTRS_PAINT_MINB 14
+#endif
+constexpr int kPaintNW = 2, kPaintMinB = FASTRS_PAINT_MINB;
 template <int NW, bool FUSED>
 struct PaintSmem {  // K5b (one tile per warp)
   uint16_t val[NW][FUSED ? 1 : kRows * 32];  // LT^2 per element of each warp's tile (D <= 65535 here)
@@ -1074,10 +1078,11 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
         }
         __syncwarp();
         const int ns = __popc(act);
+        n_painted += ns;
+#ifdef FASTRS_PAINT_OLD
         for (int j = 0; j < ns; ++j) {
           const int4 bp = sball[j];
           const int jR2 = bp.w - 1;
-          ++n_painted;
           uint32_t ecnt = 0, escnt = 0;  // fused: cells of my rows this ball covers first
           int efirst = -1;
           const uint2 jc2 = reinterpret_cast<const uint2*>(scand)[j];  // candidate rows 0-31 | 32-63
@@ -1140,6 +1145,71 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
             }
           }
         }
+#else
+        // per ball: both of my rows in straight-line code (a row that is not a candidate, or
+        // that the chord misses, gets an empty mask); the rare covering ball takes the branch
+        const uint32_t lbit = 1u << lane;
+        for (int j = 0; j < ns; ++j) {
+          const int4 bp = sball[j];
+          const uint2 jc2 = reinterpret_cast<const uint2*>(scand)[j];  // candidate rows 0-31 | 32-63
+          const int jR2 = bp.w - 1;
+          int h0, h1;
+          if (IS3D) {  // rows lane and lane + 32 share ly and lie 4 layers apart
+            const int dy0 = ly0 - bp.y, dz0 = lz0 - bp.z, dz1 = dz0 + 4;
+            const int base0 = jR2 - dy0 * dy0;
+            h0 = base0 - dz0 * dz0;
+            h1 = base0 - dz1 * dz1;
+          } else {
+            const int dy0 = ly0 - bp.y, dy1 = ly1 - bp.y;
+            h0 = jR2 - dy0 * dy0;
+            h1 = jR2 - dy1 * dy1;
+          }
+          // the nearest uncovered cell of each row must lie within the chord (cheap reject)
+          const int dd0 = max(max(ul0 - bp.x, bp.x - uh0), 0), dd1 = max(max(ul1 - bp.x, bp.x - uh1), 0);
+          const bool t0 = (jc2.x & lbit) && dd0 * dd0 <= h0, t1 = (jc2.y & lbit) && dd1 * dd1 <= h1;
+          uint32_t m0 = 0, m1 = 0;
+          if (t0) {
+            const int w = isqrt16(h0);
+            m0 = (f0 & ~c0) & range_mask(max(bp.x - w, 0), min(bp.x + w, kTX - 1));
+          }
+          if (t1) {
+            const int w = isqrt16(h1);
+            m1 = (f1 & ~c1) & range_mask(max(bp.x - w, 0), min(bp.x + w, kTX - 1));
+          }
+          const uint32_t who = __ballot_sync(kFull, (m0 | m1) != 0);
+          if (who) {
+            dirty = true;
+            if (m0) {
+              c0 |= m0;
+              uncovered_range(f0 & ~c0, ul0, uh0);
+            }
+            if (m1) {
+              c1 |= m1;
+              uncovered_range(f1 & ~c1, ul1, uh1);
+            }
+            if (FUSED) {
+              ++n_covering;
+              const uint32_t ecnt = __popc(m0) + __popc(m1), escnt = __popc(m0 & s0) + __popc(m1 & s1);
+              const int efirst = m0 ? lane * 32 + __ffs(m0) - 1 : (32 + lane) * 32 + __ffs(m1) - 1;
+              const uint32_t tc = __reduce_add_sync(kFull, ecnt), ts = __reduce_add_sync(kFull, escnt);
+              const int off = __shfl_sync(kFull, efirst, __ffs(who) - 1);
+              ev_push((uint32_t)off, tc, (uint32_t)bp.w, ts);
+            } else {
+              const uint16_t dv = (uint16_t)bp.w;
+#pragma unroll
+              for (int hf = 0; hf < 2; ++hf) {
+                uint32_t m = hf ? m1 : m0;
+                uint16_t* vr = val + (32 * hf + lane) * 32;
+                while (m) {
+                  const int c = __ffs(m) - 1;
+                  m &= m - 1;
+                  vr[c] = dv;
+                }
+              }
+            }
+          }
+        }
+#endif
         __syncwarp();
       }
       // refresh the uncovered-row masks (only when this batch covered something)
