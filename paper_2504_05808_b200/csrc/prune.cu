@@ -246,15 +246,43 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
   // Both staging paths zero-fill outside the grid, so "foreground" is D != 0 (cells of the
   // tile beyond the grid edge read 0), and neighbours outside the grid read 0 (never contain).
   constexpr int dcap = IS3D ? kDcap3 : kDcap2;
+  {
+    // a tile without foreground (C4: 21 % of the tiles) writes empty outputs and leaves
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < kTileVol / 256; ++k) {
+      const int v = tid + 256 * k;
+      const int lx = v & 31, ly = (v >> 5) % P::TY, lz = v / (32 * P::TY);
+      any |= s[((lz + P::HZ) * P::PY + (ly + P::H)) * P::PX + (lx + P::HX)] != 0u;
+    }
+    if (!__syncthreads_or(any)) {
+      if (tid < kRows) {
+        shm[tile * kRows + tid] = 0u;
+        fgm[tile * kRows + tid] = 0u;
+      } else if (tid < kRows + kOctPerTile) {
+        oct[tile * kOctPerTile + (tid - kRows)] = 0;
+      } else if (tid == kRows + kOctPerTile) {
+        meta[tile] = TileMeta{0u, 0u, 0u, 0u};
+      }
+      return;
+    }
+  }
   uint32_t nfg = 0, maxd = 0;
   // stage-1 survivors are appended to the CTA-wide list (one shared atomic per warp row; the
   // list order does not matter: the output is sorted by D bucket, arbitrary inside a bucket)
   auto emit_row = [&](int row, uint32_t d, bool keep) {
     const bool fg = d != 0;
+    const uint32_t fgb = __ballot_sync(kFullMask, fg);
+    if (fgb == 0u) {  // a background row (C4: 43 % of the rows)
+      if (lane == 0) {
+        shm[tile * kRows + row] = 0u;
+        fgm[tile * kRows + row] = 0u;
+      }
+      return;
+    }
     // shell <=> D == 1 (a face neighbour or the flagged border is a site):
     // the per-row shell mask for the fused reductions of K5; the foreground mask for its coverage
     const uint32_t shb = __ballot_sync(kFullMask, d == 1u);
-    const uint32_t fgb = __ballot_sync(kFullMask, fg);
     const uint32_t kb = __ballot_sync(kFullMask, keep);
     uint32_t base = 0;
     if (lane == 0) {
