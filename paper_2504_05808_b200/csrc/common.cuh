@@ -42,6 +42,35 @@ constexpr int kDcap2 = 32768;  // 2D
 constexpr int kClasses3 = 12;  // offset classes with |s|^2 <= 12 (178 offsets; first 3 = 26-nbhd)
 constexpr int kClasses2 = 5;   // offset classes with |s|^2 <= 8 (24 offsets; first 2 = 8-nbhd)
 
+// Division of 32-bit unsigned values by a runtime-invariant divisor d >= 1 (Granlund-Montgomery:
+// one multiply-high, an add and two shifts instead of a ~20-instruction integer division);
+// kernels split flat tile / group indices into coordinates with it.
+struct FastDiv {
+  uint32_t d = 1, m = 0, s = 0;
+  FastDiv() = default;
+  __host__ explicit FastDiv(uint32_t div) : d(div) {
+    if (d <= 1) {
+      d = 1;
+      return;
+    }
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    m = (uint32_t)(((((unsigned long long)1 << l) - d) << 32) / d + 1);
+    s = l - 1;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    if (d == 1) return n;
+    const uint32_t t = __umulhi(n, m);
+    return (t + ((n - t) >> 1)) >> s;
+  }
+  // n = q * d + r
+  __device__ __forceinline__ uint32_t divmod(uint32_t n, uint32_t& r) const {
+    const uint32_t q = div(n);
+    r = n - q * d;
+    return q;
+  }
+};
+
 struct Geom {
   int ndim;
   int64_t B, Z, Y, X;  // 2D: Z = 1

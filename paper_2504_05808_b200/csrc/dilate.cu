@@ -98,6 +98,18 @@ struct PaintSmem {  // K5b (one tile per warp)
 };
 
 
+struct GroupDivs {  // a flat group index -> (gx, gy, gz, item)
+  FastDiv x, y, z;
+};
+__host__ inline GroupDivs group_divs(const Geom& g) {
+  const int GX = g.ndim == 3 ? 1 : 2, GY = 2, GZ = g.ndim == 3 ? 2 : 1;
+  GroupDivs d;
+  d.x = FastDiv((uint32_t)((g.ntx + GX - 1) / GX));
+  d.y = FastDiv((uint32_t)((g.nty + GY - 1) / GY));
+  d.z = FastDiv((uint32_t)((g.tz_hi - g.tz_lo + GZ - 1) / GZ));
+  return d;
+}
+
 template <bool IS3D>
 struct Shape {
   static constexpr int TY = IS3D ? 8 : 64, TZ = IS3D ? 8 : 1;
@@ -429,7 +441,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
                                                                unsigned long long pool_cap,
                                                                uint32_t* __restrict__ gcount,
                                                                uint32_t* __restrict__ goff,
-                                                               WsHeader* __restrict__ hdr) {
+                                                               WsHeader* __restrict__ hdr, GroupDivs gd) {
   using P = Shape<IS3D>;
   constexpr int TY = P::TY, TZ = P::TZ;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -440,15 +452,14 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
 
   // ---- group / tile coordinates --------------------------------------------------------
   // groups tile the layers [tz_lo, tz_hi) (all layers except on the slab path)
-  const int64_t ngx = (g.ntx + P::GX - 1) / P::GX, ngy = (g.nty + P::GY - 1) / P::GY;
-  const int64_t ngz = (g.tz_hi - g.tz_lo + P::GZ - 1) / P::GZ;
-  int64_t t = blockIdx.x;
-  const int64_t gxi = t % ngx;
-  t /= ngx;
-  const int64_t gyi = t % ngy;
-  t /= ngy;
-  const int64_t gzi = t % ngz;
-  const int64_t b = t / ngz;
+  uint32_t t = blockIdx.x, rq;
+  t = gd.x.divmod(t, rq);
+  const int64_t gxi = rq;
+  t = gd.y.divmod(t, rq);
+  const int64_t gyi = rq;
+  t = gd.z.divmod(t, rq);
+  const int64_t gzi = rq;
+  const int64_t b = t;
   const int64_t tx0 = gxi * P::GX, ty0 = gyi * P::GY, tz0 = g.tz_lo + gzi * P::GZ;
   const int wx = warp % P::GX, wy = (warp / P::GX) % P::GY, wz = warp / (P::GX * P::GY);
   const int64_t mtx = tx0 + wx, mty = ty0 + wy, mtz = tz0 + wz;
@@ -746,7 +757,8 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
                                            const uint32_t* __restrict__ gcount, const uint32_t* __restrict__ goff,
                                            int point_at, uint32_t* __restrict__ ltp, const int32_t* __restrict__ labels,
                                            const Accum& acc, const unsigned long long* __restrict__ fxlut,
-                                           const uint32_t* __restrict__ Dp, int approx, WsHeader* __restrict__ hdr) {
+                                           const uint32_t* __restrict__ Dp, int approx, WsHeader* __restrict__ hdr,
+                                           const GroupDivs& gd) {
   using P = Shape<IS3D>;
   constexpr int TY = P::TY, TZ = P::TZ;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -758,15 +770,14 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
 
   // ---- group / tile coordinates --------------------------------------------------------
   // groups tile the layers [tz_lo, tz_hi) (all layers except on the slab path)
-  const int64_t ngx = (g.ntx + P::GX - 1) / P::GX, ngy = (g.nty + P::GY - 1) / P::GY;
-  const int64_t ngz = (g.tz_hi - g.tz_lo + P::GZ - 1) / P::GZ;
-  int64_t t = group;
-  const int64_t gxi = t % ngx;
-  t /= ngx;
-  const int64_t gyi = t % ngy;
-  t /= ngy;
-  const int64_t gzi = t % ngz;
-  const int64_t b = t / ngz;
+  uint32_t t = (uint32_t)group, rq;
+  t = gd.x.divmod(t, rq);
+  const int64_t gxi = rq;
+  t = gd.y.divmod(t, rq);
+  const int64_t gyi = rq;
+  t = gd.z.divmod(t, rq);
+  const int64_t gzi = rq;
+  const int64_t b = t;
   const int64_t tx0 = gxi * P::GX, ty0 = gyi * P::GY, tz0 = g.tz_lo + gzi * P::GZ;
   const int64_t rox = tx0 * kTX, roy = ty0 * TY, roz = tz0 * TZ;  // group origin
   const int wx = warp % P::GX, wy = (warp / P::GX) % P::GY, wz = warp / (P::GX * P::GY);
@@ -1301,7 +1312,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* 
                                                               const int32_t* __restrict__ labels, Accum acc,
                                                               const unsigned long long* __restrict__ fxlut,
                                                               const uint32_t* __restrict__ Dp, int approx,
-                                                              WsHeader* __restrict__ hdr, uint32_t nbid) {
+                                                              WsHeader* __restrict__ hdr, uint32_t nbid, GroupDivs gd) {
   if (hdr->dmax > kU16Max) return;  // k_dilate_atomic handles it
   const int lane = threadIdx.x & 31;
   for (;;) {
@@ -1310,7 +1321,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* 
     bid = __shfl_sync(kFull, bid, 0);
     if (bid >= nbid) break;
     paint_tile<IS3D, NW, FUSED>(bid, fgm, shm, meta, g, pool, gcount, goff, point_at, ltp, labels, acc, fxlut, Dp, approx,
-                                hdr);
+                                hdr, gd);
     __syncwarp();
   }
 }
@@ -1352,11 +1363,11 @@ void launch_dilate_gather(const uint32_t* fgm, TileMeta* meta, const uint2* cent
   if (g.ndim == 3)
     k_dilate_gather<true><<<(unsigned)ngroups, kWarps * 32, sizeof(Smem), st>>>(fgm, meta, centres, oct, fbl, g,
                                                                                  gather_mode, pool, pool_cap, gcount,
-                                                                                 goff, hdr);
+                                                                                 goff, hdr, group_divs(g));
   else
     k_dilate_gather<false><<<(unsigned)ngroups, kWarps * 32, sizeof(Smem), st>>>(fgm, meta, centres, oct, fbl, g,
                                                                                   gather_mode, pool, pool_cap, gcount,
-                                                                                  goff, hdr);
+                                                                                  goff, hdr, group_divs(g));
 #ifdef FASTRS_GATHER_STATS
   cudaMemcpyFromSymbolAsync(hdr->g_stats, g_stats_ptr, 3 * sizeof(unsigned long long), 0, cudaMemcpyDeviceToDevice, st);
 #endif
@@ -1376,7 +1387,8 @@ void paint_go(int64_t ngroups, const uint32_t* fgm, const uint32_t* shm, const T
   const uint32_t grid = ((nbid < cap ? nbid : cap) + NW - 1) / NW;
   cudaMemsetAsync(&hdr->paint_next, 0, sizeof(uint32_t), st);
   k_dilate_paint<IS3D, NW, MINB, FUSED><<<grid, NW * 32, sizeof(PaintSmem<NW, FUSED>), st>>>(
-      fgm, shm, meta, g, pool, gcount, goff, point_at_knob(), ltp, labels, acc, device_fxlut(dev), D, approx, hdr, nbid);
+      fgm, shm, meta, g, pool, gcount, goff, point_at_knob(), ltp, labels, acc, device_fxlut(dev), D, approx, hdr, nbid,
+      group_divs(g));
 }
 }  // namespace
 

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256, FASTRS_K1_MINB) k_edt_x_seg(const int32_t
                                                    const int32_t* __restrict__ below, const int32_t* __restrict__ sent,
                                                    uint32_t* __restrict__ out, int64_t nrows, int X, int64_t Y,
                                                    int64_t Z, int32_t max_label, int border, int is3d,
-                                                   WsHeader* __restrict__ hdr) {
+                                                   WsHeader* __restrict__ hdr, FastDiv fY, FastDiv fZ) {
   extern __shared__ __align__(16) uint32_t s_seg[];
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -149,8 +149,16 @@ __global__ void __launch_bounds__(256, FASTRS_K1_MINB) k_edt_x_seg(const int32_t
   uint32_t* sF = sB + NS;
   int* sP = reinterpret_cast<int*>(sF + NS);
   int* sN = sP + NS;
-  const int64_t y = row % Y;
-  const int64_t z = (row / Y) % Z;
+  int64_t y, z;
+  if (nrows < (1ll << 32)) {  // 32-bit split (multiply-high) instead of 64-bit divisions
+    uint32_t yr;
+    const uint32_t q = fY.divmod((uint32_t)row, yr);
+    y = yr;
+    z = q - fZ.div(q) * fZ.d;
+  } else {
+    y = row % Y;
+    z = (row / Y) % Z;
+  }
   const int32_t* L = lab + row * X;
   const int32_t* Ly = y > 0 ? L - X : sent;
   const int32_t* Lz = is3d ? (z > 0 ? L - X * Y : (below ? below + y * X : sent)) : sent;
@@ -343,6 +351,7 @@ struct ColArgs {
   uint32_t chbit;
   int border;
   int64_t p_lo, p_hi, gofs, Lg;
+  FastDiv f_nxb, f_nseg, f_ninner;  // the CTA index split (block indices are 32-bit)
 };
 
 // ---- exact 32-bit column pass (one CTA = 256 positions x 32 columns) --------------------
@@ -357,12 +366,15 @@ __device__ __forceinline__ void col32_body(const ColArgs& a, int64_t bid, uint32
   const int64_t L = a.L, astride = a.astride;
   const uint32_t chbit = a.chbit;
   const int border = a.border;
-  const int xb = (int)(bid % a.nxb);
-  bid /= a.nxb;
-  const int seg = (int)(bid % a.nseg);
-  const int64_t outer = bid / a.nseg;
+  uint32_t bq = (uint32_t)bid, xbr, segr, inr;
+  bq = a.f_nxb.divmod(bq, xbr);
+  const int xb = (int)xbr;
+  bq = a.f_nseg.divmod(bq, segr);
+  const int seg = (int)segr;
+  const uint32_t outer = bq;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t base = (outer / a.n_inner) * a.outer_mult + (outer % a.n_inner) * a.inner_mult + (int64_t)xb * 32 + lane;
+  const uint32_t oq = a.f_ninner.divmod(outer, inr);
+  const int64_t base = (int64_t)oq * a.outer_mult + (int64_t)inr * a.inner_mult + (int64_t)xb * 32 + lane;
   const bool xin = xb * 32 + lane < a.X;
   const int64_t s0 = a.p_lo + (int64_t)seg * kColS;
   const int64_t lo = s0 - kColH > 0 ? s0 - kColH : 0;
@@ -495,12 +507,15 @@ __global__ void __launch_bounds__(256) k_edt_col16(ColArgs a, uint32_t* __restri
   const int64_t L = a.L, astride = a.astride;
   const uint32_t chbit = a.chbit;
   int64_t bid = blockIdx.x;
-  const int xb = (int)(bid % a.nxb);
-  bid /= a.nxb;
-  const int seg = (int)(bid % a.nseg);
-  const int64_t outer = bid / a.nseg;
+  uint32_t bq = (uint32_t)bid, xbr, segr, inr;
+  bq = a.f_nxb.divmod(bq, xbr);
+  const int xb = (int)xbr;
+  bq = a.f_nseg.divmod(bq, segr);
+  const int seg = (int)segr;
+  const uint32_t outer = bq;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t base = (outer / a.n_inner) * a.outer_mult + (outer % a.n_inner) * a.inner_mult + (int64_t)xb * 32 + lane;
+  const uint32_t oq = a.f_ninner.divmod(outer, inr);
+  const int64_t base = (int64_t)oq * a.outer_mult + (int64_t)inr * a.inner_mult + (int64_t)xb * 32 + lane;
   const bool xin = xb * 32 + lane < a.X;
   const int64_t s0 = a.p_lo + (int64_t)seg * kColS;
   const int64_t lo = s0 - kColH;  // staged rows [lo, lo + kColRows), virtual outside [0, L)
@@ -727,7 +742,8 @@ void launch_edt_x(const int32_t* labels, const int32_t* labels_below, uint32_t* 
     const int64_t sblocks = (nrows + sw - 1) / sw;
     k_edt_x_seg<<<(unsigned)sblocks, sw * 32, sw * per_warp, st>>>(labels, labels_below, g_sent[dev], out, nrows,
                                                                    (int)g.X, g.Y, g.Z, max_label, border ? 1 : 0,
-                                                                   g.ndim == 3 ? 1 : 0, hdr);
+                                                                   g.ndim == 3 ? 1 : 0, hdr,
+                                                                   FastDiv((uint32_t)g.Y), FastDiv((uint32_t)g.Z));
     return;
   }
   // sweep unroll 2: measured on C4 4.13 ms vs 4.46 (4), 4.35 (8), 4.26 (16) (round 1)
@@ -783,6 +799,9 @@ void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, 
   a.nxb = (int)((g.X + 31) / 32);
   a.nseg = (int)((p_hi - p_lo + kColS - 1) / kColS);
   if (a.nseg <= 0) return;
+  a.f_nxb = FastDiv((uint32_t)a.nxb);
+  a.f_nseg = FastDiv((uint32_t)a.nseg);
+  a.f_ninner = FastDiv((uint32_t)a.n_inner);
   const int64_t blocks = (int64_t)a.nxb * a.nseg * n_outer;
   if (!satlist) {
     if (final_pass) k_edt_col<true><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, nullptr, hdr);

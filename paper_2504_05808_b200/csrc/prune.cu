@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
                                                uint32_t* __restrict__ shm, uint16_t* __restrict__ oct,
                                                const uint32_t* __restrict__ M, const uint4* __restrict__ M1,
                                                int64_t tile0, WsHeader* __restrict__ hdr,
-                                               const __grid_constant__ CUtensorMap tmap) {
+                                               const __grid_constant__ CUtensorMap tmap, FastDiv dx, FastDiv dy,
+                                               FastDiv dz) {
   using P = PruneTile<IS3D>;
   __shared__ __align__(128) uint32_t s[P::PZ * P::PY * P::PX];
   __shared__ __align__(8) uint64_t s_bar;
@@ -165,14 +166,14 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
   const uint32_t lt_mask = (1u << lane) - 1u;
   const int64_t tile = tile0 + blockIdx.x;
   // tile -> (tx, ty, tz, b) in 32-bit arithmetic (ntiles < 2^32, checked in make_geom)
-  uint32_t t = (uint32_t)tile;
-  const uint32_t ntx = (uint32_t)g.ntx, nty = (uint32_t)g.nty, ntz = (uint32_t)g.ntz;
-  const int64_t tx = t % ntx;
-  t /= ntx;
-  const int64_t ty = t % nty;
-  t /= nty;
-  const int64_t tz = t % ntz;
-  const int64_t b = t / ntz;
+  uint32_t t = (uint32_t)tile, r;
+  t = dx.divmod(t, r);
+  const int64_t tx = r;
+  t = dy.divmod(t, r);
+  const int64_t ty = r;
+  t = dz.divmod(t, r);
+  const int64_t tz = r;
+  const int64_t b = t;
   const int64_t z0 = tz * P::TZ - P::HZ, y0 = ty * P::TY - P::H, x0 = tx * kTX - P::HX;
   const uint32_t* Db = D + b * g.Z * g.Y * g.X;
   for (int k = tid; k < 128; k += 256) bhist[k] = 0;
@@ -613,16 +614,17 @@ void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centr
   if (n <= 0) return;
   CUtensorMap tmap;
   const bool tma = prune_tensor_map(&tmap, D, g);
+  const FastDiv fdx((uint32_t)g.ntx), fdy((uint32_t)g.nty), fdz((uint32_t)g.ntz);
   if (g.ndim == 3) {
     if (tma)
-      k_prune<true, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m3, g_tables[dev].m3s1, tile0, hdr, tmap);
+      k_prune<true, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m3, g_tables[dev].m3s1, tile0, hdr, tmap, fdx, fdy, fdz);
     else
-      k_prune<true, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m3, g_tables[dev].m3s1, tile0, hdr, tmap);
+      k_prune<true, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m3, g_tables[dev].m3s1, tile0, hdr, tmap, fdx, fdy, fdz);
   } else {
     if (tma)
-      k_prune<false, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m2, nullptr, tile0, hdr, tmap);
+      k_prune<false, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m2, nullptr, tile0, hdr, tmap, fdx, fdy, fdz);
     else
-      k_prune<false, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m2, nullptr, tile0, hdr, tmap);
+      k_prune<false, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m2, nullptr, tile0, hdr, tmap, fdx, fdy, fdz);
   }
 }
 
