@@ -81,6 +81,9 @@ enum {
                                     for the dilation instead of the kept-centre halo (N4)        */
   FASTRS_NO_LIST_STAGING = 1024u,/* test hook: a K5 candidate list that overflows the shared list is
                                     regathered (a second pass) instead of staged in the pool      */
+  FASTRS_NO_COVER_CUT = 2048u,   /* test hook: K5a keeps every ball that reaches a tile group even
+                                    when the largest one contains all of its foreground (the cut
+                                    is exact; this exercises the long-list paths it avoids)       */
   FASTRS_APPROX_LT = 256u        /* approximate local thickness (SPEC.md:153
                                     local_thickness_fast): each 2048-element tile stops its exact
                                     cover once at most 4 % of its foreground is uncovered, and those

@@ -173,6 +173,9 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
   TileMeta* meta = (TileMeta*)(w + L.meta);
   uint2* cent = (uint2*)(w + L.cent);
   uint32_t* sat = (uint32_t*)(w + L.sat);
+  // the candidate pool is idle during the EDT passes: scratch of the column passes' envelope fix-up
+  void* scr = w + L.pool;
+  const size_t scr_bytes = (size_t)dilate_pool_entries(g) * 8;
   const bool border = (flags & kFlagBorder) != 0;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -211,17 +214,17 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
   if (g.ndim == 2) {
     D = stage == kEdtOnly ? d2_out : B;
     Nvtx r("K2 edt_y (final)");
-    launch_edt_col(A, D, g, 1, true, border, hdr, sat, st);
+    launch_edt_col(A, D, g, 1, true, border, hdr, sat, st, 0, -1, 0, -1, scr, scr_bytes);
     tm.mark(1);
   } else {
     {
       Nvtx r("K2 edt_y");
-      launch_edt_col(A, B, g, 1, false, border, hdr, sat, st);
+      launch_edt_col(A, B, g, 1, false, border, hdr, sat, st, 0, -1, 0, -1, scr, scr_bytes);
     }
     tm.mark(1);
     D = stage == kEdtOnly ? d2_out : A;
     Nvtx r("K3 edt_z");
-    launch_edt_col(B, D, g, 2, true, border, hdr, sat, st);
+    launch_edt_col(B, D, g, 2, true, border, hdr, sat, st, 0, -1, 0, -1, scr, scr_bytes);
     tm.mark(2);
   }
   if (stage != kEdtOnly) {
@@ -450,6 +453,9 @@ int run_host_pipelined(const int32_t* labels_host, int32_t* dlab, const Geom& g,
   uint32_t* gcount = (uint32_t*)(w + L.gcount);
   uint32_t* goff = (uint32_t*)(w + L.goff);
   uint32_t* sat = (uint32_t*)(w + L.sat);
+  // the candidate pool is idle during the EDT passes: scratch of the column passes' envelope fix-up
+  void* scr = w + L.pool;
+  const size_t scr_bytes = (size_t)dilate_pool_entries(g) * 8;
   const bool border = (flags & kFlagBorder) != 0;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -493,11 +499,11 @@ int run_host_pipelined(const int32_t* labels_host, int32_t* dlab, const Geom& g,
       make_geom(cd, 3, 1, gc);
       launch_edt_x(dlab + z0 * YX, z0 > 0 ? dlab + (z0 - 1) * YX : nullptr, A + z0 * YX, gc, max_label, border, hdr,
                    st);
-      launch_edt_col(A + z0 * YX, B + z0 * YX, gc, 1, false, border, hdr, sat, st);
+      launch_edt_col(A + z0 * YX, B + z0 * YX, gc, 1, false, border, hdr, sat, st, 0, -1, 0, -1, scr, scr_bytes);
     }
     if (step >= 1 && step - 1 < nc) {  // K3 on chunk step-1: D into A
       zr(step - 1, z0, z1);
-      launch_edt_col(B, A + z0 * YX, g, 2, true, border, hdr, sat, st, z0, z1);
+      launch_edt_col(B, A + z0 * YX, g, 2, true, border, hdr, sat, st, z0, z1, 0, -1, scr, scr_bytes);
     }
     if (step >= 2 && step - 2 < nc) {  // K4 on chunk step-2
       zr(step - 2, z0, z1);
@@ -734,7 +740,8 @@ int fastrs_slab_edt_xy(const int32_t* labels, const int32_t* labels_below, const
   uint32_t* tmp = (uint32_t*)((char*)ws + L.P);
   const bool border = (flags & kFlagBorder) != 0;
   launch_edt_x(labels, labels_below, tmp, g, max_label > 0 ? max_label : INT32_MAX, border, hdr, st);
-  launch_edt_col(tmp, packed_out, g, 1, false, border, hdr, (uint32_t*)((char*)ws + L.sat), st);
+  launch_edt_col(tmp, packed_out, g, 1, false, border, hdr, (uint32_t*)((char*)ws + L.sat), st, 0, -1, 0, -1,
+                 (char*)ws + L.pool, (size_t)dilate_pool_entries(g) * 8);
   rc = header_word_out(hdr, &hdr->dxymax, dxy_max, st);
   if (rc) return rc;
   return finish_call(hdr, flags, st);
@@ -753,7 +760,7 @@ int fastrs_slab_edt_z(const uint32_t* packed_ext, const int64_t* dims_ext, int64
   if (own_lo < 0 || own_hi > g.Z || own_lo >= own_hi || z_ext0 < 0 || z_ext0 + g.Z > Z)
     return fail(FASTRS_EINVAL, "slab range outside the extended slab / the grid");
   launch_edt_col(packed_ext, d_out, g, 2, true, (flags & kFlagBorder) != 0, hdr, (uint32_t*)((char*)ws + L.sat), st, own_lo,
-                 own_hi, z_ext0, Z);
+                 own_hi, z_ext0, Z, (char*)ws + L.pool, (size_t)dilate_pool_entries(g) * 8);
   rc = header_word_out(hdr, &hdr->dmax, dmax_out, st);
   if (rc) return rc;
   return finish_call(hdr, flags, st);

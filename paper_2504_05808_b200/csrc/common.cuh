@@ -17,10 +17,12 @@ constexpr uint32_t kStBadLabel = 1u, kStNoSite = 2u, kStInternal = 4u, kStShell 
 
 constexpr uint32_t kFlagBorder = 1u, kFlagAsync = 4u, kFlagHostIO = 8u, kFlagForceFallback = 16u;
 constexpr uint32_t kFlagNoListStaging = 1024u;  // test hook: K5a list overflow regathers instead of staging
+constexpr uint32_t kFlagNoCoverCut = 2048u;     // test hook: K5a without the cover cut
 // launch_dilate_gather mode bits
-constexpr int kGatherForceFallback = 1, kGatherNoStaging = 2;
+constexpr int kGatherForceFallback = 1, kGatherNoStaging = 2, kGatherNoCoverCut = 4;
 __host__ inline int gather_mode_of(uint32_t flags) {
-  return ((flags & kFlagForceFallback) ? kGatherForceFallback : 0) | ((flags & kFlagNoListStaging) ? kGatherNoStaging : 0);
+  return ((flags & kFlagForceFallback) ? kGatherForceFallback : 0) | ((flags & kFlagNoListStaging) ? kGatherNoStaging : 0) |
+         ((flags & kFlagNoCoverCut) ? kGatherNoCoverCut : 0);
 }
 constexpr uint32_t kFlagEdgeSkipZlo = 32u, kFlagEdgeSkipZhi = 64u, kFlagSlabTranspose = 128u, kFlagApproxLt = 256u;
 
@@ -184,9 +186,12 @@ void launch_edt_x(const int32_t* labels, const int32_t* labels_below, uint32_t* 
 // (the border convention applies at global 0 and Lg).  Default: p_lo = 0, p_hi = L, gofs = 0.
 // satlist: workspace list of col_blocks(g) u32 for the CTAs the 16-bit kernel hands to the exact
 // 32-bit kernel (NULL: the 32-bit kernel everywhere).
+// scratch (nullable): device memory idle during the pass (the K5 candidate pool) for the exact
+// lower-envelope fix-up of the CTAs the 16-bit kernel lists (else the windowed 32-bit kernel)
 void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, bool final_pass,
                     bool border, WsHeader* hdr, uint32_t* satlist, cudaStream_t st, int64_t p_lo = 0,
-                    int64_t p_hi = -1, int64_t gofs = 0, int64_t Lg = -1);
+                    int64_t p_hi = -1, int64_t gofs = 0, int64_t Lg = -1, void* scratch = nullptr,
+                    size_t scratch_bytes = 0);
 int64_t col_blocks(const Geom& g);  // column-pass CTAs of the larger of the y / z passes
 cudaError_t ensure_mtables(int device);  // builds the per-device lattice tables (sync, once)
 const unsigned long long* device_fxlut(int device);  // fx(c) for c < kFxLut (after ensure_mtables)

@@ -64,13 +64,15 @@ struct Smem {  // K5a (gather + sort)
   unsigned long long base;           // the group's offset in the global candidate pool
   uint32_t wsum[kWarps];
   uint32_t count, total, nrec;
-  int round_lo, round_hi, round_top, next_hi, fallback, rounds;
+  int round_lo, round_hi, round_top, next_hi, fallback, rounds, bigbucket;
   int bb[6];                         // bounding box of the group's foreground (group coordinates)
   // single-pass list overflow staged in the pool's top half, one block per record chunk:
   // list position pos >= stg_lo[k] of chunk k lives at stage[stg_off[k] + pos]
   unsigned long long stg_off[kStgChunks];
   uint32_t stg_lo[kStgChunks];
   int nstg, stg_fail;
+  unsigned long long topkey;         // cover cut: (max D << 32) | home tile of the largest reaching ball
+  int qstar[4];                      // its centre (group coordinates) and D
 };
 
 // K5b CTAs hold NW of a group's kWarps tiles (one warp each).  The warps share
@@ -195,7 +197,8 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t* a, int n, uin
 enum { kListBucketHist = 0,  // append to S.list (up to kCap) and count its D bucket in S.bhist
        kListOnly = 1,        // append to S.list
        kListExactHist = 2,   // append to S.list and count its exact D in S.dh (bin dtop - D)
-       kScatter = 3 };       // store it at out[S.dh[dtop - D]++] (S.dh holds the sorted cursors)
+       kScatter = 3,         // store it at out[S.dh[dtop - D]++] (S.dh holds the sorted cursors)
+       kExactCount = 4 };    // count its exact D in S.dh (bin dtop - D), no list
 
 #ifdef FASTRS_GATHER_STATS
 __device__ unsigned long long g_stats_ptr[3];  // examined, D-cut by the record's own gap, taken
@@ -207,7 +210,8 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
                                        int64_t ty0, int64_t tz0, int nrx, int nry, int nrz, int blo, int bhi,
                                        uint32_t dtop = 0, unsigned long long* out = nullptr,
                                        unsigned long long* stage = nullptr, unsigned long long* stage_used = nullptr,
-                                       unsigned long long stage_cap = 0) {
+                                       unsigned long long stage_cap = 0, uint32_t dlo_f = 0u,
+                                       uint32_t dhi_f = 0xFFFFFFFFu) {
   using P = Shape<IS3D>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nx = P::GX + 2 * nrx, ny = P::GY + 2 * nry, nz = P::GZ + 2 * nrz;
@@ -366,6 +370,8 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
           bk = dbucket(en.y);
           inr = bk >= blo && bk <= bhi;
         }
+        if (dlo_f != 0u || dhi_f != 0xFFFFFFFFu)  // (warp-uniform) the cover cut / an exact-D sub-range
+          inr = inr && en.y >= dlo_f && en.y <= dhi_f;
 #ifdef FASTRS_GATHER_STATS
         {
           const int hox = (int)(o & 0xFFFFu) - kOff, hoy = (int)(o >> 16) - kOff, hoz = (int)recz[lo];
@@ -389,6 +395,8 @@ __device__ __forceinline__ void gather(Smem& S, const TileMeta* __restrict__ met
       if (tm) {
         if (MODE == kScatter) {
           if (take) out[atomicAdd(&S.dh[dtop - (uint32_t)(pe & 0xFFFFu)], 1u)] = pe;
+        } else if (MODE == kExactCount) {
+          if (take) atomicAdd(&S.dh[dtop - (uint32_t)(pe & 0xFFFFu)], 1u);
         } else {
           if (MODE == kListBucketHist) {
             const uint32_t grp = __match_any_sync(kFull, take ? bk : -1);
@@ -511,6 +519,87 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
   __syncthreads();
   const int rmax = dmax > 0 ? isqrt16((int)(dmax - 1)) : 0;
   const int nrx = (rmax + kTX - 1) / kTX, nry = (rmax + TY - 1) / TY, nrz = IS3D ? (rmax + TZ - 1) / TZ : 0;
+  // ---- cover cut.  The largest kept ball that reaches the group: when it contains every
+  // foreground cell of the group, no ball with a smaller D can carry the maximum at any of them
+  // (LT^2 = max over the covering balls), so the gather keeps D >= its D only.  Exact, and it
+  // turns the candidate lists of large objects (the centre ball of a big sphere covers whole
+  // groups; thousands of nearly tangent balls reach them) into a handful of entries.
+  // (only for Dmax > kHist, the D-bucket rounds path: below it the candidate lists are bounded by
+  // the reach of balls of radius < 40 and the cut's extra dependent loads cost more than it saves
+  // -- C4: k5 11.56 -> 12.64 ms with the cut on every group)
+  uint32_t dcut = 0;
+  if (!(gather_mode & kGatherNoCoverCut) && dmax > (uint32_t)kHist) {
+    if (tid == 0) {
+      S.topkey = 0ull;
+      S.qstar[3] = 0;
+    }
+    __syncthreads();
+    const int nx = P::GX + 2 * nrx, ny = P::GY + 2 * nry, nz = P::GZ + 2 * nrz;
+    const int bb0 = S.bb[0], bb1 = S.bb[1], bb2 = S.bb[2], bb3 = S.bb[3], bb4 = S.bb[4], bb5 = S.bb[5];
+    for (int n = tid; n < nx * ny * nz; n += kWarps * 32) {
+      const int ix = n % nx, iy = (n / nx) % ny, iz = n / (nx * ny);
+      const int64_t hx = tx0 + ix - nrx, hy = ty0 + iy - nry, hz = tz0 + iz - nrz;
+      if (hx < 0 || hx >= g.ntx || hy < 0 || hy >= g.nty || hz < 0 || hz >= g.ntz) continue;
+      const int64_t ht = ((b * g.ntz + hz) * g.nty + hy) * g.ntx + hx;
+      const TileMeta hm = meta[ht];
+      if (!hm.count) continue;
+      const int hox = (ix - nrx) * kTX, hoy = (iy - nry) * TY, hoz = (iz - nrz) * TZ;
+      const int gx = max(0, max(hox - bb1, bb0 - (hox + kTX - 1)));
+      const int gy = max(0, max(hoy - bb3, bb2 - (hoy + TY - 1)));
+      const int gz = max(0, max(hoz - bb5, bb4 - (hoz + TZ - 1)));
+      if (gx * gx + gy * gy + gz * gz > (int)hm.maxD - 1) continue;
+      atomicMax(&S.topkey, ((unsigned long long)hm.maxD << 32) | (unsigned long long)n);
+    }
+    __syncthreads();
+    const unsigned long long key = S.topkey;
+    if (key) {
+      const uint32_t dstar = (uint32_t)(key >> 32);
+      const int n = (int)(key & 0xFFFFFFFFu);
+      const int ix = n % nx, iy = (n / nx) % ny, iz = n / (nx * ny);
+      if (warp == 0) {  // an entry with D == dstar in the head of that tile's bucket-sorted list
+        const int64_t ht = ((b * g.ntz + (tz0 + iz - nrz)) * g.nty + (ty0 + iy - nry)) * g.ntx + (tx0 + ix - nrx);
+        const uint32_t cnt = meta[ht].count;
+        const uint2* lst = cent + (size_t)ht * kTileVol;
+        for (uint32_t k0 = 0; k0 < cnt; k0 += 32) {
+          const uint2 en = k0 + lane < cnt ? lst[k0 + lane] : make_uint2(0u, 0u);
+          const uint32_t hit = __ballot_sync(kFull, k0 + lane < cnt && en.y == dstar);
+          if (hit) {
+            if (lane == __ffs(hit) - 1) {
+              const uint32_t v = en.x;
+              S.qstar[0] = (ix - nrx) * kTX + (int)(v & 31u);
+              S.qstar[1] = (iy - nry) * TY + (int)((v >> 5) & (uint32_t)(TY - 1));
+              S.qstar[2] = (iz - nrz) * TZ + (int)(v / (32u * TY));
+              S.qstar[3] = 1;
+            }
+            break;
+          }
+        }
+      }
+      __syncthreads();
+      bool ok = S.qstar[3] != 0;
+      if (ok && active) {  // every foreground row of my tile inside the chord of B(q*)
+        const int qx = S.qstar[0] - mox;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int row = lane + 32 * k;
+          const uint32_t f = fgm[mtile * kRows + row];
+          if (!f) continue;
+          const int dy = row % TY + moy - S.qstar[1], dz = row / TY + moz - S.qstar[2];
+          const int h = (int)dstar - 1 - dy * dy - dz * dz;
+          if (h < 0) {
+            ok = false;
+            continue;
+          }
+          const int w = isqrt16(h);
+          const int l = qx - w, r = qx + w;
+          const uint32_t allowed = (r < 0 || l > 31) ? 0u : range_mask(max(l, 0), min(r, 31));
+          if (f & ~allowed) ok = false;
+        }
+      }
+      if (__syncthreads_and(ok)) dcut = dstar;
+    }
+  }
+  const int bcut = dcut ? dbucket(dcut) : 0;
   uint32_t written = 0;
   if (tid == 0) {
     S.fallback = 0;
@@ -533,6 +622,8 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
     // reserves room for all its examined entries, so the reservation is ~2x what is taken
     const unsigned long long main_cap = pool_cap - pool_cap / 2;
     unsigned long long* stage = (gather_mode & kGatherNoStaging) ? nullptr : pool + main_cap;
+    // (no cover cut on this path: dmax <= kHist, see above; literal full-range arguments keep
+    // the bucket and D-range tests out of the entry loop)
     gather<IS3D, kListExactHist, IS3D>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, 0, kBuckets - 1, dtop,
                                        nullptr, stage, &hdr->stage_used, pool_cap / 2);
     const uint32_t total = S.count;
@@ -579,7 +670,8 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
     for (int i = tid; i < kBuckets; i += kWarps * 32) S.bhist[i] = 0;
     if (tid == 0) S.count = 0;
     __syncthreads();
-    gather<IS3D, kListBucketHist>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, 0, rhi);
+    gather<IS3D, kListBucketHist>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, bcut, rhi, 0, nullptr,
+                                  nullptr, nullptr, 0, dcut);
     __syncthreads();
     // --- this round's bucket range [rlo, rhi]: as many buckets as fit the list and the sort
     // range (warp 0: descending inclusive scan of the histogram, 4 buckets per lane)
@@ -631,7 +723,10 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
       __syncwarp();
       if (lane == 0) {
         // a single bucket exceeds the list / range, or (defensive) too many rounds
-        S.fallback = (S.fallback || (lo == top && lo >= 0) || ++S.rounds > kBuckets) ? 1 : 0;
+        // a single bucket that exceeds the list / sort range (large objects: thousands of kept
+        // balls of similar D reach the group) is written by exact-D scatter rounds below
+        S.bigbucket = (lo == top && lo >= 0) ? 1 : 0;
+        S.fallback = (S.fallback || ++S.rounds > kBuckets) ? 1 : 0;
         S.round_lo = lo + 1;
         S.round_top = top;
         S.next_hi = below ? lo : -1;
@@ -639,13 +734,44 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
     }
     __syncthreads();
     if (S.fallback) break;
+    if (S.bigbucket) {
+      // exact-D scatter rounds over the bucket `top`, kHist D values at a time, highest first:
+      // count the exact D of every candidate in the sub-range (no list), prefix-sum the counts
+      // into cursors, gather again and store each candidate at its cursor.  Equal D may land in
+      // any order (ties do not change the first cover), so no capacity limit applies.
+      const int bk = S.round_top;
+      const uint32_t dmin_b = bk == 0 ? 1u : dbucket_max(bk - 1) + 1u, dmax_b = min(dbucket_max(bk), dmax);
+      for (int64_t dh = dmax_b; dh >= (int64_t)dmin_b; dh -= kHist) {
+        const uint32_t dhu = (uint32_t)dh;
+        if (dhu < dcut) break;
+        const uint32_t dl = max(max(dmin_b, dcut), dhu >= (uint32_t)kHist ? dhu - (uint32_t)kHist + 1u : 1u);
+        const int nbins = (int)(dhu - dl) + 1;
+        for (int k = tid; k < kHist; k += kWarps * 32) S.dh[k] = 0;
+        __syncthreads();
+        gather<IS3D, kExactCount>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, bk, bk, dhu, nullptr,
+                                  nullptr, nullptr, 0, dl, dhu);
+        const uint32_t cnt = block_exclusive_scan(S.dh, nbins, S.wsum);
+        if (cnt) {
+          gather<IS3D, kScatter>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, bk, bk, dhu,
+                                 pool + S.base + written, nullptr, nullptr, 0, dl, dhu);
+          written += cnt;
+        }
+        if (tid == 0) atomicAdd(&hdr->n_rounds_extra, 1u);
+        __syncthreads();
+      }
+      if (bk == 0) break;
+      if (tid == 0) S.round_hi = bk - 1;
+      __syncthreads();
+      continue;
+    }
     const int rlo = S.round_lo;
     if (S.count > kCap) {  // the list overflowed: gather again, keeping [rlo, rhi] only (they fit)
       if (tid == 0) atomicAdd(&hdr->n_regathers, 1u);
       __syncthreads();
       if (tid == 0) S.count = 0;
       __syncthreads();
-      gather<IS3D, kListOnly>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, rlo, rhi);
+      gather<IS3D, kListOnly>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, max(rlo, bcut), rhi, 0, nullptr,
+                              nullptr, nullptr, 0, dcut);
       __syncthreads();
     }
     // --- exact counting sort of the list indices by D (descending), D in [dlo, dhi]

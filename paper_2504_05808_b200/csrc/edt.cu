@@ -352,6 +352,7 @@ struct ColArgs {
   int border;
   int64_t p_lo, p_hi, gofs, Lg;
   FastDiv f_nxb, f_nseg, f_ninner;  // the CTA index split (block indices are 32-bit)
+  int defer;  // 16-bit kernel: a scan that leaves the staged window lists its CTA for the envelope pass
 };
 
 // ---- exact 32-bit column pass (one CTA = 256 positions x 32 columns) --------------------
@@ -476,6 +477,138 @@ __global__ void __launch_bounds__(256) k_edt_col(ColArgs a, const uint32_t* __re
   }
 }
 
+// ---- exact lower-envelope column pass for the CTAs the 16-bit kernel lists ----------------
+// The windowed scan costs O(sqrt(D)) per element, which is unbounded for large objects (a sphere
+// of radius 240 takes 0.35 s per 512^3 pass).  The CTAs the 16-bit kernel cannot finish (a value
+// >= 2^14-1 or a window beyond the staged rows) are recomputed here by the lower envelope of the
+// parabolas (x - q)^2 + g(q) (Felzenszwalb-Huttenlocher), O(1) amortised per element:
+//  * one warp per listed CTA, lane = column (32 columns of the CTA), sequential along the axis;
+//  * only positions within R = isqrt(max g over the CTA's positions) + 1 of [s0, pend) can hold
+//    an argmin (the minimum is <= g(p) <= R^2), so each lane walks [s0 - R, pend - 1 + R];
+//  * the envelope is built per same-label run, with the run-end sites as parabolas of height 0
+//    (the element before a run start / after a run end; the virtual border layer with the flag);
+//  * intersections are compared exactly as fractions in 64-bit integers;
+//  * the per-lane stack lives in global scratch (the K5 candidate pool, idle during the EDT):
+//    entry k of a lane at scratch[slot][k][lane] (coalesced when the lanes are in step).
+// Same results as the windowed scan, bit for bit (the minimum of integers is unique).
+__device__ __forceinline__ bool fh_le(const uint2 a, const uint2 b, const uint2 c) {
+  // isect(b, c) <= isect(a, b) for positions a < b < c; isect(i, j) = ((g_j + j^2) - (g_i + i^2)) / (2 (j - i))
+  const long long ia = (int)a.x, ib = (int)b.x, ic = (int)c.x;
+  const long long nab = ((long long)b.y + ib * ib) - ((long long)a.y + ia * ia), dab = 2 * (ib - ia);
+  const long long nbc = ((long long)c.y + ic * ic) - ((long long)b.y + ib * ib), dbc = 2 * (ic - ib);
+  return nbc * dab <= nab * dbc;
+}
+
+template <bool FINAL>
+__global__ void __launch_bounds__(256) k_edt_col_fh(ColArgs a, const uint32_t* __restrict__ listed,
+                                                    WsHeader* __restrict__ hdr, uint2* __restrict__ scratch,
+                                                    int nslots) {
+  const int lane = threadIdx.x & 31;
+  const int slot = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  if (slot >= nslots) return;
+  const uint32_t n = *(volatile uint32_t*)&hdr->sat_n;
+  const int64_t L = a.L, astride = a.astride;
+  const uint32_t chbit = a.chbit;
+  uint2* env = scratch + (size_t)slot * 32 * (size_t)(L + 2) + lane;
+  for (uint32_t t = slot; t < n; t += nslots) {
+    uint32_t bq = listed[t], xbr, segr, inr;
+    bq = a.f_nxb.divmod(bq, xbr);
+    bq = a.f_nseg.divmod(bq, segr);
+    const uint32_t oq = a.f_ninner.divmod(bq, inr);
+    const int64_t base = (int64_t)oq * a.outer_mult + (int64_t)inr * a.inner_mult + (int64_t)xbr * 32 + lane;
+    const bool xin = (int)xbr * 32 + lane < a.X;
+    const int64_t s0 = a.p_lo + (int64_t)segr * kColS;
+    const int64_t pend = s0 + kColS < a.p_hi ? s0 + kColS : a.p_hi;
+    uint32_t dmax = 0, nfg = 0, nosite = 0;
+    if (xin) {
+      const uint32_t* col = a.in + base;
+      auto word = [&](int64_t q) { return __ldg(col + q * astride); };
+      uint32_t mg = 0;
+      for (int64_t p = s0; p < pend; ++p) mg = max(mg, word(p) & kMask);
+      int64_t R = L;
+      if (mg < kInf) {
+        R = (int64_t)sqrtf((float)mg);
+        while (R * R > (int64_t)mg) --R;
+        while ((R + 1) * (R + 1) <= (int64_t)mg) ++R;
+        R += 1;
+      }
+      const int64_t lo = s0 - R > 0 ? s0 - R : 0, hi = pend - 1 + R < L - 1 ? pend - 1 + R : L - 1;
+      int64_t q = lo;
+      while (q < pend) {
+        // the run [ra, rb] of the walked range that starts at q
+        const int64_t ra = q;
+        uint32_t w = word(q);
+        const bool true_start = q == 0 || (w & chbit) != 0u;
+        int ne = 0;
+        auto push = [&](int pos, uint32_t gq) {
+          const uint2 c = make_uint2((uint32_t)pos, gq);
+          while (ne >= 2 && fh_le(env[(size_t)(ne - 2) * 32], env[(size_t)(ne - 1) * 32], c)) --ne;
+          env[(size_t)ne * 32] = c;
+          ++ne;
+        };
+        if (true_start && (a.gofs + ra - 1 >= 0 || a.border)) push((int)(ra - 1), 0u);
+        for (;;) {
+          const uint32_t gq = w & kMask;
+          if (gq < kInf) push((int)q, gq);
+          ++q;
+          if (q > hi) break;
+          w = word(q);
+          if (w & chbit) break;  // q starts the next run
+        }
+        const int64_t rb = q - 1;
+        const bool true_end = q <= hi || q >= L;  // (q > hi and q < L: the run continues past the walk)
+        if (true_end && (rb + 1 < L || (a.border && a.gofs + L >= a.Lg))) push((int)(rb + 1), 0u);
+        // evaluate the run's positions inside [s0, pend)
+        const int64_t pa = ra > s0 ? ra : s0, pb = rb < pend - 1 ? rb : pend - 1;
+        int k = 0;
+        for (int64_t p = pa; p <= pb; ++p) {
+          const uint32_t v = word(p);
+          const uint32_t g = v & kMask;
+          uint32_t res = FINAL ? 0u : v;
+          if (g != 0) {
+            uint32_t best = kInf;
+            if (ne > 0) {
+              uint2 ek = env[(size_t)k * 32];
+              while (k + 1 < ne) {  // advance while the next parabola is at least as low at p
+                const uint2 en = env[(size_t)(k + 1) * 32];
+                const long long i0 = (int)ek.x, i1 = (int)en.x;
+                const long long num = ((long long)en.y + i1 * i1) - ((long long)ek.y + i0 * i0), den = 2 * (i1 - i0);
+                if (num > (long long)p * den) break;
+                ek = en;
+                ++k;
+              }
+              const long long d = p - (long long)(int)ek.x;
+              const long long f = d * d + (long long)ek.y;
+              best = f < (long long)kInf ? (uint32_t)f : kInf;
+            }
+            dmax = max(dmax, best);
+            if (FINAL) {
+              res = best;
+              nfg += 1;
+              nosite |= best >= kInf;
+            } else {
+              res = best | (v & (kBitY | kBitZ));
+            }
+          }
+          a.out[base + (p - a.p_lo) * astride] = res;
+        }
+      }
+    }
+    dmax = __reduce_max_sync(kFull, dmax);
+    if (!FINAL) {
+      if (lane == 0 && dmax) atomicMax(&hdr->dxymax, dmax);
+    } else {
+      nfg = __reduce_add_sync(kFull, nfg);
+      nosite = __any_sync(kFull, nosite);
+      if (lane == 0) {
+        if (dmax) atomicMax(&hdr->dmax, dmax);
+        if (nfg) atomicAdd(&hdr->n_fg, (unsigned long long)nfg);
+        if (nosite) atomicOr(&hdr->status, kStNoSite);
+      }
+    }
+  }
+}
+
 // ---- 16-bit two-sided column pass (the default) -------------------------------------------
 // Same exact windowed scan, restated so that one SIMD instruction advances both sides:
 //  * a site met on the way is folded into the staged values: scanning up from p, element q is
@@ -492,6 +625,10 @@ __global__ void __launch_bounds__(256) k_edt_col(ColArgs a, const uint32_t* __re
 // itself and the exact 32-bit kernel above recomputes it (`sat_n` / `listed`).  Below kCap16
 // the result is exact: the winning term involves an unclamped value (K2/K3).
 constexpr uint32_t kCap16 = 16383u;
+// a scan longer than this leaves its element to the envelope pass (its CTA is listed); shorter
+// scans beyond the staged window read L2 per element (C4: a few elements of prolate grains;
+// deferring them costs a whole-CTA envelope pass, edt_y 4.52 -> 5.34 ms)
+constexpr int kDeferReach = 128;
 
 // PP = 2 (the default): each thread scans two consecutive positions i, i+1 of its column at once.
 // The halves of the SIMD pairs are the two positions: up pair (up(i+dq), up(i+1+dq)) and down
@@ -629,8 +766,12 @@ __global__ void __launch_bounds__(256) k_edt_col16(ColArgs a, uint32_t* __restri
           best0 = m2 & 0xFFFFu;
           best1 = m2 >> 16;
         } else {  // exact, 32-bit
-          if (g0) best0 = scan_global(in, base, astride, s0 + j, L, v0, chbit, a.border, a.gofs, a.Lg);
-          if (g1) best1 = scan_global(in, base, astride, s0 + j + 1, L, v1, chbit, a.border, a.gofs, a.Lg);
+          if (a.defer && reach > kDeferReach) {  // the exact envelope pass recomputes this CTA (O(1) per element)
+            best0 = best1 = kCap16;
+          } else {
+            if (g0) best0 = scan_global(in, base, astride, s0 + j, L, v0, chbit, a.border, a.gofs, a.Lg);
+            if (g1) best1 = scan_global(in, base, astride, s0 + j + 1, L, v1, chbit, a.border, a.gofs, a.Lg);
+          }
         }
       }
       const uint32_t r0 = finish(v0, best0), r1 = finish(v1, best1);
@@ -680,7 +821,8 @@ __global__ void __launch_bounds__(256) k_edt_col16(ColArgs a, uint32_t* __restri
           }
           best = bmin2 & 0xFFFFu;
         } else {
-          best = scan_global(in, base, astride, s0 + j, L, v, chbit, a.border, a.gofs, a.Lg);  // exact, 32-bit
+          best = (a.defer && reach > kDeferReach) ? kCap16
+                                                  : scan_global(in, base, astride, s0 + j, L, v, chbit, a.border, a.gofs, a.Lg);
         }
         sat |= best >= kCap16;  // clamped, or no site at all (ENOSITE comes from the 32-bit kernel)
         dmax = max(dmax, best);
@@ -697,6 +839,7 @@ __global__ void __launch_bounds__(256) k_edt_col16(ColArgs a, uint32_t* __restri
     }
   }
   // a CTA that saw a saturated value is recomputed by the 32-bit kernel (its statistics too)
+  if (a.defer == 2) sat = 1;
   if (__syncthreads_or(sat)) {
     if (threadIdx.x == 0) satlist[atomicAdd(&hdr->sat_n, 1u)] = blockIdx.x;
     return;
@@ -768,7 +911,7 @@ int64_t col_blocks(const Geom& g) {
 // (satlist NULL: the 32-bit kernel everywhere).
 void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, bool final_pass, bool border,
                     WsHeader* hdr, uint32_t* satlist, cudaStream_t st, int64_t p_lo, int64_t p_hi, int64_t gofs,
-                    int64_t Lg) {
+                    int64_t Lg, void* scratch, size_t scratch_bytes) {
   ColArgs a{};
   a.in = in;
   a.out = out;
@@ -813,6 +956,22 @@ void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, 
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cudaMemsetAsync(&hdr->sat_n, 0, sizeof(uint32_t), st);
   const unsigned fix_grid = (unsigned)(nsm * 2);
+  // the envelope fix-up: one warp per listed CTA, a (L + 2)-entry stack per lane in the scratch
+  const size_t per_slot = (size_t)32 * (size_t)(a.L + 2) * sizeof(uint2);
+  int64_t nslots = scratch ? (int64_t)(scratch_bytes / per_slot) : 0;
+  if (nslots > (int64_t)nsm * 16) nslots = (int64_t)nsm * 16;
+  if (nslots > 0 && !getenv("FASTRS_COL_WINDOWED")) {
+    a.defer = getenv("FASTRS_COL_FH_ALL") ? 2 : 1;  // 2 (test hook): every CTA takes the envelope pass
+    const unsigned fh_grid = (unsigned)((nslots + 7) / 8);
+    if (final_pass) {
+      k_edt_col16<true, kScan16U, kColPP><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, satlist, hdr);
+      k_edt_col_fh<true><<<fh_grid, 256, 0, st>>>(a, satlist, hdr, (uint2*)scratch, (int)nslots);
+    } else {
+      k_edt_col16<false, kScan16U, kColPP><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, satlist, hdr);
+      k_edt_col_fh<false><<<fh_grid, 256, 0, st>>>(a, satlist, hdr, (uint2*)scratch, (int)nslots);
+    }
+    return;
+  }
   if (final_pass) {
     k_edt_col16<true, kScan16U, kColPP><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, satlist, hdr);
     k_edt_col<true><<<fix_grid, kColWarps * 32, 0, st>>>(a, satlist, hdr);

@@ -118,6 +118,58 @@ def test_k1_segment_form(F, shape, border):
         np.testing.assert_array_equal(got, warp_form)
 
 
+@pytest.mark.parametrize("border", [1, 0])
+@pytest.mark.parametrize("seed", range(12))
+def test_envelope_column_pass(F, seed, border):
+    """The exact lower-envelope column pass (K2/K3 fix-up for the CTAs the 16-bit scan cannot
+    finish) forced on EVERY CTA (FASTRS_COL_FH_ALL): D element by element against the oracle on
+    random touching-label grids, ragged sizes, both border modes, short and long runs."""
+    rng = np.random.default_rng(1000 + seed)
+    shape = tuple(int(v) for v in rng.integers(3, 60, 3)) if seed % 2 else tuple(int(v) for v in rng.integers(3, 300, 2))
+    lab = synth.random_labels(shape, nlabels=int(rng.integers(1, 6)), seed=seed, fill=float(rng.uniform(0.3, 0.95)),
+                              blob=int(rng.integers(1, 12)))
+    lab.flat[0] = 0
+    if lab.max() == 0:
+        lab.flat[1] = 1
+    try:
+        want = oracle.edt_sq(lab, flags=border)
+    except oracle.OracleError as e:
+        assert e.code == 2
+        return
+    t = _dev(lab)
+    os.environ["FASTRS_COL_FH_ALL"] = "1"
+    try:
+        got = _u32(F.edt_sq(t, flags=border))
+        lt2 = _u32(F.local_thickness(t, flags=border))
+    finally:
+        del os.environ["FASTRS_COL_FH_ALL"]
+    np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(lt2, _u32(F.local_thickness(t, flags=border)))
+
+
+def test_envelope_column_pass_large_objects(F):
+    """Objects far wider than the staged window (radius 95 sphere, a 150 x 60 ellipse and
+    touching neighbours): the envelope pass against scipy's EDT, and against the windowed 32-bit
+    scan (FASTRS_COL_WINDOWED) bit for bit."""
+    import scipy.ndimage
+    lab = synth.sphere(95, canvas=200)
+    lab[150:, :, :] = np.where(lab[150:, :, :] > 0, 2, 0)  # cut the cap off as a touching label
+    yy, xx = np.ogrid[:400, :700]
+    ell = (((yy - 200) / 150.0) ** 2 + ((xx - 350) / 330.0) ** 2 <= 1).astype(np.int32)
+    for img in (lab, ell):
+        t = _dev(img)
+        got = _u32(F.edt_sq(t))
+        os.environ["FASTRS_COL_WINDOWED"] = "1"
+        try:
+            win = _u32(F.edt_sq(t))
+        finally:
+            del os.environ["FASTRS_COL_WINDOWED"]
+        np.testing.assert_array_equal(got, win)
+        if img.max() == 1:
+            ref = np.rint(scipy.ndimage.distance_transform_edt(np.pad(img > 0, 1)) ** 2).astype(np.uint32)
+            np.testing.assert_array_equal(got, ref[(slice(1, -1),) * img.ndim])
+
+
 @pytest.mark.parametrize("shape", [(1, 1), (1, 77), (77, 1), (2, 3, 1), (1, 1, 1), (9, 1, 40), (33, 65),
                                    (17, 9, 33), (8, 8, 32), (8, 64, 64), (3, 16384)])
 def test_ragged_and_degenerate_shapes(F, shape):
@@ -170,6 +222,51 @@ def test_large_balls_beyond_table_and_halo(F):
         got = F.sphericity_roundness(t, max_label=1, stats=True)
         assert got["roundness"][0].item() == 1.0
         assert int(got["volume"][0]) == int((lab > 0).sum())
+
+
+def test_big_bucket_scatter_rounds(F):
+    """Large objects (radii 32-50, Dmax > 1536): thousands of nearly tangent kept balls of similar D
+    reach a tile group.  The cover cut (the largest reaching ball contains the group's foreground)
+    drops them; without it (NO_COVER_CUT) one D bucket overflows the gather's shared list and its
+    sort range, and K5a writes that bucket by exact-D scatter rounds (count, prefix sum, scatter)
+    instead of handing the group to the atomic fallback.  LT^2 element by element against the fallback kernel (an independent
+    dilation: per-tile reverse sparse tables), D against scipy's EDT (labels separated by
+    background), the centre-ball closed form LT^2 = r^2 + 1 in the core of the big sphere, and the
+    per-label outputs of both paths."""
+    import scipy.ndimage
+    Z, Y, X = 224, 160, 160
+    z, y, x = np.ogrid[:Z, :Y, :X]
+    lab = np.zeros((Z, Y, X), np.int32)
+    big = (z - 64) ** 2 + (y - 80) ** 2 + (x - 80) ** 2 <= 50 ** 2
+    small = (z - 140) ** 2 + (y - 80) ** 2 + (x - 80) ** 2 <= 32 ** 2  # overlaps the big one: a dumbbell
+    lab[big | small] = 1
+    other = (z - 180) ** 2 + (y - 124) ** 2 + (x - 118) ** 2 <= 34 ** 2  # 2 voxels clear of the dumbbell
+    lab[other & ~(big | small)] = 2
+    lab[(z - 190) ** 2 + (y - 40) ** 2 + (x - 40) ** 2 <= 12 ** 2] = 3
+    t = _dev(lab)
+    ref = np.rint(scipy.ndimage.distance_transform_edt(np.pad(lab > 0, 1)) ** 2).astype(np.uint32)[1:-1, 1:-1, 1:-1]
+    sep = scipy.ndimage.binary_dilation(lab == 2) & (lab == 1)
+    assert not sep.any()  # label 2 does not touch label 1: the binary EDT is the label-aware one
+    np.testing.assert_array_equal(_u32(F.edt_sq(t)), ref)
+    lt2 = _u32(F.local_thickness(t))
+    d = F.diagnostics(F.last_workspace())
+    assert d["n_fallback"] == 0, d
+    # without the cover cut every reaching ball is listed: one D bucket overflows -> scatter rounds
+    lt2_long = _u32(F.local_thickness(t, flags=1 | F.NO_COVER_CUT))
+    d_long = F.diagnostics(F.last_workspace())
+    assert d_long["n_fallback"] == 0 and d_long["n_rounds_extra"] > 0, d_long
+    assert d_long["sum_group_list"] > d["sum_group_list"], (d_long, d)
+    lt2_fb = _u32(F.local_thickness(t, flags=1 | F.FORCE_FALLBACK))
+    np.testing.assert_array_equal(lt2, lt2_fb)
+    np.testing.assert_array_equal(lt2_long, lt2_fb)
+    core = (z - 64) ** 2 + (y - 80) ** 2 + (x - 80) ** 2 <= 20 ** 2
+    assert (lt2[core & (lab == 1)] == 50 * 50 + 1).all()
+    fg = lab > 0
+    assert (lt2[fg] >= ref[fg]).all() and (lt2[~fg] == 0).all()
+    got = F.sphericity_roundness(t, max_label=3, stats=True)
+    want = F.sphericity_roundness(t, max_label=3, stats=True, flags=1 | F.FORCE_FALLBACK)
+    for k in ("volume", "n_shell", "max_lt2", "sphericity", "roundness", "mean_lt", "shell_mean_lt"):
+        assert torch.equal(got[k], want[k]), k
 
 
 def test_empty_and_single_element_objects(F):

@@ -19,6 +19,7 @@ p = argparse.ArgumentParser()
 p.add_argument("--n", type=int, default=512)
 p.add_argument("--radii", type=int, nargs="+", default=[20, 40, 80, 160, 240])
 p.add_argument("--iters", type=int, default=3)
+p.add_argument("--flags", type=int, default=1)
 a = p.parse_args()
 for r in a.radii:
     n = a.n
@@ -37,17 +38,18 @@ for r in a.radii:
                        (zz[sl[2]] - c[2])[None, None, :] ** 2) <= r * r
                 t[sl[0], sl[1], sl[2]][sub] = lab
     fill = float((t != 0).float().mean())
-    F.sphericity_roundness(t, max_label=lab)
+    F.sphericity_roundness(t, max_label=lab, flags=a.flags)
     torch.cuda.synchronize()
     F.profile(True)
     for _ in range(a.iters):
-        F.sphericity_roundness(t, max_label=lab)
+        F.sphericity_roundness(t, max_label=lab, flags=a.flags)
     acc, calls = F.profile_read()
     ms = {kk: v / max(calls, 1) for kk, v in acc.items()}
     F.profile(False)
     tot = sum(ms.values())
+    diag = F.diagnostics(F.last_workspace())
     print(json.dumps({"n": n, "radius": r, "objects": lab, "fill": round(fill, 3), "ms_total": round(tot, 3),
-                      "gvox_s": round(n ** 3 / tot / 1e6, 2), "stages_ms": {kk: round(v, 3) for kk, v in ms.items()}}),
-          flush=True)
+                      "gvox_s": round(n ** 3 / tot / 1e6, 2), "stages_ms": {kk: round(v, 3) for kk, v in ms.items()},
+                      "diagnostics": diag}), flush=True)
     del t
     torch.cuda.empty_cache()
