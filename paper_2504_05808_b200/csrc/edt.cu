@@ -637,7 +637,10 @@ constexpr int kDeferReach = 128;
 // loads, 2 PRMT, 2 VIADDMNMX and the dq^2 step, against 2 loads, 1 PRMT, 1 VIADDMNMX and the step
 // per element for PP = 1.  A background position enters with best = 0 and never extends the scan.
 template <bool FINAL, int U, int PP>
-__global__ void __launch_bounds__(256) k_edt_col16(ColArgs a, uint32_t* __restrict__ satlist,
+#ifndef FASTRS_COL_MINB
+#define FASTRS_COL_MINB 1
+#endif
+__global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, uint32_t* __restrict__ satlist,
                                                    WsHeader* __restrict__ hdr) {
   __shared__ uint32_t tile[kColRows * 32];
   const uint32_t* __restrict__ in = a.in;
@@ -723,10 +726,20 @@ __global__ void __launch_bounds__(256) k_edt_col16(ColArgs a, uint32_t* __restri
       }
       return res;
     };
+#ifdef FASTRS_COL_PREFETCH
+    uint32_t n0 = (xin && 2 * warp < np) ? __ldg(src2) : 0u;
+    uint32_t n1 = (xin && 2 * warp + 1 < np) ? __ldg(src2 + astride) : 0u;
+#endif
     for (int j = 2 * warp; j < np; j += 2 * kColWarps) {
       const bool has1 = j + 1 < np;
+#ifdef FASTRS_COL_PREFETCH
+      const uint32_t v0 = n0, v1 = n1;
+      if (xin && j + 2 * kColWarps < np) n0 = __ldg(src2 + step2);
+      if (xin && j + 2 * kColWarps + 1 < np) n1 = __ldg(src2 + step2 + astride);
+#else
       const uint32_t v0 = xin ? __ldg(src2) : 0u;
       const uint32_t v1 = (xin && has1) ? __ldg(src2 + astride) : 0u;
+#endif
       const uint32_t g0 = v0 & kMask, g1 = v1 & kMask;
       uint32_t best0 = 0, best1 = 0;
       if ((g0 | g1) != 0) {
