@@ -637,8 +637,14 @@ constexpr int kDeferReach = 128;
 // loads, 2 PRMT, 2 VIADDMNMX and the dq^2 step, against 2 loads, 1 PRMT, 1 VIADDMNMX and the step
 // per element for PP = 1.  A background position enters with best = 0 and never extends the scan.
 template <bool FINAL, int U, int PP>
+// C4 sweep (round 2b): MINB 5 + prefetch: edt_y 4.41 / edt_z 4.24 ms; MINB 5 alone 4.53 / 4.52;
+// MINB 4 (+ prefetch) 5.22 / 5.14 (4.81 / 4.72); no bound (62 registers) 4.56 / 4.50.  Five CTAs
+// (45 KB of shared memory each) fill the SM's 228 KB.
 #ifndef FASTRS_COL_MINB
-#define FASTRS_COL_MINB 1
+#define FASTRS_COL_MINB 5
+#endif
+#ifndef FASTRS_COL_NO_PREFETCH
+#define FASTRS_COL_PREFETCH
 #endif
 __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, uint32_t* __restrict__ satlist,
                                                    WsHeader* __restrict__ hdr) {
