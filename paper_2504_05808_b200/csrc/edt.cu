@@ -130,7 +130,7 @@ constexpr int kSegFar = 1 << 20;  // "no boundary on this side" (|distance| stay
 __device__ __forceinline__ int swz(int G) { return G ^ ((G >> 3) & 7); }  // 16-byte granule swizzle
 
 #ifndef FASTRS_K1_MINB
-#define FASTRS_K1_MINB 4
+#define FASTRS_K1_MINB 5
 #endif
 __global__ void __launch_bounds__(256, FASTRS_K1_MINB) k_edt_x_seg(const int32_t* __restrict__ lab,
                                                    const int32_t* __restrict__ below, const int32_t* __restrict__ sent,
