@@ -296,7 +296,7 @@ constexpr int kScan16U = FASTRS_SCAN_U;  // row pairs per iteration of the 16-bi
 #ifndef FASTRS_COL_PP
 #define FASTRS_COL_PP 2
 #endif
-constexpr int kColPP = FASTRS_COL_PP;  // positions per thread of the 16-bit column scan (1 or 2)
+constexpr int kColPP = FASTRS_COL_PP;  // positions per thread of the 16-bit column scan (1, 2 or 4)
 
 // Slow path of the column scan for an element whose window leaves the staged rows: the same
 // exact scan in 32-bit arithmetic, every read from global memory (L2).
@@ -714,7 +714,86 @@ __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, u
   const int64_t step = (int64_t)kColWarps * astride;
   const uint32_t* src = in + base + (s0 + warp) * astride;
   uint32_t* dst = a.out + base + (s0 + warp - a.p_lo) * astride;
-  if constexpr (PP == 2) {
+  if constexpr (PP == 4) {
+    // four consecutive positions i..i+3 per thread: SIMD pairs A = (i, i+1), B = (i+2, i+3) per
+    // side; per dq one new staged row per side (sliding windows of four rows), 4 PRMT and 4
+    // VIADDMNMX for four elements (PP = 2: 2 and 2 for two)
+    const int64_t step4 = (int64_t)(4 * kColWarps) * astride;
+    const uint32_t* src4 = in + base + (s0 + 4 * warp) * astride;
+    uint32_t* dst4 = a.out + base + (s0 + 4 * warp - a.p_lo) * astride;
+    auto finish = [&](uint32_t v, uint32_t best) -> uint32_t {
+      uint32_t res = FINAL ? 0u : v;
+      if ((v & kMask) != 0) {
+        sat |= best >= kCap16;
+        dmax = max(dmax, best);
+        if (FINAL) {
+          res = best;
+          nfg += 1;
+        } else {
+          res = best | (v & (kBitY | kBitZ));
+        }
+      }
+      return res;
+    };
+    for (int j = 4 * warp; j < np; j += 4 * kColWarps) {
+      uint32_t v[4], bst[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int m = 0; m < 4; ++m) v[m] = (xin && j + m < np) ? __ldg(src4 + m * astride) : 0u;
+      const uint32_t g0 = v[0] & kMask, g1 = v[1] & kMask, g2 = v[2] & kMask, g3 = v[3] & kMask;
+      if ((g0 | g1 | g2 | g3) != 0) {
+        const uint32_t gc0 = min(g0, kCap16), gc1 = min(g1, kCap16), gc2 = min(g2, kCap16), gc3 = min(g3, kCap16);
+        const int i = kColH + j;
+        const uint32_t gm = max(max(gc0, gc1), max(gc2, gc3));
+        float r;
+        asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)gm));
+        const int reach = (int)r + 1;
+        if (reach + U - 1 <= min(i, kColRows - 4 - i)) {
+          uint32_t buA = gc0 | (gc1 << 16), buB = gc2 | (gc3 << 16), bdA = buA, bdB = buB;
+          uint32_t bmax2 = gm * 0x00010001u;
+          uint32_t dq2p = 0x00010001u, incp = 0x00030003u;
+          const uint32_t* t = tile + i * 32 + lane;  // row i
+          uint32_t u0 = t[32], u1 = t[64], u2 = t[96];  // up window: rows i+dq .. i+2+dq (dq = 1)
+          uint32_t d1 = t[0], d2 = t[32], d3 = t[64];   // down window: rows i+1-dq .. i+3-dq
+          const uint32_t* up = t + 128;                  // row i+4 (= i+3+dq at dq = 1)
+          const uint32_t* dn = t - 32;                   // row i-1 (= i-dq)
+          while (dq2p < bmax2) {
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {
+              const uint32_t u3 = up[32 * uu];   // row i+3+dq
+              const uint32_t d0 = dn[-32 * uu];  // row i-dq
+              buA = __viaddmin_u16x2(__byte_perm(u0, u1, 0x5410), dq2p, buA);
+              buB = __viaddmin_u16x2(__byte_perm(u2, u3, 0x5410), dq2p, buB);
+              bdA = __viaddmin_u16x2(__byte_perm(d0, d1, 0x7632), dq2p, bdA);
+              bdB = __viaddmin_u16x2(__byte_perm(d2, d3, 0x7632), dq2p, bdB);
+              dq2p += incp;
+              incp += 0x00020002u;
+              u0 = u1, u1 = u2, u2 = u3;
+              d3 = d2, d2 = d1, d1 = d0;
+            }
+            up += 32 * U;
+            dn -= 32 * U;
+            const uint32_t mA = __vminu2(buA, bdA), mB = __vminu2(buB, bdB), mm = __vmaxu2(mA, mB);
+            bmax2 = __vmaxu2(mm, __byte_perm(mm, 0, 0x1032));
+          }
+          const uint32_t mA = __vminu2(buA, bdA), mB = __vminu2(buB, bdB);
+          bst[0] = mA & 0xFFFFu, bst[1] = mA >> 16, bst[2] = mB & 0xFFFFu, bst[3] = mB >> 16;
+        } else if (a.defer && reach > kDeferReach) {  // the exact envelope pass recomputes this CTA
+          bst[0] = bst[1] = bst[2] = bst[3] = kCap16;
+        } else {  // exact, 32-bit
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+            if (v[m] & kMask) bst[m] = scan_global(in, base, astride, s0 + j + m, L, v[m], chbit, a.border, a.gofs, a.Lg);
+        }
+      }
+      if (xin) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          if (j + m < np) dst4[m * astride] = finish(v[m], bst[m]);
+      }
+      src4 += step4;
+      dst4 += step4;
+    }
+  } else if constexpr (PP == 2) {
     const int64_t step2 = (int64_t)(2 * kColWarps) * astride;
     const uint32_t* src2 = in + base + (s0 + 2 * warp) * astride;
     uint32_t* dst2 = a.out + base + (s0 + 2 * warp - a.p_lo) * astride;
