@@ -294,9 +294,11 @@ constexpr int kColWarps = 8;
 #endif
 constexpr int kScan16U = FASTRS_SCAN_U;  // row pairs per iteration of the 16-bit two-sided scan loop
 #ifndef FASTRS_COL_PP
-#define FASTRS_COL_PP 2
+#define FASTRS_COL_PP 4
 #endif
-constexpr int kColPP = FASTRS_COL_PP;  // positions per thread of the 16-bit column scan (1, 2 or 4)
+// positions per thread of the 16-bit column scan (1, 2 or 4).  C4 (round 2b): PP 2 4.41 / 4.24 ms
+// (y / z), PP 4 4.12 / 4.08 (U = 2: 4.19 / 4.15; 4 CTAs/SM: 4.66 / 4.62)
+constexpr int kColPP = FASTRS_COL_PP;
 
 // Slow path of the column scan for an element whose window leaves the staged rows: the same
 // exact scan in 32-bit arithmetic, every read from global memory (L2).
