@@ -87,12 +87,19 @@ struct Smem {  // K5a (gather + sort)
 #define FASTRS_PAINT_MINB 14
 #endif
 constexpr int kPaintNW = 2, kPaintMinB = FASTRS_PAINT_MINB;
+// x chunks of the uncovered-row masks the K5b screen intersects with a ball's x-extent (4 chunks of
+// 8 columns or 8 of 4)
+#ifndef FASTRS_UC_CHUNKS
+#define FASTRS_UC_CHUNKS 4
+#endif
+constexpr int kUcChunks = FASTRS_UC_CHUNKS, kUcW = 32 / kUcChunks;
+constexpr uint32_t kUcBits = (1u << kUcW) - 1u;
 template <int NW, bool FUSED>
 struct PaintSmem {  // K5b (one tile per warp)
   uint16_t val[NW][FUSED ? 1 : kRows * 32];  // LT^2 per element of each warp's tile (D <= 65535 here)
   int4 sball[NW][32];             // survivors of a screened batch: centre (tile coords), D
   unsigned long long scand[NW][32];  // their candidate rows
-  alignas(16) unsigned long long uc[NW][4];  // rows with uncovered foreground per 8-column chunk of x
+  alignas(16) unsigned long long uc[NW][kUcChunks];  // rows with uncovered foreground per x chunk
   uint16_t ulist[NW][kPoint];     // point mode: the still-uncovered cells (row*32 + x)
   uint2 pcell[NW][kPoint];        // the same cells for the dot-product test: (2x, 2y, 2z) bytes, -|p|^2
   uint32_t qa[NW][32];            // fused: covering events, (cell offset | count << 16)
@@ -958,9 +965,9 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
   // of eight registers the paint loop would push to local memory)
   unsigned long long* Uc = S.uc[wl];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const unsigned long long m = (unsigned long long)__ballot_sync(kFull, (f0 >> (8 * c)) & 0xFFu) |
-                                 ((unsigned long long)__ballot_sync(kFull, (f1 >> (8 * c)) & 0xFFu) << 32);
+  for (int c = 0; c < kUcChunks; ++c) {
+    const unsigned long long m = (unsigned long long)__ballot_sync(kFull, (f0 >> (kUcW * c)) & kUcBits) |
+                                 ((unsigned long long)__ballot_sync(kFull, (f1 >> (kUcW * c)) & kUcBits) << 32);
     if (lane == 0) Uc[c] = m;
   }
   __syncwarp();
@@ -1196,11 +1203,12 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
           const int hz = IS3D ? isqrt16(R2 - gx2 - gy2) : 0;
           const int xa = max(cx - hx, ub[0]), xb = min(cx + hx, ub[1]);
           unsigned long long ux = 0;  // rows with uncovered foreground inside the ball's x-extent
-          const ulonglong2 ua = reinterpret_cast<const ulonglong2*>(Uc)[0], ub2 = reinterpret_cast<const ulonglong2*>(Uc)[1];
-          const unsigned long long uc4[4] = {ua.x, ua.y, ub2.x, ub2.y};
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (xa <= 8 * c + 7 && xb >= 8 * c) ux |= uc4[c];
+          for (int c2 = 0; c2 < kUcChunks / 2; ++c2) {
+            const ulonglong2 ua = reinterpret_cast<const ulonglong2*>(Uc)[c2];
+            if (xa <= kUcW * (2 * c2) + kUcW - 1 && xb >= kUcW * (2 * c2)) ux |= ua.x;
+            if (xa <= kUcW * (2 * c2 + 1) + kUcW - 1 && xb >= kUcW * (2 * c2 + 1)) ux |= ua.y;
+          }
           cand = row_box<IS3D>(max(cy - hy, ub[2]), min(cy + hy, ub[3]), max(cz - hz, ub[4]), min(cz + hz, ub[5])) & ux;
         }
       }
@@ -1354,9 +1362,9 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
         dirty = false;
         const uint32_t left[2] = {f0 & ~c0, f1 & ~c1};
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const unsigned long long m = (unsigned long long)__ballot_sync(kFull, (left[0] >> (8 * c)) & 0xFFu) |
-                                       ((unsigned long long)__ballot_sync(kFull, (left[1] >> (8 * c)) & 0xFFu) << 32);
+        for (int c = 0; c < kUcChunks; ++c) {
+          const unsigned long long m = (unsigned long long)__ballot_sync(kFull, (left[0] >> (kUcW * c)) & kUcBits) |
+                                       ((unsigned long long)__ballot_sync(kFull, (left[1] >> (kUcW * c)) & kUcBits) << 32);
           if (lane == 0) Uc[c] = m;
         }
         nu = (int)__reduce_add_sync(kFull, (uint32_t)(__popc(left[0]) + __popc(left[1])));

@@ -737,10 +737,23 @@ __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, u
       }
       return res;
     };
+#ifdef FASTRS_COL_PREFETCH4
+    uint32_t nx4[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) nx4[m] = (xin && 4 * warp + m < np) ? __ldg(src4 + m * astride) : 0u;
+#endif
     for (int j = 4 * warp; j < np; j += 4 * kColWarps) {
       uint32_t v[4], bst[4] = {0u, 0u, 0u, 0u};
+#ifdef FASTRS_COL_PREFETCH4
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        v[m] = nx4[m];
+        nx4[m] = (xin && j + 4 * kColWarps + m < np) ? __ldg(src4 + step4 + m * astride) : 0u;
+      }
+#else
 #pragma unroll
       for (int m = 0; m < 4; ++m) v[m] = (xin && j + m < np) ? __ldg(src4 + m * astride) : 0u;
+#endif
       const uint32_t g0 = v[0] & kMask, g1 = v[1] & kMask, g2 = v[2] & kMask, g3 = v[3] & kMask;
       if ((g0 | g1 | g2 | g3) != 0) {
         const uint32_t gc0 = min(g0, kCap16), gc1 = min(g1, kCap16), gc2 = min(g2, kCap16), gc3 = min(g3, kCap16);
