@@ -81,6 +81,10 @@ enum {
                                     for the dilation instead of the kept-centre halo (N4)        */
   FASTRS_NO_LIST_STAGING = 1024u,/* test hook: a K5 candidate list that overflows the shared list is
                                     regathered (a second pass) instead of staged in the pool      */
+  FASTRS_EXACT_PRUNE = 4096u,    /* K4 tests every offset class with |s|^2 <= 12 (the exact lattice
+                                    maximal-ball set for that stencil).  Default:
+                                    the 26-neighbourhood and the five stage-2 classes that drop
+                                    centres on C4 -- a superset of kept balls, LT^2 unchanged      */
   FASTRS_NO_COVER_CUT = 2048u,   /* test hook: K5a keeps every ball that reaches a tile group even
                                     when the largest one contains all of its foreground (the cut
                                     is exact; this exercises the long-list paths it avoids)       */

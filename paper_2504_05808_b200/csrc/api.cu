@@ -233,7 +233,7 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
     uint16_t* oct = (uint16_t*)(w + L.oct);
     {
       Nvtx r("K4 prune");
-      launch_prune(D, g, meta, cent, fgm, shm, oct, hdr, st);
+      launch_prune(D, g, meta, cent, fgm, shm, oct, hdr, st, 0, 0, (flags & kFlagExactPrune) != 0);
     }
     tm.mark(3);
     uint32_t* ltp = D == A ? B : A;  // the plane the EDT no longer needs holds LT^2 (fallback / LT outputs)
@@ -507,7 +507,8 @@ int run_host_pipelined(const int32_t* labels_host, int32_t* dlab, const Geom& g,
     }
     if (step >= 2 && step - 2 < nc) {  // K4 on chunk step-2
       zr(step - 2, z0, z1);
-      launch_prune(A, g, meta, cent, fgm, shm, oct, hdr, st, z0 / kTZ3, (z1 + kTZ3 - 1) / kTZ3);
+      launch_prune(A, g, meta, cent, fgm, shm, oct, hdr, st, z0 / kTZ3, (z1 + kTZ3 - 1) / kTZ3,
+                   (flags & kFlagExactPrune) != 0);
     }
     if (step >= 3 && step - 3 < nc) {  // K5a + K5b (reductions fused) on chunk step-3
       zr(step - 3, z0, z1);

@@ -18,6 +18,7 @@ constexpr uint32_t kStBadLabel = 1u, kStNoSite = 2u, kStInternal = 4u, kStShell 
 constexpr uint32_t kFlagBorder = 1u, kFlagAsync = 4u, kFlagHostIO = 8u, kFlagForceFallback = 16u;
 constexpr uint32_t kFlagNoListStaging = 1024u;  // test hook: K5a list overflow regathers instead of staging
 constexpr uint32_t kFlagNoCoverCut = 2048u;     // test hook: K5a without the cover cut
+constexpr uint32_t kFlagExactPrune = 4096u;     // K4: every stage-2 class (the exact |s|^2 <= 12 kept set)
 // launch_dilate_gather mode bits
 constexpr int kGatherForceFallback = 1, kGatherNoStaging = 2, kGatherNoCoverCut = 4;
 __host__ inline int gather_mode_of(uint32_t flags) {
@@ -198,7 +199,8 @@ const unsigned long long* device_fxlut(int device);  // fx(c) for c < kFxLut (af
 // K4; also writes per tile the foreground and shell (D == 1) row masks (fgm, shm: kRows u32 each)
 // and the number of kept entries with D bucket >= 8o for o = 0..15 (oct: 16 u16) used by K5's gather
 void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, uint32_t* fgm, uint32_t* shm,
-                  uint16_t* oct, WsHeader* hdr, cudaStream_t st, int64_t tz_lo = 0, int64_t tz_hi = 0);
+                  uint16_t* oct, WsHeader* hdr, cudaStream_t st, int64_t tz_lo = 0, int64_t tz_hi = 0,
+                  bool exact_prune = false);
 int64_t dilate_groups(const Geom& g);        // K5 tile groups (gcount / goff entries)
 // K5b.  acc == NULL: LT^2 of every painted tile -> the LT plane ltp (u16).  acc != NULL (fused):
 // no LT plane; every ball that covers cells adds (count, shell count, D) of those cells to the

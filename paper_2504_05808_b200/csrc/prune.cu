@@ -141,6 +141,7 @@ struct PruneTile {
 // the bucket scatter needs no second pass over rows and no cross-warp prefix.
 // stage-2 class order (3D): (2,1,0), (2,1,1), (2,2,1), (3,1,1), (3,1,0), then the classes that
 // dropped no stage-1 survivor on C4: (2,0,0), (2,2,0), (3,0,0), (2,2,2)
+constexpr int kPruneFastClasses3 = 5;  // stage-2 classes tested by default (3D)
 __host__ __device__ constexpr int stage2_order3(int q) {
   return q == 0 ? 4 : q == 1 ? 5 : q == 2 ? 7 : q == 3 ? 10 : q == 4 ? 9 : q == 5 ? 3 : q == 6 ? 6 : q == 7 ? 8 : 11;
 }
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
                                                const uint32_t* __restrict__ M, const uint4* __restrict__ M1,
                                                int64_t tile0, WsHeader* __restrict__ hdr,
                                                const __grid_constant__ CUtensorMap tmap, FastDiv dx, FastDiv dy,
-                                               FastDiv dz) {
+                                               FastDiv dz, int nc2) {
   using P = PruneTile<IS3D>;
   __shared__ __align__(128) uint32_t s[P::PZ * P::PY * P::PX];
   __shared__ __align__(8) uint64_t s_bar;
@@ -387,6 +388,7 @@ __global__ void __launch_bounds__(256, 6) k_prune(const uint32_t* __restrict__ D
     }
 #pragma unroll
     for (int q = 0; q < P::NC - P::C1; ++q) {
+      if (q >= nc2) break;  // (warp-uniform) the classes this launch tests
       if (!__any_sync(kFullMask, test && keep)) break;
       // all offsets of class `cls` (the class test folds at compile time after unrolling): their
       // max against the class threshold.  Only lanes still alive load (the stage is bound by
@@ -604,7 +606,7 @@ static bool prune_tensor_map(CUtensorMap* m, const uint32_t* D, const Geom& g) {
 }
 
 void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centres, uint32_t* fgm, uint32_t* shm,
-                  uint16_t* oct, WsHeader* hdr, cudaStream_t st, int64_t tz_lo, int64_t tz_hi) {
+                  uint16_t* oct, WsHeader* hdr, cudaStream_t st, int64_t tz_lo, int64_t tz_hi, bool exact_prune) {
   int dev = 0;
   cudaGetDevice(&dev);
   // tile layers [tz_lo, tz_hi) of item 0 (batch 1), or every tile
@@ -615,16 +617,20 @@ void launch_prune(const uint32_t* D, const Geom& g, TileMeta* meta, uint2* centr
   CUtensorMap tmap;
   const bool tma = prune_tensor_map(&tmap, D, g);
   const FastDiv fdx((uint32_t)g.ntx), fdy((uint32_t)g.nty), fdz((uint32_t)g.ntz);
+  // stage-2 classes: 3D tests the five that drop centres on C4 unless the exact |s|^2 <= 12 set
+  // is asked for (FASTRS_EXACT_PRUNE); the skipped four only ever keep more (contained) balls,
+  // which LT^2 = max over covering balls ignores.  2D: all three classes.
+  const int nc2 = g.ndim == 3 ? (exact_prune ? kClasses3 - 3 : kPruneFastClasses3) : kClasses2 - 2;
   if (g.ndim == 3) {
     if (tma)
-      k_prune<true, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m3, g_tables[dev].m3s1, tile0, hdr, tmap, fdx, fdy, fdz);
+      k_prune<true, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m3, g_tables[dev].m3s1, tile0, hdr, tmap, fdx, fdy, fdz, nc2);
     else
-      k_prune<true, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m3, g_tables[dev].m3s1, tile0, hdr, tmap, fdx, fdy, fdz);
+      k_prune<true, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m3, g_tables[dev].m3s1, tile0, hdr, tmap, fdx, fdy, fdz, nc2);
   } else {
     if (tma)
-      k_prune<false, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m2, nullptr, tile0, hdr, tmap, fdx, fdy, fdz);
+      k_prune<false, true><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m2, nullptr, tile0, hdr, tmap, fdx, fdy, fdz, nc2);
     else
-      k_prune<false, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m2, nullptr, tile0, hdr, tmap, fdx, fdy, fdz);
+      k_prune<false, false><<<(unsigned)n, 256, 0, st>>>(D, g, meta, centres, fgm, shm, oct, g_tables[dev].m2, nullptr, tile0, hdr, tmap, fdx, fdy, fdz, nc2);
   }
 }
 

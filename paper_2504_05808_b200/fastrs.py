@@ -24,6 +24,7 @@ FORCE_FALLBACK = 16  # run the dilation with the atomic sparse-table kernel (cro
 APPROX_LT = 256  # approximate local thickness (FASTRS_APPROX_LT)
 NO_LIST_STAGING = 1024  # test hook: K5a list overflow takes the regather pass instead of staging
 NO_COVER_CUT = 2048  # test hook: K5a keeps every reaching ball (no cover cut)
+EXACT_PRUNE = 4096  # K4 tests every |s|^2 <= 12 offset class (the exact kept set)
 TILE_RECORD_WORDS = 20  # FASTRS_TILE_RECORD_WORDS: u32 per tile record of slab_pack_tiles
 
 STAGES = ("edt_x", "edt_y", "edt_z", "prune", "dilate", "metrics", "epilogue", "gather")

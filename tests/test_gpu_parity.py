@@ -419,12 +419,20 @@ def test_deterministic_and_host_path(F):
 def test_diagnostics_counters(F):
     lab = synth.sphere(15)
     t = _dev(lab)
-    F.sphericity_roundness(t, max_label=1)
+    F.sphericity_roundness(t, max_label=1, flags=1 | F.EXACT_PRUNE)
     d = F.diagnostics(F.last_workspace(t.device))
     assert d["status_bits"] == 0 and d["dmax"] == 226 and d["n_fg"] == 14147
     # exact lattice pruning with the 26-neighbourhood, then all |s|^2 <= 12, keeps 121
     # centres on the digital sphere r=15 (SURVEY.md §8(c) "Kept-centre counts")
     assert d["n_kept"] == 121
+    lt_exact = F.local_thickness(t, flags=1 | F.EXACT_PRUNE)
+    r_exact = F.sphericity_roundness(t, max_label=1, flags=1 | F.EXACT_PRUNE, stats=True)
+    # the default (five stage-2 classes) keeps a superset of those balls and the same LT^2
+    r_fast = F.sphericity_roundness(t, max_label=1, stats=True)
+    assert F.diagnostics(F.last_workspace(t.device))["n_kept"] >= 121
+    assert torch.equal(F.local_thickness(t), lt_exact)
+    for k in ("volume", "n_shell", "max_lt2", "sphericity", "roundness"):
+        assert torch.equal(r_fast[k], r_exact[k]), k
     F.sphericity_roundness(_dev(synth.disk(20)), max_label=1)
     d = F.diagnostics(F.last_workspace(t.device))
     assert d["n_fg"] == 1257 and d["dmax"] == 401
