@@ -54,7 +54,7 @@ STAGE_KERNELS = {"edt_x": ["k_edt_x_seg", "k_edt_x"], "edt_y": ["k_edt_col16<0",
                                                "k_epilogue_fallback<1"], "metrics": ["k_metrics"]}
 STAGE_KERNELS_2D = dict(STAGE_KERNELS, edt_y=["k_edt_col16<1", "k_edt_col<1", "k_edt_col_fh<1"], prune=["k_prune<0"],
                         k5=["k_dilate_gather<0", "k_dilate_paint<0", "k_dilate_atomic<0", "k_epilogue_fallback<0"])
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02d_ncu_summary_c4.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02e_ncu_summary_c4.json")
 
 
 def parse():
@@ -374,12 +374,16 @@ def run_fastrs(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-        "scaling": "strong" if shard else "weak",
+        # the N > 1 defaults split this same workload (C2-C4: z-slabs of the volume, C5: the one
+        # 256-image batch), so N = 1 is the first point of a strong-scaling curve; --mode volumes
+        # gives every rank its own volume (weak)
+        "scaling": "strong" if (shard or (world == 1 and args.mode == "auto")) else "weak",
         "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
         "config": {"workload": workload_name(args.config), "seed": info["seed"], "elements_per_gpu": int(n),
                    "fill": round(info["fill"], 4), "max_label": ml,
                    "parallelism": (f"images sharded over {world} GPUs ({b_total} total, rank 0: {images})" if shard
-                                   else f"dp{world} (independent volumes)"),
+                                   else ("single GPU (N > 1 splits this volume into z-slabs / shards the batch)"
+                                         if world == 1 and args.mode == "auto" else f"dp{world} (independent volumes)")),
                    "l2": "inputs larger than L2 (4 GiB labels + ~16 GiB workspace per step), no flush",
                    "input_sha256": info["sha256"], "input_hash_kind": info.get("sha256_kind")},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(lab.nbytes),

@@ -141,7 +141,10 @@ struct PruneTile {
 // the bucket scatter needs no second pass over rows and no cross-warp prefix.
 // stage-2 class order (3D): (2,1,0), (2,1,1), (2,2,1), (3,1,1), (3,1,0), then the classes that
 // dropped no stage-1 survivor on C4: (2,0,0), (2,2,0), (3,0,0), (2,2,2)
-constexpr int kPruneFastClasses3 = 5;  // stage-2 classes tested by default (3D)
+#ifndef FASTRS_PRUNE_FAST_CLASSES
+#define FASTRS_PRUNE_FAST_CLASSES 5
+#endif
+constexpr int kPruneFastClasses3 = FASTRS_PRUNE_FAST_CLASSES;  // stage-2 classes tested by default (3D)
 __host__ __device__ constexpr int stage2_order3(int q) {
   return q == 0 ? 4 : q == 1 ? 5 : q == 2 ? 7 : q == 3 ? 10 : q == 4 ? 9 : q == 5 ? 3 : q == 6 ? 6 : q == 7 ? 8 : 11;
 }
