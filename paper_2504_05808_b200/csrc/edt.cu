@@ -20,6 +20,7 @@
 //              hands CTAs with values >= 2^14-1 to the exact 32-bit kernel.  The final pass
 //              emits D, Dmax, n_fg and flags elements with no site (ENOSITE).
 #include <cstdlib>
+#include <type_traits>
 #include <mutex>
 
 #include "common.cuh"
@@ -737,77 +738,70 @@ __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, u
       }
       return res;
     };
-#ifdef FASTRS_COL_PREFETCH4
-    uint32_t nx4[4];
-#pragma unroll
-    for (int m = 0; m < 4; ++m) nx4[m] = (xin && 4 * warp + m < np) ? __ldg(src4 + m * astride) : 0u;
-#endif
-    for (int j = 4 * warp; j < np; j += 4 * kColWarps) {
-      uint32_t v[4], bst[4] = {0u, 0u, 0u, 0u};
-#ifdef FASTRS_COL_PREFETCH4
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        v[m] = nx4[m];
-        nx4[m] = (xin && j + 4 * kColWarps + m < np) ? __ldg(src4 + step4 + m * astride) : 0u;
-      }
-#else
-#pragma unroll
-      for (int m = 0; m < 4; ++m) v[m] = (xin && j + m < np) ? __ldg(src4 + m * astride) : 0u;
-#endif
-      const uint32_t g0 = v[0] & kMask, g1 = v[1] & kMask, g2 = v[2] & kMask, g3 = v[3] & kMask;
-      if ((g0 | g1 | g2 | g3) != 0) {
-        const uint32_t gc0 = min(g0, kCap16), gc1 = min(g1, kCap16), gc2 = min(g2, kCap16), gc3 = min(g3, kCap16);
-        const int i = kColH + j;
-        const uint32_t gm = max(max(gc0, gc1), max(gc2, gc3));
-        float r;
-        asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)gm));
-        const int reach = (int)r + 1;
-        if (reach + U - 1 <= min(i, kColRows - 4 - i)) {
-          uint32_t buA = gc0 | (gc1 << 16), buB = gc2 | (gc3 << 16), bdA = buA, bdB = buB;
-          uint32_t bmax2 = gm * 0x00010001u;
-          uint32_t dq2p = 0x00010001u, incp = 0x00030003u;
-          const uint32_t* t = tile + i * 32 + lane;  // row i
-          uint32_t u0 = t[32], u1 = t[64], u2 = t[96];  // up window: rows i+dq .. i+2+dq (dq = 1)
-          uint32_t d1 = t[0], d2 = t[32], d3 = t[64];   // down window: rows i+1-dq .. i+3-dq
-          const uint32_t* up = t + 128;                  // row i+4 (= i+3+dq at dq = 1)
-          const uint32_t* dn = t - 32;                   // row i-1 (= i-dq)
-          while (dq2p < bmax2) {
-#pragma unroll
-            for (int uu = 0; uu < U; ++uu) {
-              const uint32_t u3 = up[32 * uu];   // row i+3+dq
-              const uint32_t d0 = dn[-32 * uu];  // row i-dq
-              buA = __viaddmin_u16x2(__byte_perm(u0, u1, 0x5410), dq2p, buA);
-              buB = __viaddmin_u16x2(__byte_perm(u2, u3, 0x5410), dq2p, buB);
-              bdA = __viaddmin_u16x2(__byte_perm(d0, d1, 0x7632), dq2p, bdA);
-              bdB = __viaddmin_u16x2(__byte_perm(d2, d3, 0x7632), dq2p, bdB);
-              dq2p += incp;
-              incp += 0x00020002u;
-              u0 = u1, u1 = u2, u2 = u3;
-              d3 = d2, d2 = d1, d1 = d0;
+    // FB: a full CTA (256 positions, every lane inside the grid) drops the per-element bounds tests
+    auto run4 = [&](auto fb) {
+      constexpr bool FB = decltype(fb)::value;
+      for (int j = 4 * warp; j < np; j += 4 * kColWarps) {
+        uint32_t v[4], bst[4] = {0u, 0u, 0u, 0u};
+  #pragma unroll
+        for (int m = 0; m < 4; ++m) v[m] = (FB || (xin && j + m < np)) ? __ldg(src4 + m * astride) : 0u;
+        const uint32_t g0 = v[0] & kMask, g1 = v[1] & kMask, g2 = v[2] & kMask, g3 = v[3] & kMask;
+        if ((g0 | g1 | g2 | g3) != 0) {
+          const uint32_t gc0 = min(g0, kCap16), gc1 = min(g1, kCap16), gc2 = min(g2, kCap16), gc3 = min(g3, kCap16);
+          const int i = kColH + j;
+          const uint32_t gm = max(max(gc0, gc1), max(gc2, gc3));
+          float r;
+          asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)gm));
+          const int reach = (int)r + 1;
+          if (reach + U - 1 <= min(i, kColRows - 4 - i)) {
+            uint32_t buA = gc0 | (gc1 << 16), buB = gc2 | (gc3 << 16), bdA = buA, bdB = buB;
+            uint32_t bmax2 = gm * 0x00010001u;
+            uint32_t dq2p = 0x00010001u, incp = 0x00030003u;
+            const uint32_t* t = tile + i * 32 + lane;  // row i
+            uint32_t u0 = t[32], u1 = t[64], u2 = t[96];  // up window: rows i+dq .. i+2+dq (dq = 1)
+            uint32_t d1 = t[0], d2 = t[32], d3 = t[64];   // down window: rows i+1-dq .. i+3-dq
+            const uint32_t* up = t + 128;                  // row i+4 (= i+3+dq at dq = 1)
+            const uint32_t* dn = t - 32;                   // row i-1 (= i-dq)
+            while (dq2p < bmax2) {
+  #pragma unroll
+              for (int uu = 0; uu < U; ++uu) {
+                const uint32_t u3 = up[32 * uu];   // row i+3+dq
+                const uint32_t d0 = dn[-32 * uu];  // row i-dq
+                buA = __viaddmin_u16x2(__byte_perm(u0, u1, 0x5410), dq2p, buA);
+                buB = __viaddmin_u16x2(__byte_perm(u2, u3, 0x5410), dq2p, buB);
+                bdA = __viaddmin_u16x2(__byte_perm(d0, d1, 0x7632), dq2p, bdA);
+                bdB = __viaddmin_u16x2(__byte_perm(d2, d3, 0x7632), dq2p, bdB);
+                dq2p += incp;
+                incp += 0x00020002u;
+                u0 = u1, u1 = u2, u2 = u3;
+                d3 = d2, d2 = d1, d1 = d0;
+              }
+              up += 32 * U;
+              dn -= 32 * U;
+              const uint32_t mA = __vminu2(buA, bdA), mB = __vminu2(buB, bdB), mm = __vmaxu2(mA, mB);
+              bmax2 = __vmaxu2(mm, __byte_perm(mm, 0, 0x1032));
             }
-            up += 32 * U;
-            dn -= 32 * U;
-            const uint32_t mA = __vminu2(buA, bdA), mB = __vminu2(buB, bdB), mm = __vmaxu2(mA, mB);
-            bmax2 = __vmaxu2(mm, __byte_perm(mm, 0, 0x1032));
+            const uint32_t mA = __vminu2(buA, bdA), mB = __vminu2(buB, bdB);
+            bst[0] = mA & 0xFFFFu, bst[1] = mA >> 16, bst[2] = mB & 0xFFFFu, bst[3] = mB >> 16;
+          } else if (a.defer && reach > kDeferReach) {  // the exact envelope pass recomputes this CTA
+            bst[0] = bst[1] = bst[2] = bst[3] = kCap16;
+          } else {  // exact, 32-bit
+  #pragma unroll
+            for (int m = 0; m < 4; ++m)
+              if (v[m] & kMask) bst[m] = scan_global(in, base, astride, s0 + j + m, L, v[m], chbit, a.border, a.gofs, a.Lg);
           }
-          const uint32_t mA = __vminu2(buA, bdA), mB = __vminu2(buB, bdB);
-          bst[0] = mA & 0xFFFFu, bst[1] = mA >> 16, bst[2] = mB & 0xFFFFu, bst[3] = mB >> 16;
-        } else if (a.defer && reach > kDeferReach) {  // the exact envelope pass recomputes this CTA
-          bst[0] = bst[1] = bst[2] = bst[3] = kCap16;
-        } else {  // exact, 32-bit
-#pragma unroll
-          for (int m = 0; m < 4; ++m)
-            if (v[m] & kMask) bst[m] = scan_global(in, base, astride, s0 + j + m, L, v[m], chbit, a.border, a.gofs, a.Lg);
         }
+        if (FB || xin) {
+  #pragma unroll
+          for (int m = 0; m < 4; ++m)
+            if (FB || j + m < np) dst4[m * astride] = finish(v[m], bst[m]);
+        }
+        src4 += step4;
+        dst4 += step4;
       }
-      if (xin) {
-#pragma unroll
-        for (int m = 0; m < 4; ++m)
-          if (j + m < np) dst4[m * astride] = finish(v[m], bst[m]);
-      }
-      src4 += step4;
-      dst4 += step4;
-    }
+    };
+    if (np == kColS && (xb * 32 + 32 <= a.X)) run4(std::true_type{});
+    else run4(std::false_type{});
   } else if constexpr (PP == 2) {
     const int64_t step2 = (int64_t)(2 * kColWarps) * astride;
     const uint32_t* src2 = in + base + (s0 + 2 * warp) * astride;
