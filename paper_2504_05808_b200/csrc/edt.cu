@@ -724,26 +724,12 @@ __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, u
     const int64_t step4 = (int64_t)(4 * kColWarps) * astride;
     const uint32_t* src4 = in + base + (s0 + 4 * warp) * astride;
     uint32_t* dst4 = a.out + base + (s0 + 4 * warp - a.p_lo) * astride;
-    auto finish = [&](uint32_t v, uint32_t best) -> uint32_t {
-      uint32_t res = FINAL ? 0u : v;
-      if ((v & kMask) != 0) {
-        sat |= best >= kCap16;
-        dmax = max(dmax, best);
-        if (FINAL) {
-          res = best;
-          nfg += 1;
-        } else {
-          res = best | (v & (kBitY | kBitZ));
-        }
-      }
-      return res;
-    };
     // FB: a full CTA (256 positions, every lane inside the grid) drops the per-element bounds tests
     auto run4 = [&](auto fb) {
       constexpr bool FB = decltype(fb)::value;
       for (int j = 4 * warp; j < np; j += 4 * kColWarps) {
         uint32_t v[4], bst[4] = {0u, 0u, 0u, 0u};
-  #pragma unroll
+#pragma unroll
         for (int m = 0; m < 4; ++m) v[m] = (FB || (xin && j + m < np)) ? __ldg(src4 + m * astride) : 0u;
         const uint32_t g0 = v[0] & kMask, g1 = v[1] & kMask, g2 = v[2] & kMask, g3 = v[3] & kMask;
         if ((g0 | g1 | g2 | g3) != 0) {
@@ -763,7 +749,7 @@ __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, u
             const uint32_t* up = t + 128;                  // row i+4 (= i+3+dq at dq = 1)
             const uint32_t* dn = t - 32;                   // row i-1 (= i-dq)
             while (dq2p < bmax2) {
-  #pragma unroll
+#pragma unroll
               for (int uu = 0; uu < U; ++uu) {
                 const uint32_t u3 = up[32 * uu];   // row i+3+dq
                 const uint32_t d0 = dn[-32 * uu];  // row i-dq
@@ -786,22 +772,28 @@ __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, u
           } else if (a.defer && reach > kDeferReach) {  // the exact envelope pass recomputes this CTA
             bst[0] = bst[1] = bst[2] = bst[3] = kCap16;
           } else {  // exact, 32-bit
-  #pragma unroll
+#pragma unroll
             for (int m = 0; m < 4; ++m)
               if (v[m] & kMask) bst[m] = scan_global(in, base, astride, s0 + j + m, L, v[m], chbit, a.border, a.gofs, a.Lg);
           }
         }
+        // branch-free epilogue: a background element has best 0 and its word is just its run
+        // flags, so best | flags is right for both; `sat` is derived from dmax after the loop
         if (FB || xin) {
-  #pragma unroll
+#pragma unroll
           for (int m = 0; m < 4; ++m)
-            if (FB || j + m < np) dst4[m * astride] = finish(v[m], bst[m]);
+            if (FB || j + m < np) dst4[m * astride] = FINAL ? bst[m] : (bst[m] | (v[m] & (kBitY | kBitZ)));
         }
+        dmax = max(dmax, max(max(bst[0], bst[1]), max(bst[2], bst[3])));
+        if (FINAL) nfg += (uint32_t)((v[0] & kMask) != 0u) + (uint32_t)((v[1] & kMask) != 0u) +
+                          (uint32_t)((v[2] & kMask) != 0u) + (uint32_t)((v[3] & kMask) != 0u);
         src4 += step4;
         dst4 += step4;
       }
     };
     if (np == kColS && (xb * 32 + 32 <= a.X)) run4(std::true_type{});
     else run4(std::false_type{});
+    sat |= dmax >= kCap16;  // a clamped or deferred result (every result of this path is <= kCap16)
   } else if constexpr (PP == 2) {
     const int64_t step2 = (int64_t)(2 * kColWarps) * astride;
     const uint32_t* src2 = in + base + (s0 + 2 * warp) * astride;
@@ -914,7 +906,7 @@ __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, u
           const uint32_t* up = trow + 32;
           const uint32_t* dn = trow - 32;
           while (dq2p < bmin2) {
-  #pragma unroll
+#pragma unroll
             for (int u = 0; u < U; ++u) {
               // low half: up(p + dq), high half: down(p - dq)
               const uint32_t pr = __byte_perm(up[32 * u], dn[-32 * u], 0x7610);
