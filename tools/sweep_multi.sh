@@ -1,7 +1,7 @@
 #!/bin/bash
 # GPU call: C4 bench per compile-time configuration (edit the list).
 mkdir -p gpurun_out
-for cfg in "" "-DFASTRS_K1P_WARPS=8 -DFASTRS_K1P_MINB=3" "-DFASTRS_K1P_WARPS=4 -DFASTRS_K1P_MINB=7"; do
+for cfg in "" "-DFASTRS_COL_STATIC"; do
   FASTRS_NVCC_DEFS="$cfg" python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1 || { echo "build $cfg failed"; continue; }
   timeout 300 python bench.py --steps 8 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/sw.json 2>/dev/null
   python -c "
