@@ -127,7 +127,7 @@ typedef struct {
   uint64_t n_painted;      /* K5: balls painted row-parallel after the screens (S&R call) */
   uint64_t n_covering;     /* K5: painted balls that covered at least one cell (S&R call) */
   uint32_t n_staged;       /* K5: list overflows staged in the candidate pool (one pass)   */
-  uint32_t reserved;
+  uint32_t n_deferred;     /* K5: tile groups a full candidate pool deferred to a later wave */
 } fastrs_diagnostics;
 
 /* Bytes of device workspace needed by every entry point below for this geometry.

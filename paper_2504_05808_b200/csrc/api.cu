@@ -68,7 +68,8 @@ int make_geom(const int64_t* dims, int ndim, int64_t batch, Geom& g) {
 inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t hdr, A, B, meta, fgm, shm, oct, fbl, gcount, goff, pool, sat, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd, total;
+  size_t hdr, A, B, meta, fgm, shm, oct, fbl, gcount, goff, defl, pool, sat, cent, vol, nsh, sum, sumsh, mx, h_labels, h_sph, h_rnd,
+      total;
 };
 
 Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
@@ -90,6 +91,7 @@ Layout make_layout(const Geom& g, int32_t max_label, uint32_t flags) {
   L.fbl = take((size_t)g.ntiles * 4);
   L.gcount = take((size_t)dilate_groups(g) * 4);
   L.goff = take((size_t)dilate_groups(g) * 4);
+  L.defl = take((size_t)dilate_groups(g) * 8);  // K5 waves: two deferred-group lists
   L.pool = take((size_t)dilate_pool_entries(g) * 8);
   L.sat = take((size_t)col_blocks(g) * 4);
   L.cent = take((size_t)g.ntiles * kTileVol * sizeof(uint2));
@@ -241,18 +243,23 @@ int run(const int32_t* labels, const Geom& g, int32_t max_label, uint32_t flags,
     unsigned long long* pool = (unsigned long long*)(w + L.pool);
     uint32_t* gcount = (uint32_t*)(w + L.gcount);
     uint32_t* goff = (uint32_t*)(w + L.goff);
-    {
-      Nvtx r("K5a gather");
-      launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, g, gather_mode_of(flags),
-                           hdr, st);
-    }
-    tm.mark(7);
-    // K5b: with the reductions fused (S&R) or writing the LT plane (LT outputs); K5' for the
-    // tiles K5a handed over (every tile when Dmax > 65535)
-    {
-      Nvtx r("K5b paint + K5' fallback");
+    // K5a + K5b in waves over the candidate pool (wave w > 0: the groups the pool could not
+    // hold in wave w - 1; its kernels leave at once when there are none); K5b with the
+    // reductions fused (S&R) or writing the LT plane (LT outputs); K5' for the tiles K5a handed
+    // over (every tile when Dmax > 65535)
+    for (int wv = 0; wv < kDilateWaves; ++wv) {
+      {
+        Nvtx r("K5a gather");
+        launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, g, gather_mode_of(flags), hdr, st, wv,
+                             (uint32_t*)(w + L.defl));
+      }
+      if (wv == 0) tm.mark(7);
+      Nvtx r("K5b paint");
       launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, g, ltp, labels, stage == kFull ? &acc : nullptr, D,
-                          (flags & kFlagApproxLt) != 0, hdr, st);
+                          (flags & kFlagApproxLt) != 0, hdr, st, wv);
+    }
+    {
+      Nvtx r("K5' fallback");
       launch_dilate_fallback(meta, cent, fbl, g, ltp, hdr, st);
     }
     tm.mark(4);
@@ -315,7 +322,7 @@ int finish_call(WsHeader* hdr, uint32_t flags, cudaStream_t st) {
 }
 
 struct SlabLayout {
-  size_t hdr, P, meta, fgm, shm, oct, fbl, gcount, goff, pool, sat, poff, cent, total;
+  size_t hdr, P, meta, fgm, shm, oct, fbl, gcount, goff, defl, pool, sat, poff, cent, total;
 };
 SlabLayout make_slab_layout(const Geom& g) {
   SlabLayout L{};
@@ -334,6 +341,7 @@ SlabLayout make_slab_layout(const Geom& g) {
   L.fbl = take((size_t)g.ntiles * 4);
   L.gcount = take((size_t)dilate_groups(g) * 4);
   L.goff = take((size_t)dilate_groups(g) * 4);
+  L.defl = take((size_t)dilate_groups(g) * 8);  // K5 waves: two deferred-group lists
   L.pool = take((size_t)dilate_pool_entries(g) * 8);
   L.sat = take((size_t)col_blocks(g) * 4);
   L.poff = take((size_t)g.ntiles * 4 + 16);
@@ -515,8 +523,11 @@ int run_host_pipelined(const int32_t* labels_host, int32_t* dlab, const Geom& g,
       Geom gg = g;
       gg.tz_lo = z0 / kTZ3;
       gg.tz_hi = (z1 + kTZ3 - 1) / kTZ3;
-      launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, gg, 0, hdr, st);
-      launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, gg, B, dlab, &acc, A, (flags & kFlagApproxLt) != 0, hdr, st);
+      for (int wv = 0; wv < kDilateWaves; ++wv) {
+        launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, gg, 0, hdr, st, wv, (uint32_t*)(w + L.defl));
+        launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, gg, B, dlab, &acc, A, (flags & kFlagApproxLt) != 0, hdr,
+                            st, wv);
+      }
     }
   }
   // tiles handed to the atomic kernel (LT^2 into B, whose y-pass words are consumed) and their
@@ -695,6 +706,7 @@ int fastrs_read_diagnostics(const void* ws, fastrs_diagnostics* out, void* strea
   out->sum_group_list = h.sum_group_list;
   out->n_painted = h.n_painted;
   out->n_covering = h.n_covering;
+  out->n_deferred = h.n_defer[0] + h.n_defer[1] + h.n_defer[2] + h.n_defer[3];
   return FASTRS_OK;
 }
 
@@ -810,10 +822,12 @@ int slab_dilate_impl(const int32_t* labels, const uint32_t* d_ext, Geom g, const
   unsigned long long* pool = (unsigned long long*)((char*)ws + L.pool);
   uint32_t* gcount = (uint32_t*)((char*)ws + L.gcount);
   uint32_t* goff = (uint32_t*)((char*)ws + L.goff);
-  launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, g, gather_mode_of(flags), hdr,
-                       st);
-  launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, g, ltp, lab_ext, &acc, d_ext, (flags & kFlagApproxLt) != 0, hdr,
-                      st);
+  for (int wv = 0; wv < kDilateWaves; ++wv) {
+    launch_dilate_gather(fgm, meta, cent, oct, fbl, pool, gcount, goff, g, gather_mode_of(flags), hdr, st, wv,
+                         (uint32_t*)((char*)ws + L.defl));
+    launch_dilate_paint(fgm, shm, meta, pool, gcount, goff, g, ltp, lab_ext, &acc, d_ext, (flags & kFlagApproxLt) != 0,
+                        hdr, st, wv);
+  }
   launch_dilate_fallback(meta, cent, fbl, g, ltp, hdr, st);
   launch_epilogue_fallback(lab_ext, d_ext, meta, fbl, g, acc, ltp, hdr, st);
   return FASTRS_OK;

@@ -107,6 +107,7 @@ struct WsHeader {
   unsigned long long n_painted;   // K5b: balls painted (lanes over rows) after the screens
   unsigned long long n_covering;  // K5b: painted balls that covered at least one cell
   unsigned long long g_stats[3];  // K5a statistics (FASTRS_GATHER_STATS builds only): examined, D-cut, taken
+  uint32_t n_defer[4];            // K5 waves: groups wave w deferred to wave w + 1 (the pool was full)
 };
 static_assert(sizeof(WsHeader) <= 256, "header");
 
@@ -210,14 +211,19 @@ int64_t dilate_groups(const Geom& g);        // K5 tile groups (gcount / goff en
 void launch_dilate_paint(const uint32_t* fgm, const uint32_t* shm, const TileMeta* meta,
                          const unsigned long long* pool, const uint32_t* gcount, const uint32_t* goff, const Geom& g,
                          uint32_t* ltp, const int32_t* labels, const Accum* acc, const uint32_t* D, bool approx,
-                         WsHeader* hdr, cudaStream_t st);
+                         WsHeader* hdr, cudaStream_t st, int wave = 0);
 void launch_dilate_fallback(TileMeta* meta, const uint2* centres, const uint32_t* fbl, const Geom& g, uint32_t* ltp,
                             WsHeader* hdr, cudaStream_t st);
 // K5a: per tile group, gather the kept balls that reach it and write them sorted by D
-// (descending) to the candidate pool; groups that cannot be handled are listed in fbl
+// (descending) to the candidate pool; groups that cannot be handled are listed in fbl.
+// Waves: the pool is reused by kDilateWaves gather + paint rounds; wave w > 0 takes only the
+// groups the previous wave deferred because the pool was full (the last wave lists such groups
+// for the atomic fallback).  Call gather(w) then paint(w) for w = 0 .. kDilateWaves - 1.
+constexpr int kDilateWaves = 3;
 void launch_dilate_gather(const uint32_t* fgm, TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
                           unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int gather_mode,
-                          WsHeader* hdr, cudaStream_t st);
+                          WsHeader* hdr, cudaStream_t st, int wave, uint32_t* deflists);
+// workspace of the deferred-group lists of the waves: 2 * dilate_groups(g) u32
 int64_t dilate_pool_entries(const Geom& g);  // K5 candidate pool (sorted per-group lists), u64 entries
 // K5 epilogue: shell, per-label reductions (acc nullable) and LT outputs from the LT plane ltp
 void launch_epilogue(const int32_t* labels, const uint32_t* D, const Geom& g, const Accum* acc, uint32_t* lt2_out,

@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // K5 (default path): exact ball dilation LT^2(p) = max{ D(q) : |p-q|^2 < D(q) }
 // by "exact-order cover", fused with the shell test and the per-label reductions.
 //
@@ -44,7 +46,10 @@ constexpr int kHist = 1536;  // exact-D counting-sort bins per round
 constexpr int kPoint = FASTRS_KPOINT;
 static_assert(kPoint % 32 == 0 && kPoint <= 1024, "point-mode list: whole warps of entries");
 constexpr int kPointW = kPoint / 32;
-constexpr uint32_t kGroupFallback = 0xFFFFFFFFu;  // uncovered cells at which a warp switches to point tests
+// gcount[group]: (wave << 29) | list length, or one of the two sentinels
+constexpr uint32_t kGroupFallback = 0xFFFFFFFFu;  // left to the atomic fallback (k_dilate_atomic)
+constexpr uint32_t kGroupDeferred = 0xFFFFFFFEu;  // the pool was full: the next wave gathers it
+constexpr uint32_t kGroupCountMask = (1u << 29) - 1u;
 constexpr int kOff = 16384;  // coordinate bias of packed candidates
 
 constexpr int kStgChunks = 8;  // record chunks a group may stage list overflow for
@@ -71,6 +76,7 @@ struct Smem {  // K5a (gather + sort)
   unsigned long long stg_off[kStgChunks];
   uint32_t stg_lo[kStgChunks];
   int nstg, stg_fail;
+  int defer;                         // the pool is full: defer the group to the next wave
   unsigned long long topkey;         // cover cut: (max D << 32) | home tile of the largest reaching ball
   int qstar[4];                      // its centre (group coordinates) and D
 };
@@ -447,27 +453,21 @@ __device__ __forceinline__ unsigned long long row_box(int ya, int yb, int za, in
 }
 
 template <bool IS3D>
-__global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t* __restrict__ fgm,
-                                                                  const TileMeta* __restrict__ meta,
-                                                               const uint2* __restrict__ cent,
-                                                               const uint16_t* __restrict__ oct,
-                                                               uint32_t* __restrict__ fbl, Geom g, int gather_mode,
-                                                               unsigned long long* __restrict__ pool,
-                                                               unsigned long long pool_cap,
-                                                               uint32_t* __restrict__ gcount,
-                                                               uint32_t* __restrict__ goff,
-                                                               WsHeader* __restrict__ hdr, GroupDivs gd) {
+__device__ __forceinline__ void gather_group(const uint32_t group_id, Smem& S, const uint32_t* __restrict__ fgm,
+                                             const TileMeta* __restrict__ meta, const uint2* __restrict__ cent,
+                                             const uint16_t* __restrict__ oct, uint32_t* __restrict__ fbl,
+                                             const Geom& g, int gather_mode, unsigned long long* __restrict__ pool,
+                                             unsigned long long pool_cap, uint32_t* __restrict__ gcount,
+                                             uint32_t* __restrict__ goff, WsHeader* __restrict__ hdr,
+                                             const GroupDivs& gd, int wave, uint32_t* __restrict__ defer_out) {
   using P = Shape<IS3D>;
   constexpr int TY = P::TY, TZ = P::TZ;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t dmax = hdr->dmax;
-  if (dmax > kU16Max) return;  // k_dilate_atomic handles it
 
   // ---- group / tile coordinates --------------------------------------------------------
   // groups tile the layers [tz_lo, tz_hi) (all layers except on the slab path)
-  uint32_t t = blockIdx.x, rq;
+  uint32_t t = group_id, rq;
   t = gd.x.divmod(t, rq);
   const int64_t gxi = rq;
   t = gd.y.divmod(t, rq);
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
   const int64_t mtile = have_tile ? ((b * g.ntz + mtz) * g.nty + mty) * g.ntx + mtx : 0;
   const int mox = wx * kTX, moy = wy * TY, moz = wz * TZ;  // my tile origin within the group
   const bool active = have_tile && meta[mtile].nfg != 0;
-  const int64_t group = blockIdx.x;
+  const int64_t group = group_id;
   if (__syncthreads_or(active) == 0) {  // the whole group is background
     if (tid == 0) gcount[group] = 0;
     return;
@@ -610,6 +610,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
   uint32_t written = 0;
   if (tid == 0) {
     S.fallback = 0;
+    S.defer = 0;
     S.base = 0;
   }
   __syncthreads();
@@ -634,14 +635,23 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
     gather<IS3D, kListExactHist, IS3D>(S, meta, cent, oct, g, b, tx0, ty0, tz0, nrx, nry, nrz, 0, kBuckets - 1, dtop,
                                        nullptr, stage, &hdr->stage_used, pool_cap / 2);
     const uint32_t total = S.count;
+#ifdef FASTRS_DEBUG_GATHER
+    if (tid == 0 && group < 4)
+      printf("gather g%lld wave %d total %u dtop %u nrx %d nry %d nrz %d bb %d %d %d %d %d %d pool_cap %llu\n",
+             (long long)group, wave, total, dtop, nrx, nry, nrz, S.bb[0], S.bb[1], S.bb[2], S.bb[3], S.bb[4], S.bb[5],
+             pool_cap);
+#endif
     constexpr uint32_t kListCap = IS3D ? 2 * kCap : kCap;  // 3D keeps compact entries
     if (tid == 0) {
       const unsigned long long b0 = atomicAdd(&hdr->pool_used, (unsigned long long)total);
       S.base = b0;
-      if (b0 + total > main_cap) S.fallback = 1;
+      if (b0 + total > main_cap) {  // the pool is full: the next wave (the last: the fallback)
+        if (wave + 1 < kDilateWaves) S.defer = 1;
+        else S.fallback = 1;
+      }
     }
     block_exclusive_scan(S.dh, (int)dtop, S.wsum);
-    if (!S.fallback) {
+    if (!S.fallback && !S.defer) {
       unsigned long long* out = pool + S.base;
       if (total <= kListCap || (stage && !S.stg_fail)) {
         const int nstg = S.nstg;
@@ -725,7 +735,10 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
       if (lane == 31 && S.rounds == 0) {  // first round: the histogram covers every candidate
         const unsigned long long b0 = atomicAdd(&hdr->pool_used, (unsigned long long)inc);
         S.base = b0;
-        if (b0 + inc > pool_cap - pool_cap / 2) S.fallback = 1;  // the top half stages list overflow
+        if (b0 + inc > pool_cap - pool_cap / 2) {  // (the top half stages list overflow)
+          if (wave + 1 < kDilateWaves) S.defer = 1;
+          else S.fallback = 1;
+        }
       }
       __syncwarp();
       if (lane == 0) {
@@ -740,7 +753,7 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
       }
     }
     __syncthreads();
-    if (S.fallback) break;
+    if (S.fallback || S.defer) break;
     if (S.bigbucket) {
       // exact-D scatter rounds over the bucket `top`, kHist D values at a time, highest first:
       // count the exact D of every candidate in the sub-range (no list), prefix-sum the counts
@@ -842,6 +855,15 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
   }
 
   }
+  if (S.defer) {  // the pool is full: the next wave gathers this group again
+    if (tid == 0) {
+      gcount[group] = kGroupDeferred;
+      defer_out[atomicAdd(&hdr->n_defer[wave], 1u)] = (uint32_t)group;
+    }
+    return;
+  }
+  if (written > kGroupCountMask && tid == 0) S.fallback = 1;  // (no list is that long in practice)
+  __syncthreads();
   if (S.fallback) {  // leave this group to k_dilate_atomic
     if (lane == 0 && active) fbl[atomicAdd(&hdr->n_fb, 1u)] = (uint32_t)mtile;
     if (tid == 0) {
@@ -851,10 +873,49 @@ __global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t
     return;
   }
   if (tid == 0) {
-    gcount[group] = written;
+    gcount[group] = ((uint32_t)wave << 29) | written;
     goff[group] = (uint32_t)S.base;
     atomicMax(&hdr->max_group_list, written);
     atomicAdd(&hdr->sum_group_list, (unsigned long long)written);
+  }
+}
+
+__global__ void k_wave_reset(WsHeader* __restrict__ hdr, int wave) {
+  if (threadIdx.x == 0 && hdr->n_defer[wave - 1] != 0u) {
+    hdr->pool_used = 0ull;
+    hdr->stage_used = 0ull;
+    hdr->paint_next = 0u;
+  }
+}
+
+// K5a kernel: wave 0 takes one group per CTA; a later wave loops over the groups the previous
+// wave deferred (a list; few CTAs, and they leave at once when it is empty)
+template <bool IS3D>
+__global__ void __launch_bounds__(kWarps * 32, 7) k_dilate_gather(const uint32_t* __restrict__ fgm,
+                                                                  const TileMeta* __restrict__ meta,
+                                                                  const uint2* __restrict__ cent,
+                                                                  const uint16_t* __restrict__ oct,
+                                                                  uint32_t* __restrict__ fbl, Geom g, int gather_mode,
+                                                                  unsigned long long* __restrict__ pool,
+                                                                  unsigned long long pool_cap,
+                                                                  uint32_t* __restrict__ gcount,
+                                                                  uint32_t* __restrict__ goff,
+                                                                  WsHeader* __restrict__ hdr, GroupDivs gd, int wave,
+                                                                  const uint32_t* __restrict__ defer_in,
+                                                                  uint32_t* __restrict__ defer_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  if (hdr->dmax > kU16Max) return;  // k_dilate_atomic handles it
+  if (wave == 0) {
+    gather_group<IS3D>(blockIdx.x, S, fgm, meta, cent, oct, fbl, g, gather_mode, pool, pool_cap, gcount, goff, hdr, gd,
+                       wave, defer_out);
+    return;
+  }
+  const uint32_t n = *(volatile uint32_t*)&hdr->n_defer[wave - 1];
+  for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
+    gather_group<IS3D>(defer_in[k], S, fgm, meta, cent, oct, fbl, g, gather_mode, pool, pool_cap, gcount, goff, hdr,
+                       gd, wave, defer_out);
+    __syncthreads();  // the shared state is rebuilt for the next group
   }
 }
 
@@ -891,7 +952,7 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
                                            int point_at, uint32_t* __restrict__ ltp, const int32_t* __restrict__ labels,
                                            const Accum& acc, const unsigned long long* __restrict__ fxlut,
                                            const uint32_t* __restrict__ Dp, int approx, WsHeader* __restrict__ hdr,
-                                           const GroupDivs& gd) {
+                                           const GroupDivs& gd, int wave) {
   using P = Shape<IS3D>;
   constexpr int TY = P::TY, TZ = P::TZ;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -919,8 +980,10 @@ __device__ __forceinline__ void paint_tile(const uint32_t bid, const uint32_t* _
   const int64_t mtile = have_tile ? ((b * g.ntz + mtz) * g.nty + mty) * g.ntx + mtx : 0;
   const int mox = wx * kTX, moy = wy * TY, moz = wz * TZ;  // my tile origin within the group
   const bool active = have_tile && meta[mtile].nfg != 0;
-  const uint32_t total = gcount[group];
-  if (!active || total == kGroupFallback) return;  // background, or left to k_dilate_atomic
+  uint32_t total = gcount[group];
+  // background, left to k_dilate_atomic, deferred, or gathered by another wave
+  if (!active || total >= kGroupDeferred || (total >> 29) != (uint32_t)wave) return;
+  total &= kGroupCountMask;
   const unsigned long long* list = pool + goff[group];
   const int64_t item = b * g.Z * g.Y * g.X;
 
@@ -1446,8 +1509,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* 
                                                               const int32_t* __restrict__ labels, Accum acc,
                                                               const unsigned long long* __restrict__ fxlut,
                                                               const uint32_t* __restrict__ Dp, int approx,
-                                                              WsHeader* __restrict__ hdr, uint32_t nbid, GroupDivs gd) {
+                                                              WsHeader* __restrict__ hdr, uint32_t nbid, GroupDivs gd,
+                                                              int wave) {
   if (hdr->dmax > kU16Max) return;  // k_dilate_atomic handles it
+  if (wave > 0 && *(volatile uint32_t*)&hdr->n_defer[wave - 1] == 0u) return;  // nothing gathered this wave
   const int lane = threadIdx.x & 31;
   for (;;) {
     uint32_t bid = 0;
@@ -1455,7 +1520,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_dilate_paint(const uint32_t* 
     bid = __shfl_sync(kFull, bid, 0);
     if (bid >= nbid) break;
     paint_tile<IS3D, NW, FUSED>(bid, fgm, shm, meta, g, pool, gcount, goff, point_at, ltp, labels, acc, fxlut, Dp, approx,
-                                hdr, gd);
+                                hdr, gd, wave);
     __syncwarp();
   }
 }
@@ -1483,25 +1548,49 @@ int64_t launched_groups(const Geom& g) {
 
 void launch_dilate_gather(const uint32_t* fgm, TileMeta* meta, const uint2* centres, const uint16_t* oct, uint32_t* fbl,
                           unsigned long long* pool, uint32_t* gcount, uint32_t* goff, const Geom& g, int gather_mode,
-                          WsHeader* hdr, cudaStream_t st) {
+                          WsHeader* hdr, cudaStream_t st, int wave, uint32_t* deflists) {
   const int64_t ngroups = launched_groups(g);
   if (ngroups <= 0) return;
-  const unsigned long long pool_cap = (unsigned long long)dilate_pool_entries(g);
+  unsigned long long pool_cap = (unsigned long long)dilate_pool_entries(g);
+  if (const char* pd = getenv("FASTRS_POOL_DIV")) {  // test hook: a smaller pool (exercises the waves)
+    const long long dv = atoll(pd);
+    if (dv > 1) pool_cap = pool_cap / (unsigned long long)dv > 64 ? pool_cap / (unsigned long long)dv : 64;
+  }
 #ifdef FASTRS_GATHER_STATS
   {
     static const unsigned long long zero3[3] = {0, 0, 0};
     cudaMemcpyToSymbolAsync(g_stats_ptr, zero3, sizeof(zero3), 0, cudaMemcpyHostToDevice, st);
   }
 #endif
-  cudaMemsetAsync(&hdr->stage_used, 0, sizeof(hdr->stage_used), st);
-  if (g.ndim == 3)
-    k_dilate_gather<true><<<(unsigned)ngroups, kWarps * 32, sizeof(Smem), st>>>(fgm, meta, centres, oct, fbl, g,
-                                                                                 gather_mode, pool, pool_cap, gcount,
-                                                                                 goff, hdr, group_divs(g));
-  else
-    k_dilate_gather<false><<<(unsigned)ngroups, kWarps * 32, sizeof(Smem), st>>>(fgm, meta, centres, oct, fbl, g,
-                                                                                  gather_mode, pool, pool_cap, gcount,
-                                                                                  goff, hdr, group_divs(g));
+  // each wave (and chunk) reuses the pool: its counters restart (a later wave: one tiny kernel,
+  // which also restarts the paint's work counter, and only when the previous wave deferred groups)
+  if (wave == 0) {
+    cudaMemsetAsync(&hdr->stage_used, 0, sizeof(hdr->stage_used), st);
+    cudaMemsetAsync(&hdr->pool_used, 0, sizeof(hdr->pool_used), st);
+    cudaMemsetAsync(hdr->n_defer, 0, sizeof(hdr->n_defer), st);  // (the host pipeline runs waves per chunk)
+  } else {
+    k_wave_reset<<<1, 32, 0, st>>>(hdr, wave);
+  }
+  {
+    // wave 0: one CTA per group; later waves: a few CTAs loop over the previous wave's list
+    uint32_t grid = (uint32_t)ngroups;
+    if (wave > 0) {
+      int dev = 0, nsm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      grid = (uint32_t)(nsm * 7) < grid ? (uint32_t)(nsm * 7) : grid;
+    }
+    const uint32_t* din = deflists + (size_t)((wave + 1) & 1) * (size_t)ngroups;  // written by wave - 1
+    uint32_t* dout = deflists + (size_t)(wave & 1) * (size_t)ngroups;
+    if (g.ndim == 3)
+      k_dilate_gather<true><<<grid, kWarps * 32, sizeof(Smem), st>>>(fgm, meta, centres, oct, fbl, g, gather_mode, pool,
+                                                                     pool_cap, gcount, goff, hdr, group_divs(g), wave,
+                                                                     din, dout);
+    else
+      k_dilate_gather<false><<<grid, kWarps * 32, sizeof(Smem), st>>>(fgm, meta, centres, oct, fbl, g, gather_mode, pool,
+                                                                      pool_cap, gcount, goff, hdr, group_divs(g), wave,
+                                                                      din, dout);
+  }
 #ifdef FASTRS_GATHER_STATS
   cudaMemcpyFromSymbolAsync(hdr->g_stats, g_stats_ptr, 3 * sizeof(unsigned long long), 0, cudaMemcpyDeviceToDevice, st);
 #endif
@@ -1512,35 +1601,35 @@ template <bool IS3D, int NW, int MINB, bool FUSED>
 void paint_go(int64_t ngroups, const uint32_t* fgm, const uint32_t* shm, const TileMeta* meta, const Geom& g,
               const unsigned long long* pool, const uint32_t* gcount, const uint32_t* goff, uint32_t* ltp,
               const int32_t* labels, const Accum& acc, const uint32_t* D, int approx, WsHeader* hdr,
-              cudaStream_t st) {
+              cudaStream_t st, int wave) {
   const uint32_t nbid = (uint32_t)(ngroups * kWarps);
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const uint32_t cap = (uint32_t)nsm * MINB * NW;  // resident warps
   const uint32_t grid = ((nbid < cap ? nbid : cap) + NW - 1) / NW;
-  cudaMemsetAsync(&hdr->paint_next, 0, sizeof(uint32_t), st);
+  if (wave == 0) cudaMemsetAsync(&hdr->paint_next, 0, sizeof(uint32_t), st);  // (later waves: k_wave_reset)
   k_dilate_paint<IS3D, NW, MINB, FUSED><<<grid, NW * 32, sizeof(PaintSmem<NW, FUSED>), st>>>(
       fgm, shm, meta, g, pool, gcount, goff, point_at_knob(), ltp, labels, acc, device_fxlut(dev), D, approx, hdr, nbid,
-      group_divs(g));
+      group_divs(g), wave);
 }
 }  // namespace
 
 void launch_dilate_paint(const uint32_t* fgm, const uint32_t* shm, const TileMeta* meta,
                          const unsigned long long* pool, const uint32_t* gcount, const uint32_t* goff, const Geom& g,
                          uint32_t* ltp, const int32_t* labels, const Accum* acc, const uint32_t* D, bool approx,
-                         WsHeader* hdr, cudaStream_t st) {
+                         WsHeader* hdr, cudaStream_t st, int wave) {
   const int ap = approx && D ? 1 : 0;
   const int64_t ngroups = launched_groups(g);
   if (ngroups <= 0) return;
   Accum a{};
   if (acc) a = *acc;
   if (g.ndim == 3) {
-    if (acc) paint_go<true, kPaintNW, kPaintMinB, true>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, D, ap, hdr, st);
-    else paint_go<true, kPaintNW, kPaintMinB, false>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, D, ap, hdr, st);
+    if (acc) paint_go<true, kPaintNW, kPaintMinB, true>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, D, ap, hdr, st, wave);
+    else paint_go<true, kPaintNW, kPaintMinB, false>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, D, ap, hdr, st, wave);
   } else {
-    if (acc) paint_go<false, kPaintNW, kPaintMinB, true>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, D, ap, hdr, st);
-    else paint_go<false, kPaintNW, kPaintMinB, false>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, D, ap, hdr, st);
+    if (acc) paint_go<false, kPaintNW, kPaintMinB, true>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, D, ap, hdr, st, wave);
+    else paint_go<false, kPaintNW, kPaintMinB, false>(ngroups, fgm, shm, meta, g, pool, gcount, goff, ltp, labels, a, D, ap, hdr, st, wave);
   }
 }
 

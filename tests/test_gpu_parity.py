@@ -269,6 +269,31 @@ def test_big_bucket_scatter_rounds(F):
         assert torch.equal(got[k], want[k]), k
 
 
+def test_dilation_waves_on_a_full_pool(F):
+    """A candidate pool too small for the gather (FASTRS_POOL_DIV shrinks it) defers tile groups to
+    later waves of K5a + K5b over the reused pool (only the last wave's overflow goes to the atomic
+    fallback): results bit-identical to the default call, LT^2 equal to the oracle's on C2."""
+    for cfg, div in ((2, 40), (3, 24)):
+        lab, info = synth.make_config(cfg)
+        ml = info["max_label"]
+        t = _dev(lab)
+        want = F.sphericity_roundness(t, max_label=ml, stats=True)
+        lt_want = F.local_thickness(t)
+        os.environ["FASTRS_POOL_DIV"] = str(div)
+        try:
+            got = F.sphericity_roundness(t, max_label=ml, stats=True)
+            d = F.diagnostics(F.last_workspace())
+            lt_got = F.local_thickness(t)
+        finally:
+            del os.environ["FASTRS_POOL_DIV"]
+        assert d["n_deferred"] > 0, d
+        assert torch.equal(lt_got, lt_want)
+        for k in ("volume", "n_shell", "max_lt2", "mean_lt", "shell_mean_lt", "sphericity", "roundness"):
+            np.testing.assert_array_equal(got[k].cpu().numpy(), want[k].cpu().numpy(), err_msg=k)  # (NaN == NaN)
+        if cfg == 2:
+            np.testing.assert_array_equal(_u32(lt_got), oracle.fields(lab, max_label=ml, flags=1)[1])
+
+
 def test_empty_and_single_element_objects(F):
     lab = np.zeros((20, 21, 22), np.int32)
     r = F.sphericity_roundness(_dev(lab), max_label=3)

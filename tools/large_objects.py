@@ -20,10 +20,11 @@ p.add_argument("--n", type=int, default=512)
 p.add_argument("--radii", type=int, nargs="+", default=[20, 40, 80, 160, 240])
 p.add_argument("--iters", type=int, default=3)
 p.add_argument("--flags", type=int, default=1)
+p.add_argument("--gap", type=int, default=4, help="voxels between neighbouring balls (<= 0: overlapping, touching labels)")
 a = p.parse_args()
 for r in a.radii:
     n = a.n
-    k = max(1, n // (2 * r + 4))  # balls per axis
+    k = max(1, n // (2 * r + a.gap)) if 2 * r + a.gap > 0 else 1  # balls per axis
     step = n // k
     t = torch.zeros((n, n, n), dtype=torch.int32, device="cuda")
     zz = torch.arange(n, device="cuda")
@@ -36,7 +37,8 @@ for r in a.radii:
                 sl = [slice(max(0, c[d] - r), min(n, c[d] + r + 1)) for d in range(3)]
                 sub = ((zz[sl[0]] - c[0])[:, None, None] ** 2 + (zz[sl[1]] - c[1])[None, :, None] ** 2 +
                        (zz[sl[2]] - c[2])[None, None, :] ** 2) <= r * r
-                t[sl[0], sl[1], sl[2]][sub] = lab
+                view = t[sl[0], sl[1], sl[2]]
+                view[sub & (view == 0)] = lab  # overlaps keep the earlier label (touching objects)
     fill = float((t != 0).float().mean())
     F.sphericity_roundness(t, max_label=lab, flags=a.flags)
     torch.cuda.synchronize()
@@ -48,7 +50,7 @@ for r in a.radii:
     F.profile(False)
     tot = sum(ms.values())
     diag = F.diagnostics(F.last_workspace())
-    print(json.dumps({"n": n, "radius": r, "objects": lab, "fill": round(fill, 3), "ms_total": round(tot, 3),
+    print(json.dumps({"n": n, "radius": r, "gap": a.gap, "objects": lab, "fill": round(fill, 3), "ms_total": round(tot, 3),
                       "gvox_s": round(n ** 3 / tot / 1e6, 2), "stages_ms": {kk: round(v, 3) for kk, v in ms.items()},
                       "diagnostics": diag}), flush=True)
     del t
