@@ -128,6 +128,9 @@ typedef struct {
   uint64_t n_covering;     /* K5: painted balls that covered at least one cell (S&R call) */
   uint32_t n_staged;       /* K5: list overflows staged in the candidate pool (one pass)   */
   uint32_t n_deferred;     /* K5: tile groups a full candidate pool deferred to a later wave */
+  uint32_t n_col_slow;     /* last column pass (K3 in 3D): elements whose scan left the staged
+                              window, scanned by the batched-read list kernel              */
+  uint32_t reserved;
 } fastrs_diagnostics;
 
 /* Bytes of device workspace needed by every entry point below for this geometry.

@@ -707,6 +707,8 @@ int fastrs_read_diagnostics(const void* ws, fastrs_diagnostics* out, void* strea
   out->n_painted = h.n_painted;
   out->n_covering = h.n_covering;
   out->n_deferred = h.n_defer[0] + h.n_defer[1] + h.n_defer[2] + h.n_defer[3];
+  out->n_col_slow = h.slow_n;
+  out->reserved = 0;
   return FASTRS_OK;
 }
 

@@ -108,6 +108,8 @@ struct WsHeader {
   unsigned long long n_covering;  // K5b: painted balls that covered at least one cell
   unsigned long long g_stats[3];  // K5a statistics (FASTRS_GATHER_STATS builds only): examined, D-cut, taken
   uint32_t n_defer[4];            // K5 waves: groups wave w deferred to wave w + 1 (the pool was full)
+  uint32_t slow_n;                // K2/K3: elements listed for the batched 32-bit scan (reset per launch)
+  uint32_t pad4;
 };
 static_assert(sizeof(WsHeader) <= 256, "header");
 

@@ -300,49 +300,85 @@ constexpr int kScan16U = FASTRS_SCAN_U;  // row pairs per iteration of the 16-bi
 // positions per thread of the 16-bit column scan (1, 2 or 4).  C4 (round 2b): PP 2 4.41 / 4.24 ms
 // (y / z), PP 4 4.12 / 4.08 (U = 2: 4.19 / 4.15; 4 CTAs/SM: 4.66 / 4.62)
 constexpr int kColPP = FASTRS_COL_PP;
+#ifndef FASTRS_COL_CPASYNC
+#define FASTRS_COL_CPASYNC 1
+#endif
+constexpr bool kColCpAsync = FASTRS_COL_CPASYNC != 0;  // K2/K3 staging by cp.async (round 2c)
 
 // Slow path of the column scan for an element whose window leaves the staged rows: the same
-// exact scan in 32-bit arithmetic, every read from global memory (L2).
-__device__ __noinline__ uint32_t scan_global(const uint32_t* __restrict__ in, int64_t base, int64_t astride, int64_t p,
-                                             int64_t L, uint32_t v, uint32_t chbit, int border, int64_t gofs,
-                                             int64_t Lg) {
+// exact scan in 32-bit arithmetic, every read from global memory (L2).  Round 2c: the reads of
+// kSgBatch consecutive rows are issued together and then consumed in order (loads past the
+// stopping row are speculative and in bounds), so a scan of n rows waits ~n / kSgBatch L2 round
+// trips instead of n (ncu r02f: 43 % of K2/K3 stall samples were this loop's dependent loads).
+#ifndef FASTRS_SG_BATCH
+#define FASTRS_SG_BATCH 8
+#endif
+constexpr int kSgBatchList = FASTRS_SG_BATCH;
+template <int kSgBatch>
+__device__ __forceinline__ uint32_t scan_global_rows(const uint32_t* __restrict__ at, int64_t astride, int32_t n_up,
+                                                  int32_t n_dn, uint32_t v, uint32_t chbit, bool up_end_site,
+                                                  bool dn_end_site) {
+  // at = the element's word; n_up / n_dn = staged rows above / below it; up_end_site: the row
+  // just past the top of the staged axis is a site (the grid end with the border flag);
+  // dn_end_site: likewise below row 0 (more grid before the slab, or the border flag)
   uint32_t best = v & kMask;
-  {
-    uint32_t dq = 1, dq2 = 1;
-    int64_t q = p + 1;
-    while (dq2 < best) {
-      if (q >= L) {  // end of the staged axis: the grid end (slab path: h^2 >= D guarantees it)
-        if (border && gofs + q >= Lg) best = min(best, dq2);
-        break;
+  {  // upwards: row p + d; a word with its run-start bit is a site at d
+    int32_t d = 1;
+    const uint32_t* q = at + astride;
+    bool done = false;
+    while (!done && (uint32_t)(d * d) < best) {
+      uint32_t w[kSgBatch];
+#pragma unroll
+      for (int k = 0; k < kSgBatch; ++k) w[k] = (d + k <= n_up) ? __ldg(q + k * astride) : 0u;
+#pragma unroll
+      for (int k = 0; k < kSgBatch; ++k) {
+        const uint32_t d2 = (uint32_t)((d + k) * (d + k));
+        if (d2 >= best) { done = true; break; }
+        if (d + k > n_up) {  // end of the staged axis (slab path: h^2 >= D guarantees the grid end)
+          if (up_end_site) best = min(best, d2);
+          done = true;
+          break;
+        }
+        if (w[k] & chbit) { best = min(best, d2); done = true; break; }
+        best = min(best, (w[k] & kMask) + d2);
       }
-      const uint32_t w = __ldg(in + base + q * astride);
-      if (w & chbit) {
-        best = min(best, dq2);
-        break;
-      }
-      best = min(best, (w & kMask) + dq2);
-      dq2 += 2 * dq + 1;
-      ++dq;
-      ++q;
+      d += kSgBatch;
+      q += kSgBatch * astride;
     }
   }
-  {
-    uint32_t dq = 1, dq2 = 1, chk = v & chbit;
-    int64_t q = p - 1;
-    while (dq2 < best) {
-      if (chk) {
-        if (gofs + q >= 0 || border) best = min(best, dq2);
-        break;
+  {  // downwards: row p - d; the row above it starting its run puts a site at d
+    int32_t d = 1;
+    uint32_t chk = v & chbit;
+    const uint32_t* q = at - astride;
+    bool done = false;
+    while (!done && (uint32_t)(d * d) < best) {
+      uint32_t w[kSgBatch];
+#pragma unroll
+      for (int k = 0; k < kSgBatch; ++k) w[k] = (d + k <= n_dn) ? __ldg(q - k * astride) : chbit;
+#pragma unroll
+      for (int k = 0; k < kSgBatch; ++k) {
+        const uint32_t d2 = (uint32_t)((d + k) * (d + k));
+        if (d2 >= best) { done = true; break; }
+        if (chk) {
+          if (d + k <= n_dn || dn_end_site) best = min(best, d2);
+          done = true;
+          break;
+        }
+        best = min(best, (w[k] & kMask) + d2);
+        chk = w[k] & chbit;
       }
-      const uint32_t w = __ldg(in + base + q * astride);
-      best = min(best, (w & kMask) + dq2);
-      chk = w & chbit;
-      dq2 += 2 * dq + 1;
-      ++dq;
-      --q;
+      d += kSgBatch;
+      q -= kSgBatch * astride;
     }
   }
   return best;
+}
+
+__device__ __noinline__ uint32_t scan_global(const uint32_t* __restrict__ in, int64_t base, int64_t astride, int64_t p,
+                                             int64_t L, uint32_t v, uint32_t chbit, int border, int64_t gofs,
+                                             int64_t Lg) {
+  return scan_global_rows<1>(in + base + p * astride, astride, (int32_t)(L - 1 - p), (int32_t)p, v, chbit,
+                          border && gofs + L >= Lg, gofs > 0 || border);
 }
 
 struct ColArgs {
@@ -356,6 +392,11 @@ struct ColArgs {
   int64_t p_lo, p_hi, gofs, Lg;
   FastDiv f_nxb, f_nseg, f_ninner;  // the CTA index split (block indices are 32-bit)
   int defer;  // 16-bit kernel: a scan that leaves the staged window lists its CTA for the envelope pass
+  // 16-bit kernel (round 2c): an element whose scan leaves the staged window (and is not deferred to
+  // the envelope pass) is appended here as (base << 24 | p) instead of scanned in line; the list
+  // kernel scans it with batched L2 reads.  Null (or a full list): the in-line 32-bit scan.
+  unsigned long long* slow;
+  uint32_t slow_cap;
 };
 
 // ---- exact 32-bit column pass (one CTA = 256 positions x 32 columns) --------------------
@@ -468,7 +509,7 @@ __device__ __forceinline__ void col32_body(const ColArgs& a, int64_t bid, uint32
 template <bool FINAL>
 __global__ void __launch_bounds__(256) k_edt_col(ColArgs a, const uint32_t* __restrict__ listed,
                                                  WsHeader* __restrict__ hdr) {
-  __shared__ uint32_t tile[kColRows * 32];
+  __shared__ __align__(16) uint32_t tile[kColRows * 32];
   if (!listed) {
     col32_body<FINAL>(a, blockIdx.x, tile, hdr);
     return;
@@ -651,7 +692,7 @@ template <bool FINAL, int U, int PP>
 #endif
 __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, uint32_t* __restrict__ satlist,
                                                    WsHeader* __restrict__ hdr) {
-  __shared__ uint32_t tile[kColRows * 32];
+  __shared__ __align__(16) uint32_t tile[kColRows * 32];
   const uint32_t* __restrict__ in = a.in;
   const int64_t L = a.L, astride = a.astride;
   const uint32_t chbit = a.chbit;
@@ -673,8 +714,45 @@ __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, u
   const uint32_t vup = (a.border && a.gofs + L >= a.Lg) ? 0u : kCap16;
   uint32_t vdn = kCap16;
   if (lo < 0) vdn = a.gofs == 0 ? (a.border ? 0u : kCap16) : ((word(0) & chbit) ? 0u : kCap16);
-  {  // staging: warp w transforms the contiguous rows [lo + 44w, lo + 44w + 44), top down
-    constexpr int kPer = kColRows / kColWarps;
+  constexpr int kPer = kColRows / kColWarps;
+  if (kColCpAsync && (a.X & 3) == 0 && (astride & 3) == 0 && xb * 32 + 32 <= a.X) {
+    // staging (round 2c): the raw words of every in-axis row by cp.async, all 16-byte chunks in
+    // flight at once (the per-warp load batches of the register path left 42 % of the stall
+    // samples at the barrier after staging), then the (up, down) pairs in place, top down per warp
+    const uint32_t* cb = in + (base - lane);
+    for (int c = threadIdx.x; c < kColRows * 8; c += kColWarps * 32) {
+      const int r = c >> 3, part = c & 7;
+      const int64_t q = lo + r;
+      if (q >= 0 && q < L) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(tile + r * 32 + 4 * part);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(cb + q * astride + 4 * part)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    const int rb = warp * kPer;  // this warp's rows [rb, rb + kPer) of the tile
+    const int64_t qt = lo + rb + kPer;
+    __syncthreads();
+    // the raw word above the block: the next warp's first row (read before it is rewritten)
+    uint32_t wn = rb + kPer < kColRows ? ((qt >= 0 && qt < L) ? tile[(rb + kPer) * 32 + lane] : 0u) : word(qt);
+    __syncthreads();
+    uint32_t* trow = tile + (rb + kPer - 1) * 32 + lane;
+    for (int k = kPer - 1; k >= 0; --k) {
+      const int64_t q = lo + rb + k;
+      uint32_t pr, wq = 0u;
+      if (q < 0) pr = vdn | (vdn << 16);
+      else if (q >= L) pr = vup | (vup << 16);
+      else {
+        wq = *trow;
+        const uint32_t gq = min(wq & kMask, kCap16);
+        pr = ((wq & chbit) ? 0u : gq) | (((wn & chbit) ? 0u : gq) << 16);
+      }
+      *trow = pr;
+      trow -= 32;
+      wn = wq;
+    }
+  } else {  // staging: warp w transforms the contiguous rows [lo + 44w, lo + 44w + 44), top down
     const int64_t r0 = lo + (int64_t)warp * kPer;
     uint32_t* trow = tile + (r0 - lo + kPer - 1) * 32 + lane;
     if (xin && r0 >= 0 && r0 + kPer < L) {  // interior block (the common case): no bounds tests
@@ -771,6 +849,16 @@ __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, u
             bst[0] = mA & 0xFFFFu, bst[1] = mA >> 16, bst[2] = mB & 0xFFFFu, bst[3] = mB >> 16;
           } else if (a.defer && reach > kDeferReach) {  // the exact envelope pass recomputes this CTA
             bst[0] = bst[1] = bst[2] = bst[3] = kCap16;
+          } else if (a.slow) {  // exact, 32-bit, in the list kernel (placeholder 0 written here)
+            const uint32_t nm = (uint32_t)((g0 != 0u) + (g1 != 0u) + (g2 != 0u) + (g3 != 0u));
+            uint32_t at = atomicAdd(&hdr->slow_n, nm);
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+              if (v[m] & kMask) {
+                if (at < a.slow_cap) a.slow[at] = ((unsigned long long)base << 24) | (unsigned long long)(s0 + j + m);
+                else bst[m] = scan_global(in, base, astride, s0 + j + m, L, v[m], chbit, a.border, a.gofs, a.Lg);
+                ++at;
+              }
           } else {  // exact, 32-bit
 #pragma unroll
             for (int m = 0; m < 4; ++m)
@@ -955,6 +1043,33 @@ __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, u
   }
 }
 
+// the elements K2/K3 listed (their scans leave the staged window): one thread each, the exact
+// 32-bit scan with kSgBatchList L2 reads in flight; max / n-site statistics as the CTA would
+template <bool FINAL>
+__global__ void __launch_bounds__(256) k_edt_col_slow(ColArgs a, const WsHeader* __restrict__ hdr_in,
+                                                      WsHeader* __restrict__ hdr) {
+  const uint32_t n = min(hdr_in->slow_n, a.slow_cap);
+  uint32_t dmax = 0;
+  bool nosite = false;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const unsigned long long e = a.slow[t];
+    const int64_t base = (int64_t)(e >> 24), p = (int64_t)(e & 0xFFFFFFull);
+    const uint32_t* at = a.in + base + p * a.astride;
+    const uint32_t v = __ldg(at);
+    const uint32_t best = scan_global_rows<kSgBatchList>(at, a.astride, (int32_t)(a.L - 1 - p), (int32_t)p, v, a.chbit,
+                                                         a.border && a.gofs + a.L >= a.Lg, a.gofs > 0 || a.border);
+    a.out[base + (p - a.p_lo) * a.astride] = FINAL ? best : (best | (v & (kBitY | kBitZ)));
+    dmax = max(dmax, best);
+    nosite |= best >= kInf;
+  }
+  dmax = __reduce_max_sync(kFull, dmax);
+  nosite = __any_sync(kFull, nosite);
+  if ((threadIdx.x & 31) == 0) {
+    if (dmax) atomicMax(FINAL ? &hdr->dmax : &hdr->dxymax, dmax);
+    if (FINAL && nosite) atomicOr(&hdr->status, kStNoSite);
+  }
+}
+
 }  // namespace
 
 // a per-device row of -1 labels (16384 entries): the y / z neighbour row of the first row / slice
@@ -1061,12 +1176,24 @@ void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, 
   if (nslots > (int64_t)nsm * 16) nslots = (int64_t)nsm * 16;
   if (nslots > 0 && !getenv("FASTRS_COL_WINDOWED")) {
     a.defer = getenv("FASTRS_COL_FH_ALL") ? 2 : 1;  // 2 (test hook): every CTA takes the envelope pass
+    // the slow-scan list lives at the start of the scratch; the list kernel consumes it before
+    // the envelope pass reuses the scratch for its stacks.  FASTRS_COL_INLINE (test hook): none
+    if (!getenv("FASTRS_COL_INLINE") && a.L < (1 << 24) && g.B * g.Z * g.Y * g.X < (1ll << 40)) {
+      const size_t cap = scratch_bytes / sizeof(unsigned long long);
+      a.slow = (unsigned long long*)scratch;
+      a.slow_cap = (uint32_t)(cap < (size_t)(1u << 24) ? cap : (size_t)(1u << 24));
+      if (const char* sc = getenv("FASTRS_COL_SLOW_CAP")) a.slow_cap = (uint32_t)atoi(sc);  // test hook
+      cudaMemsetAsync(&hdr->slow_n, 0, sizeof(uint32_t), st);
+    }
     const unsigned fh_grid = (unsigned)((nslots + 7) / 8);
+    const unsigned slow_grid = (unsigned)(nsm * 4);
     if (final_pass) {
       k_edt_col16<true, kScan16U, kColPP><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, satlist, hdr);
+      if (a.slow) k_edt_col_slow<true><<<slow_grid, 256, 0, st>>>(a, hdr, hdr);
       k_edt_col_fh<true><<<fh_grid, 256, 0, st>>>(a, satlist, hdr, (uint2*)scratch, (int)nslots);
     } else {
       k_edt_col16<false, kScan16U, kColPP><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, satlist, hdr);
+      if (a.slow) k_edt_col_slow<false><<<slow_grid, 256, 0, st>>>(a, hdr, hdr);
       k_edt_col_fh<false><<<fh_grid, 256, 0, st>>>(a, satlist, hdr, (uint2*)scratch, (int)nslots);
     }
     return;

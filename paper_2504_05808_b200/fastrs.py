@@ -54,7 +54,8 @@ class _Diag(ctypes.Structure):
                 ("n_rounds_extra", ctypes.c_uint32), ("n_regathers", ctypes.c_uint32),
                 ("max_group_list", ctypes.c_uint32), ("sum_group_list", ctypes.c_uint64),
                 ("n_painted", ctypes.c_uint64), ("n_covering", ctypes.c_uint64),
-                ("n_staged", ctypes.c_uint32), ("n_deferred", ctypes.c_uint32)]
+                ("n_staged", ctypes.c_uint32), ("n_deferred", ctypes.c_uint32),
+                ("n_col_slow", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 class _SlabInfo(ctypes.Structure):

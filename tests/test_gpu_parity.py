@@ -170,6 +170,53 @@ def test_envelope_column_pass_large_objects(F):
             np.testing.assert_array_equal(got, ref[(slice(1, -1),) * img.ndim])
 
 
+def _edt_env(F, t, env, flags=1, ndim=None):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        got = _u32(F.edt_sq(t, flags=flags, ndim=ndim))
+        d = F.diagnostics(F.last_workspace())
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+    return got, d
+
+
+def test_column_slow_list(F):
+    """K2/K3 elements whose scan leaves the staged window go to a list scanned by a separate kernel
+    with batched L2 reads (round 2c): D against scipy / the oracle, bit-identical to the in-line
+    32-bit scan (FASTRS_COL_INLINE), and with a 3-entry list (FASTRS_COL_SLOW_CAP) whose overflow
+    takes the in-line scan; n_col_slow > 0 shows the list was used."""
+    import scipy.ndimage
+    yy, xx = np.ogrid[:300, :520]
+    ell = (((yy - 150) / 120.0) ** 2 + ((xx - 260) / 250.0) ** 2 <= 1).astype(np.int32)
+    zz, yy3, xx3 = np.ogrid[:420, :130, :130]  # a z cylinder of radius 60: K3 scans cross segment ends
+    sph = (((yy3 - 65) ** 2 + (xx3 - 65) ** 2 <= 60 ** 2) & (zz >= 5) & (zz < 400)).astype(np.int32)
+    del zz, yy3, xx3
+    blobs = synth.random_labels((500, 480), nlabels=3, seed=11, fill=0.9, blob=120)
+    blobs.flat[0] = 0
+    for img, border in ((ell, 1), (sph, 1), (sph, 0), (blobs, 1), (blobs, 0)):
+        t = _dev(img)
+        got, d = _edt_env(F, t, {})
+        if img is not blobs:
+            assert d["n_col_slow"] > 0, d
+        inline, d_in = _edt_env(F, t, {"FASTRS_COL_INLINE": "1"}, flags=border)
+        assert d_in["n_col_slow"] == 0
+        got, _ = _edt_env(F, t, {}, flags=border)
+        np.testing.assert_array_equal(got, inline)
+        capped, d_cap = _edt_env(F, t, {"FASTRS_COL_SLOW_CAP": "3"}, flags=border)
+        assert d_cap["n_col_slow"] > 3
+        np.testing.assert_array_equal(capped, inline)
+        if img.max() == 1 and border == 1:
+            ref = np.rint(scipy.ndimage.distance_transform_edt(np.pad(img > 0, 1)) ** 2).astype(np.uint32)
+            np.testing.assert_array_equal(got, ref[(slice(1, -1),) * img.ndim])
+        elif img is blobs:
+            np.testing.assert_array_equal(got, oracle.edt_sq(img, flags=border))
+
+
 @pytest.mark.parametrize("shape", [(1, 1), (1, 77), (77, 1), (2, 3, 1), (1, 1, 1), (9, 1, 40), (33, 65),
                                    (17, 9, 33), (8, 8, 32), (8, 64, 64), (3, 16384)])
 def test_ragged_and_degenerate_shapes(F, shape):
