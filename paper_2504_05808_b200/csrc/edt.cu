@@ -133,6 +133,10 @@ __device__ __forceinline__ int swz(int G) { return G ^ ((G >> 3) & 7); }  // 16-
 #ifndef FASTRS_K1_MINB
 #define FASTRS_K1_MINB 5
 #endif
+#ifndef FASTRS_K1_CPASYNC
+#define FASTRS_K1_CPASYNC 1
+#endif
+constexpr bool kK1CpAsync = FASTRS_K1_CPASYNC != 0;
 __global__ void __launch_bounds__(256, FASTRS_K1_MINB) k_edt_x_seg(const int32_t* __restrict__ lab,
                                                    const int32_t* __restrict__ below, const int32_t* __restrict__ sent,
                                                    uint32_t* __restrict__ out, int64_t nrows, int X, int64_t Y,
@@ -173,7 +177,16 @@ __global__ void __launch_bounds__(256, FASTRS_K1_MINB) k_edt_x_seg(const int32_t
     const int e0 = blk << 10;
     const int ng = min(1024, X - e0) >> 2;  // granules in this block (a multiple of 32)
     const int4* src = reinterpret_cast<const int4*>(L + e0);
-    for (int G = lane; G < ng; G += 32) buf4[swz(G)] = __ldg(src + G);
+    if (kK1CpAsync) {  // round 2c: every granule of the block in flight at once (no register hop)
+      for (int G = lane; G < ng; G += 32) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(buf4 + swz(G));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + G) : "memory");
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    } else {
+      for (int G = lane; G < ng; G += 32) buf4[swz(G)] = __ldg(src + G);
+    }
     __syncwarp();
     const int seg = (blk << 5) + lane;
     int32_t pv = lane > 0 ? (int32_t)buf[swz(lane * 8 - 1) * 4 + 3] : carry;
@@ -719,15 +732,17 @@ __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, u
     // staging (round 2c): the raw words of every in-axis row by cp.async, all 16-byte chunks in
     // flight at once (the per-warp load batches of the register path left 42 % of the stall
     // samples at the barrier after staging), then the (up, down) pairs in place, top down per warp
-    const uint32_t* cb = in + (base - lane);
-    for (int c = threadIdx.x; c < kColRows * 8; c += kColWarps * 32) {
-      const int r = c >> 3, part = c & 7;
-      const int64_t q = lo + r;
-      if (q >= 0 && q < L) {
-        const unsigned sa = (unsigned)__cvta_generic_to_shared(tile + r * 32 + 4 * part);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(cb + q * astride + 4 * part)
+    static_assert(kColRows % 32 == 0 && kColWarps == 8, "32 rows x 8 chunks per pass");
+    const int part = threadIdx.x & 7, rc = threadIdx.x >> 3;  // thread: chunk `part` of rows rc + 32 i
+    const uint32_t* gp = in + (base - lane) + (lo + rc) * astride + 4 * part;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(tile + rc * 32 + 4 * part);
+#pragma unroll
+    for (int i = 0; i < kColRows / 32; ++i) {
+      const int64_t q = lo + rc + 32 * i;
+      if (q >= 0 && q < L)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa + i * 32 * 32 * 4),
+                     "l"(gp + 32 * i * astride)
                      : "memory");
-      }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -738,19 +753,30 @@ __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, u
     uint32_t wn = rb + kPer < kColRows ? ((qt >= 0 && qt < L) ? tile[(rb + kPer) * 32 + lane] : 0u) : word(qt);
     __syncthreads();
     uint32_t* trow = tile + (rb + kPer - 1) * 32 + lane;
-    for (int k = kPer - 1; k >= 0; --k) {
-      const int64_t q = lo + rb + k;
-      uint32_t pr, wq = 0u;
-      if (q < 0) pr = vdn | (vdn << 16);
-      else if (q >= L) pr = vup | (vup << 16);
-      else {
-        wq = *trow;
+    if (lo + rb >= 0 && lo + rb + kPer <= L) {  // every row of the block inside the axis
+#pragma unroll 11
+      for (int k = kPer - 1; k >= 0; --k) {
+        const uint32_t wq = *trow;
         const uint32_t gq = min(wq & kMask, kCap16);
-        pr = ((wq & chbit) ? 0u : gq) | (((wn & chbit) ? 0u : gq) << 16);
+        *trow = ((wq & chbit) ? 0u : gq) | (((wn & chbit) ? 0u : gq) << 16);
+        trow -= 32;
+        wn = wq;
       }
-      *trow = pr;
-      trow -= 32;
-      wn = wq;
+    } else {
+      for (int k = kPer - 1; k >= 0; --k) {
+        const int64_t q = lo + rb + k;
+        uint32_t pr, wq = 0u;
+        if (q < 0) pr = vdn | (vdn << 16);
+        else if (q >= L) pr = vup | (vup << 16);
+        else {
+          wq = *trow;
+          const uint32_t gq = min(wq & kMask, kCap16);
+          pr = ((wq & chbit) ? 0u : gq) | (((wn & chbit) ? 0u : gq) << 16);
+        }
+        *trow = pr;
+        trow -= 32;
+        wn = wq;
+      }
     }
   } else {  // staging: warp w transforms the contiguous rows [lo + 44w, lo + 44w + 44), top down
     const int64_t r0 = lo + (int64_t)warp * kPer;
