@@ -15,5 +15,5 @@ except Exception as e:
     print("no bench json", e)
 PY
 if [ -n "$KREGEX" ]; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$KREGEX" -s ${SKIP:-2} -c ${COUNT:-2} -o gpurun_out/prof_${TAG:-iter} -f python tools/prof_run.py --config ${CFG:-4} --iters 1 > gpurun_out/ncu_full.log 2>&1; echo "ncu rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"$KREGEX" -o gpurun_out/prof_${TAG:-iter} -f python tools/prof_run.py --config ${CFG:-4} --iters 1 > gpurun_out/ncu_full.log 2>&1; echo "ncu rc=$?"
 fi

@@ -7,4 +7,4 @@ python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 |
 timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; echo "bench rc=$?"; tail -2 gpurun_out/bench_${TAG}.err
 CMD="python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu-baseline"
 timeout 600 $CMD > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_" -s ${SKIP:-14} -c ${COUNT:-14} -o gpurun_out/prof_${TAG}_c4 -f python tools/prof_run.py --config 4 --iters 1 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"; tail -3 gpurun_out/ncu_full.log
+timeout 1500 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"k_" -o gpurun_out/prof_${TAG}_c4 -f python tools/prof_run.py --config 4 --iters 1 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"; tail -3 gpurun_out/ncu_full.log

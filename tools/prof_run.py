@@ -22,5 +22,9 @@ for _ in range(a.iters):
     r = F.sphericity_roundness(t, max_label=info["max_label"], ndim=ndim)
 torch.cuda.synchronize()
 F.profile(True)
+torch.cuda.synchronize()
+torch.cuda.profiler.start()  # ncu --profile-from-start off captures exactly this call's kernels
 F.sphericity_roundness(t, max_label=info["max_label"], ndim=ndim)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print(F.profile_read(), F.diagnostics(F.last_workspace()))
