@@ -43,10 +43,22 @@ for d in data:
         "warp_instructions": val(d, "smsp__inst_executed.sum"),
     })
 res = {}
+ADD = ("time_ms", "dram_read_bytes", "dram_write_bytes", "warp_instructions")
 for k, lst in agg.items():
-    r = {m: (sum(x[m] for x in lst if x[m] is not None) / len(lst)) for m in lst[0]}
+    # the capture holds one call (cudaProfilerStart/Stop in tools/prof_run.py): additive metrics are
+    # summed over the call's launches of the kernel (K5 runs in waves), the rest time-weighted
+    tw = sum(x["time_ms"] or 0 for x in lst) or 1.0
+    r = {}
+    for m in lst[0]:
+        v = [x for x in lst if x[m] is not None]
+        if m in ADD:
+            r[m] = sum(x[m] for x in v)
+        elif m == "registers":
+            r[m] = max((x[m] for x in v), default=None)
+        else:
+            r[m] = sum(x[m] * (x["time_ms"] or 0) for x in v) / tw
     r["launches_captured"] = len(lst)
-    r["traffic_bytes_per_launch"] = (r["dram_read_bytes"] or 0) + (r["dram_write_bytes"] or 0)
+    r["traffic_bytes_per_launch"] = (r["dram_read_bytes"] or 0) + (r["dram_write_bytes"] or 0)  # per call
     res[k] = r
 json.dump({"title": title, "report": rep, "kernels": res}, open(out, "w"), indent=1)
 print(f"# {title}")
