@@ -54,7 +54,7 @@ STAGE_KERNELS = {"edt_x": ["k_edt_x_seg", "k_edt_x"], "edt_y": ["k_edt_col16<0",
                                                "k_epilogue_fallback<1"], "metrics": ["k_metrics"]}
 STAGE_KERNELS_2D = dict(STAGE_KERNELS, edt_y=["k_edt_col16<1", "k_edt_col<1", "k_edt_col_fh<1"], prune=["k_prune<0"],
                         k5=["k_dilate_gather<0", "k_dilate_paint<0", "k_dilate_atomic<0", "k_epilogue_fallback<0"])
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02g_ncu_summary_c4.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02i_ncu_summary_c4.json")
 
 
 def parse():
