@@ -732,26 +732,24 @@ __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, u
     // staging (round 2c): the raw words of every in-axis row by cp.async, all 16-byte chunks in
     // flight at once (the per-warp load batches of the register path left 42 % of the stall
     // samples at the barrier after staging), then the (up, down) pairs in place, top down per warp
-    static_assert(kColRows % 32 == 0 && kColWarps == 8, "32 rows x 8 chunks per pass");
-    const int part = threadIdx.x & 7, rc = threadIdx.x >> 3;  // thread: chunk `part` of rows rc + 32 i
-    const uint32_t* gp = in + (base - lane) + (lo + rc) * astride + 4 * part;
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(tile + rc * 32 + 4 * part);
+    // each warp copies its own 44 rows (lane: chunk lane & 7 of rows lane >> 3 + 4 i), so only
+    // the warp waits for them; the raw word above the block comes straight from global
+    static_assert(kPer % 4 == 0, "4 rows x 8 chunks per warp pass");
+    const int rb = warp * kPer;  // this warp's rows [rb, rb + kPer) of the tile
+    const int part = lane & 7, r4 = lane >> 3;
+    const uint32_t* gp = in + (base - lane) + (lo + rb + r4) * astride + 4 * part;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(tile + (rb + r4) * 32 + 4 * part);
 #pragma unroll
-    for (int i = 0; i < kColRows / 32; ++i) {
-      const int64_t q = lo + rc + 32 * i;
+    for (int i = 0; i < kPer / 4; ++i) {
+      const int64_t q = lo + rb + r4 + 4 * i;
       if (q >= 0 && q < L)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa + i * 32 * 32 * 4),
-                     "l"(gp + 32 * i * astride)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa + i * 4 * 32 * 4), "l"(gp + 4 * i * astride)
                      : "memory");
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
+    uint32_t wn = word(lo + rb + kPer);
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    const int rb = warp * kPer;  // this warp's rows [rb, rb + kPer) of the tile
-    const int64_t qt = lo + rb + kPer;
-    __syncthreads();
-    // the raw word above the block: the next warp's first row (read before it is rewritten)
-    uint32_t wn = rb + kPer < kColRows ? ((qt >= 0 && qt < L) ? tile[(rb + kPer) * 32 + lane] : 0u) : word(qt);
-    __syncthreads();
+    __syncwarp();
     uint32_t* trow = tile + (rb + kPer - 1) * 32 + lane;
     if (lo + rb >= 0 && lo + rb + kPer <= L) {  // every row of the block inside the axis
 #pragma unroll 11
