@@ -389,7 +389,10 @@ def run_fastrs(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(lab.nbytes),
                 "d2h_bytes_per_step": int(2 * M * 8), "ms_per_step": float(e2e_ms.item())},
         # K1 K2 (+fixup) K3 (+fixup) K4 K5a K5b K5' K5e K6 (3D); the 2D path has no K3
-        "gpu_launches": int((11 if ndim == 3 else 9) * args.steps),
+        # per call (ncu launch list of one call, profiles/r02i_ncu_summary_c4.json): K1; K2 (+ K3) as the 16-bit
+        # scan, the slow-scan list and the envelope fix-up; K4; K5a + K5b in three waves with two wave resets;
+        # K5', K5e (fallback tiles) and K6 -> 19 in 3D, 16 in 2D
+        "gpu_launches": int((19 if ndim == 3 else 16) * args.steps),
         "roofline": {"bound": "hbm", "stage": dom, "kernels": SK[dom], "achieved": achieved,
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                      "traffic": ncu_traffic(SK[dom]),
@@ -512,7 +515,7 @@ def run_slab(args):
                            "l2": "inputs larger than L2, no flush"},
                 "e2e": {"value": n / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(n * 4),
                         "d2h_bytes_per_step": int(2 * ml * 8 * world), "ms_per_step": e2e_ms},
-                "gpu_launches": int(15 * args.steps),
+                "gpu_launches": int(19 * args.steps),  # the single call's 19 (one rank; more z-pass ranges at N > 1)
                 "roofline": {"bound": "hbm", "stage": "whole path per rank (K1-K6)", "achieved": path_gbs,
                              "peak": hbm_peak, "unit": "GB/s", "frac": path_gbs / hbm_peak, "traffic": None,
                              "bytes_rule": "SURVEY.md §8(d) 33 B per own grid element; exchanges not counted"},
