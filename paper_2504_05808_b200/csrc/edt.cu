@@ -317,6 +317,10 @@ constexpr int kColPP = FASTRS_COL_PP;
 #define FASTRS_COL_CPASYNC 1
 #endif
 constexpr bool kColCpAsync = FASTRS_COL_CPASYNC != 0;  // K2/K3 staging by cp.async (round 2c)
+#ifndef FASTRS_COL_PREFETCH_L2
+#define FASTRS_COL_PREFETCH_L2 0
+#endif
+constexpr int kColPrefetch = FASTRS_COL_PREFETCH_L2;  // L2 prefetch distance in CTAs per SM (0: off; 5 measured 2.83 / 3.07 vs 2.75 / 2.66 ms)
 
 // Slow path of the column scan for an element whose window leaves the staged rows: the same
 // exact scan in 32-bit arithmetic, every read from global memory (L2).  Round 2c: the reads of
@@ -410,6 +414,7 @@ struct ColArgs {
   // kernel scans it with batched L2 reads.  Null (or a full list): the in-line 32-bit scan.
   unsigned long long* slow;
   uint32_t slow_cap;
+  int pf_ahead;  // 16-bit kernel: L2 prefetch of CTA blockIdx + pf_ahead's rows (0: off)
 };
 
 // ---- exact 32-bit column pass (one CTA = 256 positions x 32 columns) --------------------
@@ -728,6 +733,20 @@ __global__ void __launch_bounds__(256, FASTRS_COL_MINB) k_edt_col16(ColArgs a, u
   uint32_t vdn = kCap16;
   if (lo < 0) vdn = a.gofs == 0 ? (a.border ? 0u : kCap16) : ((word(0) & chbit) ? 0u : kCap16);
   constexpr int kPer = kColRows / kColWarps;
+  if (kColPrefetch > 0 && a.pf_ahead > 0 && blockIdx.x + a.pf_ahead < gridDim.x) {
+    // round 2c: warm L2 with the staged rows of the CTA launched ~one residency later (CTAs start
+    // in index order): one 128-byte line per row, rows split over the threads
+    uint32_t pq = blockIdx.x + (uint32_t)a.pf_ahead, pxr, psr, pir;
+    pq = a.f_nxb.divmod(pq, pxr);
+    pq = a.f_nseg.divmod(pq, psr);
+    const uint32_t poq = a.f_ninner.divmod(pq, pir);
+    const int64_t pbase = (int64_t)poq * a.outer_mult + (int64_t)pir * a.inner_mult + (int64_t)pxr * 32;
+    const int64_t plo = a.p_lo + (int64_t)psr * kColS - kColH;
+    for (int r = threadIdx.x; r < kColRows; r += kColWarps * 32) {
+      const int64_t q = plo + r;
+      if (q >= 0 && q < L) asm volatile("prefetch.global.L2 [%0];" ::"l"(in + pbase + q * astride));
+    }
+  }
   if (kColCpAsync && (a.X & 3) == 0 && (astride & 3) == 0 && xb * 32 + 32 <= a.X) {
     // staging (round 2c): the raw words of every in-axis row by cp.async, all 16-byte chunks in
     // flight at once (the per-warp load batches of the register path left 42 % of the stall
@@ -1211,6 +1230,7 @@ void launch_edt_col(const uint32_t* in, uint32_t* out, const Geom& g, int axis, 
     }
     const unsigned fh_grid = (unsigned)((nslots + 7) / 8);
     const unsigned slow_grid = (unsigned)(nsm * 4);
+    a.pf_ahead = nsm * kColPrefetch;
     if (final_pass) {
       k_edt_col16<true, kScan16U, kColPP><<<(unsigned)blocks, kColWarps * 32, 0, st>>>(a, satlist, hdr);
       if (a.slow) k_edt_col_slow<true><<<slow_grid, 256, 0, st>>>(a, hdr, hdr);
