@@ -54,7 +54,7 @@ STAGE_KERNELS = {"edt_x": ["k_edt_x_seg", "k_edt_x"], "edt_y": ["k_edt_col16<0",
                                                "k_epilogue_fallback<1"], "metrics": ["k_metrics"]}
 STAGE_KERNELS_2D = dict(STAGE_KERNELS, edt_y=["k_edt_col16<1", "k_edt_col<1", "k_edt_col_fh<1"], prune=["k_prune<0"],
                         k5=["k_dilate_gather<0", "k_dilate_paint<0", "k_dilate_atomic<0", "k_epilogue_fallback<0"])
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02i_ncu_summary_c4.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02k_ncu_summary_c4.json")
 
 
 def parse():
@@ -389,7 +389,7 @@ def run_fastrs(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(lab.nbytes),
                 "d2h_bytes_per_step": int(2 * M * 8), "ms_per_step": float(e2e_ms.item())},
         # K1 K2 (+fixup) K3 (+fixup) K4 K5a K5b K5' K5e K6 (3D); the 2D path has no K3
-        # per call (ncu launch list of one call, profiles/r02i_ncu_summary_c4.json): K1; K2 (+ K3) as the 16-bit
+        # per call (ncu launch list of one call, profiles/r02k_ncu_summary_c4.json): K1; K2 (+ K3) as the 16-bit
         # scan, the slow-scan list and the envelope fix-up; K4; K5a + K5b in three waves with two wave resets;
         # K5', K5e (fallback tiles) and K6 -> 19 in 3D, 16 in 2D
         "gpu_launches": int((19 if ndim == 3 else 16) * args.steps),
